@@ -1,0 +1,42 @@
+# Build of the CUDA library (product) and of the CPU oracle (test infrastructure).
+# The two targets share no sources, headers or flags.
+NVCC      ?= /usr/local/cuda/bin/nvcc
+CC        := /usr/bin/gcc
+PKG       := paper_1406_5369_b200
+CSRC      := $(PKG)/csrc
+PYSITE    := $(shell python -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")
+NCCL_DIR  := $(PYSITE)/nvidia/nccl
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC,-O2 \
+             -I include -I $(CSRC) -I $(NCCL_DIR)/include
+LIB       := $(PKG)/libmgb200.so
+
+CU_SRCS   := $(wildcard $(CSRC)/*.cu)
+CU_HDRS   := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/mg.h
+CU_OBJS   := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
+
+ORACLE_CFLAGS := -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -fopenmp -std=c99 -Wall
+
+.PHONY: all oracle lib clean
+all: lib oracle
+
+lib: $(LIB)
+
+build/%.o: $(CSRC)/%.cu $(CU_HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
+
+$(LIB): $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -L $(NCCL_DIR)/lib -l:libnccl.so.2 \
+	    -Xlinker -rpath,$(NCCL_DIR)/lib -lcuda
+
+oracle: oracle/liboracle_f64.so oracle/liboracle_f32.so
+
+oracle/liboracle_f64.so: oracle/mg_oracle.c oracle/mg_oracle.h
+	$(CC) $(ORACLE_CFLAGS) -DOR_REAL=double -o $@ oracle/mg_oracle.c -lm
+
+oracle/liboracle_f32.so: oracle/mg_oracle.c oracle/mg_oracle.h
+	$(CC) $(ORACLE_CFLAGS) -DOR_REAL=float -o $@ oracle/mg_oracle.c -lm
+
+clean:
+	rm -rf build $(LIB) oracle/*.so
