@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 V-cycle (the driver's contract).
+
+One STEP = one pass of the whole hot path over the workload: one V(2,2)-cycle
+(pre-smoothing, residual, full-weighting restriction, coarse solve,
+prolongation + correction, post-smoothing on every level) plus the residual
+norm that the paper's driver loop evaluates after every cycle.
+
+Workload (N=1): BASELINE.json configs[2], the north_star's headline case:
+3D Poisson 7-point, 513^3 nodes, red-black Gauss-Seidel V(2,2), FP64,
+W1 = the paper's f = 0 / random initial guess, seed 42, generated
+on the device by the same SplitMix64 counter generator the oracle side uses.
+Each array is 1.08 GB, far larger than the 126 MB L2, so no L2 flush is
+needed between steps.
+
+Metric: unknowns/s = 511^3 interior unknowns per step / step time (all ranks'
+unknowns / max-over-ranks time for N>1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mg|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (dim, nodes, smoother, nu1, nu2, dtype, levels, omega)
+    "C3-f64": (3, 513, "rbgs", 2, 2, "f64", 0, 1.0),
+    "C3-f32": (3, 513, "rbgs", 2, 2, "f32", 0, 1.0),
+    "C2": (3, 129, "rbgs", 2, 2, "f64", 0, 1.0),
+    "C4": (2, 8193, "jacobi", 3, 3, "f32", 0, 0.8),
+    "C5": (3, 1025, "rbgs", 2, 2, "f64", 0, 1.0),
+    "C1": (2, 65, "jacobi", 2, 2, "f64", 5, 0.8),
+}
+WORKLOAD_DESC = {
+    "C3-f64": "3D Poisson 7-point 513^3 nodes, RBGS V(2,2), FP64, W1 (f=0, u0~U[0,1) seed 42)",
+    "C3-f32": "3D Poisson 7-point 513^3 nodes, RBGS V(2,2), FP32, W1 (f=0, u0~U[0,1) seed 42)",
+    "C2": "3D Poisson 7-point 129^3 nodes, RBGS V(2,2), FP64, W1 seed 42",
+    "C4": "2D Poisson 5-point 8193^2 nodes, Jacobi(0.8) V(3,3), FP32, W1 seed 42",
+    "C5": "3D Poisson 7-point 1025^3 nodes, RBGS V(2,2), FP64, W1 seed 42",
+    "C1": "2D Poisson 5-point 65^2 nodes, 5 levels, Jacobi(0.8) V(2,2), FP64, W1 seed 42",
+}
+METRIC = "V(2,2)-cycle unknowns/s (one cycle + residual norm per step)"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def interior_unknowns(dim, nodes):
+    return (nodes - 2) ** dim
+
+
+def model_bytes_per_step(S, esz):
+    """B_alg of SURVEY §8(a) for this hierarchy (fused schedule model) + the norm pass."""
+    total = 0.0
+    nu = S.cfg.nu1 + S.cfg.nu2
+    for l in range(S.levels - 1):
+        n = 1
+        for c in S.level_cells(l):
+            n *= c + 1
+        total += n * (3 * nu + 2 * 2.0 ** -S.dim) * esz
+    n0 = 1
+    for c in S.level_cells(0):
+        n0 *= c + 1
+    return total + 2 * n0 * esz
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index):
+        self.ok = False
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs"), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, read+write bytes)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic(kernel):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(kernel)
+
+
+# --------------------------------------------------------------------- oracle (CPU) legs
+def oracle_step_time(cfgname, max_seconds=30.0):
+    """Time the CPU oracle, as it stands, on one V-cycle + norm of the workload.
+    Returns (seconds per step, unknowns per step, sample description, threads)."""
+    import numpy as np
+
+    import oracle as orc
+    from paper_1406_5369_b200 import workloads as wl
+    dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[cfgname]
+    cells = (nodes - 1,) * dim
+    # full size when it fits the budget, else the largest power-of-two grid that does
+    npdt = np.float64 if dt == "f64" else np.float32
+    for n in [nodes - 1, (nodes - 1) // 2, (nodes - 1) // 4]:
+        cells = (n,) * dim
+        c = orc.Config(dim=dim, cells=cells, levels=levels if n == nodes - 1 else 0,
+                       smoother=orc.RBGS if sm == "rbgs" else orc.JACOBI, omega=omega, nu1=nu1, nu2=nu2)
+        O = orc.Oracle(c, npdt)
+        u, f = wl.workload("W1", dim, cells, seed=42, dtype=npdt)
+        t0 = time.perf_counter()
+        O.vcycle_inplace(u, f)
+        O.norm(0, u, f)
+        t = time.perf_counter() - t0
+        if t <= max_seconds or n == (nodes - 1) // 4:
+            desc = (f"one V({nu1},{nu2})-cycle + residual norm of the CPU oracle (plain C, -O2 "
+                    f"-ffp-contract=off, OpenMP over planes) on {'x'.join(str(c + 1) for c in cells)} nodes, W1 seed 42"
+                    + ("" if n == nodes - 1 else f" (reduced from {nodes}^{dim} to fit the CPU time budget)"))
+            return t, interior_unknowns(dim, n + 1), desc, orc.num_threads(npdt), (O, u, f)
+    raise RuntimeError("unreachable")
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0  # the reference arm runs on rank 0 only
+    t_first, unk, desc, threads, (O, u, f) = oracle_step_time(args.config, max_seconds=20.0)
+    # warm-up steps beyond the first, then exactly K timed steps
+    for _ in range(max(args.warmup - 1, 0)):
+        O.vcycle_inplace(u, f)
+        O.norm(0, u, f)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.vcycle_inplace(u, f)
+        O.norm(0, u, f)
+    dt = (time.perf_counter() - t0) / args.steps
+    val = unk / dt
+    dim, nodes, *_ = CONFIGS[args.config]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "unknowns/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": CONFIGS[args.config][5], "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC[args.config], "parallelism": "cpu-oracle",
+                   "l2": "inputs larger than L2 (CPU run)"},
+        "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": threads, "kind": "oracle", "sample": desc},
+        "e2e": {"value": val, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- GPU arm
+def run_mg(args):
+    import torch
+
+    import paper_1406_5369_b200 as mgb
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[args.config]
+    esz = 8 if dt == "f64" else 4
+    S = mgb.Solver(dim, nodes, levels=levels, smoother=sm, omega=omega, nu1=nu1, nu2=nu2, dtype=dt, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    u = S.empty()
+    f = S.empty()
+    with torch.cuda.stream(stream):
+        S.workload_fill(u, 42, stream=stream)
+    torch.cuda.synchronize()
+    unk = interior_unknowns(dim, nodes)
+
+    def step():
+        S.vcycle(u, f, stream=stream)
+        return S.residual_norm(u, f, stream=stream)
+
+    r0 = S.residual_norm(u, f, stream=stream)
+    for _ in range(args.warmup):
+        step()
+    sampler = ClockSampler(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    rk = r0
+    for _ in range(args.steps):
+        rk = step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    sampler.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    launches = S.launches_per_cycle + 2  # + norm partial + norm final
+
+    # ---- per-kernel CUDA-event timing (separate instrumented pass, eager launches)
+    S.profile_enable(True)
+    nprof = max(3, min(args.steps, 10))
+    for _ in range(nprof):
+        step()
+    recs = S.profile_read()
+    S.profile_enable(False)
+    tot = sum(r["ms"] for r in recs)
+    dom = max(recs, key=lambda r: r["ms"])
+    dom_avg_ms = dom["ms"] / dom["count"]
+    peak, peak_src = measured_peaks()
+    achieved = dom["bytes"] / (dom_avg_ms * 1e-3) / 1e9
+    roofline = {
+        "bound": "hbm", "kernel": dom["name"], "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": ncu_traffic(dom["name"]), "peak_source": peak_src,
+        "alg_bytes_per_launch": dom["bytes"], "avg_launch_ms": dom_avg_ms,
+        "share_of_step": dom["ms"] / tot if tot else None,
+    }
+    B = model_bytes_per_step(S, esz)
+    breakdown = sorted(({"kernel": r["name"], "ms_per_step": r["ms"] / nprof, "launches_per_step": r["count"] / nprof,
+                         "GBps": (r["bytes"] * r["count"] / (r["ms"] * 1e-3) / 1e9) if r["ms"] else None}
+                        for r in recs), key=lambda d: -d["ms_per_step"])[:8]
+
+    # ---- end to end through the C ABI with host buffers (H2D u,f; cycle; norm; D2H u)
+    e2e = None
+    if not args.no_e2e:
+        hu = torch.empty(S.shape, dtype=S.torch_dtype).pin_memory()
+        hf = torch.empty(S.shape, dtype=S.torch_dtype).pin_memory()
+        hu.copy_(u.cpu())
+        hf.copy_(f.cpu())
+        S.vcycle_host(hu, hf, 1, stream=stream)  # warm-up (allocates staging)
+        ne = max(2, min(args.steps, 5))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ne):
+            S.vcycle_host(hu, hf, 1, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / ne
+        nbytes = hu.numel() * hu.element_size()
+        e2e = {"value": unk * world / (ems * 1e-3), "unit": "unknowns/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": nbytes,
+               "path": "mg_vcycle_host (pinned host u,f -> device, 1 cycle + norm, u -> host)"}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        t, cunk, desc, threads, _ = oracle_step_time(args.config, max_seconds=30.0)
+        cpu = {"value": cunk / t, "unit": "unknowns/s", "cores": threads, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": unk * world / (ms * 1e-3), "unit": "unknowns/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC[args.config], "grid_nodes": nodes, "dim": dim,
+                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "l2": "inputs larger than L2 (1.08 GB per array), no flush needed",
+                       "levels": S.levels},
+            "residual_reduction_per_step": (rk / r0) ** (1.0 / (args.steps + args.warmup)) if r0 else None,
+            "model_bytes_per_step": B, "model_GBps": B / (ms * 1e-3) / 1e9,
+            "roofline": roofline, "kernels": breakdown, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
+            "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mg", choices=["mg", "reference"])
+    ap.add_argument("--config", default="C3-f64", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_mg(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,163 @@
+/*
+ * mg.h — C ABI of libmgb200.so: a B200-native (sm_100a) geometric multigrid
+ * V-cycle for finite-difference Poisson-type problems on regular node-based
+ * 2D/3D grids, the data-parallel hot path of arXiv:1406.5369 (Koestler et al.,
+ * "A Scala Prototype to Generate Multigrid Solver Implementations ...").
+ *
+ * Citation keys: P:n = PAPER.md line n (the LaTeX source of arXiv:1406.5369);
+ * Alg. 1 = the recursive V-cycle; the Layer-4 listing = P:263-320.
+ *
+ * Conventions (all entry points):
+ *  - Every function returns an mg_status; nothing throws or aborts across the
+ *    ABI.  On error, mg_error_string(solver) (or mg_error_string(NULL) for a
+ *    failed mg_create) describes the last failure of the calling thread.
+ *  - `u`, `f`, `r`, `e` are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *    of the solver's dtype, laid out as a dense C-order array of shape
+ *    [planes][rows][pitch] (x fastest), see mg_layout / mg_level_layout.
+ *    3D: planes = z nodes, rows = y nodes; 2D: planes = y nodes, rows = 1.
+ *    Node (i,j,k) includes the boundary: i = 0..nx, etc. (cells per axis nx).
+ *    Padding elements (x > nx) are never read or written.
+ *  - Caller-owned buffers must stay alive until the stream work completes.
+ *    `u` and `f` must not alias.  The library never writes boundary nodes of
+ *    the caller's `u` (they hold the Dirichlet data).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  All GPU work
+ *    is enqueued on it; entry points returning a host scalar synchronise it.
+ *  - The library owns coarse-level buffers, the ping-pong buffer, reduction
+ *    partials and cached CUDA graphs (keyed by the (u, f) pointers).
+ *  - There is NO CPU fallback: without a usable sm_100 device every
+ *    compute entry point fails with MG_ERR_CUDA.
+ *  - One solver is used by one host thread at a time.
+ */
+#ifndef MG_H
+#define MG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mg_solver mg_solver;
+
+typedef enum {
+    MG_OK = 0,
+    MG_ERR_INVALID = 1,          /* bad argument / configuration              */
+    MG_ERR_NOT_COARSENABLE = 2,  /* (nodes-1) not divisible by 2^(levels-1)   */
+    MG_ERR_OOM = 3,              /* device allocation failed                  */
+    MG_ERR_CUDA = 4,             /* CUDA runtime / launch failure (poisons)   */
+    MG_ERR_NCCL = 5,             /* NCCL failure (poisons the solver)         */
+    MG_ERR_NONFINITE = 6,        /* NaN/Inf residual norm             */
+    MG_ERR_LAYOUT = 7,           /* pointer misaligned for the layout         */
+    MG_ERR_POISONED = 8          /* an earlier CUDA/NCCL error poisoned it    */
+} mg_status;
+
+typedef enum { MG_JACOBI = 0, MG_RBGS = 1 } mg_smoother;
+typedef enum { MG_FP64 = 0, MG_FP32 = 1 } mg_dtype;           /* Table 1 */
+typedef enum { MG_COARSE_DIRECT = 0, MG_COARSE_SWEEPS = 1 } mg_coarse;
+
+/* flags */
+#define MG_FLAG_NO_GRAPH 1u   /* launch eagerly instead of replaying a CUDA graph   */
+#define MG_FLAG_BASELINE 2u   /* op-by-op kernels only (no fusion; two-pass RBGS)   */
+
+typedef struct {
+    int32_t dim;         /* 2 or 3                                        */
+    int64_t nodes[3];    /* global nodes per axis incl. boundary (x, y, z); z ignored in 2D.
+                            (nodes[d]-1) % 2^(levels-1) == 0                  */
+    int32_t levels;      /* >= 1; 0 => paper rule: coarsen until the coarsest level has
+                            1 interior node along the shortest axis    */
+    double coeff[3];     /* a_d of A = -sum_d a_d d^2/dx_d^2; Poisson = {1,1,1} */
+    double h[3];         /* fine spacing per axis; 0 => unit domain 1/(nodes-1) */
+    int32_t smoother;    /* mg_smoother (default RBGS, the listing's GaussSeidel P:236) */
+    double omega;        /* default 1.0 for RBGS, 0.8 for Jacobi       */
+    int32_t nu1, nu2;    /* pre/post sweeps (Alg. 1); default 2, 2 (V(2,2))     */
+    int32_t coarse;      /* mg_coarse, default DIRECT (reading 3)                      */
+    int32_t ncoarse;     /* sweeps on the coarsest level in SWEEPS mode, def 10 */
+    int32_t dtype;       /* mg_dtype                                                    */
+    int32_t device;      /* CUDA device ordinal                                         */
+    int32_t rank, nranks;/* slab decomposition along the slowest axis; nranks==1 today  */
+    const void* nccl_id; /* 128-byte ncclUniqueId when nranks > 1, else NULL            */
+    uint32_t flags;      /* MG_FLAG_*                                                   */
+} mg_config;
+
+/* Fill `cfg` with the defaults above for a `dim`-D grid of `nodes` per axis. */
+void mg_config_default(mg_config* cfg, int32_t dim, int64_t nodes);
+
+/* Validate `cfg`, build the level hierarchy (h_l = 2^l h, re-discretised
+ * coefficients c_d = a_d/h_{l,d}^2, D = 2 sum c_d), allocate the
+ * library-owned buffers and, for DIRECT coarse mode with >1 coarsest unknown,
+ * factor the coarsest matrix on the device.  On failure nothing is allocated
+ * and *out is NULL. */
+mg_status mg_create(const mg_config* cfg, mg_solver** out);
+
+/* Shape [planes][rows][pitch] (elements) of this rank's level-0 u and f; the
+ * slab of global planes it owns is [*first_plane, *first_plane + *owned). */
+mg_status mg_layout(const mg_solver* s, int64_t shape[3], int64_t* first_plane, int64_t* owned);
+/* Shape of the level-l arrays used by the per-operation entry points below. */
+mg_status mg_level_layout(const mg_solver* s, int32_t level, int64_t shape[3]);
+int32_t mg_num_levels(const mg_solver* s);
+
+/* One V(nu1,nu2)-cycle of Alg. 1, in place on u, asynchronous on
+ * `stream`.  Replays a cached CUDA graph for this (u, f) unless
+ * MG_FLAG_NO_GRAPH. */
+mg_status mg_vcycle(mg_solver* s, void* u, const void* f, void* stream);
+
+/* ||f - A u||_2 over interior nodes, unscaled (L2Residual),
+ * FP64 accumulation, deterministic reduction order.  Blocking. */
+mg_status mg_residual_norm(mg_solver* s, const void* u, const void* f, double* out, void* stream);
+
+/* Driver loop of the `Application` listing: r0 = norm; repeat
+ * { V-cycle; r_k = norm } until r_k <= rtol * r0 or max_cycles.  history (if
+ * not NULL) receives max_cycles+1 doubles, history[0] = r0.  Blocking.
+ * Returns MG_ERR_NONFINITE if a norm is NaN/Inf. */
+mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol, int32_t max_cycles,
+                   int32_t* cycles, double* history, void* stream);
+
+/* End-to-end variant with HOST buffers u_host, f_host (dense [planes][rows][pitch],
+ * preferably pinned): copies f and u to library-owned device buffers, runs
+ * `ncycles` V-cycles, computes the residual norm into *norm_out (may be NULL),
+ * copies u back.  Blocking. */
+mg_status mg_vcycle_host(mg_solver* s, void* u_host, const void* f_host, int32_t ncycles,
+                         double* norm_out, void* stream);
+
+/* ---- per-operation entry points (one step of Alg. 1 each, for parity tests).
+ * Arrays use mg_level_layout(level).  Asynchronous unless stated. */
+/* one sweep of the configured smoother S_h (listing P:299-305):
+ * u_out = S(u_in); u_out may equal u_in.  Boundary nodes of u_out := u_in's. */
+mg_status mg_op_smooth(mg_solver* s, int32_t level, const void* u_in, const void* f, void* u_out, void* stream);
+/* r = f - A u on interior, 0 on boundary (Alg. 1 line 4) */
+mg_status mg_op_residual(mg_solver* s, int32_t level, const void* u, const void* f, void* r, void* stream);
+/* f_{l+1} = R r_l, full weighting (listing P:307-312); coarse boundary := 0 */
+mg_status mg_op_restrict(mg_solver* s, int32_t level, const void* r, void* f_coarse, void* stream);
+/* u_l += P e_{l+1}, bi/trilinear (listing P:314-319) */
+mg_status mg_op_prolong_correct(mg_solver* s, int32_t level, const void* e_coarse, void* u, void* stream);
+/* e = A_{L-1}^{-1} f on the coarsest level (Alg. 1 line 2) */
+mg_status mg_op_coarse_solve(mg_solver* s, const void* f, void* e, void* stream);
+/* residual norm of level `level`; blocking */
+mg_status mg_op_norm(mg_solver* s, int32_t level, const void* u, const void* f, double* out, void* stream);
+
+/* ---- synthetic inputs (NOT method arithmetic): the counter-based SplitMix64
+ * generator of DESIGN.md reading 10 on the device.  dst (level-0 layout of
+ * this rank) gets lo + (hi-lo) * U[0,1) of the GLOBAL unpadded node index on
+ * interior nodes and 0 on boundary nodes. */
+mg_status mg_workload_fill(mg_solver* s, void* dst, uint64_t seed, double lo, double hi, void* stream);
+
+/* ---- instrumentation */
+/* number of kernel launches per mg_vcycle (counted at plan build) */
+int64_t mg_launches_per_cycle(const mg_solver* s);
+/* enable (1) / disable (0) per-kernel CUDA-event timing; while enabled
+ * mg_vcycle launches eagerly and records events around every launch. */
+mg_status mg_profile_enable(mg_solver* s, int32_t on);
+/* Per-kernel timing since enable: for entry i (< n), names[i] points to a static string
+ * "<kernel>@L<level>", ms[i] = summed device time, count[i] = launches,
+ * bytes[i] = ALGORITHMIC bytes per launch.  Returns the number of entries
+ * (may exceed cap; only min(n,cap) written).  Synchronises the device. */
+int32_t mg_profile_read(mg_solver* s, int32_t cap, const char** names, double* ms,
+                        int64_t* count, double* bytes);
+
+const char* mg_error_string(const mg_solver* s);
+void mg_destroy(mg_solver* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MG_H */

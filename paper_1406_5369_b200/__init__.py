@@ -1,0 +1,288 @@
+"""paper_1406_5369_b200 — B200-native geometric multigrid V-cycle (arXiv:1406.5369).
+
+Thin Python binding of the C ABI in include/mg.h (libmgb200.so, built in-tree
+by `make` / __graft_entry__.build()).  This module only marshals arguments:
+every step of the V-cycle runs in the library's sm_100a kernels.  There is no
+CPU fallback — if the shared library or a B200 is missing, calls fail loudly.
+
+PyTorch supplies device memory and streams: u/f are CUDA tensors of shape
+Solver.shape (= [planes][rows][pitch], see mg.h); `from_numpy`/`to_numpy`
+convert between the dense unpadded node arrays used by the tests and that
+layout.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmgb200.so")
+
+JACOBI, RBGS = 0, 1
+FP64, FP32 = 0, 1
+COARSE_DIRECT, COARSE_SWEEPS = 0, 1
+FLAG_NO_GRAPH, FLAG_BASELINE = 1, 2
+
+# every symbol include/mg.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = [
+    "mg_config_default", "mg_create", "mg_layout", "mg_level_layout", "mg_num_levels", "mg_vcycle",
+    "mg_residual_norm", "mg_solve", "mg_vcycle_host", "mg_op_smooth", "mg_op_residual", "mg_op_restrict",
+    "mg_op_prolong_correct", "mg_op_coarse_solve", "mg_op_norm", "mg_workload_fill",
+    "mg_launches_per_cycle", "mg_profile_enable", "mg_profile_read", "mg_error_string", "mg_destroy",
+]
+
+
+class MGConfig(ctypes.Structure):
+    _fields_ = [
+        ("dim", ctypes.c_int32),
+        ("nodes", ctypes.c_int64 * 3),
+        ("levels", ctypes.c_int32),
+        ("coeff", ctypes.c_double * 3),
+        ("h", ctypes.c_double * 3),
+        ("smoother", ctypes.c_int32),
+        ("omega", ctypes.c_double),
+        ("nu1", ctypes.c_int32),
+        ("nu2", ctypes.c_int32),
+        ("coarse", ctypes.c_int32),
+        ("ncoarse", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("nranks", ctypes.c_int32),
+        ("nccl_id", ctypes.c_void_p),
+        ("flags", ctypes.c_uint32),
+    ]
+
+
+class MGError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"mg status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library():
+    """Load libmgb200.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `make lib` or __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    pI64 = ctypes.POINTER(ctypes.c_int64)
+    pD = ctypes.POINTER(ctypes.c_double)
+    lib.mg_config_default.argtypes = [ctypes.POINTER(MGConfig), I32, I64]
+    lib.mg_config_default.restype = None
+    lib.mg_create.argtypes = [ctypes.POINTER(MGConfig), ctypes.POINTER(P)]
+    lib.mg_layout.argtypes = [P, pI64, pI64, pI64]
+    lib.mg_level_layout.argtypes = [P, I32, pI64]
+    lib.mg_num_levels.argtypes = [P]
+    lib.mg_num_levels.restype = I32
+    lib.mg_vcycle.argtypes = [P, P, P, P]
+    lib.mg_residual_norm.argtypes = [P, P, P, pD, P]
+    lib.mg_solve.argtypes = [P, P, P, D, I32, ctypes.POINTER(I32), pD, P]
+    lib.mg_vcycle_host.argtypes = [P, P, P, I32, pD, P]
+    lib.mg_op_smooth.argtypes = [P, I32, P, P, P, P]
+    lib.mg_op_residual.argtypes = [P, I32, P, P, P, P]
+    lib.mg_op_restrict.argtypes = [P, I32, P, P, P]
+    lib.mg_op_prolong_correct.argtypes = [P, I32, P, P, P]
+    lib.mg_op_coarse_solve.argtypes = [P, P, P, P]
+    lib.mg_op_norm.argtypes = [P, I32, P, P, pD, P]
+    lib.mg_workload_fill.argtypes = [P, P, ctypes.c_uint64, D, D, P]
+    lib.mg_launches_per_cycle.argtypes = [P]
+    lib.mg_launches_per_cycle.restype = I64
+    lib.mg_profile_enable.argtypes = [P, I32]
+    lib.mg_profile_read.argtypes = [P, I32, ctypes.POINTER(ctypes.c_char_p), pD, pI64, pD]
+    lib.mg_profile_read.restype = I32
+    lib.mg_error_string.argtypes = [P]
+    lib.mg_error_string.restype = ctypes.c_char_p
+    lib.mg_destroy.argtypes = [P]
+    lib.mg_destroy.restype = None
+    for name in ABI_SYMBOLS:
+        if name not in ("mg_config_default", "mg_num_levels", "mg_launches_per_cycle", "mg_profile_read",
+                        "mg_error_string", "mg_destroy"):
+            getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class Solver:
+    """Owns one mg_solver (include/mg.h).  Arguments mirror mg_config."""
+
+    def __init__(self, dim, nodes, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, coarse="direct",
+                 ncoarse=10, dtype="f64", device=0, coeff=(1.0, 1.0, 1.0), h=None, flags=0, rank=0, nranks=1,
+                 nccl_id=None):
+        lib = load_library()
+        self.lib = lib
+        if isinstance(nodes, int):
+            nodes = (nodes,) * dim
+        c = MGConfig()
+        lib.mg_config_default(ctypes.byref(c), dim, int(nodes[0]))
+        for d in range(3):
+            c.nodes[d] = int(nodes[d]) if d < dim else 1
+            c.coeff[d] = float(coeff[d])
+            c.h[d] = 0.0 if h is None or d >= dim else float(h[d])
+        c.levels = levels
+        c.smoother = RBGS if smoother in ("rbgs", RBGS) else JACOBI
+        c.omega = float(omega) if omega is not None else (1.0 if c.smoother == RBGS else 0.8)
+        c.nu1, c.nu2 = nu1, nu2
+        c.coarse = COARSE_DIRECT if coarse in ("direct", COARSE_DIRECT) else COARSE_SWEEPS
+        c.ncoarse = ncoarse
+        c.dtype = FP64 if dtype in ("f64", FP64) else FP32
+        c.device = device
+        c.rank, c.nranks = rank, nranks
+        self._nccl_id = nccl_id
+        c.nccl_id = ctypes.cast(ctypes.c_char_p(nccl_id), ctypes.c_void_p) if nccl_id is not None else None
+        c.flags = flags
+        self.cfg = c
+        self.dim = dim
+        self.nodes = tuple(int(n) for n in nodes[:dim])
+        h_ = ctypes.c_void_p()
+        st = lib.mg_create(ctypes.byref(c), ctypes.byref(h_))
+        if st != 0:
+            raise MGError(st, lib.mg_error_string(None).decode())
+        self.h = h_
+        self.levels = lib.mg_num_levels(self.h)
+        torch = _torch()
+        self.torch_dtype = torch.float64 if c.dtype == FP64 else torch.float32
+        self.np_dtype = np.float64 if c.dtype == FP64 else np.float32
+
+    # ---- lifetime
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.mg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st):
+        if st != 0:
+            raise MGError(st, self.lib.mg_error_string(self.h).decode())
+
+    @staticmethod
+    def _stream(stream):
+        if stream is None:
+            return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(getattr(stream, "cuda_stream", stream))
+
+    @staticmethod
+    def _p(t):
+        return ctypes.c_void_p(t.data_ptr())
+
+    # ---- layout
+    @property
+    def shape(self):
+        s = (ctypes.c_int64 * 3)()
+        first, owned = ctypes.c_int64(), ctypes.c_int64()
+        self._chk(self.lib.mg_layout(self.h, s, ctypes.byref(first), ctypes.byref(owned)))
+        return tuple(s)
+
+    def level_shape(self, level):
+        s = (ctypes.c_int64 * 3)()
+        self._chk(self.lib.mg_level_layout(self.h, level, s))
+        return tuple(s)
+
+    def level_cells(self, level):
+        return tuple((n - 1) >> level for n in self.nodes)
+
+    def empty(self, level=0):
+        torch = _torch()
+        return torch.zeros(self.level_shape(level), dtype=self.torch_dtype, device=f"cuda:{self.cfg.device}")
+
+    def from_numpy(self, a, level=0):
+        """Dense node array (2D: (ny+1,nx+1); 3D: (nz+1,ny+1,nx+1)) -> padded device tensor."""
+        torch = _torch()
+        P, R, X = self.level_shape(level)
+        host = np.zeros((P, R, X), dtype=self.np_dtype)
+        a = np.asarray(a, dtype=self.np_dtype)
+        if self.dim == 2:
+            host[:, 0, : a.shape[1]] = a
+        else:
+            host[:, :, : a.shape[2]] = a
+        return torch.from_numpy(host).to(f"cuda:{self.cfg.device}")
+
+    def to_numpy(self, t, level=0):
+        nx = self.level_cells(level)[0] + 1
+        a = t.detach().cpu().numpy()
+        return np.ascontiguousarray(a[:, 0, :nx] if self.dim == 2 else a[:, :, :nx])
+
+    # ---- the method
+    def vcycle(self, u, f, stream=None):
+        self._chk(self.lib.mg_vcycle(self.h, self._p(u), self._p(f), self._stream(stream)))
+
+    def residual_norm(self, u, f, stream=None):
+        out = ctypes.c_double()
+        self._chk(self.lib.mg_residual_norm(self.h, self._p(u), self._p(f), ctypes.byref(out), self._stream(stream)))
+        return out.value
+
+    def solve(self, u, f, rtol, max_cycles, stream=None):
+        hist = (ctypes.c_double * (max_cycles + 1))()
+        k = ctypes.c_int32()
+        self._chk(self.lib.mg_solve(self.h, self._p(u), self._p(f), float(rtol), int(max_cycles), ctypes.byref(k),
+                                    hist, self._stream(stream)))
+        return k.value, list(hist)[: k.value + 1]
+
+    def vcycle_host(self, u_host, f_host, ncycles=1, stream=None):
+        """End-to-end through the C ABI with host (pinned) tensors; returns the residual norm."""
+        out = ctypes.c_double()
+        self._chk(self.lib.mg_vcycle_host(self.h, ctypes.c_void_p(u_host.data_ptr()),
+                                          ctypes.c_void_p(f_host.data_ptr()), int(ncycles), ctypes.byref(out),
+                                          self._stream(stream)))
+        return out.value
+
+    # ---- per-operation entry points
+    def op_smooth(self, level, u_in, f, u_out, stream=None):
+        self._chk(self.lib.mg_op_smooth(self.h, level, self._p(u_in), self._p(f), self._p(u_out),
+                                        self._stream(stream)))
+
+    def op_residual(self, level, u, f, r, stream=None):
+        self._chk(self.lib.mg_op_residual(self.h, level, self._p(u), self._p(f), self._p(r), self._stream(stream)))
+
+    def op_restrict(self, level, r, fc, stream=None):
+        self._chk(self.lib.mg_op_restrict(self.h, level, self._p(r), self._p(fc), self._stream(stream)))
+
+    def op_prolong_correct(self, level, e, u, stream=None):
+        self._chk(self.lib.mg_op_prolong_correct(self.h, level, self._p(e), self._p(u), self._stream(stream)))
+
+    def op_coarse_solve(self, f, e, stream=None):
+        self._chk(self.lib.mg_op_coarse_solve(self.h, self._p(f), self._p(e), self._stream(stream)))
+
+    def op_norm(self, level, u, f, stream=None):
+        out = ctypes.c_double()
+        self._chk(self.lib.mg_op_norm(self.h, level, self._p(u), self._p(f), ctypes.byref(out), self._stream(stream)))
+        return out.value
+
+    def workload_fill(self, dst, seed, lo=0.0, hi=1.0, stream=None):
+        self._chk(self.lib.mg_workload_fill(self.h, self._p(dst), ctypes.c_uint64(seed), float(lo), float(hi),
+                                            self._stream(stream)))
+
+    # ---- instrumentation
+    @property
+    def launches_per_cycle(self):
+        return self.lib.mg_launches_per_cycle(self.h)
+
+    def profile_enable(self, on=True):
+        self._chk(self.lib.mg_profile_enable(self.h, 1 if on else 0))
+
+    def profile_read(self):
+        n = self.lib.mg_profile_read(self.h, 0, None, None, None, None)
+        names = (ctypes.c_char_p * max(n, 1))()
+        ms = (ctypes.c_double * max(n, 1))()
+        cnt = (ctypes.c_int64 * max(n, 1))()
+        by = (ctypes.c_double * max(n, 1))()
+        n = self.lib.mg_profile_read(self.h, n, names, ms, cnt, by)
+        return [dict(name=names[i].decode(), ms=ms[i], count=cnt[i], bytes=by[i]) for i in range(n)]

@@ -1,0 +1,323 @@
+// api.cu — the C ABI (include/mg.h): validation, level hierarchy, buffers,
+// the V-cycle schedule of Alg. 1, CUDA-graph capture/replay and
+// per-kernel event timing.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "mg.h"
+#include "plan.h"
+
+using namespace mg;
+
+static thread_local std::string g_last_error;
+
+static mg_status fail(mg_solver* s, mg_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  if (s) {
+    s->err = buf;
+    if (st == MG_ERR_CUDA || st == MG_ERR_NCCL) s->poisoned = true;
+  }
+  return st;
+}
+
+#define CK(call)                                                                                 \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess)                                                                       \
+      return fail(s, MG_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+extern "C" void mg_config_default(mg_config* c, int32_t dim, int64_t nodes) {
+  memset(c, 0, sizeof *c);
+  c->dim = dim;
+  for (int d = 0; d < 3; d++) {
+    c->nodes[d] = d < dim ? nodes : 1;
+    c->coeff[d] = 1.0;
+    c->h[d] = 0.0;
+  }
+  c->levels = 0;
+  c->smoother = MG_RBGS;
+  c->omega = 1.0;
+  c->nu1 = 2;
+  c->nu2 = 2;
+  c->coarse = MG_COARSE_DIRECT;
+  c->ncoarse = 10;
+  c->dtype = MG_FP64;
+  c->device = 0;
+  c->rank = 0;
+  c->nranks = 1;
+  c->nccl_id = nullptr;
+  c->flags = 0;
+}
+
+// ------------------------------------------------------------------ creation
+static mg_status validate(const mg_config* c, int* levels_out) {
+  mg_solver* s = nullptr;
+  if (!c) return fail(s, MG_ERR_INVALID, "config is NULL");
+  if (c->dim != 2 && c->dim != 3) return fail(s, MG_ERR_INVALID, "dim must be 2 or 3 (got %d)", c->dim);
+  if (c->smoother != MG_JACOBI && c->smoother != MG_RBGS) return fail(s, MG_ERR_INVALID, "bad smoother");
+  if (!(c->omega > 0.0 && c->omega < 2.0)) return fail(s, MG_ERR_INVALID, "omega must be in (0,2) (S:46)");
+  if (c->nu1 < 0 || c->nu2 < 0) return fail(s, MG_ERR_INVALID, "nu1, nu2 must be >= 0");
+  if (c->coarse != MG_COARSE_DIRECT && c->coarse != MG_COARSE_SWEEPS) return fail(s, MG_ERR_INVALID, "bad coarse");
+  if (c->coarse == MG_COARSE_SWEEPS && c->ncoarse < 0) return fail(s, MG_ERR_INVALID, "ncoarse < 0");
+  if (c->dtype != MG_FP64 && c->dtype != MG_FP32) return fail(s, MG_ERR_INVALID, "bad dtype");
+  if (c->nranks != 1) return fail(s, MG_ERR_INVALID, "nranks > 1 requires the NCCL build (not yet enabled)");
+  int64_t mincells = INT64_MAX;
+  for (int d = 0; d < c->dim; d++) {
+    int64_t n = c->nodes[d] - 1;
+    if (n < 2) return fail(s, MG_ERR_INVALID, "nodes[%d] must be >= 3", d);
+    if (n > (1ll << 30)) return fail(s, MG_ERR_INVALID, "nodes[%d] too large", d);
+    if (!(c->coeff[d] > 0.0)) return fail(s, MG_ERR_INVALID, "coeff[%d] must be > 0", d);
+    if (c->h[d] < 0.0) return fail(s, MG_ERR_INVALID, "h[%d] < 0", d);
+    if (n < mincells) mincells = n;
+  }
+  int L = c->levels;
+  if (L < 0) return fail(s, MG_ERR_INVALID, "levels < 0");
+  if (L == 0) {  // paper rule: coarsest level has one interior node along the shortest axis
+    // "direct coarsening down to less than three unknowns per direction"
+    L = 1;
+    while ((mincells >> L) >= 2 && ((mincells >> L) << L) == mincells) L++;
+    if ((mincells >> (L - 1)) > 3)
+      return fail(s, MG_ERR_NOT_COARSENABLE,
+                  "cannot coarsen %lld cells down to < 3 unknowns per direction (P:568); give levels explicitly",
+                  (long long)mincells);
+  }
+  for (int d = 0; d < c->dim; d++) {
+    int64_t n = c->nodes[d] - 1;
+    if (L - 1 >= 62 || (n % (1ll << (L - 1))) != 0)
+      return fail(s, MG_ERR_NOT_COARSENABLE, "nodes[%d]-1 = %lld not divisible by 2^(levels-1) = 2^%d (S:242)", d,
+                  (long long)n, L - 1);
+    if ((n >> (L - 1)) < 2)
+      return fail(s, MG_ERR_NOT_COARSENABLE, "coarsest level has no interior node along axis %d", d);
+  }
+  *levels_out = L;
+  return MG_OK;
+}
+
+static int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+extern "C" mg_status mg_create(const mg_config* cfg, mg_solver** out) {
+  if (!out) return fail(nullptr, MG_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  int L = 0;
+  mg_status st = validate(cfg, &L);
+  if (st != MG_OK) return st;
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0)
+    return fail(nullptr, MG_ERR_CUDA, "no CUDA device (%s); there is no CPU fallback", cudaGetErrorString(ce));
+  if (cfg->device < 0 || cfg->device >= ndev) return fail(nullptr, MG_ERR_INVALID, "bad device %d", cfg->device);
+
+  mg_solver* s = new mg_solver();
+  s->cfg = *cfg;
+  s->L = L;
+  s->esz = cfg->dtype == MG_FP64 ? 8 : 4;
+  st = plan_build(s);
+  if (st != MG_OK) {
+    plan_free(s);
+    delete s;
+    return st;
+  }
+  *out = s;
+  return MG_OK;
+}
+
+extern "C" void mg_destroy(mg_solver* s) {
+  if (!s) return;
+  plan_free(s);
+  delete s;
+}
+
+extern "C" const char* mg_error_string(const mg_solver* s) {
+  if (s && !s->err.empty()) return s->err.c_str();
+  return g_last_error.c_str();
+}
+
+extern "C" int32_t mg_num_levels(const mg_solver* s) { return s ? s->L : 0; }
+
+extern "C" mg_status mg_layout(const mg_solver* s, int64_t shape[3], int64_t* first, int64_t* owned) {
+  if (!s || !shape) return fail(nullptr, MG_ERR_INVALID, "NULL argument");
+  const Level& lv = s->lv[0];
+  for (int d = 0; d < 3; d++) shape[d] = lv.shape[d];
+  if (first) *first = 0;
+  if (owned) *owned = lv.shape[0];
+  return MG_OK;
+}
+
+extern "C" mg_status mg_level_layout(const mg_solver* s, int32_t level, int64_t shape[3]) {
+  if (!s || !shape) return fail(nullptr, MG_ERR_INVALID, "NULL argument");
+  if (level < 0 || level >= s->L) return fail(nullptr, MG_ERR_INVALID, "level %d out of range", level);
+  for (int d = 0; d < 3; d++) shape[d] = s->lv[level].shape[d];
+  return MG_OK;
+}
+
+extern "C" int64_t mg_launches_per_cycle(const mg_solver* s) { return s ? s->launches_per_cycle : -1; }
+
+// ------------------------------------------------------------------ execution
+static mg_status guard(mg_solver* s) {
+  if (!s) return fail(nullptr, MG_ERR_INVALID, "solver is NULL");
+  if (s->poisoned) return fail(s, MG_ERR_POISONED, "solver poisoned by an earlier error: %s", s->err.c_str());
+  cudaError_t e = cudaSetDevice(s->cfg.device);
+  if (e != cudaSuccess) return fail(s, MG_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  return MG_OK;
+}
+
+static bool aligned(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+extern "C" mg_status mg_vcycle(mg_solver* s, void* u, const void* f, void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  if (!u || !f) return fail(s, MG_ERR_INVALID, "u or f is NULL");
+  if (u == f) return fail(s, MG_ERR_INVALID, "u and f must not alias");
+  if (!aligned(u) || !aligned(f)) return fail(s, MG_ERR_LAYOUT, "u and f must be 16-byte aligned");
+  cudaStream_t cs = (cudaStream_t)stream;
+  bool eager = (s->cfg.flags & MG_FLAG_NO_GRAPH) || s->prof_on;
+  if (eager) return plan_run_vcycle(s, u, f, cs);
+  return plan_graph_vcycle(s, u, f, cs);
+}
+
+extern "C" mg_status mg_residual_norm(mg_solver* s, const void* u, const void* f, double* out, void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  if (!u || !f || !out) return fail(s, MG_ERR_INVALID, "NULL argument");
+  return plan_norm(s, 0, u, f, out, (cudaStream_t)stream, true);
+}
+
+extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol, int32_t max_cycles, int32_t* cycles,
+                              double* history, void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  if (!u || !f || max_cycles < 0 || !(rtol >= 0.0)) return fail(s, MG_ERR_INVALID, "bad argument");
+  double r0 = 0.0;
+  st = mg_residual_norm(s, u, f, &r0, stream);
+  if (st != MG_OK) return st;
+  if (history) history[0] = r0;
+  if (!std::isfinite(r0)) return fail(s, MG_ERR_NONFINITE, "initial residual norm is not finite");
+  int k = 0;
+  while (k < max_cycles) {
+    st = mg_vcycle(s, u, f, stream);
+    if (st != MG_OK) return st;
+    k++;
+    double rk = 0.0;
+    st = mg_residual_norm(s, u, f, &rk, stream);
+    if (st != MG_OK) return st;
+    if (history) history[k] = rk;
+    if (!std::isfinite(rk)) {
+      if (cycles) *cycles = k;
+      return fail(s, MG_ERR_NONFINITE, "residual norm not finite after cycle %d (S:535)", k);
+    }
+    if (rk <= rtol * r0) break;
+  }
+  if (cycles) *cycles = k;
+  return MG_OK;
+}
+
+extern "C" mg_status mg_vcycle_host(mg_solver* s, void* u_host, const void* f_host, int32_t ncycles,
+                                    double* norm_out, void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  if (!u_host || !f_host || ncycles < 0) return fail(s, MG_ERR_INVALID, "bad argument");
+  cudaStream_t cs = (cudaStream_t)stream;
+  const Level& lv = s->lv[0];
+  size_t bytes = lv.elems * s->esz;
+  if (!s->stage_u) {
+    if (cudaMalloc(&s->stage_u, bytes) != cudaSuccess || cudaMalloc(&s->stage_f, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(s, MG_ERR_OOM, "staging allocation failed");
+    }
+  }
+  CK(cudaMemcpyAsync(s->stage_f, f_host, bytes, cudaMemcpyHostToDevice, cs));
+  CK(cudaMemcpyAsync(s->stage_u, u_host, bytes, cudaMemcpyHostToDevice, cs));
+  for (int c = 0; c < ncycles; c++) {
+    st = mg_vcycle(s, s->stage_u, s->stage_f, stream);
+    if (st != MG_OK) return st;
+  }
+  if (norm_out) {
+    st = plan_norm(s, 0, s->stage_u, s->stage_f, norm_out, cs, false);
+    if (st != MG_OK) return st;
+  }
+  CK(cudaMemcpyAsync(u_host, s->stage_u, bytes, cudaMemcpyDeviceToHost, cs));
+  CK(cudaStreamSynchronize(cs));
+  if (norm_out) *norm_out = *s->h_norm;
+  return MG_OK;
+}
+
+// ------------------------------------------------------------------ per-op entry points
+#define LEVEL_CHECK(l)                                                                        \
+  do {                                                                                        \
+    if ((l) < 0 || (l) >= s->L) return fail(s, MG_ERR_INVALID, "level %d out of range", (l)); \
+  } while (0)
+
+extern "C" mg_status mg_op_smooth(mg_solver* s, int32_t level, const void* u_in, const void* f, void* u_out,
+                                  void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  LEVEL_CHECK(level);
+  return plan_op_smooth(s, level, u_in, f, u_out, (cudaStream_t)stream);
+}
+extern "C" mg_status mg_op_residual(mg_solver* s, int32_t level, const void* u, const void* f, void* r,
+                                    void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  LEVEL_CHECK(level);
+  return plan_op_residual(s, level, u, f, r, (cudaStream_t)stream);
+}
+extern "C" mg_status mg_op_restrict(mg_solver* s, int32_t level, const void* r, void* fc, void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  LEVEL_CHECK(level + 1);
+  return plan_op_restrict(s, level, r, fc, (cudaStream_t)stream);
+}
+extern "C" mg_status mg_op_prolong_correct(mg_solver* s, int32_t level, const void* e, void* u, void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  LEVEL_CHECK(level + 1);
+  return plan_op_prolong(s, level, e, u, (cudaStream_t)stream);
+}
+extern "C" mg_status mg_op_coarse_solve(mg_solver* s, const void* f, void* e, void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  return plan_op_coarse(s, f, e, (cudaStream_t)stream);
+}
+extern "C" mg_status mg_op_norm(mg_solver* s, int32_t level, const void* u, const void* f, double* out,
+                                void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  LEVEL_CHECK(level);
+  return plan_norm(s, level, u, f, out, (cudaStream_t)stream, true);
+}
+
+extern "C" mg_status mg_workload_fill(mg_solver* s, void* dst, uint64_t seed, double lo, double hi, void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  if (!dst) return fail(s, MG_ERR_INVALID, "dst is NULL");
+  return plan_workload_fill(s, dst, seed, lo, hi, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ profiling
+extern "C" mg_status mg_profile_enable(mg_solver* s, int32_t on) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  return plan_profile_enable(s, on != 0);
+}
+
+extern "C" int32_t mg_profile_read(mg_solver* s, int32_t cap, const char** names, double* ms, int64_t* count,
+                                   double* bytes) {
+  if (!s) return -1;
+  return plan_profile_read(s, cap, names, ms, count, bytes);
+}
+
+// used by plan.cu for error reporting
+mg_status mg::plan_fail(mg_solver* s, mg_status st, const char* msg) { return fail(s, st, "%s", msg); }

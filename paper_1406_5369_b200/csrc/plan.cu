@@ -1,0 +1,577 @@
+// plan.cu — level hierarchy, buffers and the V-cycle schedule (Alg. 1,
+// P:187-219; Layer-4 VCycle listing P:278-297), executed eagerly or captured
+// once per (u, f) pair into a CUDA graph and replayed.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "kernels.h"
+#include "plan.h"
+
+namespace mg {
+
+enum Kind {
+  K_JACOBI = 0,
+  K_RBGS_COLOUR,
+  K_RESIDUAL,
+  K_RESTRICT,
+  K_PROLONG,
+  K_COPY_BOUNDARY,
+  K_COPY_INTERIOR,
+  K_NORM_PARTIAL,
+  K_NORM_FINAL,
+  K_COARSE_DIRECT,
+  K_MEMSET,
+  K_ADD,
+  K_NUM
+};
+static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
+                                       "prolong_correct", "copy_boundary", "copy_interior", "norm_partial",
+                                       "norm_final",    "coarse_direct", "memset",       "add_interior"};
+
+static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
+  char buf[384];
+  snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+  return plan_fail(s, MG_ERR_CUDA, buf);
+}
+
+// One kernel launch through the instrumentation wrapper.
+template <class Fn>
+static mg_status launch(mg_solver* s, cudaStream_t st, Kind kind, int level, double bytes, Fn&& fn) {
+  ProfRec rec{};
+  if (s->prof_on) {
+    rec.kind = kind;
+    rec.level = level;
+    rec.bytes = bytes;
+    cudaEventCreate(&rec.a);
+    cudaEventCreate(&rec.b);
+    cudaEventRecord(rec.a, st);
+  }
+  cudaError_t e = fn();
+  if (s->prof_on) {
+    cudaEventRecord(rec.b, st);
+    s->prof.push_back(rec);
+  }
+  if (kind != K_MEMSET) s->launch_counter++;  // kernels only
+  if (e != cudaSuccess) return cuda_fail(s, e, kKindName[kind]);
+  return MG_OK;
+}
+
+static double nodes_of(const Level& L) { return (double)(L.g.nx + 1) * L.shape[1] * L.shape[0]; }
+
+// ---------------------------------------------------------------- small kernels
+template <typename T>
+__global__ void k_copy_interior(Geom g, const T* __restrict__ src, T* __restrict__ dst) {
+  long long q = (long long)blockIdx.x * blockDim.y + threadIdx.y;
+  int nrow = g.three_d ? g.ny - 1 : 1;
+  if (q >= (long long)nrow * (g.p_hi - g.p_lo)) return;
+  int j = g.three_d ? (int)(q % nrow) + 1 : 0;
+  int pl = g.p_lo + (int)(q / nrow);
+  long long base = (long long)pl * g.pstride + (long long)j * g.pitch;
+  for (int i = 1 + threadIdx.x; i < g.nx; i += blockDim.x)
+    dst[base + i] = src[base + i];
+}
+
+template <typename T>
+__global__ void k_add_interior(Geom g, const T* __restrict__ e, T* __restrict__ u) {
+  long long q = (long long)blockIdx.x * blockDim.y + threadIdx.y;
+  int nrow = g.three_d ? g.ny - 1 : 1;
+  if (q >= (long long)nrow * (g.p_hi - g.p_lo)) return;
+  int j = g.three_d ? (int)(q % nrow) + 1 : 0;
+  int pl = g.p_lo + (int)(q / nrow);
+  long long base = (long long)pl * g.pstride + (long long)j * g.pitch;
+  for (int i = 1 + threadIdx.x; i < g.nx; i += blockDim.x)
+    u[base + i] = add(u[base + i], e[base + i]);
+}
+
+static dim3 rows_grid(const Geom& g) {
+  int nrow = g.three_d ? g.ny - 1 : 1;
+  long long q = (long long)nrow * (g.p_hi - g.p_lo);
+  return dim3((unsigned)((q + 1) / 2));
+}
+
+// ---------------------------------------------------------------- build / free
+mg_status plan_build(mg_solver* s) {
+  const mg_config& c = s->cfg;
+  cudaError_t e = cudaSetDevice(c.device);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaSetDevice");
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c.device);
+  if (major != 10) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "device %d has compute capability %d.x; libmgb200 is built for sm_100a only", c.device,
+             major);
+    return plan_fail(s, MG_ERR_CUDA, buf);
+  }
+  const int esz = (int)s->esz;
+  const int64_t align = 128 / esz;
+  s->lv.resize(s->L);
+  for (int l = 0; l < s->L; l++) {
+    Level& L = s->lv[l];
+    int64_t n[3];
+    double hh[3];
+    for (int d = 0; d < 3; d++) {
+      n[d] = d < c.dim ? (c.nodes[d] - 1) >> l : 0;
+      double h0 = c.h[d] > 0.0 ? c.h[d] : (d < c.dim ? 1.0 / (double)(c.nodes[d] - 1) : 0.0);
+      hh[d] = std::ldexp(h0, l);
+    }
+    // coefficients in double in the paper's axis order x, y, z (reading 13)
+    double cd[3] = {0, 0, 0}, sum = 0.0;
+    for (int d = 0; d < c.dim; d++) {
+      cd[d] = c.coeff[d] / (hh[d] * hh[d]);
+      sum += cd[d];
+    }
+    double D = 2.0 * sum, wd = c.omega / D;
+    Geom& g = L.g;
+    g.three_d = c.dim == 3;
+    g.nx = (int)n[0];
+    if (c.dim == 3) {
+      g.ny = (int)n[1];
+      g.nz = (int)n[2];
+      g.rows = g.ny + 1;
+      L.cx = cd[0];
+      L.cy = cd[1];
+      L.cz = cd[2];
+    } else {
+      g.ny = 0;
+      g.nz = (int)n[1];  // the paper's y is the plane axis
+      g.rows = 1;
+      L.cx = cd[0];
+      L.cy = 0.0;
+      L.cz = cd[1];
+    }
+    L.D = D;
+    g.pitch = (g.nx + 1 + align - 1) / align * align;
+    g.pstride = g.pitch * g.rows;
+    g.p_lo = 1;
+    g.p_hi = g.nz;
+    g.p_glob0 = 0;
+    L.shape[0] = g.nz + 1;
+    L.shape[1] = g.rows;
+    L.shape[2] = g.pitch;
+    L.elems = (size_t)L.shape[0] * L.shape[1] * L.shape[2];
+    L.c64 = Coef<double>{L.cx, L.cy, L.cz, D, wd};
+    L.c32 = Coef<float>{(float)L.cx, (float)L.cy, (float)L.cz, (float)D, (float)wd};
+    size_t bytes = L.elems * esz;
+    void** bufs[4] = {&L.u, &L.f, &L.r, &L.t};
+    for (int b = 0; b < 4; b++) {
+      if (l == 0 && b < 2) continue;  // level 0 u, f are the caller's
+      if (cudaMalloc(bufs[b], bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return plan_fail(s, MG_ERR_OOM, "device allocation of level buffers failed");
+      }
+      e = cudaMemset(*bufs[b], 0, bytes);
+      if (e != cudaSuccess) return cuda_fail(s, e, "cudaMemset");
+    }
+  }
+  // norm partials sized for the largest level
+  int np = 1;
+  for (int l = 0; l < s->L; l++) {
+    int a = s->esz == 8 ? norm_num_partials<double>(s->lv[l].g) : norm_num_partials<float>(s->lv[l].g);
+    if (a > np) np = a;
+  }
+  s->n_partial_cap = np;
+  if (cudaMalloc(&s->d_partial, sizeof(double) * np) != cudaSuccess ||
+      cudaMalloc(&s->d_norm, sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&s->h_norm, sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return plan_fail(s, MG_ERR_OOM, "allocation of norm buffers failed");
+  }
+  // coarsest-level direct solve: factor once (reading 3)
+  Level& C = s->lv[s->L - 1];
+  int m = (C.g.nx - 1) * (C.g.three_d ? C.g.ny - 1 : 1) * (C.g.nz - 1);
+  s->m_coarse = m;
+  if (c.coarse == MG_COARSE_DIRECT && m > 1) {
+    if (m > 1024) {
+      char buf[200];
+      snprintf(buf, sizeof buf,
+               "DIRECT coarse solve with %d unknowns exceeds the 1024 limit: use more levels or MG_COARSE_SWEEPS", m);
+      return plan_fail(s, MG_ERR_INVALID, buf);
+    }
+    int* d_status = nullptr;
+    if (cudaMalloc(&s->d_chol, sizeof(double) * (size_t)m * m) != cudaSuccess ||
+        cudaMalloc(&s->d_work, sizeof(double) * m) != cudaSuccess || cudaMalloc(&d_status, sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      return plan_fail(s, MG_ERR_OOM, "allocation of the coarse factor failed");
+    }
+    e = launch_cholesky_factor(C.g, C.cx, C.cy, C.cz, C.D, s->d_chol, m, d_status, 0);
+    int hs = 1;
+    if (e == cudaSuccess) e = cudaMemcpy(&hs, d_status, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(d_status);
+    if (e != cudaSuccess) return cuda_fail(s, e, "coarse Cholesky factorisation");
+    if (hs != 0) return plan_fail(s, MG_ERR_INVALID, "coarsest matrix is not positive definite");
+  }
+  e = cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamCreate");
+  // count launches of one cycle with a dry capture
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(s, e, "setup");
+  return MG_OK;
+}
+
+void plan_free(mg_solver* s) {
+  cudaSetDevice(s->cfg.device);
+  for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
+  s->graphs.clear();
+  for (auto& L : s->lv) {
+    cudaFree(L.u);
+    cudaFree(L.f);
+    cudaFree(L.r);
+    cudaFree(L.t);
+  }
+  s->lv.clear();
+  cudaFree(s->d_chol);
+  cudaFree(s->d_work);
+  cudaFree(s->d_partial);
+  cudaFree(s->d_norm);
+  if (s->h_norm) cudaFreeHost(s->h_norm);
+  cudaFree(s->stage_u);
+  cudaFree(s->stage_f);
+  for (auto& r : s->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+}
+
+// ---------------------------------------------------------------- typed schedule
+template <typename T>
+struct Exec {
+  mg_solver* s;
+  cudaStream_t st;
+  const Coef<T>& coef(int l) const;
+  double w(int l) const { return nodes_of(s->lv[l]) * sizeof(T); }  // one word per node of level l
+
+  mg_status smooth(int l, T*& cur, T*& other, const T* f) {
+    const Level& L = s->lv[l];
+    if (s->cfg.smoother == MG_JACOBI) {
+      mg_status r = launch(s, st, K_JACOBI, l, 3 * w(l),
+                           [&] { return launch_jacobi<T>(L.g, coef(l), cur, f, other, st); });
+      std::swap(cur, other);
+      return r;
+    }
+    for (int colour = 0; colour < 2; colour++) {
+      mg_status r = launch(s, st, K_RBGS_COLOUR, l, 3 * w(l),
+                           [&] { return launch_rbgs_colour<T>(L.g, coef(l), cur, f, colour, st); });
+      if (r != MG_OK) return r;
+    }
+    return MG_OK;
+  }
+
+  mg_status memset0(int l, T* p) {
+    return launch(s, st, K_MEMSET, l, w(l),
+                  [&] { return cudaMemsetAsync(p, 0, s->lv[l].elems * sizeof(T), st); });
+  }
+
+  mg_status coarse(T* e, const T* f, T*& cur, T*& other) {
+    int l = s->L - 1;
+    const Level& L = s->lv[l];
+    if (s->cfg.coarse == MG_COARSE_SWEEPS) {
+      for (int k = 0; k < s->cfg.ncoarse; k++) {
+        mg_status r = smooth(l, cur, other, f);
+        if (r != MG_OK) return r;
+      }
+      return MG_OK;
+    }
+    return launch(s, st, K_COARSE_DIRECT, l, 2 * w(l), [&] {
+      return launch_coarse_direct<T>(L.g, L.D, s->d_chol, s->m_coarse, f, e, s->d_work, st);
+    });
+  }
+
+  mg_status vcycle(T* u0, const T* f0) {
+    const int Lv = s->L;
+    const bool jac = s->cfg.smoother == MG_JACOBI;
+    std::vector<T*> cur(Lv), oth(Lv);
+    mg_status r;
+    // Jacobi ping-pongs between u and t: t's boundary must hold u's Dirichlet data
+    if (jac && (s->cfg.nu1 + s->cfg.nu2 > 0 || Lv == 1)) {
+      r = launch(s, st, K_COPY_BOUNDARY, 0, 0,
+                 [&] { return launch_copy_boundary<T>(s->lv[0].g, u0, (T*)s->lv[0].t, st); });
+      if (r != MG_OK) return r;
+    }
+    for (int l = 0; l < Lv; l++) {
+      cur[l] = l == 0 ? u0 : (T*)s->lv[l].u;
+      oth[l] = (T*)s->lv[l].t;
+    }
+    if (Lv == 1) {
+      // single-level hierarchy: solve in correction form (honours Dirichlet data)
+      if (s->cfg.coarse == MG_COARSE_SWEEPS) {
+        r = coarse(nullptr, f0, cur[0], oth[0]);
+        if (r != MG_OK) return r;
+      } else {
+        const Level& L = s->lv[0];
+        T* res = (T*)L.r;
+        T* e = (T*)L.t;
+        if ((r = launch(s, st, K_RESIDUAL, 0, 3 * w(0),
+                        [&] { return launch_residual<T>(L.g, coef(0), u0, f0, res, st); })) != MG_OK)
+          return r;
+        if ((r = coarse(e, res, cur[0], oth[0])) != MG_OK) return r;
+        if ((r = launch(s, st, K_ADD, 0, 3 * w(0), [&] {
+               k_add_interior<T><<<rows_grid(L.g), dim3(128, 2), 0, st>>>(L.g, e, u0);
+               return cudaGetLastError();
+             })) != MG_OK)
+          return r;
+      }
+    } else {
+      // ---- descend: pre-smooth, residual, restrict (Alg. 1 lines 3-5)
+      for (int l = 0; l < Lv - 1; l++) {
+        const Level& L = s->lv[l];
+        const T* f = l == 0 ? f0 : (const T*)L.f;
+        if (l > 0 && (r = memset0(l, cur[l])) != MG_OK) return r;  // V_H(0, ...)
+        for (int k = 0; k < s->cfg.nu1; k++)
+          if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+        T* res = (T*)L.r;
+        T* fc = (T*)s->lv[l + 1].f;
+        if ((r = launch(s, st, K_RESIDUAL, l, 3 * w(l),
+                        [&] { return launch_residual<T>(L.g, coef(l), cur[l], f, res, st); })) != MG_OK)
+          return r;
+        if ((r = launch(s, st, K_RESTRICT, l, w(l) + w(l + 1),
+                        [&] { return launch_restrict<T>(L.g, s->lv[l + 1].g, res, fc, st); })) != MG_OK)
+          return r;
+      }
+      // ---- coarsest level (Alg. 1 line 2)
+      {
+        int l = Lv - 1;
+        if (s->cfg.coarse == MG_COARSE_SWEEPS && (r = memset0(l, cur[l])) != MG_OK) return r;
+        if ((r = coarse(cur[l], (const T*)s->lv[l].f, cur[l], oth[l])) != MG_OK) return r;
+      }
+      // ---- ascend: prolongate + correct, post-smooth (Alg. 1 lines 6-7)
+      for (int l = Lv - 2; l >= 0; l--) {
+        const Level& L = s->lv[l];
+        const T* f = l == 0 ? f0 : (const T*)L.f;
+        const T* e = cur[l + 1];
+        if ((r = launch(s, st, K_PROLONG, l, 2 * w(l) + w(l + 1), [&] {
+               return launch_prolong_correct<T>(L.g, s->lv[l + 1].g, e, cur[l], st);
+             })) != MG_OK)
+          return r;
+        for (int k = 0; k < s->cfg.nu2; k++)
+          if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+      }
+    }
+    if (cur[0] != u0) {
+      const Level& L = s->lv[0];
+      T* src = cur[0];
+      if ((r = launch(s, st, K_COPY_INTERIOR, 0, 2 * w(0), [&] {
+             k_copy_interior<T><<<rows_grid(L.g), dim3(128, 2), 0, st>>>(L.g, src, u0);
+             return cudaGetLastError();
+           })) != MG_OK)
+        return r;
+    }
+    return MG_OK;
+  }
+
+  mg_status norm(int l, const T* u, const T* f, double* out_dev) {
+    const Level& L = s->lv[l];
+    int np = norm_num_partials<T>(L.g);
+    mg_status r = launch(s, st, K_NORM_PARTIAL, l, 2 * w(l),
+                         [&] { return launch_norm_partial<T>(L.g, coef(l), u, f, s->d_partial, st); });
+    if (r != MG_OK) return r;
+    return launch(s, st, K_NORM_FINAL, l, 8.0 * np,
+                  [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });
+  }
+};
+
+template <>
+const Coef<double>& Exec<double>::coef(int l) const {
+  return s->lv[l].c64;
+}
+template <>
+const Coef<float>& Exec<float>::coef(int l) const {
+  return s->lv[l].c32;
+}
+
+// ---------------------------------------------------------------- entry points
+mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st) {
+  s->launch_counter = 0;
+  mg_status r;
+  if (s->esz == 8)
+    r = Exec<double>{s, st}.vcycle((double*)u, (const double*)f);
+  else
+    r = Exec<float>{s, st}.vcycle((float*)u, (const float*)f);
+  s->launches_per_cycle = s->launch_counter;
+  return r;
+}
+
+mg_status plan_graph_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st) {
+  auto key = std::make_pair(u, f);
+  auto it = s->graphs.find(key);
+  if (it == s->graphs.end()) {
+    cudaGraph_t graph;
+    cudaError_t e = cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamBeginCapture");
+    mg_status r = plan_run_vcycle(s, u, f, s->cap_stream);
+    e = cudaStreamEndCapture(s->cap_stream, &graph);
+    if (r != MG_OK) return r;
+    if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamEndCapture");
+    cudaGraphExec_t exec;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(s, e, "cudaGraphInstantiate");
+    if (s->graphs.size() >= 16) {  // bound the cache
+      cudaGraphExecDestroy(s->graphs.begin()->second);
+      s->graphs.erase(s->graphs.begin());
+    }
+    it = s->graphs.emplace(key, exec).first;
+  }
+  cudaError_t e = cudaGraphLaunch(it->second, st);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaGraphLaunch");
+  return MG_OK;
+}
+
+mg_status plan_norm(mg_solver* s, int level, const void* u, const void* f, double* out, cudaStream_t st, bool sync) {
+  mg_status r = s->esz == 8 ? Exec<double>{s, st}.norm(level, (const double*)u, (const double*)f, s->d_norm)
+                            : Exec<float>{s, st}.norm(level, (const float*)u, (const float*)f, s->d_norm);
+  if (r != MG_OK) return r;
+  cudaError_t e = cudaMemcpyAsync(s->h_norm, s->d_norm, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(s, e, "norm readback");
+  if (sync) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(s, e, "norm synchronise");
+    *out = *s->h_norm;
+  }
+  return MG_OK;
+}
+
+template <typename T>
+static mg_status op_smooth_T(mg_solver* s, int l, const T* uin, const T* f, T* uout, cudaStream_t st) {
+  Exec<T> x{s, st};
+  const Level& L = s->lv[l];
+  if (s->cfg.smoother == MG_JACOBI) {
+    if (uin == uout) {  // in place: sweep into t, copy back
+      T* tmp = (T*)L.t;
+      mg_status r = launch(s, st, K_COPY_BOUNDARY, l, 0, [&] { return launch_copy_boundary<T>(L.g, uin, tmp, st); });
+      if (r != MG_OK) return r;
+      T* cur = (T*)uin;
+      T* oth = tmp;
+      if ((r = x.smooth(l, cur, oth, f)) != MG_OK) return r;
+      return launch(s, st, K_COPY_INTERIOR, l, 0, [&] {
+        k_copy_interior<T><<<rows_grid(L.g), dim3(128, 2), 0, st>>>(L.g, tmp, uout);
+        return cudaGetLastError();
+      });
+    }
+    mg_status r = launch(s, st, K_COPY_BOUNDARY, l, 0, [&] { return launch_copy_boundary<T>(L.g, uin, uout, st); });
+    if (r != MG_OK) return r;
+    T* cur = (T*)uin;
+    T* oth = uout;
+    return x.smooth(l, cur, oth, f);
+  }
+  if (uin != uout) {
+    cudaError_t e = cudaMemcpyAsync(uout, uin, L.elems * sizeof(T), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(s, e, "copy");
+  }
+  T* cur = uout;
+  T* oth = (T*)L.t;
+  return x.smooth(l, cur, oth, f);
+}
+
+mg_status plan_op_smooth(mg_solver* s, int l, const void* uin, const void* f, void* uout, cudaStream_t st) {
+  if (s->esz == 8) return op_smooth_T<double>(s, l, (const double*)uin, (const double*)f, (double*)uout, st);
+  return op_smooth_T<float>(s, l, (const float*)uin, (const float*)f, (float*)uout, st);
+}
+
+mg_status plan_op_residual(mg_solver* s, int l, const void* u, const void* f, void* r, cudaStream_t st) {
+  const Level& L = s->lv[l];
+  return launch(s, st, K_RESIDUAL, l, 0, [&] {
+    return s->esz == 8 ? launch_residual<double>(L.g, L.c64, (const double*)u, (const double*)f, (double*)r, st)
+                       : launch_residual<float>(L.g, L.c32, (const float*)u, (const float*)f, (float*)r, st);
+  });
+}
+
+mg_status plan_op_restrict(mg_solver* s, int l, const void* r, void* fc, cudaStream_t st) {
+  const Level& F = s->lv[l];
+  const Level& C = s->lv[l + 1];
+  cudaError_t e = cudaMemsetAsync(fc, 0, C.elems * s->esz, st);
+  if (e != cudaSuccess) return cuda_fail(s, e, "memset");
+  return launch(s, st, K_RESTRICT, l, 0, [&] {
+    return s->esz == 8 ? launch_restrict<double>(F.g, C.g, (const double*)r, (double*)fc, st)
+                       : launch_restrict<float>(F.g, C.g, (const float*)r, (float*)fc, st);
+  });
+}
+
+mg_status plan_op_prolong(mg_solver* s, int l, const void* e, void* u, cudaStream_t st) {
+  const Level& F = s->lv[l];
+  const Level& C = s->lv[l + 1];
+  return launch(s, st, K_PROLONG, l, 0, [&] {
+    return s->esz == 8 ? launch_prolong_correct<double>(F.g, C.g, (const double*)e, (double*)u, st)
+                       : launch_prolong_correct<float>(F.g, C.g, (const float*)e, (float*)u, st);
+  });
+}
+
+template <typename T>
+static mg_status op_coarse_T(mg_solver* s, const T* f, T* e, cudaStream_t st) {
+  Exec<T> x{s, st};
+  int l = s->L - 1;
+  cudaError_t ce = cudaMemsetAsync(e, 0, s->lv[l].elems * sizeof(T), st);
+  if (ce != cudaSuccess) return cuda_fail(s, ce, "memset");
+  T* cur = e;
+  T* oth = (T*)s->lv[l].t;
+  mg_status r = x.coarse(e, f, cur, oth);
+  if (r != MG_OK) return r;
+  if (cur != e) {
+    ce = cudaMemcpyAsync(e, cur, s->lv[l].elems * sizeof(T), cudaMemcpyDeviceToDevice, st);
+    if (ce != cudaSuccess) return cuda_fail(s, ce, "copy");
+  }
+  return MG_OK;
+}
+
+mg_status plan_op_coarse(mg_solver* s, const void* f, void* e, cudaStream_t st) {
+  if (s->esz == 8) return op_coarse_T<double>(s, (const double*)f, (double*)e, st);
+  return op_coarse_T<float>(s, (const float*)f, (float*)e, st);
+}
+
+mg_status plan_workload_fill(mg_solver* s, void* dst, uint64_t seed, double lo, double hi, cudaStream_t st) {
+  const Level& L = s->lv[0];
+  cudaError_t e = s->esz == 8 ? launch_workload_fill<double>(L.g, seed, lo, hi, (double*)dst, st)
+                              : launch_workload_fill<float>(L.g, seed, lo, hi, (float*)dst, st);
+  if (e != cudaSuccess) return cuda_fail(s, e, "workload_fill");
+  return MG_OK;
+}
+
+// ---------------------------------------------------------------- profiling
+static void prof_drain(mg_solver* s) {
+  if (s->prof.empty()) return;
+  cudaDeviceSynchronize();
+  for (auto& r : s->prof) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    char name[64];
+    snprintf(name, sizeof name, "%s@L%d", kKindName[r.kind], r.level);
+    ProfSum* sum = nullptr;
+    for (auto& p : s->prof_done)
+      if (p.name == name) sum = &p;
+    if (!sum) {
+      s->prof_done.push_back(ProfSum{name, 0, r.bytes, 0});
+      sum = &s->prof_done.back();
+    }
+    sum->ms += ms;
+    sum->count++;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  s->prof.clear();
+}
+
+mg_status plan_profile_enable(mg_solver* s, bool on) {
+  if (on) {
+    prof_drain(s);
+    s->prof_done.clear();
+  }
+  s->prof_on = on;
+  return MG_OK;
+}
+
+int plan_profile_read(mg_solver* s, int cap, const char** names, double* ms, int64_t* count, double* bytes) {
+  prof_drain(s);
+  int n = (int)s->prof_done.size();
+  for (int i = 0; i < n && i < cap; i++) {
+    if (names) names[i] = s->prof_done[i].name.c_str();
+    if (ms) ms[i] = s->prof_done[i].ms;
+    if (count) count[i] = s->prof_done[i].count;
+    if (bytes) bytes[i] = s->prof_done[i].bytes;
+  }
+  return n;
+}
+
+}  // namespace mg

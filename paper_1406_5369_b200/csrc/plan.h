@@ -1,0 +1,89 @@
+// plan.h — solver state shared by api.cu and plan.cu (host side only).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "mg.h"
+#include "mg_common.cuh"
+
+namespace mg {
+
+struct Level {
+  Geom g;
+  Coef<double> c64;
+  Coef<float> c32;
+  double cx, cy, cz, D;   // double-precision coefficients (coarse direct solve)
+  int64_t shape[3];       // [planes][rows][pitch]
+  size_t elems;           // planes*rows*pitch
+  void* u = nullptr;      // library-owned iterate (levels >= 1)
+  void* f = nullptr;      // library-owned right-hand side (levels >= 1)
+  void* r = nullptr;      // residual scratch (op-by-op schedule)
+  void* t = nullptr;      // ping-pong partner of u
+};
+
+struct ProfRec {
+  int kind;               // index into the kernel-name table
+  int level;
+  double bytes;           // algorithmic bytes of this launch
+  cudaEvent_t a, b;
+};
+
+struct ProfSum {
+  std::string name;
+  double ms = 0, bytes = 0;
+  int64_t count = 0;
+};
+
+}  // namespace mg
+
+struct mg_solver {
+  mg_config cfg;
+  int L = 0;
+  size_t esz = 8;
+  std::vector<mg::Level> lv;
+  // coarsest direct solve
+  int m_coarse = 0;
+  double* d_chol = nullptr;
+  double* d_work = nullptr;
+  // norm
+  double* d_partial = nullptr;
+  int n_partial_cap = 0;
+  double* d_norm = nullptr;
+  double* h_norm = nullptr;  // pinned
+  // graphs keyed by (u, f)
+  cudaStream_t cap_stream = nullptr;
+  std::map<std::pair<void*, const void*>, cudaGraphExec_t> graphs;
+  // e2e staging
+  void* stage_u = nullptr;
+  void* stage_f = nullptr;
+  // instrumentation
+  int64_t launches_per_cycle = 0;
+  int64_t launch_counter = 0;
+  bool prof_on = false;
+  std::vector<mg::ProfRec> prof;
+  std::vector<mg::ProfSum> prof_done;
+  // errors
+  std::string err;
+  bool poisoned = false;
+};
+
+namespace mg {
+mg_status plan_fail(mg_solver* s, mg_status st, const char* msg);
+mg_status plan_build(mg_solver* s);
+void plan_free(mg_solver* s);
+mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st);
+mg_status plan_graph_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st);
+mg_status plan_norm(mg_solver* s, int level, const void* u, const void* f, double* out, cudaStream_t st, bool sync);
+mg_status plan_op_smooth(mg_solver* s, int level, const void* uin, const void* f, void* uout, cudaStream_t st);
+mg_status plan_op_residual(mg_solver* s, int level, const void* u, const void* f, void* r, cudaStream_t st);
+mg_status plan_op_restrict(mg_solver* s, int level, const void* r, void* fc, cudaStream_t st);
+mg_status plan_op_prolong(mg_solver* s, int level, const void* e, void* u, cudaStream_t st);
+mg_status plan_op_coarse(mg_solver* s, const void* f, void* e, cudaStream_t st);
+mg_status plan_workload_fill(mg_solver* s, void* dst, uint64_t seed, double lo, double hi, cudaStream_t st);
+mg_status plan_profile_enable(mg_solver* s, bool on);
+int plan_profile_read(mg_solver* s, int cap, const char** names, double* ms, int64_t* count, double* bytes);
+}  // namespace mg
