@@ -1,0 +1,18 @@
+// kernels_pm.h — launchers of the TMA plane-marching kernels (3D levels).
+#pragma once
+#include "mg_common.cuh"
+
+namespace mg {
+namespace pm {
+// true when a level is large enough for the plane-marching kernels
+bool supported(const Geom& g);
+// one RBGS (rbgs=true) or Jacobi sweep u_out = S(u_in); zero_in: u_in is taken as 0 (not read)
+template <typename T>
+cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
+                         int zc, cudaStream_t st);
+// fc (coarse interior) = FW(f - A u) ; coarse boundary untouched
+template <typename T>
+cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>& c, const T* u, const T* f, T* fc,
+                                  int zcc, cudaStream_t st);
+}  // namespace pm
+}  // namespace mg

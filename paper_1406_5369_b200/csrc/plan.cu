@@ -8,6 +8,8 @@
 #include <cstring>
 
 #include "kernels.h"
+#include "kernels_pm.h"
+#include <cstdlib>
 #include "plan.h"
 
 namespace mg {
@@ -25,11 +27,15 @@ enum Kind {
   K_COARSE_DIRECT,
   K_MEMSET,
   K_ADD,
+  K_SWEEP_RBGS,
+  K_SWEEP_JACOBI,
+  K_RESID_RESTRICT,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
                                        "prolong_correct", "copy_boundary", "copy_interior", "norm_partial",
-                                       "norm_final",    "coarse_direct", "memset",       "add_interior"};
+                                       "norm_final",    "coarse_direct", "memset",       "add_interior",
+                                       "rbgs_fused",    "jacobi_pm",     "resid_restrict"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -244,8 +250,36 @@ struct Exec {
   const Coef<T>& coef(int l) const;
   double w(int l) const { return nodes_of(s->lv[l]) * sizeof(T); }  // one word per node of level l
 
-  mg_status smooth(int l, T*& cur, T*& other, const T* f) {
+  bool pm(int l) const { return !(s->cfg.flags & MG_FLAG_BASELINE) && pm::supported(s->lv[l].g); }
+  int zc(int l) const {
+    const Geom& g = s->lv[l].g;
+    const char* e = getenv("MG_ZC");
+    if (e && atoi(e) > 0) return atoi(e);
+    long long tiles = (long long)((g.nx + 63) / 64) * ((g.ny + 7) / 8);
+    long long want = 148 * 2 * 4;
+    long long chunks = (want + tiles - 1) / tiles;
+    int np = g.p_hi - g.p_lo;
+    int z = (int)((np + chunks - 1) / chunks);
+    return z < 8 ? 8 : z;
+  }
+
+  // one sweep; zero_in: the iterate is known to be 0 (first sweep after V_H(0,...))
+  mg_status smooth(int l, T*& cur, T*& other, const T* f, bool zero_in = false) {
     const Level& L = s->lv[l];
+    if (pm(l)) {
+      const bool rb = s->cfg.smoother == MG_RBGS;
+      T* in = cur;
+      T* out = other;
+      mg_status r = launch(s, st, rb ? K_SWEEP_RBGS : K_SWEEP_JACOBI, l, (zero_in ? 2 : 3) * w(l), [&] {
+        return pm::launch_sweep<T>(L.g, coef(l), rb, zero_in ? nullptr : in, f, out, zero_in, zc(l), st);
+      });
+      std::swap(cur, other);
+      return r;
+    }
+    if (zero_in) {
+      mg_status r = memset0(l, cur);
+      if (r != MG_OK) return r;
+    }
     if (s->cfg.smoother == MG_JACOBI) {
       mg_status r = launch(s, st, K_JACOBI, l, 3 * w(l),
                            [&] { return launch_jacobi<T>(L.g, coef(l), cur, f, other, st); });
@@ -286,7 +320,7 @@ struct Exec {
     std::vector<T*> cur(Lv), oth(Lv);
     mg_status r;
     // Jacobi ping-pongs between u and t: t's boundary must hold u's Dirichlet data
-    if (jac && (s->cfg.nu1 + s->cfg.nu2 > 0 || Lv == 1)) {
+    if ((jac || pm(0)) && (s->cfg.nu1 + s->cfg.nu2 > 0 || Lv == 1)) {
       r = launch(s, st, K_COPY_BOUNDARY, 0, 0,
                  [&] { return launch_copy_boundary<T>(s->lv[0].g, u0, (T*)s->lv[0].t, st); });
       if (r != MG_OK) return r;
@@ -319,11 +353,20 @@ struct Exec {
       for (int l = 0; l < Lv - 1; l++) {
         const Level& L = s->lv[l];
         const T* f = l == 0 ? f0 : (const T*)L.f;
-        if (l > 0 && (r = memset0(l, cur[l])) != MG_OK) return r;  // V_H(0, ...)
+        // V_H(0, ...): the zero guess is folded into the first sweep (bitwise identical)
+        if (l > 0 && s->cfg.nu1 == 0 && (r = memset0(l, cur[l])) != MG_OK) return r;
         for (int k = 0; k < s->cfg.nu1; k++)
-          if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+          if ((r = smooth(l, cur[l], oth[l], f, l > 0 && k == 0)) != MG_OK) return r;
         T* res = (T*)L.r;
         T* fc = (T*)s->lv[l + 1].f;
+        if (pm(l) && pm::supported(s->lv[l].g)) {
+          const T* uc = cur[l];
+          if ((r = launch(s, st, K_RESID_RESTRICT, l, 2 * w(l) + w(l + 1), [&] {
+                 return pm::launch_resid_restrict<T>(L.g, s->lv[l + 1].g, coef(l), uc, f, fc, zc(l + 1), st);
+               })) != MG_OK)
+            return r;
+          continue;
+        }
         if ((r = launch(s, st, K_RESIDUAL, l, 3 * w(l),
                         [&] { return launch_residual<T>(L.g, coef(l), cur[l], f, res, st); })) != MG_OK)
           return r;
@@ -438,24 +481,19 @@ template <typename T>
 static mg_status op_smooth_T(mg_solver* s, int l, const T* uin, const T* f, T* uout, cudaStream_t st) {
   Exec<T> x{s, st};
   const Level& L = s->lv[l];
-  if (s->cfg.smoother == MG_JACOBI) {
-    if (uin == uout) {  // in place: sweep into t, copy back
-      T* tmp = (T*)L.t;
-      mg_status r = launch(s, st, K_COPY_BOUNDARY, l, 0, [&] { return launch_copy_boundary<T>(L.g, uin, tmp, st); });
-      if (r != MG_OK) return r;
-      T* cur = (T*)uin;
-      T* oth = tmp;
-      if ((r = x.smooth(l, cur, oth, f)) != MG_OK) return r;
-      return launch(s, st, K_COPY_INTERIOR, l, 0, [&] {
-        k_copy_interior<T><<<rows_grid(L.g), dim3(128, 2), 0, st>>>(L.g, tmp, uout);
-        return cudaGetLastError();
-      });
-    }
-    mg_status r = launch(s, st, K_COPY_BOUNDARY, l, 0, [&] { return launch_copy_boundary<T>(L.g, uin, uout, st); });
+  const bool pingpong = s->cfg.smoother == MG_JACOBI || x.pm(l);
+  if (pingpong) {
+    T* dst = uin == uout ? (T*)L.t : uout;  // in place: sweep into t, copy back
+    mg_status r = launch(s, st, K_COPY_BOUNDARY, l, 0, [&] { return launch_copy_boundary<T>(L.g, uin, dst, st); });
     if (r != MG_OK) return r;
     T* cur = (T*)uin;
-    T* oth = uout;
-    return x.smooth(l, cur, oth, f);
+    T* oth = dst;
+    if ((r = x.smooth(l, cur, oth, f)) != MG_OK) return r;
+    if (dst == uout) return MG_OK;
+    return launch(s, st, K_COPY_INTERIOR, l, 0, [&] {
+      k_copy_interior<T><<<rows_grid(L.g), dim3(128, 2), 0, st>>>(L.g, dst, uout);
+      return cudaGetLastError();
+    });
   }
   if (uin != uout) {
     cudaError_t e = cudaMemcpyAsync(uout, uin, L.elems * sizeof(T), cudaMemcpyDeviceToDevice, st);
