@@ -28,7 +28,7 @@ build/%.o: $(CSRC)/%.cu $(CU_HDRS)
 
 $(LIB): $(CU_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -L $(NCCL_DIR)/lib -l:libnccl.so.2 \
-	    -Xlinker -rpath,$(NCCL_DIR)/lib -lcuda
+	    -Xlinker -rpath,$(NCCL_DIR)/lib
 
 oracle: oracle/liboracle_f64.so oracle/liboracle_f32.so
 

@@ -77,6 +77,9 @@ typedef struct {
     int32_t rank, nranks;/* slab decomposition along the slowest axis; nranks==1 today  */
     const void* nccl_id; /* 128-byte ncclUniqueId when nranks > 1, else NULL            */
     uint32_t flags;      /* MG_FLAG_*                                                   */
+    int32_t pm_min_nx;   /* smallest x-extent (cells) of a 3D level that uses the plane-
+                            marching kernels; 0 => 128.  Smaller levels use one thread per
+                            node.  Results are bitwise identical either way.              */
 } mg_config;
 
 /* Fill `cfg` with the defaults above for a `dim`-D grid of `nodes` per axis. */

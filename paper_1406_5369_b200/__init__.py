@@ -53,6 +53,7 @@ class MGConfig(ctypes.Structure):
         ("nranks", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p),
         ("flags", ctypes.c_uint32),
+        ("pm_min_nx", ctypes.c_int32),
     ]
 
 
@@ -121,7 +122,7 @@ class Solver:
 
     def __init__(self, dim, nodes, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, coarse="direct",
                  ncoarse=10, dtype="f64", device=0, coeff=(1.0, 1.0, 1.0), h=None, flags=0, rank=0, nranks=1,
-                 nccl_id=None):
+                 nccl_id=None, pm_min_nx=0):
         lib = load_library()
         self.lib = lib
         if isinstance(nodes, int):
@@ -144,6 +145,7 @@ class Solver:
         self._nccl_id = nccl_id
         c.nccl_id = ctypes.cast(ctypes.c_char_p(nccl_id), ctypes.c_void_p) if nccl_id is not None else None
         c.flags = flags
+        c.pm_min_nx = pm_min_nx
         self.cfg = c
         self.dim = dim
         self.nodes = tuple(int(n) for n in nodes[:dim])

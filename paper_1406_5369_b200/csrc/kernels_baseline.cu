@@ -155,20 +155,44 @@ __global__ void __launch_bounds__(BX* BY) k_prolong_correct(Geom gf, Geom gc, co
 }
 
 // ---- copy the boundary nodes of the local planes (ping-pong buffers) -------
+// One thread per boundary node, enumerated as: (A) whole boundary planes,
+// (B) boundary rows of interior planes (3D), (C) the two x-ends of interior rows.
 template <typename T>
 __global__ void k_copy_boundary(Geom g, const T* __restrict__ src, T* __restrict__ dst, int nplanes) {
-  long long q = (long long)blockIdx.x * blockDim.y + threadIdx.y;  // one warp row per (plane,row)
-  if (q >= (long long)nplanes * g.rows) return;
-  int row = (int)(q % g.rows);
-  int pl = (int)(q / g.rows);
-  int pg = pl + g.p_glob0;
-  bool full = pg == 0 || pg == g.nz || (g.three_d && (row == 0 || row == g.ny));
-  long long base = (long long)pl * g.pstride + (long long)row * g.pitch;
-  if (full) {
-    for (int i = threadIdx.x; i <= g.nx; i += 32) dst[base + i] = src[base + i];
-  } else if (threadIdx.x == 0) {
-    dst[base] = src[base];
-    dst[base + g.nx] = src[base + g.nx];
+  const long long nxn = g.nx + 1;
+  const int irows = g.three_d ? g.ny - 1 : 1;  // interior rows per plane
+  const int rlo = g.three_d ? 1 : 0;
+  // local planes holding global boundary planes
+  const int pb0 = 0 - g.p_glob0, pb1 = g.nz - g.p_glob0;
+  const bool has0 = pb0 >= 0 && pb0 < nplanes, has1 = pb1 >= 0 && pb1 < nplanes;
+  const long long nA = (long long)((has0 ? 1 : 0) + (has1 ? 1 : 0)) * g.rows * nxn;
+  const int iplanes = g.p_hi - g.p_lo;  // interior planes
+  const long long nB = g.three_d ? (long long)iplanes * 2 * nxn : 0;
+  const long long nC = (long long)iplanes * irows * 2;
+  const long long n = nA + nB + nC;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    long long off;
+    if (t < nA) {
+      const long long per = (long long)g.rows * nxn;
+      const int which = (int)(t / per);
+      const long long rem = t - which * per;
+      const int pl = (which == 0 && has0) ? pb0 : pb1;
+      off = (long long)pl * g.pstride + (rem / nxn) * g.pitch + rem % nxn;
+    } else if (t < nA + nB) {
+      const long long q = t - nA;
+      const long long per = 2 * nxn;
+      const int pl = g.p_lo + (int)(q / per);
+      const long long rem = q % per;
+      const int row = rem < nxn ? 0 : g.ny;
+      off = (long long)pl * g.pstride + (long long)row * g.pitch + rem % nxn;
+    } else {
+      const long long q = t - nA - nB;
+      const long long rr = q >> 1;
+      const int pl = g.p_lo + (int)(rr / irows);
+      const int row = rlo + (int)(rr % irows);
+      off = (long long)pl * g.pstride + (long long)row * g.pitch + ((q & 1) ? g.nx : 0);
+    }
+    dst[off] = src[off];
   }
 }
 
@@ -353,9 +377,7 @@ cudaError_t launch_prolong_correct(const Geom& gf, const Geom& gc, const T* e, T
 template <typename T>
 cudaError_t launch_copy_boundary(const Geom& g, const T* src, T* dst, cudaStream_t st) {
   int nplanes = g.p_hi - g.p_lo + 2;  // local planes incl. the two outer ones
-  long long q = (long long)nplanes * g.rows;
-  dim3 blk(32, 8);
-  k_copy_boundary<T><<<(unsigned)((q + 7) / 8), blk, 0, st>>>(g, src, dst, nplanes);
+  k_copy_boundary<T><<<148 * 4, 256, 0, st>>>(g, src, dst, nplanes);
   return cudaGetLastError();
 }
 template <typename T>

@@ -25,6 +25,7 @@
 //                    full weighting as x/y sums per plane and the z
 //                    sum in registers: read u, f; write f_H = 2 + 1/8 words.
 #include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -194,10 +195,14 @@ __device__ __forceinline__ void black_node(const Coef<T>& c, const T* P, const T
   store_pair(orow, ox, in0, in1, KB ? pr_own : o, KB ? o : pr_own);
 }
 
-template <typename T, bool RB, bool ZERO>
+// MODE 0: Jacobi sweep; 1: red-black GS sweep; 2: residual-norm partials (one
+// double per CTA in `partial`, fixed reduction tree: deterministic).
+template <typename T, int MODE, bool ZERO>
 __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     k_sweep3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f, Geom g,
-              Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems) {
+              Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems,
+              double* __restrict__ partial) {
+  constexpr bool RB = MODE == 1;
   extern __shared__ __align__(128) unsigned char sm[];
   using G = Geo<T>;
   constexpr int BX = G::BX, HX = G::HX;
@@ -212,6 +217,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
   const int fo = (ry + 1) * BX + 2 * lane + HX;  // f-box offset of (ox, oy)
   const int po = (ry + 1) * PX + 2 * lane + 1;    // PR offset of (ox, oy)
   uint32_t seq = 0;
+  double nsum = 0.0;  // MODE 2: this thread's sum of r^2
   for (int k = blockIdx.x; k < nitems; k += gridDim.x) {
     int tile, pa, pb;
     item_of(k, ntiles, zc, g.p_lo, g.p_hi, tile, pa, pb);
@@ -316,10 +322,20 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         const T* U0 = R.U(N(p - 1));
         up = S.upair(R.U(N(p)), bo);
         const Pair<T> fp = ld_pair(R.F(N(p)) + fo);
-        const T v0 = relax(c, u0.x, S.u(U0, bo - 1), u0.y, S.u(U0, bo - BX), S.u(U0, bo + BX), um.x, up.x, fp.x);
-        const T v1 =
-            relax(c, u0.y, u0.x, S.u(U0, bo + 2), S.u(U0, bo + 1 - BX), S.u(U0, bo + 1 + BX), um.y, up.y, fp.y);
-        store_pair(orow + (long long)p * g.pstride, ox, in0, in1, in0 ? v0 : u0.x, in1 ? v1 : u0.y);
+        if (MODE == 2) {  // r = f - A u, squares accumulated in FP64 (reading 11)
+          const double r0 = (double)sub(
+              fp.x, apply_A(c, u0.x, S.u(U0, bo - 1), u0.y, S.u(U0, bo - BX), S.u(U0, bo + BX), um.x, up.x));
+          const double r1 = (double)sub(
+              fp.y, apply_A(c, u0.y, u0.x, S.u(U0, bo + 2), S.u(U0, bo + 1 - BX), S.u(U0, bo + 1 + BX), um.y, up.y));
+          if (in0) nsum = __dadd_rn(nsum, __dmul_rn(r0, r0));
+          if (in1) nsum = __dadd_rn(nsum, __dmul_rn(r1, r1));
+        } else {
+          const T v0 =
+              relax(c, u0.x, S.u(U0, bo - 1), u0.y, S.u(U0, bo - BX), S.u(U0, bo + BX), um.x, up.x, fp.x);
+          const T v1 =
+              relax(c, u0.y, u0.x, S.u(U0, bo + 2), S.u(U0, bo + 1 - BX), S.u(U0, bo + 1 + BX), um.y, up.y, fp.y);
+          store_pair(orow + (long long)p * g.pstride, ox, in0, in1, in0 ? v0 : u0.x, in1 ? v1 : u0.y);
+        }
         __syncthreads();
         if (tid == 0 && p - 1 + G::NS <= qlast) {
           fence_proxy_async();
@@ -331,6 +347,18 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     }
     seq = N(qlast) + 1;
     __syncthreads();
+  }
+  if (MODE == 2) {  // fixed-order block reduction -> one partial per CTA
+    double* red = reinterpret_cast<double*>(sm);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nsum = __dadd_rn(nsum, __shfl_down_sync(0xffffffffu, nsum, o));
+    if (lane == 0) red[ry] = nsum;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w2 = 0; w2 < NT / 32; w2++) t = __dadd_rn(t, red[w2]);
+      partial[blockIdx.x] = t;
+    }
   }
 }
 
@@ -452,7 +480,23 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
 }
 
 // ---------------------------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point, so that the
+// library does not link libcuda (it must load on GPU-less hosts for the ABI tests).
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
 static CUresult encode(CUtensorMap* tm, const void* base, const Geom& g, int esz, int box_rows) {
+  PFN_cuTensorMapEncodeTiled_v12000 cuTensorMapEncodeTiled = encode_fn();
+  if (!cuTensorMapEncodeTiled) return CUDA_ERROR_NOT_FOUND;
   cuuint64_t dims[3] = {(cuuint64_t)(g.nx + 1), (cuuint64_t)g.rows, (cuuint64_t)(g.p_hi + 1)};
   cuuint64_t strides[2] = {(cuuint64_t)(g.pitch * esz), (cuuint64_t)(g.pstride * esz)};
   cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * (16 / esz)), (cuuint32_t)box_rows, 1};
@@ -463,7 +507,13 @@ static CUresult encode(CUtensorMap* tm, const void* base, const Geom& g, int esz
                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
-bool supported(const Geom& g) { return g.three_d && g.nx >= 16 && g.ny >= 16 && (g.p_hi - g.p_lo) >= 4; }
+// Plane marching pays off once a level has enough planes per CTA to hide the
+// per-plane barrier latency: measured, a 65^3 level is 2x slower marched than
+// with the one-thread-per-node kernels, 129^3 is ~1.5x faster.  The plan passes
+// mg_config.pm_min_nx (default 128; tests lower it to cover small grids).
+bool supported(const Geom& g, int min_nx) {
+  return g.three_d && g.nx >= (min_nx < 16 ? 16 : min_nx) && g.ny >= 16 && (g.p_hi - g.p_lo) >= 4;
+}
 
 // First use of a kernel: opt in to its dynamic shared memory and return the
 // number of CTAs the device keeps resident (cached per kernel).
@@ -486,18 +536,23 @@ static int prepare_kernel(K kernel, int smem) {
   return r;
 }
 
-// z-chunk size: minimise (waves) x (planes per item incl. ~halo re-loads); waves are
-// counted in units of the resident CTA count, so the last wave is nearly full.
+// z-chunk size.  Measured on the 513^3 RBGS sweep (tools/scan_zc.py): what
+// matters is a nearly full last wave of resident CTAs and enough waves (>= ~8)
+// to balance SMs; the halo re-loads of short chunks mostly hit L2.  So: among
+// chunk lengths >= 16 planes, minimise (ceil(waves)/waves) * (1 + halo/(2 zc))
+// plus a small penalty below 8 waves.
 static int choose_zc(long long ntiles, int np, int resident, int halo) {
   int best = np;
   double best_cost = 1e300;
-  for (int c = 1; c <= 64 && c <= np; c++) {
+  for (int c = 1; c <= 256 && c <= np; c++) {
     const int zc = (np + c - 1) / c;
+    if (zc < 16 && c > 1) break;
     const int chunks = (np + zc - 1) / zc;
     const long long items = ntiles * chunks;
-    const long long waves = (items + resident - 1) / resident;
-    const double cost = (double)waves * (zc + 0.6 * halo);
-    if (cost < best_cost - 1e-9) {
+    const double wx = (double)items / resident;
+    const double wc = (double)((items + resident - 1) / resident);
+    const double cost = (wc / wx) * (1.0 + 0.5 * halo / zc) + (wx < 8.0 ? 0.02 * (8.0 - wx) : 0.0);
+    if (cost < best_cost - 1e-12) {
       best_cost = cost;
       best = zc;
     }
@@ -521,14 +576,127 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
     const int zc = zc_override > 0 ? zc_override : choose_zc(ntiles, np, resident, rbgs ? 4 : 2);
     const int nitems = ntiles * ((np + zc - 1) / zc);
     if (getenv("MG_DEBUG"))
-      fprintf(stderr, "launch_sweep: resident=%d zc=%d nitems=%d smem=%d err=%s\n", resident, zc, nitems, G::SMEM,
-              cudaGetErrorString(cudaGetLastError()));
-    kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems);
+      fprintf(stderr, "launch_sweep: resident=%d zc=%d nitems=%d smem=%d\n", resident, zc, nitems, G::SMEM);
+    kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, nullptr);
   };
   if (rbgs)
-    zero_in ? go(k_sweep3d<T, true, true>) : go(k_sweep3d<T, true, false>);
+    zero_in ? go(k_sweep3d<T, 1, true>) : go(k_sweep3d<T, 1, false>);
   else
-    zero_in ? go(k_sweep3d<T, false, true>) : go(k_sweep3d<T, false, false>);
+    zero_in ? go(k_sweep3d<T, 0, true>) : go(k_sweep3d<T, 0, false>);
+  return cudaGetLastError();
+}
+
+template <typename T>
+int norm_partials(const Geom& g) {
+  using G = Geo<T>;
+  const int ntiles = ((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
+  const int np = g.p_hi - g.p_lo;
+  const int resident = prepare_kernel(k_sweep3d<T, 2, false>, G::SMEM);
+  const int zc = choose_zc(ntiles, np, resident, 2);
+  return ntiles * ((np + zc - 1) / zc);
+}
+
+template <typename T>
+cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f, double* partial, int* npartial,
+                        cudaStream_t st) {
+  using G = Geo<T>;
+  CUtensorMap tu, tf;
+  if (encode(&tu, u, g, sizeof(T), G::BYU) != CUDA_SUCCESS || encode(&tf, f, g, sizeof(T), G::BYF) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  const int tiles_x = (g.nx + TX - 1) / TX, tiles_y = (g.ny + TY - 1) / TY;
+  const int ntiles = tiles_x * tiles_y;
+  const int np = g.p_hi - g.p_lo;
+  auto kernel = k_sweep3d<T, 2, false>;
+  const int resident = prepare_kernel(kernel, G::SMEM);
+  const int zc = choose_zc(ntiles, np, resident, 2);
+  const int nitems = ntiles * ((np + zc - 1) / zc);
+  *npartial = nitems;
+  kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, g, c, nullptr, tiles_x, ntiles, zc, nitems, partial);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Bi-/trilinear prolongation + correction u += P e, 3D.
+// Pointwise in u, so no staging: thread = fine x-pair (2X, 2X+1) of one row,
+// marching z.  The pair's coarse values after the x- and y-interpolation of a
+// coarse plane K, V(K), stay in registers for the 3 fine planes that use it;
+// fine plane z = 2Z+dz gets dz ? (V(Z)+V(Z+1))/2 : V(Z) (reading 13 order).
+template <typename T>
+__global__ void __launch_bounds__(NT) k_prolong3d(Geom gf, Geom gc, const T* __restrict__ e, T* __restrict__ u,
+                                                 int tiles_x, int ntiles, int zc, int nitems) {
+  const int lane = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const T half = (T)0.5;
+  for (int k = blockIdx.x; k < nitems; k += gridDim.x) {
+    int tile, pa, pb;
+    item_of(k, ntiles, zc, gf.p_lo, gf.p_hi, tile, pa, pb);
+    const int x0 = (tile % tiles_x) * TX, y0 = (tile / tiles_x) * TY;
+    const int ox = x0 + 2 * lane, oy = y0 + ry;
+    const bool rin = oy >= 1 && oy <= gf.ny - 1;
+    const bool in0 = rin && ox >= 1 && ox <= gf.nx - 1;
+    const bool in1 = rin && ox + 1 <= gf.nx - 1;
+    if (!(in0 || in1)) continue;
+    const int X = ox >> 1, Y = oy >> 1, dy = oy & 1;
+    const T* ec = e + (long long)Y * gc.pitch + X;
+    auto V = [&](int Zg) -> Pair<T> {  // x- then y-interpolated pair of coarse plane Zg (global)
+      const T* p0 = ec + (long long)(Zg - gc.p_glob0) * gc.pstride;
+      const T a0 = __ldg(p0), a1 = __ldg(p0 + 1);
+      Pair<T> v{a0, mul(half, add(a0, a1))};
+      if (dy) {
+        const T b0 = __ldg(p0 + gc.pitch), b1 = __ldg(p0 + gc.pitch + 1);
+        const Pair<T> w{b0, mul(half, add(b0, b1))};
+        v = Pair<T>{mul(half, add(v.x, w.x)), mul(half, add(v.y, w.y))};
+      }
+      return v;
+    };
+    T* urow = u + (long long)oy * gf.pitch + ox;
+    int Z = (pa + gf.p_glob0) >> 1;
+    Pair<T> A = V(Z), B = A;
+    bool haveB = false;
+    for (int z = pa; z < pb; z++) {
+      const int zg = z + gf.p_glob0;
+      if ((zg >> 1) != Z) {
+        Z++;
+        A = haveB ? B : V(Z);
+        haveB = false;
+      }
+      Pair<T> v = A;
+      if (zg & 1) {
+        if (!haveB) {
+          B = V(Z + 1);
+          haveB = true;
+        }
+        v = Pair<T>{mul(half, add(A.x, B.x)), mul(half, add(A.y, B.y))};
+      }
+      T* up = urow + (long long)z * gf.pstride;
+      if (in0 && in1) {
+        const Pair<T> uu = ld_pair(up);
+        typename V2<T>::t o;
+        o.x = add(uu.x, v.x);
+        o.y = add(uu.y, v.y);
+        *reinterpret_cast<typename V2<T>::t*>(up) = o;
+      } else {
+        if (in0) up[0] = add(up[0], v.x);
+        if (in1) up[1] = add(up[1], v.y);
+      }
+    }
+  }
+}
+
+template <typename T>
+cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cudaStream_t st) {
+  const int tiles_x = (gf.nx + TX - 1) / TX, tiles_y = (gf.ny + TY - 1) / TY;
+  const int ntiles = tiles_x * tiles_y;
+  const int np = gf.p_hi - gf.p_lo;
+  static int resident = 0;
+  if (!resident) {
+    int sms = 0, occ = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_prolong3d<T>, NT, 0);
+    resident = (occ < 1 ? 1 : occ) * (sms < 1 ? 1 : sms);
+  }
+  const int zc = choose_zc(ntiles, np, resident, 0);
+  const int nitems = ntiles * ((np + zc - 1) / zc);
+  k_prolong3d<T><<<nitems, NT, 0, st>>>(gf, gc, e, u, tiles_x, ntiles, zc, nitems);
   return cudaGetLastError();
 }
 
@@ -554,6 +722,14 @@ template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool
                                           double*, bool, int, cudaStream_t);
 template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
                                          bool, int, cudaStream_t);
+template int norm_partials<double>(const Geom&);
+template int norm_partials<float>(const Geom&);
+template cudaError_t launch_norm<double>(const Geom&, const Coef<double>&, const double*, const double*, double*,
+                                         int*, cudaStream_t);
+template cudaError_t launch_norm<float>(const Geom&, const Coef<float>&, const float*, const float*, double*, int*,
+                                        cudaStream_t);
+template cudaError_t launch_prolong<double>(const Geom&, const Geom&, const double*, double*, cudaStream_t);
+template cudaError_t launch_prolong<float>(const Geom&, const Geom&, const float*, float*, cudaStream_t);
 template cudaError_t launch_resid_restrict<double>(const Geom&, const Geom&, const Coef<double>&, const double*,
                                                    const double*, double*, int, cudaStream_t);
 template cudaError_t launch_resid_restrict<float>(const Geom&, const Geom&, const Coef<float>&, const float*,

@@ -5,7 +5,7 @@
 namespace mg {
 namespace pm {
 // true when a level is large enough for the plane-marching kernels
-bool supported(const Geom& g);
+bool supported(const Geom& g, int min_nx);
 // one RBGS (rbgs=true) or Jacobi sweep u_out = S(u_in); zero_in: u_in is taken as 0 (not read)
 template <typename T>
 cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
@@ -14,5 +14,14 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
 template <typename T>
 cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>& c, const T* u, const T* f, T* fc,
                                   int zcc, cudaStream_t st);
+// residual-norm partials (one double per CTA); *npartial = count written
+template <typename T>
+cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f, double* partial, int* npartial,
+                        cudaStream_t st);
+template <typename T>
+int norm_partials(const Geom& g);
+// u += P e (3D, interior fine nodes)
+template <typename T>
+cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cudaStream_t st);
 }  // namespace pm
 }  // namespace mg

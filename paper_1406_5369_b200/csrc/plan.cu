@@ -177,6 +177,10 @@ mg_status plan_build(mg_solver* s) {
   for (int l = 0; l < s->L; l++) {
     int a = s->esz == 8 ? norm_num_partials<double>(s->lv[l].g) : norm_num_partials<float>(s->lv[l].g);
     if (a > np) np = a;
+    if (pm::supported(s->lv[l].g, 16)) {
+      a = s->esz == 8 ? pm::norm_partials<double>(s->lv[l].g) : pm::norm_partials<float>(s->lv[l].g);
+      if (a > np) np = a;
+    }
   }
   s->n_partial_cap = np;
   if (cudaMalloc(&s->d_partial, sizeof(double) * np) != cudaSuccess ||
@@ -250,17 +254,13 @@ struct Exec {
   const Coef<T>& coef(int l) const;
   double w(int l) const { return nodes_of(s->lv[l]) * sizeof(T); }  // one word per node of level l
 
-  bool pm(int l) const { return !(s->cfg.flags & MG_FLAG_BASELINE) && pm::supported(s->lv[l].g); }
-  int zc(int l) const {
-    const Geom& g = s->lv[l].g;
+  bool pm(int l) const {
+    return !(s->cfg.flags & MG_FLAG_BASELINE) && pm::supported(s->lv[l].g, s->cfg.pm_min_nx ? s->cfg.pm_min_nx : 128);
+  }
+  // z-chunk override for tuning (MG_ZC); 0 = the launcher's own choice
+  int zc(int) const {
     const char* e = getenv("MG_ZC");
-    if (e && atoi(e) > 0) return atoi(e);
-    long long tiles = (long long)((g.nx + 63) / 64) * ((g.ny + 7) / 8);
-    long long want = 148 * 2 * 4;
-    long long chunks = (want + tiles - 1) / tiles;
-    int np = g.p_hi - g.p_lo;
-    int z = (int)((np + chunks - 1) / chunks);
-    return z < 8 ? 8 : z;
+    return e ? atoi(e) : 0;
   }
 
   // one sweep; zero_in: the iterate is known to be 0 (first sweep after V_H(0,...))
@@ -359,7 +359,7 @@ struct Exec {
           if ((r = smooth(l, cur[l], oth[l], f, l > 0 && k == 0)) != MG_OK) return r;
         T* res = (T*)L.r;
         T* fc = (T*)s->lv[l + 1].f;
-        if (pm(l) && pm::supported(s->lv[l].g)) {
+        if (pm(l)) {
           const T* uc = cur[l];
           if ((r = launch(s, st, K_RESID_RESTRICT, l, 2 * w(l) + w(l + 1), [&] {
                  return pm::launch_resid_restrict<T>(L.g, s->lv[l + 1].g, coef(l), uc, f, fc, zc(l + 1), st);
@@ -385,8 +385,10 @@ struct Exec {
         const Level& L = s->lv[l];
         const T* f = l == 0 ? f0 : (const T*)L.f;
         const T* e = cur[l + 1];
+        const bool pml = pm(l);
         if ((r = launch(s, st, K_PROLONG, l, 2 * w(l) + w(l + 1), [&] {
-               return launch_prolong_correct<T>(L.g, s->lv[l + 1].g, e, cur[l], st);
+               return pml ? pm::launch_prolong<T>(L.g, s->lv[l + 1].g, e, cur[l], st)
+                          : launch_prolong_correct<T>(L.g, s->lv[l + 1].g, e, cur[l], st);
              })) != MG_OK)
           return r;
         for (int k = 0; k < s->cfg.nu2; k++)
@@ -408,8 +410,11 @@ struct Exec {
   mg_status norm(int l, const T* u, const T* f, double* out_dev) {
     const Level& L = s->lv[l];
     int np = norm_num_partials<T>(L.g);
-    mg_status r = launch(s, st, K_NORM_PARTIAL, l, 2 * w(l),
-                         [&] { return launch_norm_partial<T>(L.g, coef(l), u, f, s->d_partial, st); });
+    const bool pml = pm(l);
+    mg_status r = launch(s, st, K_NORM_PARTIAL, l, 2 * w(l), [&] {
+      return pml ? pm::launch_norm<T>(L.g, coef(l), u, f, s->d_partial, &np, st)
+                 : launch_norm_partial<T>(L.g, coef(l), u, f, s->d_partial, st);
+    });
     if (r != MG_OK) return r;
     return launch(s, st, K_NORM_FINAL, l, 8.0 * np,
                   [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });

@@ -17,12 +17,12 @@ TOL = {"f64": 1e-12, "f32": 1e-5}
 
 
 def make(dim, cells, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, dtype="f64", coarse="direct",
-         ncoarse=10, flags=0):
+         ncoarse=10, flags=0, pm_min_nx=16):
     import paper_1406_5369_b200 as mgb
     if omega is None:
         omega = 1.0 if smoother == "rbgs" else 0.8
     S = mgb.Solver(dim, tuple(c + 1 for c in cells), levels=levels, smoother=smoother, omega=omega, nu1=nu1,
-                   nu2=nu2, coarse=coarse, ncoarse=ncoarse, dtype=dtype, flags=flags)
+                   nu2=nu2, coarse=coarse, ncoarse=ncoarse, dtype=dtype, flags=flags, pm_min_nx=pm_min_nx)
     O = orc.Oracle(orc.Config(dim=dim, cells=tuple(cells), levels=S.levels,
                               smoother=orc.RBGS if smoother == "rbgs" else orc.JACOBI, omega=omega, nu1=nu1,
                               nu2=nu2, coarse=orc.COARSE_DIRECT if coarse == "direct" else orc.COARSE_SWEEPS,
@@ -224,3 +224,20 @@ def test_profile_counts_launches():
     S.profile_enable(False)
     assert sum(r["count"] for r in recs if not r["name"].startswith("memset")) == n
     assert all(r["ms"] > 0 for r in recs)
+
+
+@pytest.mark.parametrize("variant", ["default-threshold", "baseline"])
+def test_schedule_variants_identical(variant):
+    """The plane-marching, mixed (default threshold) and op-by-op (MG_FLAG_BASELINE)
+    schedules give bitwise identical iterates (same canonical arithmetic)."""
+    import paper_1406_5369_b200 as mgb
+    kw = dict(pm_min_nx=0) if variant == "default-threshold" else dict(flags=mgb.FLAG_BASELINE)
+    outs = []
+    for extra in (dict(), kw):
+        S, _ = make(3, (128, 128, 128), **extra)
+        u, f = wl.workload("W4", 3, (128, 128, 128), seed=11)
+        du, df = S.from_numpy(u), S.from_numpy(f)
+        for _ in range(2):
+            S.vcycle(du, df)
+        outs.append(S.to_numpy(du))
+    assert np.array_equal(outs[0], outs[1])
