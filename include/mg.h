@@ -58,6 +58,7 @@ typedef enum { MG_COARSE_DIRECT = 0, MG_COARSE_SWEEPS = 1 } mg_coarse; /* P:191,
 /* flags */
 #define MG_FLAG_NO_GRAPH 1u   /* launch eagerly instead of replaying a CUDA graph   */
 #define MG_FLAG_BASELINE 2u   /* op-by-op kernels only (no fusion; two-pass RBGS)   */
+#define MG_FLAG_SLAB 4u       /* slab layout (halos, agglomeration) even with nranks == 1 */
 
 typedef struct {
     int32_t dim;         /* 2 or 3                                        */
@@ -74,8 +75,11 @@ typedef struct {
     int32_t ncoarse;     /* sweeps on the coarsest level in SWEEPS mode, def 10 */
     int32_t dtype;       /* mg_dtype                                                    */
     int32_t device;      /* CUDA device ordinal                                         */
-    int32_t rank, nranks;/* slab decomposition along the slowest axis; nranks==1 today  */
-    const void* nccl_id; /* 128-byte ncclUniqueId when nranks > 1, else NULL            */
+    int32_t rank, nranks;/* slab decomposition along the slowest (plane) axis over nranks
+                            GPUs, one process per GPU                   */
+    const void* nccl_id; /* 128-byte ncclUniqueId when nranks > 1 (the same bytes on every
+                            rank, e.g. broadcast with torch.distributed), else NULL.
+                            mg_create is then collective: all ranks must call it.      */
     uint32_t flags;      /* MG_FLAG_*                                                   */
     int32_t pm_min_nx;   /* smallest x-extent (cells) of a 3D level that uses the plane-
                             marching kernels; 0 => 128.  Smaller levels use one thread per
@@ -93,8 +97,18 @@ void mg_config_default(mg_config* cfg, int32_t dim, int64_t nodes);
 mg_status mg_create(const mg_config* cfg, mg_solver** out);
 
 /* Shape [planes][rows][pitch] (elements) of this rank's level-0 u and f; the
- * slab of global planes it owns is [*first_plane, *first_plane + *owned). */
+ * slab of global planes it owns is [*first_plane, *first_plane + *owned).  In slab
+ * mode (nranks > 1 or MG_FLAG_SLAB) local plane i holds global plane
+ * first_plane - halo + i (halo from mg_partition); the halo planes are library
+ * scratch (rewritten by halo exchanges), the owned planes are the caller's. */
 mg_status mg_layout(const mg_solver* s, int64_t shape[3], int64_t* first_plane, int64_t* owned);
+/* Host-only (no GPU needed): the slab decomposition mg_create would use for
+ * `cfg` at `level`: owned global planes [*first_plane, +*owned_planes), whether
+ * the level is distributed (else held in full on every rank: agglomeration),
+ * and the halo depth.  Rank p owns planes [p n_l/P, (p+1) n_l/P), the last rank
+ * also plane n_l; levels stay distributed while n_l/P >= 8 and even. */
+mg_status mg_partition(const mg_config* cfg, int32_t level, int64_t* first_plane, int64_t* owned_planes,
+                       int32_t* distributed, int32_t* halo);
 /* Shape of the level-l arrays used by the per-operation entry points below. */
 mg_status mg_level_layout(const mg_solver* s, int32_t level, int64_t shape[3]);
 int32_t mg_num_levels(const mg_solver* s);
@@ -156,6 +170,10 @@ mg_status mg_profile_enable(mg_solver* s, int32_t on);
  * (may exceed cap; only min(n,cap) written).  Synchronises the device. */
 int32_t mg_profile_read(mg_solver* s, int32_t cap, const char** names, double* ms,
                         int64_t* count, double* bytes);
+
+/* Host-only: write a fresh 128-byte ncclUniqueId into out (rank 0 calls it and
+ * broadcasts the bytes to the other ranks before mg_create). */
+mg_status mg_nccl_unique_id(void* out128);
 
 const char* mg_error_string(const mg_solver* s);
 void mg_destroy(mg_solver* s);

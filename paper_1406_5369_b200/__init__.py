@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libmgb200.so")
 JACOBI, RBGS = 0, 1
 FP64, FP32 = 0, 1
 COARSE_DIRECT, COARSE_SWEEPS = 0, 1
-FLAG_NO_GRAPH, FLAG_BASELINE = 1, 2
+FLAG_NO_GRAPH, FLAG_BASELINE, FLAG_SLAB = 1, 2, 4
 
 # every symbol include/mg.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = [
@@ -31,6 +31,7 @@ ABI_SYMBOLS = [
     "mg_residual_norm", "mg_solve", "mg_vcycle_host", "mg_op_smooth", "mg_op_residual", "mg_op_restrict",
     "mg_op_prolong_correct", "mg_op_coarse_solve", "mg_op_norm", "mg_workload_fill",
     "mg_launches_per_cycle", "mg_profile_enable", "mg_profile_read", "mg_error_string", "mg_destroy",
+    "mg_partition", "mg_nccl_unique_id",
 ]
 
 
@@ -102,6 +103,9 @@ def load_library():
     lib.mg_profile_read.restype = I32
     lib.mg_error_string.argtypes = [P]
     lib.mg_error_string.restype = ctypes.c_char_p
+    lib.mg_partition.argtypes = [ctypes.POINTER(MGConfig), I32, pI64, pI64, ctypes.POINTER(I32),
+                                 ctypes.POINTER(I32)]
+    lib.mg_nccl_unique_id.argtypes = [P]
     lib.mg_destroy.argtypes = [P]
     lib.mg_destroy.restype = None
     for name in ABI_SYMBOLS:
@@ -115,6 +119,64 @@ def load_library():
 def _torch():
     import torch
     return torch
+
+
+def make_config(dim, nodes, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, coarse="direct", ncoarse=10,
+                dtype="f64", device=0, coeff=(1.0, 1.0, 1.0), h=None, flags=0, rank=0, nranks=1, pm_min_nx=0):
+    """Build an mg_config (argument marshalling only)."""
+    lib = load_library()
+    if isinstance(nodes, int):
+        nodes = (nodes,) * dim
+    c = MGConfig()
+    lib.mg_config_default(ctypes.byref(c), dim, int(nodes[0]))
+    for d in range(3):
+        c.nodes[d] = int(nodes[d]) if d < dim else 1
+        c.coeff[d] = float(coeff[d])
+        c.h[d] = 0.0 if h is None or d >= dim else float(h[d])
+    c.levels = levels
+    c.smoother = RBGS if smoother in ("rbgs", RBGS) else JACOBI
+    c.omega = float(omega) if omega is not None else (1.0 if c.smoother == RBGS else 0.8)
+    c.nu1, c.nu2 = nu1, nu2
+    c.coarse = COARSE_DIRECT if coarse in ("direct", COARSE_DIRECT) else COARSE_SWEEPS
+    c.ncoarse = ncoarse
+    c.dtype = FP64 if dtype in ("f64", FP64) else FP32
+    c.device = device
+    c.rank, c.nranks = rank, nranks
+    c.flags = flags
+    c.pm_min_nx = pm_min_nx
+    return c
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it; broadcast it to the other ranks)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.mg_nccl_unique_id(buf)
+    if st != 0:
+        raise MGError(st, lib.mg_error_string(None).decode())
+    return buf.raw
+
+
+def distributed_solver(dim, nodes, **kw):
+    """Collective: one Solver per rank of the default torch.distributed group, z-slab
+    decomposed over NCCL (the unique id is broadcast through torch.distributed)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return Solver(dim, nodes, rank=rank, nranks=world, nccl_id=obj[0], **kw)
+
+
+def partition(level, **kw):
+    """Host-only mg_partition: (first_plane, owned_planes, distributed, halo) of `level`."""
+    lib = load_library()
+    c = make_config(**kw)
+    a, n = ctypes.c_int64(), ctypes.c_int64()
+    d, hh = ctypes.c_int32(), ctypes.c_int32()
+    st = lib.mg_partition(ctypes.byref(c), level, ctypes.byref(a), ctypes.byref(n), ctypes.byref(d), ctypes.byref(hh))
+    if st != 0:
+        raise MGError(st, lib.mg_error_string(None).decode())
+    return a.value, n.value, bool(d.value), hh.value
 
 
 class Solver:
@@ -158,6 +220,8 @@ class Solver:
         torch = _torch()
         self.torch_dtype = torch.float64 if c.dtype == FP64 else torch.float32
         self.np_dtype = np.float64 if c.dtype == FP64 else np.float32
+        self.first_plane, self.owned_planes, self.distributed, self.halo = partition(
+            0, dim=dim, nodes=nodes, levels=levels, flags=flags, rank=rank, nranks=nranks)
 
     # ---- lifetime
     def close(self):
@@ -206,20 +270,27 @@ class Solver:
         return torch.zeros(self.level_shape(level), dtype=self.torch_dtype, device=f"cuda:{self.cfg.device}")
 
     def from_numpy(self, a, level=0):
-        """Dense node array (2D: (ny+1,nx+1); 3D: (nz+1,ny+1,nx+1)) -> padded device tensor."""
+        """Dense GLOBAL node array (2D: (ny+1,nx+1); 3D: (nz+1,ny+1,nx+1)) -> padded device
+        tensor of this rank's layout (in slab mode: its planes plus halo planes)."""
         torch = _torch()
         P, R, X = self.level_shape(level)
         host = np.zeros((P, R, X), dtype=self.np_dtype)
         a = np.asarray(a, dtype=self.np_dtype)
         if self.dim == 2:
-            host[:, 0, : a.shape[1]] = a
-        else:
-            host[:, :, : a.shape[2]] = a
+            a = a[:, None, :]
+        g0 = self.first_plane - self.halo if (level == 0 and self.distributed) else 0
+        for i in range(P):
+            gp = g0 + i
+            if 0 <= gp < a.shape[0]:
+                host[i, :, : a.shape[2]] = a[gp]
         return torch.from_numpy(host).to(f"cuda:{self.cfg.device}")
 
     def to_numpy(self, t, level=0):
+        """Device tensor -> dense node array; in slab mode the rank's OWNED planes only."""
         nx = self.level_cells(level)[0] + 1
         a = t.detach().cpu().numpy()
+        if level == 0 and self.distributed:
+            a = a[self.halo: self.halo + self.owned_planes]
         return np.ascontiguousarray(a[:, 0, :nx] if self.dim == 2 else a[:, :, :nx])
 
     # ---- the method

@@ -11,7 +11,10 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "mg.h"
+#include "partition.h"
 #include "plan.h"
 
 using namespace mg;
@@ -73,7 +76,7 @@ static mg_status validate(const mg_config* c, int* levels_out) {
   if (c->coarse != MG_COARSE_DIRECT && c->coarse != MG_COARSE_SWEEPS) return fail(s, MG_ERR_INVALID, "bad coarse");
   if (c->coarse == MG_COARSE_SWEEPS && c->ncoarse < 0) return fail(s, MG_ERR_INVALID, "ncoarse < 0");
   if (c->dtype != MG_FP64 && c->dtype != MG_FP32) return fail(s, MG_ERR_INVALID, "bad dtype");
-  if (c->nranks != 1) return fail(s, MG_ERR_INVALID, "nranks > 1 requires the NCCL build (not yet enabled)");
+  if (c->nranks < 1 || c->rank < 0 || c->rank >= c->nranks) return fail(s, MG_ERR_INVALID, "bad rank/nranks");
   int64_t mincells = INT64_MAX;
   for (int d = 0; d < c->dim; d++) {
     int64_t n = c->nodes[d] - 1;
@@ -103,6 +106,28 @@ static mg_status validate(const mg_config* c, int* levels_out) {
       return fail(s, MG_ERR_NOT_COARSENABLE, "coarsest level has no interior node along axis %d", d);
   }
   *levels_out = L;
+  mg::Partition pt;
+  std::string perr;
+  mg_status ps = mg::compute_partition(c, L, &pt, &perr);
+  if (ps != MG_OK) return fail(s, ps, "%s", perr.c_str());
+  return MG_OK;
+}
+
+extern "C" mg_status mg_partition(const mg_config* cfg, int32_t level, int64_t* first_plane, int64_t* owned_planes,
+                                  int32_t* distributed, int32_t* halo) {
+  int L = 0;
+  mg_status st = validate(cfg, &L);
+  if (st != MG_OK) return st;
+  if (level < 0 || level >= L) return fail(nullptr, MG_ERR_INVALID, "level %d out of range", level);
+  mg::Partition pt;
+  std::string perr;
+  st = mg::compute_partition(cfg, L, &pt, &perr);
+  if (st != MG_OK) return fail(nullptr, st, "%s", perr.c_str());
+  const bool dist = pt.slab && level < pt.la;
+  if (first_plane) *first_plane = dist ? pt.a[level] : 0;
+  if (owned_planes) *owned_planes = dist ? pt.b[level] - pt.a[level] : pt.n[level] + 1;
+  if (distributed) *distributed = dist ? 1 : 0;
+  if (halo) *halo = dist ? pt.H : 0;
   return MG_OK;
 }
 
@@ -114,6 +139,7 @@ extern "C" mg_status mg_create(const mg_config* cfg, mg_solver** out) {
   int L = 0;
   mg_status st = validate(cfg, &L);
   if (st != MG_OK) return st;
+  if (cfg->nranks > 1 && !cfg->nccl_id) return fail(nullptr, MG_ERR_INVALID, "nranks > 1 needs nccl_id (ncclUniqueId)");
   int ndev = 0;
   cudaError_t ce = cudaGetDeviceCount(&ndev);
   if (ce != cudaSuccess || ndev == 0)
@@ -151,8 +177,8 @@ extern "C" mg_status mg_layout(const mg_solver* s, int64_t shape[3], int64_t* fi
   if (!s || !shape) return fail(nullptr, MG_ERR_INVALID, "NULL argument");
   const Level& lv = s->lv[0];
   for (int d = 0; d < 3; d++) shape[d] = lv.shape[d];
-  if (first) *first = 0;
-  if (owned) *owned = lv.shape[0];
+  if (first) *first = lv.dist ? s->pt.a[0] : 0;
+  if (owned) *owned = lv.dist ? s->pt.b[0] - s->pt.a[0] : lv.shape[0];
   return MG_OK;
 }
 
@@ -321,3 +347,12 @@ extern "C" int32_t mg_profile_read(mg_solver* s, int32_t cap, const char** names
 
 // used by plan.cu for error reporting
 mg_status mg::plan_fail(mg_solver* s, mg_status st, const char* msg) { return fail(s, st, "%s", msg); }
+
+extern "C" mg_status mg_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, MG_ERR_INVALID, "out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, MG_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  memcpy(out128, &id, sizeof id);
+  return MG_OK;
+}

@@ -25,7 +25,8 @@ int norm_num_partials(const Geom& g);
 template <typename T>
 cudaError_t launch_norm_partial(const Geom& g, const Coef<T>& c, const T* u, const T* f, double* partial,
                                 cudaStream_t st);
-cudaError_t launch_norm_final(const double* partial, int n, double* out, cudaStream_t st);
+cudaError_t launch_norm_final(const double* partial, int n, double* out, cudaStream_t st, bool take_sqrt = true);
+cudaError_t launch_norm_combine(const double* sums, int P, double* out, cudaStream_t st);
 
 // --- coarsest level direct solve (Cholesky factor computed once at setup) ---
 // A assembled from the stencil (interior unknowns, x fastest), factor L (m x m, row major)

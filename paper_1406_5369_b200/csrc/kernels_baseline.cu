@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(NB) k_norm_partial(Geom g, Coef<T> c, const T*
 }
 
 __global__ void __launch_bounds__(1024) k_norm_final(const double* __restrict__ partial, int n,
-                                                     double* __restrict__ out) {
+                                                     double* __restrict__ out, int take_sqrt) {
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += 1024) s = __dadd_rn(s, partial[i]);
   __shared__ double sh[32];
@@ -242,8 +242,16 @@ __global__ void __launch_bounds__(1024) k_norm_final(const double* __restrict__ 
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < 32; w++) t = __dadd_rn(t, sh[w]);
-    *out = __dsqrt_rn(t);
+    *out = take_sqrt ? __dsqrt_rn(t) : t;
   }
+}
+
+// sqrt of the rank sums added in rank order (identical on every rank)
+__global__ void k_norm_combine(const double* __restrict__ sums, int P, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double t = 0.0;
+  for (int p = 0; p < P; p++) t = __dadd_rn(t, sums[p]);
+  *out = __dsqrt_rn(t);
 }
 
 // ---- coarsest direct solve (Alg. 1 line 2; reading 3) ------------
@@ -376,7 +384,7 @@ cudaError_t launch_prolong_correct(const Geom& gf, const Geom& gc, const T* e, T
 }
 template <typename T>
 cudaError_t launch_copy_boundary(const Geom& g, const T* src, T* dst, cudaStream_t st) {
-  int nplanes = g.p_hi - g.p_lo + 2;  // local planes incl. the two outer ones
+  int nplanes = g.planes;
   k_copy_boundary<T><<<148 * 4, 256, 0, st>>>(g, src, dst, nplanes);
   return cudaGetLastError();
 }
@@ -394,8 +402,12 @@ cudaError_t launch_norm_partial(const Geom& g, const Coef<T>& c, const T* u, con
   k_norm_partial<T><<<nb, NB, 0, st>>>(g, c, u, f, partial);
   return cudaGetLastError();
 }
-cudaError_t launch_norm_final(const double* partial, int n, double* out, cudaStream_t st) {
-  k_norm_final<<<1, 1024, 0, st>>>(partial, n, out);
+cudaError_t launch_norm_final(const double* partial, int n, double* out, cudaStream_t st, bool take_sqrt) {
+  k_norm_final<<<1, 1024, 0, st>>>(partial, n, out, take_sqrt ? 1 : 0);
+  return cudaGetLastError();
+}
+cudaError_t launch_norm_combine(const double* sums, int P, double* out, cudaStream_t st) {
+  k_norm_combine<<<1, 32, 0, st>>>(sums, P, out);
   return cudaGetLastError();
 }
 cudaError_t launch_cholesky_factor(const Geom& g, double cx, double cy, double cz, double D, double* L, int m,
@@ -411,7 +423,7 @@ cudaError_t launch_coarse_direct(const Geom& g, double D, const double* L, int m
 }
 template <typename T>
 cudaError_t launch_workload_fill(const Geom& g, uint64_t seed, double lo, double hi, T* dst, cudaStream_t st) {
-  int nplanes = g.p_hi - g.p_lo + 2;
+  int nplanes = g.planes;
   long long q = (long long)nplanes * g.rows;
   dim3 blk(128, 2);
   dim3 grd((unsigned)((q + 1) / 2));

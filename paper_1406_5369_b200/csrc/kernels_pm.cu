@@ -497,7 +497,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 static CUresult encode(CUtensorMap* tm, const void* base, const Geom& g, int esz, int box_rows) {
   PFN_cuTensorMapEncodeTiled_v12000 cuTensorMapEncodeTiled = encode_fn();
   if (!cuTensorMapEncodeTiled) return CUDA_ERROR_NOT_FOUND;
-  cuuint64_t dims[3] = {(cuuint64_t)(g.nx + 1), (cuuint64_t)g.rows, (cuuint64_t)(g.p_hi + 1)};
+  cuuint64_t dims[3] = {(cuuint64_t)(g.nx + 1), (cuuint64_t)g.rows, (cuuint64_t)g.planes};
   cuuint64_t strides[2] = {(cuuint64_t)(g.pitch * esz), (cuuint64_t)(g.pstride * esz)};
   cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * (16 / esz)), (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};

@@ -34,6 +34,7 @@ struct Geom {
   int rows;           // rows per plane in memory (3D: ny+1, 2D: 1)
   int p_lo, p_hi;     // local planes holding interior nodes to update: [p_lo, p_hi)
   int p_glob0;        // global plane index of local plane 0
+  int planes;         // local planes in memory (incl. halo planes of a slab)
   long long pitch;    // elements between rows
   long long pstride;  // elements between planes
 };

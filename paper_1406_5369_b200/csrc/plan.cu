@@ -7,7 +7,10 @@
 #include <cstdio>
 #include <cstring>
 
+#include <nccl.h>
+
 #include "kernels.h"
+#include "partition.h"
 #include "kernels_pm.h"
 #include <cstdlib>
 #include "plan.h"
@@ -30,12 +33,15 @@ enum Kind {
   K_SWEEP_RBGS,
   K_SWEEP_JACOBI,
   K_RESID_RESTRICT,
+  K_HALO,
+  K_ALLGATHER,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
                                        "prolong_correct", "copy_boundary", "copy_interior", "norm_partial",
                                        "norm_final",    "coarse_direct", "memset",       "add_interior",
-                                       "rbgs_fused",    "jacobi_pm",     "resid_restrict"};
+                                       "rbgs_fused",    "jacobi_pm",     "resid_restrict",
+                                       "nccl_halo",     "nccl_allgather"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -60,7 +66,7 @@ static mg_status launch(mg_solver* s, cudaStream_t st, Kind kind, int level, dou
     cudaEventRecord(rec.b, st);
     s->prof.push_back(rec);
   }
-  if (kind != K_MEMSET) s->launch_counter++;  // kernels only
+  if (kind != K_MEMSET && kind != K_HALO && kind != K_ALLGATHER) s->launch_counter++;  // our kernels only
   if (e != cudaSuccess) return cuda_fail(s, e, kKindName[kind]);
   return MG_OK;
 }
@@ -113,6 +119,20 @@ mg_status plan_build(mg_solver* s) {
   }
   const int esz = (int)s->esz;
   const int64_t align = 128 / esz;
+  {
+    std::string perr;
+    mg_status ps = compute_partition(&c, s->L, &s->pt, &perr);
+    if (ps != MG_OK) return plan_fail(s, ps, perr.c_str());
+  }
+  if (c.nranks > 1) {  // NCCL communicator over NVLink (unique id broadcast by the caller)
+    ncclUniqueId id;
+    memcpy(&id, c.nccl_id, sizeof id);
+    ncclResult_t nr = ncclCommInitRank(&s->comm, c.nranks, id, c.rank);
+    if (nr != ncclSuccess) {
+      s->comm = nullptr;
+      return plan_fail(s, MG_ERR_NCCL, ncclGetErrorString(nr));
+    }
+  }
   s->lv.resize(s->L);
   for (int l = 0; l < s->L; l++) {
     Level& L = s->lv[l];
@@ -154,7 +174,23 @@ mg_status plan_build(mg_solver* s) {
     g.p_lo = 1;
     g.p_hi = g.nz;
     g.p_glob0 = 0;
-    L.shape[0] = g.nz + 1;
+    g.planes = g.nz + 1;
+    L.dist = s->pt.slab && l < s->pt.la;
+    if (L.dist) {  // slab: owned planes [a, b) + H halo planes on each side
+      const int H = s->pt.H;
+      const int a = (int)s->pt.a[l], b = (int)s->pt.b[l];
+      g.p_glob0 = a - H;
+      g.planes = (b - a) + 2 * H;
+      g.p_lo = H + (a == 0 ? 1 : 0);
+      g.p_hi = H + ((b < g.nz ? b : g.nz) - a);
+    }
+    L.gown = g;
+    if (s->pt.slab && l == s->pt.la) {  // first full level: this rank restricts into its own planes
+      const int a = (int)s->pt.a[l], b = (int)s->pt.b[l];
+      L.gown.p_lo = a > 1 ? a : 1;
+      L.gown.p_hi = b < g.nz ? b : g.nz;
+    }
+    L.shape[0] = g.planes;
     L.shape[1] = g.rows;
     L.shape[2] = g.pitch;
     L.elems = (size_t)L.shape[0] * L.shape[1] * L.shape[2];
@@ -185,6 +221,7 @@ mg_status plan_build(mg_solver* s) {
   s->n_partial_cap = np;
   if (cudaMalloc(&s->d_partial, sizeof(double) * np) != cudaSuccess ||
       cudaMalloc(&s->d_norm, sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&s->d_rank_sums, sizeof(double) * c.nranks) != cudaSuccess ||
       cudaMallocHost(&s->h_norm, sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     return plan_fail(s, MG_ERR_OOM, "allocation of norm buffers failed");
@@ -236,6 +273,8 @@ void plan_free(mg_solver* s) {
   cudaFree(s->d_work);
   cudaFree(s->d_partial);
   cudaFree(s->d_norm);
+  cudaFree(s->d_rank_sums);
+  if (s->comm) ncclCommDestroy(s->comm);
   if (s->h_norm) cudaFreeHost(s->h_norm);
   cudaFree(s->stage_u);
   cudaFree(s->stage_f);
@@ -263,11 +302,53 @@ struct Exec {
     return e ? atoi(e) : 0;
   }
 
+  static ncclDataType_t nccl_type() { return sizeof(T) == 8 ? ncclDouble : ncclFloat; }
+
+  // Slab halo exchange of a distributed level: my h top owned planes
+  // go to rank+1's lower halo, my h bottom owned planes to rank-1's upper halo.
+  mg_status exchange(int l, T* buf, int h) {
+    const Level& L = s->lv[l];
+    if (!L.dist || !s->comm) return MG_OK;
+    const int H = s->pt.H, P = s->pt.P, rk = s->pt.rank;
+    const size_t ps = (size_t)L.g.pstride;
+    const int owned = L.g.planes - 2 * H;
+    return launch(s, st, K_HALO, l, 2.0 * h * ps * sizeof(T), [&] {
+      ncclResult_t nr = ncclGroupStart();
+      if (rk < P - 1 && nr == ncclSuccess) {
+        nr = ncclSend(buf + (size_t)(H + owned - h) * ps, h * ps, nccl_type(), rk + 1, s->comm, st);
+        if (nr == ncclSuccess) nr = ncclRecv(buf + (size_t)(H + owned) * ps, h * ps, nccl_type(), rk + 1, s->comm, st);
+      }
+      if (rk > 0 && nr == ncclSuccess) {
+        nr = ncclSend(buf + (size_t)H * ps, h * ps, nccl_type(), rk - 1, s->comm, st);
+        if (nr == ncclSuccess) nr = ncclRecv(buf + (size_t)(H - h) * ps, h * ps, nccl_type(), rk - 1, s->comm, st);
+      }
+      ncclResult_t ne = ncclGroupEnd();
+      return (nr == ncclSuccess && ne == ncclSuccess) ? cudaSuccess : cudaErrorUnknown;
+    });
+  }
+
+  // Agglomeration: every rank restricted into its own planes of the full first
+  // undistributed level; all-gather the equal chunks (the top boundary plane stays 0).
+  mg_status allgather_level(int l, T* buf) {
+    const Level& L = s->lv[l];
+    if (!s->comm) return MG_OK;
+    const size_t ps = (size_t)L.g.pstride;
+    const size_t chunk = (size_t)(s->pt.n[l] / s->pt.P) * ps;
+    return launch(s, st, K_ALLGATHER, l, (double)chunk * s->pt.P * sizeof(T), [&] {
+      ncclResult_t nr = ncclAllGather(buf + (size_t)s->pt.rank * chunk, buf, chunk, nccl_type(), s->comm, st);
+      return nr == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+    });
+  }
+
   // one sweep; zero_in: the iterate is known to be 0 (first sweep after V_H(0,...))
   mg_status smooth(int l, T*& cur, T*& other, const T* f, bool zero_in = false) {
     const Level& L = s->lv[l];
     if (pm(l)) {
       const bool rb = s->cfg.smoother == MG_RBGS;
+      if (!zero_in) {
+        mg_status r = exchange(l, cur, rb ? 2 : 1);
+        if (r != MG_OK) return r;
+      }
       T* in = cur;
       T* out = other;
       mg_status r = launch(s, st, rb ? K_SWEEP_RBGS : K_SWEEP_JACOBI, l, (zero_in ? 2 : 3) * w(l), [&] {
@@ -281,13 +362,16 @@ struct Exec {
       if (r != MG_OK) return r;
     }
     if (s->cfg.smoother == MG_JACOBI) {
-      mg_status r = launch(s, st, K_JACOBI, l, 3 * w(l),
-                           [&] { return launch_jacobi<T>(L.g, coef(l), cur, f, other, st); });
+      mg_status r = exchange(l, cur, 1);
+      if (r != MG_OK) return r;
+      r = launch(s, st, K_JACOBI, l, 3 * w(l), [&] { return launch_jacobi<T>(L.g, coef(l), cur, f, other, st); });
       std::swap(cur, other);
       return r;
     }
     for (int colour = 0; colour < 2; colour++) {
-      mg_status r = launch(s, st, K_RBGS_COLOUR, l, 3 * w(l),
+      mg_status r = exchange(l, cur, 1);
+      if (r != MG_OK) return r;
+      r = launch(s, st, K_RBGS_COLOUR, l, 3 * w(l),
                            [&] { return launch_rbgs_colour<T>(L.g, coef(l), cur, f, colour, st); });
       if (r != MG_OK) return r;
     }
@@ -329,6 +413,8 @@ struct Exec {
       cur[l] = l == 0 ? u0 : (T*)s->lv[l].u;
       oth[l] = (T*)s->lv[l].t;
     }
+    // f is constant during the cycle: one halo exchange of level 0 (caller halo planes are scratch)
+    if ((r = exchange(0, const_cast<T*>(f0), 1)) != MG_OK) return r;
     if (Lv == 1) {
       // single-level hierarchy: solve in correction form (honours Dirichlet data)
       if (s->cfg.coarse == MG_COARSE_SWEEPS) {
@@ -359,20 +445,32 @@ struct Exec {
           if ((r = smooth(l, cur[l], oth[l], f, l > 0 && k == 0)) != MG_OK) return r;
         T* res = (T*)L.r;
         T* fc = (T*)s->lv[l + 1].f;
+        const Level& C = s->lv[l + 1];
+        // coarse planes this rank produces: all of a distributed or single-GPU level, its own
+        // chunk of the first agglomerated level
+        const Geom gcw = (s->pt.slab && l + 1 == s->pt.la) ? C.gown : C.g;
         if (pm(l)) {
+          if ((r = exchange(l, cur[l], 2)) != MG_OK) return r;
           const T* uc = cur[l];
           if ((r = launch(s, st, K_RESID_RESTRICT, l, 2 * w(l) + w(l + 1), [&] {
-                 return pm::launch_resid_restrict<T>(L.g, s->lv[l + 1].g, coef(l), uc, f, fc, zc(l + 1), st);
+                 return pm::launch_resid_restrict<T>(L.g, gcw, coef(l), uc, f, fc, zc(l + 1), st);
                })) != MG_OK)
             return r;
-          continue;
+        } else {
+          if ((r = exchange(l, cur[l], 1)) != MG_OK) return r;
+          if ((r = launch(s, st, K_RESIDUAL, l, 3 * w(l),
+                          [&] { return launch_residual<T>(L.g, coef(l), cur[l], f, res, st); })) != MG_OK)
+            return r;
+          if ((r = exchange(l, res, 1)) != MG_OK) return r;
+          if ((r = launch(s, st, K_RESTRICT, l, w(l) + w(l + 1),
+                          [&] { return launch_restrict<T>(L.g, gcw, res, fc, st); })) != MG_OK)
+            return r;
         }
-        if ((r = launch(s, st, K_RESIDUAL, l, 3 * w(l),
-                        [&] { return launch_residual<T>(L.g, coef(l), cur[l], f, res, st); })) != MG_OK)
-          return r;
-        if ((r = launch(s, st, K_RESTRICT, l, w(l) + w(l + 1),
-                        [&] { return launch_restrict<T>(L.g, s->lv[l + 1].g, res, fc, st); })) != MG_OK)
-          return r;
+        if (C.dist) {
+          if ((r = exchange(l + 1, fc, 1)) != MG_OK) return r;
+        } else if (s->pt.slab && l + 1 == s->pt.la) {
+          if ((r = allgather_level(l + 1, fc)) != MG_OK) return r;
+        }
       }
       // ---- coarsest level (Alg. 1 line 2)
       {
@@ -384,6 +482,7 @@ struct Exec {
       for (int l = Lv - 2; l >= 0; l--) {
         const Level& L = s->lv[l];
         const T* f = l == 0 ? f0 : (const T*)L.f;
+        if ((r = exchange(l + 1, cur[l + 1], 1)) != MG_OK) return r;  // e_H plane above (slabs)
         const T* e = cur[l + 1];
         const bool pml = pm(l);
         if ((r = launch(s, st, K_PROLONG, l, 2 * w(l) + w(l + 1), [&] {
@@ -416,8 +515,21 @@ struct Exec {
                  : launch_norm_partial<T>(L.g, coef(l), u, f, s->d_partial, st);
     });
     if (r != MG_OK) return r;
-    return launch(s, st, K_NORM_FINAL, l, 8.0 * np,
-                  [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });
+    if (!L.dist)
+      return launch(s, st, K_NORM_FINAL, l, 8.0 * np,
+                    [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });
+    // slabs: per-rank sum of r^2 -> all-gather -> summed in rank order (identical on every rank)
+    double* mine = s->d_rank_sums + s->pt.rank;
+    if ((r = launch(s, st, K_NORM_FINAL, l, 8.0 * np,
+                    [&] { return launch_norm_final(s->d_partial, np, mine, st, false); })) != MG_OK)
+      return r;
+    if (s->comm && (r = launch(s, st, K_ALLGATHER, l, 8.0 * s->pt.P, [&] {
+                      ncclResult_t nr = ncclAllGather(mine, s->d_rank_sums, 1, ncclDouble, s->comm, st);
+                      return nr == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
+                    })) != MG_OK)
+      return r;
+    return launch(s, st, K_NORM_FINAL, l, 8.0 * s->pt.P,
+                  [&] { return launch_norm_combine(s->d_rank_sums, s->pt.P, out_dev, st); });
   }
 };
 

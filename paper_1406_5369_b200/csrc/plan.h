@@ -9,11 +9,16 @@
 
 #include "mg.h"
 #include "mg_common.cuh"
+#include "partition.h"
+
+typedef struct ncclComm* ncclComm_t;
 
 namespace mg {
 
 struct Level {
   Geom g;
+  Geom gown;              // g restricted to the planes this rank writes when restricting into it
+  bool dist = false;      // slab-distributed level
   Coef<double> c64;
   Coef<float> c32;
   double cx, cy, cz, D;   // double-precision coefficients (coarse direct solve)
@@ -49,6 +54,10 @@ struct mg_solver {
   int m_coarse = 0;
   double* d_chol = nullptr;
   double* d_work = nullptr;
+  // slab decomposition / NCCL
+  mg::Partition pt;
+  ncclComm_t comm = nullptr;
+  double* d_rank_sums = nullptr;  // per-rank sums of r^2 (all-gathered)
   // norm
   double* d_partial = nullptr;
   int n_partial_cap = 0;

@@ -241,3 +241,32 @@ def test_schedule_variants_identical(variant):
             S.vcycle(du, df)
         outs.append(S.to_numpy(du))
     assert np.array_equal(outs[0], outs[1])
+
+
+SLAB_CASES = [
+    dict(dim=3, cells=(128, 128, 128), smoother="rbgs"),
+    dict(dim=3, cells=(64, 64, 64), smoother="jacobi", nu1=2, nu2=1),
+    dict(dim=2, cells=(64, 64), levels=5, smoother="jacobi"),
+    dict(dim=3, cells=(64, 64, 64), smoother="rbgs", dtype="f32"),
+]
+
+
+@pytest.mark.parametrize("case", SLAB_CASES, ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
+def test_slab_mode_single_rank(case):
+    """Slab layout (halo planes, p_glob0 != 0, agglomerated coarse levels, rank-sum norm)
+    on one GPU (MG_FLAG_SLAB, nranks = 1): bitwise identical to the oracle."""
+    import paper_1406_5369_b200 as mgb
+    dt = case.get("dtype", "f64")
+    S, O = make(**case, flags=mgb.FLAG_SLAB)
+    assert S.distributed and S.halo == 2
+    u, f = wl.workload("W1", case["dim"], case["cells"], seed=42, dtype=S.np_dtype)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    uo = u.copy()
+    for k in range(3):
+        S.vcycle(du, df)
+        O.vcycle_inplace(uo, f)
+        got = S.to_numpy(du)
+        assert relerr(got, uo) <= TOL[dt], (k, relerr(got, uo))
+        if dt == "f64":
+            assert np.array_equal(got, uo), ("expected bitwise equality", k)
+        assert abs(S.residual_norm(du, df) / O.norm(0, uo, f) - 1) <= 1e-12
