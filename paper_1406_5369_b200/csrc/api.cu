@@ -226,6 +226,40 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
   mg_status st = guard(s);
   if (st != MG_OK) return st;
   if (!u || !f || max_cycles < 0 || !(rtol >= 0.0)) return fail(s, MG_ERR_INVALID, "bad argument");
+  if (u == f) return fail(s, MG_ERR_INVALID, "u and f must not alias");
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (plan_can_split(s)) {
+    // pipelined driver loop: head(k) = first sweep of cycle k+1 into the ping-pong buffer
+    // + ||f - A u_k|| of its input; tail(k) = the rest of cycle k+1.  u holds u_k
+    // whenever a norm is read, so stopping after a head is exact.
+    const bool eager = (s->cfg.flags & MG_FLAG_NO_GRAPH) || s->prof_on;
+    auto part = [&](int p) { return eager ? plan_run_part(s, p, u, f, cs) : plan_graph_part(s, p, u, f, cs); };
+    auto read = [&](double* out) -> mg_status {
+      CK(cudaMemcpyAsync(s->h_norm, s->d_norm, sizeof(double), cudaMemcpyDeviceToHost, cs));
+      CK(cudaStreamSynchronize(cs));
+      *out = *s->h_norm;
+      return MG_OK;
+    };
+    double r0 = 0.0;
+    if ((st = part(1)) != MG_OK || (st = read(&r0)) != MG_OK) return st;
+    if (history) history[0] = r0;
+    if (!std::isfinite(r0)) return fail(s, MG_ERR_NONFINITE, "initial residual norm is not finite");
+    int k = 0;
+    while (k < max_cycles) {
+      if ((st = part(2)) != MG_OK) return st;
+      k++;
+      double rk = 0.0;
+      if ((st = part(1)) != MG_OK || (st = read(&rk)) != MG_OK) return st;
+      if (history) history[k] = rk;
+      if (!std::isfinite(rk)) {
+        if (cycles) *cycles = k;
+        return fail(s, MG_ERR_NONFINITE, "residual norm not finite after cycle %d (S:535)", k);
+      }
+      if (rk <= rtol * r0) break;
+    }
+    if (cycles) *cycles = k;
+    return MG_OK;
+  }
   double r0 = 0.0;
   st = mg_residual_norm(s, u, f, &r0, stream);
   if (st != MG_OK) return st;

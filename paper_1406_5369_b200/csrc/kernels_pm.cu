@@ -197,7 +197,10 @@ __device__ __forceinline__ void black_node(const Coef<T>& c, const T* P, const T
 
 // MODE 0: Jacobi sweep; 1: red-black GS sweep; 2: residual-norm partials (one
 // double per CTA in `partial`, fixed reduction tree: deterministic).
-template <typename T, int MODE, bool ZERO>
+// NRM (modes 0, 1): also accumulate ||f - A u_in||^2 partials of the sweep's INPUT
+// (the norm after the previous cycle comes for free with the next cycle's first
+// sweep: u and f are read anyway).
+template <typename T, int MODE, bool ZERO, bool NRM = false>
 __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     k_sweep3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f, Geom g,
               Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems,
@@ -217,7 +220,18 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
   const int fo = (ry + 1) * BX + 2 * lane + HX;  // f-box offset of (ox, oy)
   const int po = (ry + 1) * PX + 2 * lane + 1;    // PR offset of (ox, oy)
   uint32_t seq = 0;
-  double nsum = 0.0;  // MODE 2: this thread's sum of r^2
+  double nsum = 0.0;  // MODE 2 / NRM: this thread's sum of r^2
+  // r^2 of the pair at plane p from the registers u(p-1), u(p), u(p+1) and smem u(p), f(p)
+  auto acc_norm = [&](const T* U0, const T* F0, const Pair<T>& um, const Pair<T>& u0, const Pair<T>& up, bool ok0,
+                      bool ok1) {
+    const Pair<T> fp = ld_pair(F0 + fo);
+    const double r0 =
+        (double)sub(fp.x, apply_A(c, u0.x, S.u(U0, bo - 1), u0.y, S.u(U0, bo - BX), S.u(U0, bo + BX), um.x, up.x));
+    const double r1 = (double)sub(
+        fp.y, apply_A(c, u0.y, u0.x, S.u(U0, bo + 2), S.u(U0, bo + 1 - BX), S.u(U0, bo + 1 + BX), um.y, up.y));
+    if (ok0) nsum = __dadd_rn(nsum, __dmul_rn(r0, r0));
+    if (ok1) nsum = __dadd_rn(nsum, __dmul_rn(r1, r1));
+  };
   for (int k = blockIdx.x; k < nitems; k += gridDim.x) {
     int tile, pa, pb;
     item_of(k, ntiles, zc, g.p_lo, g.p_hi, tile, pa, pb);
@@ -281,6 +295,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         const int pgl = p + pg0;
         const bool pl_in = pgl >= 1 && pgl <= g.nz - 1;
         const int kr = (oy + pgl) & 1;  // warp uniform
+        if (NRM && p >= pa && p < pb) acc_norm(U0, F0, um, u0, up, in0, in1);
         const T pr0 = kr ? red_node<T, ZERO, 1>(S, U0, F0, PR, bo, fo, po, um, u0, up, pl_in && in1)
                          : red_node<T, ZERO, 0>(S, U0, F0, PR, bo, fo, po, um, u0, up, pl_in && in0);
         if (ring) {  // red ring node of plane p
@@ -322,14 +337,8 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         const T* U0 = R.U(N(p - 1));
         up = S.upair(R.U(N(p)), bo);
         const Pair<T> fp = ld_pair(R.F(N(p)) + fo);
-        if (MODE == 2) {  // r = f - A u, squares accumulated in FP64 (reading 11)
-          const double r0 = (double)sub(
-              fp.x, apply_A(c, u0.x, S.u(U0, bo - 1), u0.y, S.u(U0, bo - BX), S.u(U0, bo + BX), um.x, up.x));
-          const double r1 = (double)sub(
-              fp.y, apply_A(c, u0.y, u0.x, S.u(U0, bo + 2), S.u(U0, bo + 1 - BX), S.u(U0, bo + 1 + BX), um.y, up.y));
-          if (in0) nsum = __dadd_rn(nsum, __dmul_rn(r0, r0));
-          if (in1) nsum = __dadd_rn(nsum, __dmul_rn(r1, r1));
-        } else {
+        if (MODE == 2 || NRM) acc_norm(U0, R.F(N(p)), um, u0, up, in0, in1);  // r = f - A u, FP64 squares
+        if (MODE != 2) {
           const T v0 =
               relax(c, u0.x, S.u(U0, bo - 1), u0.y, S.u(U0, bo - BX), S.u(U0, bo + BX), um.x, up.x, fp.x);
           const T v1 =
@@ -348,7 +357,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     seq = N(qlast) + 1;
     __syncthreads();
   }
-  if (MODE == 2) {  // fixed-order block reduction -> one partial per CTA
+  if (MODE == 2 || NRM) {  // fixed-order block reduction -> one partial per CTA
     double* red = reinterpret_cast<double*>(sm);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nsum = __dadd_rn(nsum, __shfl_down_sync(0xffffffffu, nsum, o));
@@ -562,7 +571,7 @@ static int choose_zc(long long ntiles, int np, int resident, int halo) {
 
 template <typename T>
 cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
-                         int zc_override, cudaStream_t st) {
+                         int zc_override, cudaStream_t st, double* partial, int* npartial) {
   using G = Geo<T>;
   CUtensorMap tu, tf;
   CUresult e1 = encode(&tu, uin ? uin : f, g, sizeof(T), G::BYU), e2 = encode(&tf, f, g, sizeof(T), G::BYF);
@@ -577,13 +586,33 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
     const int nitems = ntiles * ((np + zc - 1) / zc);
     if (getenv("MG_DEBUG"))
       fprintf(stderr, "launch_sweep: resident=%d zc=%d nitems=%d smem=%d\n", resident, zc, nitems, G::SMEM);
-    kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, nullptr);
+    if (npartial) *npartial = nitems;
+    kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial);
   };
-  if (rbgs)
+  if (partial && !zero_in)
+    rbgs ? go(k_sweep3d<T, 1, false, true>) : go(k_sweep3d<T, 0, false, true>);
+  else if (rbgs)
     zero_in ? go(k_sweep3d<T, 1, true>) : go(k_sweep3d<T, 1, false>);
   else
     zero_in ? go(k_sweep3d<T, 0, true>) : go(k_sweep3d<T, 0, false>);
   return cudaGetLastError();
+}
+
+// upper bound of the partials launch_sweep(..., partial, ...) writes for a level
+template <typename T>
+int sweep_partials(const Geom& g, bool rbgs) {
+  using G = Geo<T>;
+  const int ntiles = ((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
+  const int np = g.p_hi - g.p_lo;
+  const int resident = rbgs ? prepare_kernel(k_sweep3d<T, 1, false, true>, G::SMEM)
+                            : prepare_kernel(k_sweep3d<T, 0, false, true>, G::SMEM);
+  int best = 0;
+  for (int halo : {2, 4}) {
+    const int zc = choose_zc(ntiles, np, resident, halo);
+    const int n = ntiles * ((np + zc - 1) / zc);
+    if (n > best) best = n;
+  }
+  return best;
 }
 
 template <typename T>
@@ -719,9 +748,11 @@ cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>&
 }
 
 template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool, const double*, const double*,
-                                          double*, bool, int, cudaStream_t);
+                                          double*, bool, int, cudaStream_t, double*, int*);
 template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
-                                         bool, int, cudaStream_t);
+                                         bool, int, cudaStream_t, double*, int*);
+template int sweep_partials<double>(const Geom&, bool);
+template int sweep_partials<float>(const Geom&, bool);
 template int norm_partials<double>(const Geom&);
 template int norm_partials<float>(const Geom&);
 template cudaError_t launch_norm<double>(const Geom&, const Coef<double>&, const double*, const double*, double*,

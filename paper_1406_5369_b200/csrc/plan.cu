@@ -35,13 +35,14 @@ enum Kind {
   K_RESID_RESTRICT,
   K_HALO,
   K_ALLGATHER,
+  K_SWEEP_NORM,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
                                        "prolong_correct", "copy_boundary", "copy_interior", "norm_partial",
                                        "norm_final",    "coarse_direct", "memset",       "add_interior",
                                        "rbgs_fused",    "jacobi_pm",     "resid_restrict",
-                                       "nccl_halo",     "nccl_allgather"};
+                                       "nccl_halo",     "nccl_allgather", "sweep+norm"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -217,6 +218,11 @@ mg_status plan_build(mg_solver* s) {
       a = s->esz == 8 ? pm::norm_partials<double>(s->lv[l].g) : pm::norm_partials<float>(s->lv[l].g);
       if (a > np) np = a;
     }
+  }
+  if (pm::supported(s->lv[0].g, 16)) {
+    const bool rb = c.smoother == MG_RBGS;
+    int a = s->esz == 8 ? pm::sweep_partials<double>(s->lv[0].g, rb) : pm::sweep_partials<float>(s->lv[0].g, rb);
+    if (a > np) np = a;
   }
   s->n_partial_cap = np;
   if (cudaMalloc(&s->d_partial, sizeof(double) * np) != cudaSuccess ||
@@ -398,23 +404,55 @@ struct Exec {
     });
   }
 
-  mg_status vcycle(T* u0, const T* f0) {
-    const int Lv = s->L;
+  // The cycle can be split into a HEAD (boundary refresh, f halo, first pre-sweep of
+  // level 0 with the residual norm of its input accumulated on the fly) and a TAIL
+  // (the rest).  mg_solve pipelines tail(k) + head(k+1): the norm after cycle k is
+  // computed by the next cycle's first sweep, which reads u and f anyway.
+  bool can_split() const { return s->L > 1 && s->cfg.nu1 >= 1 && pm(0); }
+
+  mg_status cycle_start(T* u0, const T* f0) {
     const bool jac = s->cfg.smoother == MG_JACOBI;
-    std::vector<T*> cur(Lv), oth(Lv);
     mg_status r;
-    // Jacobi ping-pongs between u and t: t's boundary must hold u's Dirichlet data
-    if ((jac || pm(0)) && (s->cfg.nu1 + s->cfg.nu2 > 0 || Lv == 1)) {
+    // ping-pong partners: t's boundary must hold u's Dirichlet data
+    if ((jac || pm(0)) && (s->cfg.nu1 + s->cfg.nu2 > 0 || s->L == 1)) {
       r = launch(s, st, K_COPY_BOUNDARY, 0, 0,
                  [&] { return launch_copy_boundary<T>(s->lv[0].g, u0, (T*)s->lv[0].t, st); });
       if (r != MG_OK) return r;
     }
+    // f is constant during the cycle: one halo exchange of level 0 (caller halo planes are scratch)
+    return exchange(0, const_cast<T*>(f0), 1);
+  }
+
+  // head: cycle_start + the first level-0 sweep u0 -> t0 + ||f - A u0|| into out_dev
+  mg_status head(T* u0, const T* f0, double* out_dev) {
+    mg_status r = cycle_start(u0, f0);
+    if (r != MG_OK) return r;
+    if ((r = exchange(0, u0, s->cfg.smoother == MG_RBGS ? 2 : 1)) != MG_OK) return r;
+    const Level& L = s->lv[0];
+    const bool rb = s->cfg.smoother == MG_RBGS;
+    int np = 0;
+    T* t0 = (T*)L.t;
+    if ((r = launch(s, st, K_SWEEP_NORM, 0, 3 * w(0), [&] {
+           return pm::launch_sweep<T>(L.g, coef(0), rb, u0, f0, t0, false, zc(0), st, s->d_partial, &np);
+         })) != MG_OK)
+      return r;
+    return norm_finish(0, np, out_dev);
+  }
+
+  mg_status vcycle(T* u0, const T* f0) { return vcycle_impl(u0, f0, false); }
+  mg_status tail(T* u0, const T* f0) { return vcycle_impl(u0, f0, true); }
+
+  // after_head: the head already ran (first level-0 sweep result is in t0)
+  mg_status vcycle_impl(T* u0, const T* f0, bool after_head) {
+    const int Lv = s->L;
+    std::vector<T*> cur(Lv), oth(Lv);
+    mg_status r;
+    if (!after_head && (r = cycle_start(u0, f0)) != MG_OK) return r;
     for (int l = 0; l < Lv; l++) {
       cur[l] = l == 0 ? u0 : (T*)s->lv[l].u;
       oth[l] = (T*)s->lv[l].t;
     }
-    // f is constant during the cycle: one halo exchange of level 0 (caller halo planes are scratch)
-    if ((r = exchange(0, const_cast<T*>(f0), 1)) != MG_OK) return r;
+    if (after_head) std::swap(cur[0], oth[0]);
     if (Lv == 1) {
       // single-level hierarchy: solve in correction form (honours Dirichlet data)
       if (s->cfg.coarse == MG_COARSE_SWEEPS) {
@@ -441,7 +479,7 @@ struct Exec {
         const T* f = l == 0 ? f0 : (const T*)L.f;
         // V_H(0, ...): the zero guess is folded into the first sweep (bitwise identical)
         if (l > 0 && s->cfg.nu1 == 0 && (r = memset0(l, cur[l])) != MG_OK) return r;
-        for (int k = 0; k < s->cfg.nu1; k++)
+        for (int k = (after_head && l == 0) ? 1 : 0; k < s->cfg.nu1; k++)
           if ((r = smooth(l, cur[l], oth[l], f, l > 0 && k == 0)) != MG_OK) return r;
         T* res = (T*)L.r;
         T* fc = (T*)s->lv[l + 1].f;
@@ -515,6 +553,13 @@ struct Exec {
                  : launch_norm_partial<T>(L.g, coef(l), u, f, s->d_partial, st);
     });
     if (r != MG_OK) return r;
+    return norm_finish(l, np, out_dev);
+  }
+
+  // partials (np doubles in d_partial) -> ||r|| in out_dev (rank sums all-gathered on slabs)
+  mg_status norm_finish(int l, int np, double* out_dev) {
+    const Level& L = s->lv[l];
+    mg_status r;
     if (!L.dist)
       return launch(s, st, K_NORM_FINAL, l, 8.0 * np,
                     [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });
@@ -543,25 +588,38 @@ const Coef<float>& Exec<float>::coef(int l) const {
 }
 
 // ---------------------------------------------------------------- entry points
-mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st) {
+// part: 0 whole cycle, 1 head (first sweep + norm of the input into d_norm), 2 tail
+template <typename T>
+static mg_status run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
+  Exec<T> x{s, st};
+  if (part == 1) return x.head((T*)u, (const T*)f, s->d_norm);
+  if (part == 2) return x.tail((T*)u, (const T*)f);
+  return x.vcycle((T*)u, (const T*)f);
+}
+
+mg_status plan_run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
   s->launch_counter = 0;
-  mg_status r;
-  if (s->esz == 8)
-    r = Exec<double>{s, st}.vcycle((double*)u, (const double*)f);
-  else
-    r = Exec<float>{s, st}.vcycle((float*)u, (const float*)f);
-  s->launches_per_cycle = s->launch_counter;
+  mg_status r = s->esz == 8 ? run_part<double>(s, part, u, f, st) : run_part<float>(s, part, u, f, st);
+  if (part == 0) s->launches_per_cycle = s->launch_counter;
   return r;
 }
 
-mg_status plan_graph_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st) {
-  auto key = std::make_pair(u, f);
+mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st) {
+  return plan_run_part(s, 0, u, f, st);
+}
+
+bool plan_can_split(mg_solver* s) {
+  return s->esz == 8 ? Exec<double>{s, 0}.can_split() : Exec<float>{s, 0}.can_split();
+}
+
+mg_status plan_graph_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
+  auto key = std::make_tuple(u, f, part);
   auto it = s->graphs.find(key);
   if (it == s->graphs.end()) {
     cudaGraph_t graph;
     cudaError_t e = cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamBeginCapture");
-    mg_status r = plan_run_vcycle(s, u, f, s->cap_stream);
+    mg_status r = plan_run_part(s, part, u, f, s->cap_stream);
     e = cudaStreamEndCapture(s->cap_stream, &graph);
     if (r != MG_OK) return r;
     if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamEndCapture");
@@ -578,6 +636,10 @@ mg_status plan_graph_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t s
   cudaError_t e = cudaGraphLaunch(it->second, st);
   if (e != cudaSuccess) return cuda_fail(s, e, "cudaGraphLaunch");
   return MG_OK;
+}
+
+mg_status plan_graph_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st) {
+  return plan_graph_part(s, 0, u, f, st);
 }
 
 mg_status plan_norm(mg_solver* s, int level, const void* u, const void* f, double* out, cudaStream_t st, bool sync) {

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <tuple>
 #include <string>
 #include <utility>
 #include <vector>
@@ -65,7 +66,7 @@ struct mg_solver {
   double* h_norm = nullptr;  // pinned
   // graphs keyed by (u, f)
   cudaStream_t cap_stream = nullptr;
-  std::map<std::pair<void*, const void*>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<void*, const void*, int>, cudaGraphExec_t> graphs;  // (u, f, part)
   // e2e staging
   void* stage_u = nullptr;
   void* stage_f = nullptr;
@@ -86,6 +87,10 @@ mg_status plan_build(mg_solver* s);
 void plan_free(mg_solver* s);
 mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st);
 mg_status plan_graph_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st);
+// part: 0 whole cycle, 1 head (first sweep + input norm -> d_norm), 2 tail
+mg_status plan_run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st);
+mg_status plan_graph_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st);
+bool plan_can_split(mg_solver* s);
 mg_status plan_norm(mg_solver* s, int level, const void* u, const void* f, double* out, cudaStream_t st, bool sync);
 mg_status plan_op_smooth(mg_solver* s, int level, const void* uin, const void* f, void* uout, cudaStream_t st);
 mg_status plan_op_residual(mg_solver* s, int level, const void* u, const void* f, void* r, cudaStream_t st);
