@@ -36,8 +36,12 @@
 namespace mg {
 namespace pm {
 
-constexpr int TX = 64, TY = 8;     // output tile (fine nodes) per CTA and plane
-constexpr int NT = (TX / 2) * TY;  // 256 threads: one x-pair each, one warp per row
+#ifndef MG_PM_TY
+#define MG_PM_TY 16
+#endif
+constexpr int TX = 64, TY = MG_PM_TY;  // output tile (fine nodes) per CTA and plane
+constexpr int NT = (TX / 2) * TY;      // one thread per x-pair, one warp per tile row
+constexpr int RCOL = TY / 2;           // red ring nodes per ring column and plane
 constexpr int PX = TX + 2, PY = TY + 2;  // PR / r planes: tile + 1-node ring
 
 __host__ __device__ constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
@@ -54,8 +58,9 @@ struct Geo {
   static constexpr int UB = rup(BX * BYU * (int)sizeof(T), 128);
   static constexpr int FB = rup(BX * BYF * (int)sizeof(T), 128);
   static constexpr int PB = rup(PX * PY * (int)sizeof(T), 128);
-  static constexpr int NS = 4;                       // step slots (power of two): 2 steps in flight
-  static constexpr int MINB = sizeof(T) == 8 ? 3 : 6;  // resident CTAs per SM
+  static constexpr int NS = 4;  // step slots (power of two): 2 steps in flight
+  // resident CTAs per SM (registers / shared memory)
+  static constexpr int MINB = TY == 8 ? (sizeof(T) == 8 ? 3 : 6) : (sizeof(T) == 8 ? 2 : 3);
   static constexpr int SMEM = NS * (UB + FB) + 2 * PB + NS * 8;
 };
 
@@ -251,15 +256,15 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     R.wait(N(qlo + 1));
     Pair<T> um = S.upair(R.U(N(qlo)), bo), u0 = S.upair(R.U(N(qlo + 1)), bo), up;
     T rzm = (T)0;  // RB ring thread: u(p-1) at its plane-p ring node
-    if (RB && (ry < 2 || (ry == 2 && lane < 8))) {
+    if (RB && (ry < 2 || (ry == 2 && lane < 2 * RCOL))) {
       const int pgl = pa - 1 + pg0;
       int x, y;
       if (ry < 2) {
         y = ry == 0 ? y0 - 1 : y0 + TY;
         x = x0 + 2 * lane + ((y + pgl) & 1);
       } else {
-        x = lane < 4 ? x0 - 1 : x0 + TX;
-        y = y0 + 2 * (lane & 3) + ((x + y0 + pgl) & 1);
+        x = lane < RCOL ? x0 - 1 : x0 + TX;
+        y = y0 + 2 * (lane % RCOL) + ((x + y0 + pgl) & 1);
       }
       rzm = S.u(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
     }
@@ -269,19 +274,19 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
       R.issue(N(qlo + G::NS), &tm_u, &tm_f, x0, y0, qlo + G::NS + 1, qlo + G::NS, !ZERO);
     }
     if (RB) {
-      // ring threads: warp 0 top row (y0-1), warp 1 bottom row (y0+TY), warp 2 lanes 0-3 left column
-      // (x0-1), lanes 4-7 right column (x0+TX); each computes the red ring node of its slot
-      const bool ring = ry < 2 || (ry == 2 && lane < 8);
+      // ring threads: warp 0 top row (y0-1), warp 1 bottom row (y0+TY), warp 2 lanes [0,RCOL) left column
+      // (x0-1), lanes [RCOL,2 RCOL) right column (x0+TX); each computes the red ring node of its slot
+      const bool ring = ry < 2 || (ry == 2 && lane < 2 * RCOL);
       auto ring_pos = [&](int pgl, int& x, int& y) {
         if (ry < 2) {
           y = ry == 0 ? y0 - 1 : y0 + TY;
           x = x0 + 2 * lane + ((y + pgl) & 1);  // x0 even
-        } else if (lane < 4) {
+        } else if (lane < RCOL) {
           x = x0 - 1;
           y = y0 + 2 * lane + ((x + y0 + pgl) & 1);
         } else {
           x = x0 + TX;
-          y = y0 + 2 * (lane - 4) + ((x + y0 + pgl) & 1);
+          y = y0 + 2 * (lane - RCOL) + ((x + y0 + pgl) & 1);
         }
       };
       T pr1 = (T)0, pr2 = (T)0;  // own red value of planes p-1, p-2
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     const bool rin = oy >= 1 && oy <= gf.ny - 1;
     const bool in0 = rin && ox >= 1 && ox <= gf.nx - 1;
     const bool in1 = rin && ox + 1 <= gf.nx - 1;
-    // low-side ring: row y0-1 for x in [x0-1, x0+TX-1] (65 nodes), column x0-1 for y in [y0, y0+TY-1] (8)
+    // low-side ring: row y0-1 for x in [x0-1, x0+TX-1] (65 nodes), column x0-1 for y in [y0, y0+TY-1] (TY)
     const bool has_ring = tid < TX + 1 + TY;
     const int rx = tid < TX + 1 ? x0 - 1 + tid : x0 - 1;
     const int ryy = tid < TX + 1 ? y0 - 1 : y0 + tid - (TX + 1);
