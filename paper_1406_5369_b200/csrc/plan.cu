@@ -12,6 +12,7 @@
 #include "kernels.h"
 #include "partition.h"
 #include "kernels_pm.h"
+#include "kernels_tail.h"
 #include <cstdlib>
 #include "plan.h"
 
@@ -36,13 +37,15 @@ enum Kind {
   K_HALO,
   K_ALLGATHER,
   K_SWEEP_NORM,
+  K_TAIL,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
                                        "prolong_correct", "copy_boundary", "copy_interior", "norm_partial",
                                        "norm_final",    "coarse_direct", "memset",       "add_interior",
                                        "rbgs_fused",    "jacobi_pm",     "resid_restrict",
-                                       "nccl_halo",     "nccl_allgather", "sweep+norm"};
+                                       "nccl_halo",     "nccl_allgather", "sweep+norm",
+                                       "coarse_tail"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -302,6 +305,46 @@ struct Exec {
   bool pm(int l) const {
     return !(s->cfg.flags & MG_FLAG_BASELINE) && pm::supported(s->lv[l].g, s->cfg.pm_min_nx ? s->cfg.pm_min_nx : 128);
   }
+  // First level of the single-CTA coarse tail (levels >= lt run in one launch): the
+  // first non-distributed level whose interior has <= 48K nodes.  L if none / disabled.
+  int tail_level() const {
+    if (s->cfg.flags & MG_FLAG_BASELINE) return s->L;
+    const int first = s->pt.slab ? s->pt.la : 0;
+    for (int l = first; l < s->L; l++) {
+      const Geom& g = s->lv[l].g;
+      const long long n = (long long)(g.nx - 1) * (g.three_d ? g.ny - 1 : 1) * (g.nz - 1);
+      if (n <= 48 * 1024 && s->L - l <= kTailMax && (l > 0 || s->L > 1)) return l;
+    }
+    return s->L;
+  }
+
+  mg_status run_tail(int lt, T* u_top, const T* f_top) {
+    TailParams<T> P{};
+    P.nl = s->L - lt;
+    P.rbgs = s->cfg.smoother == MG_RBGS;
+    P.nu1 = s->cfg.nu1;
+    P.nu2 = s->cfg.nu2;
+    P.sweeps = s->cfg.coarse == MG_COARSE_SWEEPS;
+    P.ncoarse = s->cfg.ncoarse;
+    P.zero_first = lt > 0;
+    P.m = s->m_coarse;
+    P.D_coarse = s->lv[s->L - 1].D;
+    P.chol = s->d_chol;
+    P.work = s->d_work;
+    for (int k = 0; k < P.nl; k++) {
+      const Level& L = s->lv[lt + k];
+      P.g[k] = L.g;
+      P.c[k] = coef(lt + k);
+      P.u[k] = k == 0 ? u_top : (T*)L.u;
+      P.f[k] = k == 0 ? const_cast<T*>(f_top) : (T*)L.f;
+      P.t[k] = (T*)L.t;
+      P.r[k] = (T*)L.r;
+    }
+    double bytes = 0;
+    for (int k = 0; k < P.nl; k++) bytes += w(lt + k) * (3.0 * (P.nu1 + P.nu2) + 6.0);
+    return launch(s, st, K_TAIL, lt, bytes, [&] { return launch_tail<T>(P, st); });
+  }
+
   // z-chunk override for tuning (MG_ZC); 0 = the launcher's own choice
   int zc(int) const {
     const char* e = getenv("MG_ZC");
@@ -453,6 +496,8 @@ struct Exec {
       oth[l] = (T*)s->lv[l].t;
     }
     if (after_head) std::swap(cur[0], oth[0]);
+    const int lt = tail_level();
+    if (lt == 0) return run_tail(0, u0, f0);  // small grid: the whole cycle in one launch
     if (Lv == 1) {
       // single-level hierarchy: solve in correction form (honours Dirichlet data)
       if (s->cfg.coarse == MG_COARSE_SWEEPS) {
@@ -474,7 +519,7 @@ struct Exec {
       }
     } else {
       // ---- descend: pre-smooth, residual, restrict (Alg. 1 lines 3-5)
-      for (int l = 0; l < Lv - 1; l++) {
+      for (int l = 0; l < Lv - 1 && l < lt; l++) {
         const Level& L = s->lv[l];
         const T* f = l == 0 ? f0 : (const T*)L.f;
         // V_H(0, ...): the zero guess is folded into the first sweep (bitwise identical)
@@ -510,14 +555,18 @@ struct Exec {
           if ((r = allgather_level(l + 1, fc)) != MG_OK) return r;
         }
       }
-      // ---- coarsest level (Alg. 1 line 2)
-      {
+      if (lt < Lv) {
+        // ---- levels lt..L-1: V_lt(0, f_lt) in one single-CTA launch (kernels_tail.cu)
+        if ((r = run_tail(lt, (T*)s->lv[lt].u, (const T*)s->lv[lt].f)) != MG_OK) return r;
+        cur[lt] = (T*)s->lv[lt].u;
+      } else {
+        // ---- coarsest level (Alg. 1 line 2)
         int l = Lv - 1;
         if (s->cfg.coarse == MG_COARSE_SWEEPS && (r = memset0(l, cur[l])) != MG_OK) return r;
         if ((r = coarse(cur[l], (const T*)s->lv[l].f, cur[l], oth[l])) != MG_OK) return r;
       }
       // ---- ascend: prolongate + correct, post-smooth (Alg. 1 lines 6-7)
-      for (int l = Lv - 2; l >= 0; l--) {
+      for (int l = (lt < Lv ? lt : Lv - 1) - 1; l >= 0; l--) {
         const Level& L = s->lv[l];
         const T* f = l == 0 ? f0 : (const T*)L.f;
         if ((r = exchange(l + 1, cur[l + 1], 1)) != MG_OK) return r;  // e_H plane above (slabs)
