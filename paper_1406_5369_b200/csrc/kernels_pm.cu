@@ -29,6 +29,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "kernels_pm.h"
 #include "tma.cuh"
@@ -62,6 +63,13 @@ struct Geo {
   // resident CTAs per SM (registers / shared memory)
   static constexpr int MINB = TY == 8 ? (sizeof(T) == 8 ? 3 : 6) : (sizeof(T) == 8 ? 2 : 3);
   static constexpr int SMEM = NS * (UB + FB) + 2 * PB + NS * 8;
+  // coarse boxes of the fused prolongation (CORR): x from X0 - 16/sizeof(T), y from Y0 - 1
+  static constexpr int CHX = 16 / (int)sizeof(T);
+  static constexpr int CBX = rup(TX / 2 + 2 + CHX, CHX);  // 36 (FP64) / 40 (FP32)
+  static constexpr int CBY = TY / 2 + 3;
+  static constexpr int CB = rup(CBX * CBY * (int)sizeof(T), 128);
+  static constexpr int COFF = rup(SMEM, 128);  // coarse ring (3 slots) after the barriers
+  static constexpr int SMEM_CORR = COFF + 3 * CB;
 };
 
 template <typename T>
@@ -205,11 +213,17 @@ __device__ __forceinline__ void black_node(const Coef<T>& c, const T* P, const T
 // NRM (modes 0, 1): also accumulate ||f - A u_in||^2 partials of the sweep's INPUT
 // (the norm after the previous cycle comes for free with the next cycle's first
 // sweep: u and f are read anyway).
-template <typename T, int MODE, bool ZERO, bool NRM = false>
+// CORR (modes 0, 1): the sweep's input is u + P e (Alg. 1 line 6), the
+// coarse-grid correction applied to every u box in shared memory as it arrives, so
+// the corrected iterate never makes an HBM round trip (prolongation fused into the
+// first post-smoothing sweep).  Same separable order as k_prolong3d.
+constexpr int NRING_CORR = 4 * (TX + 4) + 4 * TY;  // box nodes outside the tile that are read
+
+template <typename T, int MODE, bool ZERO, bool NRM = false, bool CORR = false>
 __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     k_sweep3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f, Geom g,
               Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems,
-              double* __restrict__ partial) {
+              double* __restrict__ partial, const __grid_constant__ CUtensorMap tm_e, Geom gc) {
   constexpr bool RB = MODE == 1;
   extern __shared__ __align__(128) unsigned char sm[];
   using G = Geo<T>;
@@ -250,10 +264,102 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     const int qlo = RB ? pa - 3 : pa - 2, qlast = RB ? pb : pb - 1;
     const uint32_t nlo = seq;
     auto N = [&](int q) { return nlo + (uint32_t)(q - qlo); };
+    // CORR: coarse plane K lives in coarse slot K % 3; step q (fine u plane z = q+1) also
+    // loads coarse plane (z+1)/2 when z is odd (first needed there), the first step also
+    // z/2 (TMA, zero-filled outside the coarse array)
+    const int X0c = x0 / 2, Y0c = y0 / 2;
+    auto Cs = [&](int K) -> T* {
+      return reinterpret_cast<T*>(sm + G::COFF + (size_t)(((K % 3) + 3) % 3) * G::CB);
+    };
+    auto issue_step = [&](int q) {  // thread 0
+      if (CORR) {
+        uint64_t* bar = &R.full[N(q) % G::NS];
+        const int zg = q + 1 + pg0;
+        auto ld = [&](int K) {
+          mbar_add_tx(bar, (uint32_t)(G::CBX * G::CBY * sizeof(T)));
+          tma_load_3d(Cs(K), &tm_e, X0c - G::CHX, Y0c - 1, K - gc.p_glob0, bar);
+        };
+        if (q == qlo) ld(zg >> 1);
+        if (zg & 1) ld((zg + 1) >> 1);
+      }
+      R.issue(N(q), &tm_u, &tm_f, x0, y0, q + 1, q, !ZERO);
+    };
     if (tid == 0)
-      for (int q = qlo; q < qlo + G::NS && q <= qlast; q++) R.issue(N(q), &tm_u, &tm_f, x0, y0, q + 1, q, !ZERO);
+      for (int q = qlo; q < qlo + G::NS && q <= qlast; q++) issue_step(q);
+    // ---- CORR: u += P e on the u box of fine local plane zl (in smem, right after its arrival)
+    const T half = (T)0.5;
+    int cZ = -1000000;
+    Pair<T> cA{0, 0}, cB{0, 0};
+    bool cHaveB = false;
+    auto e_at = [&](int X, int Y, int Zg) -> T {
+      return Cs(Zg)[(Y - Y0c + 1) * G::CBX + (X - X0c + G::CHX)];
+    };
+    auto Vpair = [&](int Zg) -> Pair<T> {  // pair (2X, 2X+1) of row oy after the x- and y-interpolation
+      const int X = ox >> 1, Y = oy >> 1;
+      const T a0 = e_at(X, Y, Zg), a1 = e_at(X + 1, Y, Zg);
+      Pair<T> v{a0, mul(half, add(a0, a1))};
+      if (oy & 1) {
+        const T b0 = e_at(X, Y + 1, Zg), b1 = e_at(X + 1, Y + 1, Zg);
+        v = Pair<T>{mul(half, add(v.x, b0)), mul(half, add(v.y, mul(half, add(b0, b1))))};
+      }
+      return v;
+    };
+    auto interp = [&](int x, int y, int zg) -> T {  // single node, reading 13 order
+      const int X = x >> 1, dx = x & 1, Y = y >> 1, dy = y & 1, Z = zg >> 1, dz = zg & 1;
+      T vy[2];
+      for (int zz = 0; zz <= dz; zz++) {
+        T vx[2];
+        for (int yy = 0; yy <= dy; yy++)
+          vx[yy] = dx ? mul(half, add(e_at(X, Y + yy, Z + zz), e_at(X + 1, Y + yy, Z + zz))) : e_at(X, Y + yy, Z + zz);
+        vy[zz] = dy ? mul(half, add(vx[0], vx[1])) : vx[0];
+      }
+      return dz ? mul(half, add(vy[0], vy[1])) : vy[0];
+    };
+    auto correct = [&](T* Ub, int zl) {
+      const int zg = zl + pg0;
+      if (zg < 1 || zg > g.nz - 1) return;  // boundary / outside planes: no correction
+      if (in0 || in1) {
+        if ((zg >> 1) != cZ) {
+          cA = (cHaveB && (zg >> 1) == cZ + 1) ? cB : Vpair(zg >> 1);
+          cZ = zg >> 1;
+          cHaveB = false;
+        }
+        Pair<T> v = cA;
+        if (zg & 1) {
+          if (!cHaveB) {
+            cB = Vpair(cZ + 1);
+            cHaveB = true;
+          }
+          v = Pair<T>{mul(half, add(cA.x, cB.x)), mul(half, add(cA.y, cB.y))};
+        }
+        T* up_ = Ub + bo;
+        if (in0) up_[0] = add(up_[0], v.x);
+        if (in1) up_[1] = add(up_[1], v.y);
+      }
+      if (tid < NRING_CORR) {  // box nodes around the tile that the stencils read
+        int x, y;
+        if (tid < 4 * (TX + 4)) {
+          const int rr = tid / (TX + 4);
+          y = rr < 2 ? y0 - 2 + rr : y0 + TY + rr - 2;
+          x = x0 - 2 + tid % (TX + 4);
+        } else {
+          const int t2 = tid - 4 * (TX + 4), cc = t2 / TY;
+          x = cc < 2 ? x0 - 2 + cc : x0 + TX + cc - 2;
+          y = y0 + t2 % TY;
+        }
+        if (x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1) {
+          T* q = Ub + (y - y0 + 2) * BX + (x - x0 + HX);
+          *q = add(*q, interp(x, y, zg));
+        }
+      }
+    };
     R.wait(N(qlo));
     R.wait(N(qlo + 1));
+    if (CORR) {
+      correct(R.U(N(qlo)), qlo + 1);
+      correct(R.U(N(qlo + 1)), qlo + 2);
+      __syncthreads();
+    }
     Pair<T> um = S.upair(R.U(N(qlo)), bo), u0 = S.upair(R.U(N(qlo + 1)), bo), up;
     T rzm = (T)0;  // RB ring thread: u(p-1) at its plane-p ring node
     if (RB && (ry < 2 || (ry == 2 && lane < 2 * RCOL))) {
@@ -271,7 +377,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     __syncthreads();  // step qlo lives on in registers only: refill its slot
     if (tid == 0 && qlo + G::NS <= qlast) {
       fence_proxy_async();
-      R.issue(N(qlo + G::NS), &tm_u, &tm_f, x0, y0, qlo + G::NS + 1, qlo + G::NS, !ZERO);
+      issue_step(qlo + G::NS);
     }
     if (RB) {
       // ring threads: warp 0 top row (y0-1), warp 1 bottom row (y0+TY), warp 2 lanes [0,RCOL) left column
@@ -292,6 +398,10 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
       T pr1 = (T)0, pr2 = (T)0;  // own red value of planes p-1, p-2
       for (int p = pa - 1; p <= pb; p++) {
         R.wait(N(p));
+        if (CORR) {
+          correct(R.U(N(p)), p + 1);
+          __syncthreads();
+        }
         const T* U0 = R.U(N(p - 1));  // u(p)
         const T* Up = R.U(N(p));      // u(p+1)
         const T* F0 = R.F(N(p));      // f(p)
@@ -329,7 +439,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         __syncthreads();
         if (tid == 0 && p - 1 + G::NS <= qlast) {  // step p-1 (u(p), f(p-1)) is consumed
           fence_proxy_async();
-          R.issue(N(p - 1 + G::NS), &tm_u, &tm_f, x0, y0, p + G::NS, p - 1 + G::NS, !ZERO);
+          issue_step(p - 1 + G::NS);
         }
         um = u0;
         u0 = up;
@@ -339,6 +449,10 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     } else {
       for (int p = pa; p < pb; p++) {
         R.wait(N(p));
+        if (CORR) {
+          correct(R.U(N(p)), p + 1);
+          __syncthreads();
+        }
         const T* U0 = R.U(N(p - 1));
         up = S.upair(R.U(N(p)), bo);
         const Pair<T> fp = ld_pair(R.F(N(p)) + fo);
@@ -353,7 +467,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         __syncthreads();
         if (tid == 0 && p - 1 + G::NS <= qlast) {
           fence_proxy_async();
-          R.issue(N(p - 1 + G::NS), &tm_u, &tm_f, x0, y0, p + G::NS, p - 1 + G::NS, !ZERO);
+          issue_step(p - 1 + G::NS);
         }
         um = u0;
         u0 = up;
@@ -525,6 +639,19 @@ static CUresult encode(CUtensorMap* tm, const void* base, const Geom& g, int esz
 // per-plane barrier latency: measured, a 65^3 level is 2x slower marched than
 // with the one-thread-per-node kernels, 129^3 is ~1.5x faster.  The plan passes
 // mg_config.pm_min_nx (default 128; tests lower it to cover small grids).
+static CUresult encode_coarse(CUtensorMap* tm, const void* base, const Geom& g, int esz, int box_x, int box_y) {
+  PFN_cuTensorMapEncodeTiled_v12000 cuTensorMapEncodeTiled = encode_fn();
+  if (!cuTensorMapEncodeTiled) return CUDA_ERROR_NOT_FOUND;
+  cuuint64_t dims[3] = {(cuuint64_t)(g.nx + 1), (cuuint64_t)g.rows, (cuuint64_t)g.planes};
+  cuuint64_t strides[2] = {(cuuint64_t)(g.pitch * esz), (cuuint64_t)(g.pstride * esz)};
+  cuuint32_t box[3] = {(cuuint32_t)box_x, (cuuint32_t)box_y, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return cuTensorMapEncodeTiled(tm, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
 bool supported(const Geom& g, int min_nx) {
   return g.three_d && g.nx >= (min_nx < 16 ? 16 : min_nx) && g.ny >= 16 && (g.p_hi - g.p_lo) >= 4;
 }
@@ -574,9 +701,17 @@ static int choose_zc(long long ntiles, int np, int resident, int halo) {
   return best;
 }
 
+static CUresult encode_coarse(CUtensorMap* tm, const void* base, const Geom& g, int esz, int box_x, int box_y);
+
 template <typename T>
 cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
-                         int zc_override, cudaStream_t st, double* partial, int* npartial) {
+                         int zc_override, cudaStream_t st, double* partial, int* npartial, const T* ecoarse,
+                         const Geom* gcoarse) {
+  const Geom gce = gcoarse ? *gcoarse : Geom{};
+  CUtensorMap te;
+  memset(&te, 0, sizeof te);
+  if (ecoarse && encode_coarse(&te, ecoarse, gce, sizeof(T), Geo<T>::CBX, Geo<T>::CBY) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
   using G = Geo<T>;
   CUtensorMap tu, tf;
   CUresult e1 = encode(&tu, uin ? uin : f, g, sizeof(T), G::BYU), e2 = encode(&tf, f, g, sizeof(T), G::BYF);
@@ -586,15 +721,20 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   const int ntiles = tiles_x * tiles_y;
   const int np = g.p_hi - g.p_lo;
   auto go = [&](auto kernel) {
-    const int resident = prepare_kernel(kernel, G::SMEM);
+    const int resident = prepare_kernel(kernel, ecoarse ? G::SMEM_CORR : G::SMEM);
     const int zc = zc_override > 0 ? zc_override : choose_zc(ntiles, np, resident, rbgs ? 4 : 2);
     const int nitems = ntiles * ((np + zc - 1) / zc);
     if (getenv("MG_DEBUG"))
       fprintf(stderr, "launch_sweep: resident=%d zc=%d nitems=%d smem=%d\n", resident, zc, nitems, G::SMEM);
     if (npartial) *npartial = nitems;
-    kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial);
+    const int smem = ecoarse ? G::SMEM_CORR : G::SMEM;
+    const int resident2 = ecoarse ? prepare_kernel(kernel, smem) : resident;
+    (void)resident2;
+    kernel<<<nitems, NT, smem, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial, te, gce);
   };
-  if (partial && !zero_in)
+  if (ecoarse)
+    rbgs ? go(k_sweep3d<T, 1, false, false, true>) : go(k_sweep3d<T, 0, false, false, true>);
+  else if (partial && !zero_in)
     rbgs ? go(k_sweep3d<T, 1, false, true>) : go(k_sweep3d<T, 0, false, true>);
   else if (rbgs)
     zero_in ? go(k_sweep3d<T, 1, true>) : go(k_sweep3d<T, 1, false>);
@@ -645,7 +785,9 @@ cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f,
   const int zc = choose_zc(ntiles, np, resident, 2);
   const int nitems = ntiles * ((np + zc - 1) / zc);
   *npartial = nitems;
-  kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, g, c, nullptr, tiles_x, ntiles, zc, nitems, partial);
+  CUtensorMap te;
+  memset(&te, 0, sizeof te);
+  kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, g, c, nullptr, tiles_x, ntiles, zc, nitems, partial, te, Geom{});
   return cudaGetLastError();
 }
 
@@ -753,9 +895,10 @@ cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>&
 }
 
 template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool, const double*, const double*,
-                                          double*, bool, int, cudaStream_t, double*, int*);
+                                          double*, bool, int, cudaStream_t, double*, int*, const double*,
+                                          const Geom*);
 template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
-                                         bool, int, cudaStream_t, double*, int*);
+                                         bool, int, cudaStream_t, double*, int*, const float*, const Geom*);
 template int sweep_partials<double>(const Geom&, bool);
 template int sweep_partials<float>(const Geom&, bool);
 template int norm_partials<double>(const Geom&);

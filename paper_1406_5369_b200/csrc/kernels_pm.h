@@ -8,9 +8,11 @@ namespace pm {
 bool supported(const Geom& g, int min_nx);
 // one RBGS (rbgs=true) or Jacobi sweep u_out = S(u_in); zero_in: u_in is taken as 0 (not read)
 // partial != nullptr: also write ||f - A u_in||^2 partials (one per CTA, *npartial of them)
+// ecoarse != nullptr: the input is u_in + P ecoarse (prolongation + correction fused, 3D)
 template <typename T>
 cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
-                         int zc, cudaStream_t st, double* partial = nullptr, int* npartial = nullptr);
+                         int zc, cudaStream_t st, double* partial = nullptr, int* npartial = nullptr,
+                         const T* ecoarse = nullptr, const Geom* gcoarse = nullptr);
 template <typename T>
 int sweep_partials(const Geom& g, bool rbgs);
 // fc (coarse interior) = FW(f - A u) ; coarse boundary untouched

@@ -38,6 +38,7 @@ enum Kind {
   K_ALLGATHER,
   K_SWEEP_NORM,
   K_TAIL,
+  K_SWEEP_CORR,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -45,7 +46,7 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "norm_final",    "coarse_direct", "memset",       "add_interior",
                                        "rbgs_fused",    "jacobi_pm",     "resid_restrict",
                                        "nccl_halo",     "nccl_allgather", "sweep+norm",
-                                       "coarse_tail"};
+                                       "coarse_tail",   "prolong+sweep"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -569,9 +570,26 @@ struct Exec {
       for (int l = (lt < Lv ? lt : Lv - 1) - 1; l >= 0; l--) {
         const Level& L = s->lv[l];
         const T* f = l == 0 ? f0 : (const T*)L.f;
-        if ((r = exchange(l + 1, cur[l + 1], 1)) != MG_OK) return r;  // e_H plane above (slabs)
+        if ((r = exchange(l + 1, cur[l + 1], 1)) != MG_OK) return r;  // e_H neighbour planes (slabs)
         const T* e = cur[l + 1];
         const bool pml = pm(l);
+        if (pml && s->cfg.nu2 >= 1 && !(s->cfg.flags & MG_FLAG_NO_FUSE)) {
+          // prolongation + correction fused into the first post-sweep: u + P e is formed in
+          // shared memory, only S(u + P e) is written
+          const bool rb = s->cfg.smoother == MG_RBGS;
+          if ((r = exchange(l, cur[l], rb ? 2 : 1)) != MG_OK) return r;
+          T* in = cur[l];
+          T* out = oth[l];
+          const Geom gcg = s->lv[l + 1].g;
+          if ((r = launch(s, st, K_SWEEP_CORR, l, (3 + 1.0 / (1 << s->cfg.dim)) * w(l), [&] {
+                 return pm::launch_sweep<T>(L.g, coef(l), rb, in, f, out, false, zc(l), st, nullptr, nullptr, e, &gcg);
+               })) != MG_OK)
+            return r;
+          std::swap(cur[l], oth[l]);
+          for (int k = 1; k < s->cfg.nu2; k++)
+            if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+          continue;
+        }
         if ((r = launch(s, st, K_PROLONG, l, 2 * w(l) + w(l + 1), [&] {
                return pml ? pm::launch_prolong<T>(L.g, s->lv[l + 1].g, e, cur[l], st)
                           : launch_prolong_correct<T>(L.g, s->lv[l + 1].g, e, cur[l], st);

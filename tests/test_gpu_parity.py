@@ -226,12 +226,13 @@ def test_profile_counts_launches():
     assert all(r["ms"] > 0 for r in recs)
 
 
-@pytest.mark.parametrize("variant", ["default-threshold", "baseline"])
+@pytest.mark.parametrize("variant", ["default-threshold", "baseline", "no-fuse"])
 def test_schedule_variants_identical(variant):
     """The plane-marching, mixed (default threshold) and op-by-op (MG_FLAG_BASELINE)
     schedules give bitwise identical iterates (same canonical arithmetic)."""
     import paper_1406_5369_b200 as mgb
-    kw = dict(pm_min_nx=0) if variant == "default-threshold" else dict(flags=mgb.FLAG_BASELINE)
+    kw = {"default-threshold": dict(pm_min_nx=0), "baseline": dict(flags=mgb.FLAG_BASELINE),
+          "no-fuse": dict(flags=mgb.FLAG_NO_FUSE)}[variant]
     outs = []
     for extra in (dict(), kw):
         S, _ = make(3, (128, 128, 128), **extra)
