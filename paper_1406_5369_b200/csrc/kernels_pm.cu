@@ -62,13 +62,16 @@ struct Geo {
   static constexpr int NS = 4;  // step slots (power of two): 2 steps in flight
   // resident CTAs per SM (registers / shared memory)
   static constexpr int MINB = TY == 8 ? (sizeof(T) == 8 ? 3 : 6) : (sizeof(T) == 8 ? 2 : 3);
-  static constexpr int SMEM = NS * (UB + FB) + 2 * PB + NS * 8;
+  // layout: [NS u boxes][NS f boxes][NS mbarriers][3 PR / r planes][(CORR) 3 coarse boxes]
+  static constexpr int BAR_OFF = NS * (UB + FB);
+  static constexpr int PR_OFF = BAR_OFF + 128;
+  static constexpr int SMEM = PR_OFF + 3 * PB;
   // coarse boxes of the fused prolongation (CORR): x from X0 - 16/sizeof(T), y from Y0 - 1
   static constexpr int CHX = 16 / (int)sizeof(T);
   static constexpr int CBX = rup(TX / 2 + 2 + CHX, CHX);  // 36 (FP64) / 40 (FP32)
   static constexpr int CBY = TY / 2 + 3;
   static constexpr int CB = rup(CBX * CBY * (int)sizeof(T), 128);
-  static constexpr int COFF = rup(SMEM, 128);  // coarse ring (3 slots) after the barriers
+  static constexpr int COFF = PR_OFF + 2 * PB;  // CORR keeps 2 PR planes (two barriers per plane)
   static constexpr int SMEM_CORR = COFF + 3 * CB;
 };
 
@@ -152,7 +155,7 @@ template <typename T>
 __device__ __forceinline__ Ring<T> ring_setup(unsigned char* sm, const CUtensorMap* tu, const CUtensorMap* tf) {
   Ring<T> R;
   R.sm = sm;
-  R.full = reinterpret_cast<uint64_t*>(sm + Geo<T>::NS * (Geo<T>::UB + Geo<T>::FB) + 2 * Geo<T>::PB);
+  R.full = reinterpret_cast<uint64_t*>(sm + Geo<T>::BAR_OFF);
   if (threadIdx.x == 0) {
     prefetch_tmap(tu);
     prefetch_tmap(tf);
@@ -229,8 +232,13 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
   using G = Geo<T>;
   constexpr int BX = G::BX, HX = G::HX;
   const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
-  T* spr = reinterpret_cast<T*>(sm + G::NS * (G::UB + G::FB));
-  auto PRb = [&](int q) { return spr + (size_t)(q & 1) * (G::PB / sizeof(T)); };
+  // One barrier per plane (3 PR planes, refill one plane later) except with CORR, whose
+  // in-smem correction pass needs the shared-memory budget of the third PR plane.
+  constexpr bool ONESYNC = !CORR;
+  T* spr = reinterpret_cast<T*>(sm + G::PR_OFF);
+  auto PRb = [&](int q) {
+    return spr + (size_t)(ONESYNC ? ((q % 3) + 3) % 3 : (q & 1)) * (G::PB / sizeof(T));
+  };
   const Sweep<T, ZERO> S{c, R};
 
   const int tid = threadIdx.x, lane = tid & 31, ry = tid >> 5;
@@ -426,6 +434,11 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
           rzm = S.u(U0, (y - y0 + 2) * BX + (x - x0 + HX));
         }
         __syncthreads();
+        // ONESYNC: every thread has finished plane p-2's black update: step p-2 is free
+        if (ONESYNC && tid == 0 && p >= pa && p - 2 + G::NS <= qlast) {
+          fence_proxy_async();
+          issue_step(p - 2 + G::NS);
+        }
         const int bp = p - 1;  // black nodes of plane p-1: they sit where plane p's red nodes are
         if (bp >= pa) {
           const T* P = PRb(bp);
@@ -436,10 +449,12 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
           else
             black_node<T, 0>(c, P, Fb, fo, po, um.x, pr1, pr2, pr0, in0, in1, orow_b, ox);
         }
-        __syncthreads();
-        if (tid == 0 && p - 1 + G::NS <= qlast) {  // step p-1 (u(p), f(p-1)) is consumed
-          fence_proxy_async();
-          issue_step(p - 1 + G::NS);
+        if (!ONESYNC) {
+          __syncthreads();
+          if (tid == 0 && p - 1 + G::NS <= qlast) {  // step p-1 (u(p), f(p-1)) is consumed
+            fence_proxy_async();
+            issue_step(p - 1 + G::NS);
+          }
         }
         um = u0;
         u0 = up;
@@ -506,7 +521,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
   using G = Geo<T>;
   constexpr int BX = G::BX, HX = G::HX;
   const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
-  T* Rr = reinterpret_cast<T*>(sm + G::NS * (G::UB + G::FB));
+  T* Rr = reinterpret_cast<T*>(sm + G::PR_OFF);
 
   const int tid = threadIdx.x, lane = tid & 31, ry = tid >> 5;
   const int pgf0 = gf.p_glob0;
