@@ -59,7 +59,8 @@ typedef enum { MG_COARSE_DIRECT = 0, MG_COARSE_SWEEPS = 1 } mg_coarse; /* P:191,
 #define MG_FLAG_NO_GRAPH 1u   /* launch eagerly instead of replaying a CUDA graph   */
 #define MG_FLAG_BASELINE 2u   /* op-by-op kernels only (no fusion; two-pass RBGS)   */
 #define MG_FLAG_SLAB 4u       /* slab layout (halos, agglomeration) even with nranks == 1 */
-#define MG_FLAG_NO_FUSE 8u    /* keep prolongation and the first post-sweep as separate passes */
+#define MG_FLAG_FUSE_PROLONG 8u /* fuse prolongation+correction into the first post-sweep (u+Pe formed
+                                   in smem); off by default: the sweep is issue-bound, the gain is small */
 
 typedef struct {
     int32_t dim;         /* 2 or 3                                        */

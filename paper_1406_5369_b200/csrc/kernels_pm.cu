@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "kernels_pm.h"
 #include "tma.cuh"
@@ -40,10 +41,11 @@ namespace pm {
 #ifndef MG_PM_TY
 #define MG_PM_TY 16
 #endif
-constexpr int TX = 64, TY = MG_PM_TY;  // output tile (fine nodes) per CTA and plane
-constexpr int NT = (TX / 2) * TY;      // one thread per x-pair, one warp per tile row
-constexpr int RCOL = TY / 2;           // red ring nodes per ring column and plane
-constexpr int PX = TX + 2, PY = TY + 2;  // PR / r planes: tile + 1-node ring
+// A thread owns one 16-byte vector of W consecutive x nodes (W = 2 in FP64, 4 in
+// FP32: the same bytes per instruction in both precisions); a warp is one tile row
+// of TX = 32 W nodes, so every colour decision is warp-uniform.
+constexpr int TY = MG_PM_TY;  // tile rows
+constexpr int NT = 32 * TY;   // threads per CTA
 
 __host__ __device__ constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
 
@@ -52,61 +54,75 @@ __host__ __device__ constexpr int rup(int a, int b) { return (a + b - 1) / b * b
 // 16/sizeof(T) nodes left of the tile (2 in FP64, 4 in FP32).
 template <typename T>
 struct Geo {
-  static constexpr int HX = 16 / (int)sizeof(T);
+  static constexpr int W = 16 / (int)sizeof(T);  // nodes per thread
+  static constexpr int TX = 32 * W;              // tile width (64 / 128)
+  static constexpr int HX = W;
+  static constexpr int PY = TY + 2;                // PR / r planes: tile + 1-node ring rows
   static constexpr int BX = TX + 2 * HX;  // box width (u and f)
   static constexpr int BYU = TY + 4;      // u box rows: ring 2
   static constexpr int BYF = TY + 2;      // f box rows: ring 1
   static constexpr int UB = rup(BX * BYU * (int)sizeof(T), 128);
   static constexpr int FB = rup(BX * BYF * (int)sizeof(T), 128);
+  // PR / r planes use the box row stride BX and x offset HX, so per-thread vectors are 16-B aligned
+  static constexpr int PX = BX;
   static constexpr int PB = rup(PX * PY * (int)sizeof(T), 128);
-  static constexpr int NS = 4;  // step slots (power of two): 2 steps in flight
-  // resident CTAs per SM (registers / shared memory)
-  static constexpr int MINB = TY == 8 ? (sizeof(T) == 8 ? 3 : 6) : (sizeof(T) == 8 ? 2 : 3);
+  static constexpr int NS = 4;     // step slots (power of two)
+  static constexpr int MINB = 2;   // resident CTAs per SM (shared memory: ~111 KB each)
   // layout: [NS u boxes][NS f boxes][NS mbarriers][3 PR / r planes][(CORR) 3 coarse boxes]
   static constexpr int BAR_OFF = NS * (UB + FB);
   static constexpr int PR_OFF = BAR_OFF + 128;
   static constexpr int SMEM = PR_OFF + 3 * PB;
-  // coarse boxes of the fused prolongation (CORR): x from X0 - 16/sizeof(T), y from Y0 - 1
-  static constexpr int CHX = 16 / (int)sizeof(T);
-  static constexpr int CBX = rup(TX / 2 + 2 + CHX, CHX);  // 36 (FP64) / 40 (FP32)
+  // coarse boxes of the fused prolongation (CORR): x from X0 - CHX, y from Y0 - 1
+  static constexpr int CHX = W;
+  static constexpr int CBX = rup(TX / 2 + 2 + CHX, CHX);  // 36 (FP64) / 72 (FP32)
   static constexpr int CBY = TY / 2 + 3;
   static constexpr int CB = rup(CBX * CBY * (int)sizeof(T), 128);
   static constexpr int COFF = PR_OFF + 2 * PB;  // CORR keeps 2 PR planes (two barriers per plane)
   static constexpr int SMEM_CORR = COFF + 3 * CB;
+  static constexpr int NRED = W / 2;  // red (and black) nodes per thread and plane
+  static constexpr int RCOL = TY / 2;  // red ring nodes per ring column and plane
+  static constexpr int NRING_CORR = 4 * (TX + 4) + 4 * TY;  // box nodes outside the tile that are read
+};
+
+template <typename T, int W>
+struct Vec {
+  T v[W];
 };
 
 template <typename T>
-struct V2;
-template <>
-struct V2<double> {
-  using t = double2;
-};
-template <>
-struct V2<float> {
-  using t = float2;
-};
-
-template <typename T>
-struct Pair {
-  T x, y;
-};
-
-template <typename T>
-__device__ __forceinline__ Pair<T> ld_pair(const T* p) {
-  typename V2<T>::t v = *reinterpret_cast<const typename V2<T>::t*>(p);
-  return Pair<T>{v.x, v.y};
+__device__ __forceinline__ Vec<T, 16 / sizeof(T)> ld_vec(const T* p) {
+  Vec<T, 16 / sizeof(T)> r;
+  if constexpr (sizeof(T) == 8) {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    r.v[0] = a.x;
+    r.v[1] = a.y;
+  } else {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    r.v[0] = a.x;
+    r.v[1] = a.y;
+    r.v[2] = a.z;
+    r.v[3] = a.w;
+  }
+  return r;
 }
 
+// store the vector at dst[x..x+W), element k only if ok[k]
 template <typename T>
-__device__ __forceinline__ void store_pair(T* dst, int x, bool ok0, bool ok1, T v0, T v1) {
-  if (ok0 && ok1) {
-    typename V2<T>::t v;
-    v.x = v0;
-    v.y = v1;
-    *reinterpret_cast<typename V2<T>::t*>(dst + x) = v;
+__device__ __forceinline__ void store_vec(T* dst, int x, const bool* ok, const Vec<T, 16 / sizeof(T)>& o) {
+  constexpr int W = 16 / sizeof(T);
+  bool all = true;
+#pragma unroll
+  for (int k = 0; k < W; k++) all = all && ok[k];
+  if (all) {
+    if constexpr (sizeof(T) == 8) {
+      *reinterpret_cast<double2*>(dst + x) = make_double2(o.v[0], o.v[1]);
+    } else {
+      *reinterpret_cast<float4*>(dst + x) = make_float4(o.v[0], o.v[1], o.v[2], o.v[3]);
+    }
   } else {
-    if (ok0) dst[x] = v0;
-    if (ok1) dst[x + 1] = v1;
+#pragma unroll
+    for (int k = 0; k < W; k++)
+      if (ok[k]) dst[x + k] = o.v[k];
   }
 }
 
@@ -177,42 +193,9 @@ __device__ __forceinline__ void item_of(int k, int ntiles, int zc, int p_lo, int
 }
 
 // ---------------------------------------------------------------------------
-template <typename T, bool ZERO>
-struct Sweep {
-  const Coef<T>& c;
-  const Ring<T>& R;
-  __device__ T u(const T* base, int off) const { return ZERO ? (T)0 : base[off]; }
-  __device__ Pair<T> upair(const T* base, int off) const { return ZERO ? Pair<T>{0, 0} : ld_pair(base + off); }
-};
-
-// red node (ox + KR) of plane p; returns its post-red value and stores it in PR
-template <typename T, bool ZERO, int KR>
-__device__ __forceinline__ T red_node(const Sweep<T, ZERO>& S, const T* U0, const T* F0, T* PR, int bo, int fo,
-                                      int po, const Pair<T>& um, const Pair<T>& u0, const Pair<T>& up, bool ok) {
-  constexpr int BX = Geo<T>::BX;
-  const T ctr = KR ? u0.y : u0.x;
-  const T l = KR ? u0.x : S.u(U0, bo - 1);
-  const T r = KR ? S.u(U0, bo + 2) : u0.y;
-  const T v = relax(S.c, ctr, l, r, S.u(U0, bo + KR - BX), S.u(U0, bo + KR + BX), KR ? um.y : um.x,
-                    KR ? up.y : up.x, F0[fo + KR]);
-  const T pr = ok ? v : ctr;
-  PR[po + KR] = pr;
-  return pr;
-}
-
-// black node (ox + KB) of plane bp from the post-red values
-template <typename T, int KB>
-__device__ __forceinline__ void black_node(const Coef<T>& c, const T* P, const T* Fb, int fo, int po, T ctr,
-                                           T pr_own, T pr_below, T pr_above, bool in0, bool in1, T* orow, int ox) {
-  const T l = KB ? pr_own : P[po - 1];
-  const T r = KB ? P[po + 2] : pr_own;
-  const T v = relax(c, ctr, l, r, P[po + KB - PX], P[po + KB + PX], pr_below, pr_above, Fb[fo + KB]);
-  const T o = (KB ? in1 : in0) ? v : ctr;
-  store_pair(orow, ox, in0, in1, KB ? pr_own : o, KB ? o : pr_own);
-}
-
 // MODE 0: Jacobi sweep; 1: red-black GS sweep; 2: residual-norm partials (one
 // double per CTA in `partial`, fixed reduction tree: deterministic).
+// ZERO: the input iterate is 0 (first coarse sweep after V_H(0, ...)); u not read.
 // NRM (modes 0, 1): also accumulate ||f - A u_in||^2 partials of the sweep's INPUT
 // (the norm after the previous cycle comes for free with the next cycle's first
 // sweep: u and f are read anyway).
@@ -220,54 +203,69 @@ __device__ __forceinline__ void black_node(const Coef<T>& c, const T* P, const T
 // coarse-grid correction applied to every u box in shared memory as it arrives, so
 // the corrected iterate never makes an HBM round trip (prolongation fused into the
 // first post-smoothing sweep).  Same separable order as k_prolong3d.
-constexpr int NRING_CORR = 4 * (TX + 4) + 4 * TY;  // box nodes outside the tile that are read
-
 template <typename T, int MODE, bool ZERO, bool NRM = false, bool CORR = false>
 __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     k_sweep3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f, Geom g,
               Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems,
               double* __restrict__ partial, const __grid_constant__ CUtensorMap tm_e, Geom gc) {
-  constexpr bool RB = MODE == 1;
-  extern __shared__ __align__(128) unsigned char sm[];
   using G = Geo<T>;
-  constexpr int BX = G::BX, HX = G::HX;
-  const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
-  // One barrier per plane (3 PR planes, refill one plane later) except with CORR, whose
-  // in-smem correction pass needs the shared-memory budget of the third PR plane.
+  using V = Vec<T, G::W>;
+  constexpr int W = G::W, TX = G::TX, BX = G::BX, HX = G::HX, PX = G::PX, NR = G::NRED, RCOL = G::RCOL;
+  constexpr bool RB = MODE == 1;
+  // one barrier per plane (3 PR planes, refill one plane later) except with CORR, whose
+  // in-smem correction pass needs the shared-memory budget of the third PR plane
   constexpr bool ONESYNC = !CORR;
+  // keep f(p-1) in registers for the black stage, except in the register-tight FP64 CORR variant
+  constexpr bool FKEEP = !(CORR && sizeof(T) == 8);
+  extern __shared__ __align__(128) unsigned char sm[];
+  const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
   T* spr = reinterpret_cast<T*>(sm + G::PR_OFF);
   auto PRb = [&](int q) {
     return spr + (size_t)(ONESYNC ? ((q % 3) + 3) % 3 : (q & 1)) * (G::PB / sizeof(T));
   };
-  const Sweep<T, ZERO> S{c, R};
+  auto su = [&](const T* base, int off) -> T { return ZERO ? (T)0 : base[off]; };
+  auto svec = [&](const T* base, int off) -> V {
+    if (ZERO) {
+      V z;
+#pragma unroll
+      for (int k = 0; k < W; k++) z.v[k] = (T)0;
+      return z;
+    }
+    return ld_vec(base + off);
+  };
 
   const int tid = threadIdx.x, lane = tid & 31, ry = tid >> 5;
   const int pg0 = g.p_glob0;
-  const int bo = (ry + 2) * BX + 2 * lane + HX;  // u-box offset of (ox, oy)
-  const int fo = (ry + 1) * BX + 2 * lane + HX;  // f-box offset of (ox, oy)
-  const int po = (ry + 1) * PX + 2 * lane + 1;    // PR offset of (ox, oy)
+  const int bo = (ry + 2) * BX + W * lane + HX;  // u-box offset of (ox, oy)
+  const int fo = (ry + 1) * BX + W * lane + HX;  // f-box offset of (ox, oy)
+  const int po = (ry + 1) * PX + W * lane + HX;  // PR offset of (ox, oy)
   uint32_t seq = 0;
   double nsum = 0.0;  // MODE 2 / NRM: this thread's sum of r^2
-  // r^2 of the pair at plane p from the registers u(p-1), u(p), u(p+1) and smem u(p), f(p)
-  auto acc_norm = [&](const T* U0, const T* F0, const Pair<T>& um, const Pair<T>& u0, const Pair<T>& up, bool ok0,
-                      bool ok1) {
-    const Pair<T> fp = ld_pair(F0 + fo);
-    const double r0 =
-        (double)sub(fp.x, apply_A(c, u0.x, S.u(U0, bo - 1), u0.y, S.u(U0, bo - BX), S.u(U0, bo + BX), um.x, up.x));
-    const double r1 = (double)sub(
-        fp.y, apply_A(c, u0.y, u0.x, S.u(U0, bo + 2), S.u(U0, bo + 1 - BX), S.u(U0, bo + 1 + BX), um.y, up.y));
-    if (ok0) nsum = __dadd_rn(nsum, __dmul_rn(r0, r0));
-    if (ok1) nsum = __dadd_rn(nsum, __dmul_rn(r1, r1));
-  };
+
   for (int k = blockIdx.x; k < nitems; k += gridDim.x) {
     int tile, pa, pb;
     item_of(k, ntiles, zc, g.p_lo, g.p_hi, tile, pa, pb);
     const int x0 = (tile % tiles_x) * TX, y0 = (tile / tiles_x) * TY;
-    const int ox = x0 + 2 * lane, oy = y0 + ry;
+    const int ox = x0 + W * lane, oy = y0 + ry;
     const bool rin = oy >= 1 && oy <= g.ny - 1;
-    const bool in0 = rin && ox >= 1 && ox <= g.nx - 1;
-    const bool in1 = rin && ox + 1 <= g.nx - 1;
+    bool in[W];
+#pragma unroll
+    for (int j = 0; j < W; j++) in[j] = rin && ox + j >= 1 && ox + j <= g.nx - 1;
     T* orow = unew + (long long)oy * g.pitch;
+
+    // r^2 of the thread's nodes at plane p from registers u(p-1), u(p), u(p+1) and smem u(p), f(p)
+    auto acc_norm = [&](const T* U0, const T* F0, const V& um, const V& u0, const V& up) {
+      const V fv = ld_vec(F0 + fo), dn = svec(U0, bo - BX), upr = svec(U0, bo + BX);
+      const T el = su(U0, bo - 1), er = su(U0, bo + W);
+#pragma unroll
+      for (int j = 0; j < W; j++) {
+        const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
+        const T r = j == W - 1 ? er : u0.v[j < W - 1 ? j + 1 : 0];
+        const double rr = (double)sub(fv.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
+        if (in[j]) nsum = __dadd_rn(nsum, __dmul_rn(rr, rr));
+      }
+    };
+
     // step for plane q carries u(q+1), f(q); steps q = qlo .. qlast
     const int qlo = RB ? pa - 3 : pa - 2, qlast = RB ? pb : pb - 1;
     const uint32_t nlo = seq;
@@ -294,21 +292,34 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     };
     if (tid == 0)
       for (int q = qlo; q < qlo + G::NS && q <= qlast; q++) issue_step(q);
+
     // ---- CORR: u += P e on the u box of fine local plane zl (in smem, right after its arrival)
     const T half = (T)0.5;
     int cZ = -1000000;
-    Pair<T> cA{0, 0}, cB{0, 0};
+    V cA, cB;
     bool cHaveB = false;
     auto e_at = [&](int X, int Y, int Zg) -> T {
       return Cs(Zg)[(Y - Y0c + 1) * G::CBX + (X - X0c + G::CHX)];
     };
-    auto Vpair = [&](int Zg) -> Pair<T> {  // pair (2X, 2X+1) of row oy after the x- and y-interpolation
+    auto Vvec = [&](int Zg) -> V {  // the thread's W nodes of row oy after the x- and y-interpolation
       const int X = ox >> 1, Y = oy >> 1;
-      const T a0 = e_at(X, Y, Zg), a1 = e_at(X + 1, Y, Zg);
-      Pair<T> v{a0, mul(half, add(a0, a1))};
+      T a[NR + 1], b[NR + 1];
+#pragma unroll
+      for (int i = 0; i <= NR; i++) a[i] = e_at(X + i, Y, Zg);
+      V v;
+#pragma unroll
+      for (int i = 0; i < NR; i++) {
+        v.v[2 * i] = a[i];
+        v.v[2 * i + 1] = mul(half, add(a[i], a[i + 1]));
+      }
       if (oy & 1) {
-        const T b0 = e_at(X, Y + 1, Zg), b1 = e_at(X + 1, Y + 1, Zg);
-        v = Pair<T>{mul(half, add(v.x, b0)), mul(half, add(v.y, mul(half, add(b0, b1))))};
+#pragma unroll
+        for (int i = 0; i <= NR; i++) b[i] = e_at(X + i, Y + 1, Zg);
+#pragma unroll
+        for (int i = 0; i < NR; i++) {
+          v.v[2 * i] = mul(half, add(v.v[2 * i], b[i]));
+          v.v[2 * i + 1] = mul(half, add(v.v[2 * i + 1], mul(half, add(b[i], b[i + 1]))));
+        }
       }
       return v;
     };
@@ -326,32 +337,37 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     auto correct = [&](T* Ub, int zl) {
       const int zg = zl + pg0;
       if (zg < 1 || zg > g.nz - 1) return;  // boundary / outside planes: no correction
-      if (in0 || in1) {
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < W; j++) any = any || in[j];
+      if (any) {
         if ((zg >> 1) != cZ) {
-          cA = (cHaveB && (zg >> 1) == cZ + 1) ? cB : Vpair(zg >> 1);
+          cA = (cHaveB && (zg >> 1) == cZ + 1) ? cB : Vvec(zg >> 1);
           cZ = zg >> 1;
           cHaveB = false;
         }
-        Pair<T> v = cA;
+        V v = cA;
         if (zg & 1) {
           if (!cHaveB) {
-            cB = Vpair(cZ + 1);
+            cB = Vvec(cZ + 1);
             cHaveB = true;
           }
-          v = Pair<T>{mul(half, add(cA.x, cB.x)), mul(half, add(cA.y, cB.y))};
+#pragma unroll
+          for (int j = 0; j < W; j++) v.v[j] = mul(half, add(cA.v[j], cB.v[j]));
         }
         T* up_ = Ub + bo;
-        if (in0) up_[0] = add(up_[0], v.x);
-        if (in1) up_[1] = add(up_[1], v.y);
+#pragma unroll
+        for (int j = 0; j < W; j++)
+          if (in[j]) up_[j] = add(up_[j], v.v[j]);
       }
-      if (tid < NRING_CORR) {  // box nodes around the tile that the stencils read
+      for (int e = tid; e < G::NRING_CORR; e += NT) {  // box nodes around the tile that the stencils read
         int x, y;
-        if (tid < 4 * (TX + 4)) {
-          const int rr = tid / (TX + 4);
+        if (e < 4 * (TX + 4)) {
+          const int rr = e / (TX + 4);
           y = rr < 2 ? y0 - 2 + rr : y0 + TY + rr - 2;
-          x = x0 - 2 + tid % (TX + 4);
+          x = x0 - 2 + e % (TX + 4);
         } else {
-          const int t2 = tid - 4 * (TX + 4), cc = t2 / TY;
+          const int t2 = e - 4 * (TX + 4), cc = t2 / TY;
           x = cc < 2 ? x0 - 2 + cc : x0 + TX + cc - 2;
           y = y0 + t2 % TY;
         }
@@ -361,6 +377,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         }
       }
     };
+
     R.wait(N(qlo));
     R.wait(N(qlo + 1));
     if (CORR) {
@@ -368,42 +385,46 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
       correct(R.U(N(qlo + 1)), qlo + 2);
       __syncthreads();
     }
-    Pair<T> um = S.upair(R.U(N(qlo)), bo), u0 = S.upair(R.U(N(qlo + 1)), bo), up;
-    T rzm = (T)0;  // RB ring thread: u(p-1) at its plane-p ring node
-    if (RB && (ry < 2 || (ry == 2 && lane < 2 * RCOL))) {
-      const int pgl = pa - 1 + pg0;
-      int x, y;
+    V um = svec(R.U(N(qlo)), bo), u0 = svec(R.U(N(qlo + 1)), bo), up;
+
+    // RB ring threads: warps 0 / 1 the red nodes of rows y0-1 / y0+TY (NR per lane), warp 2
+    // lanes [0, RCOL) column x0-1 and [RCOL, 2 RCOL) column x0+TX (one each)
+    const bool ring_row = RB && ry < 2;
+    const bool ring_col = RB && ry == 2 && lane < 2 * RCOL;
+    auto ring_pos = [&](int pgl, int m, int& x, int& y) {
       if (ry < 2) {
         y = ry == 0 ? y0 - 1 : y0 + TY;
-        x = x0 + 2 * lane + ((y + pgl) & 1);
+        x = x0 + W * lane + 2 * m + ((y + pgl) & 1);  // x0 even
       } else {
         x = lane < RCOL ? x0 - 1 : x0 + TX;
         y = y0 + 2 * (lane % RCOL) + ((x + y0 + pgl) & 1);
       }
-      rzm = S.u(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
+    };
+    T rzm[NR];  // ring thread: u(p-1) at its plane-p ring nodes
+#pragma unroll
+    for (int m = 0; m < NR; m++) rzm[m] = (T)0;
+    if (ring_row || ring_col) {
+#pragma unroll
+      for (int m = 0; m < NR; m++) {
+        if (ring_col && m > 0) break;
+        int x, y;
+        ring_pos(pa - 1 + pg0, m, x, y);
+        rzm[m] = su(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
+      }
     }
     __syncthreads();  // step qlo lives on in registers only: refill its slot
     if (tid == 0 && qlo + G::NS <= qlast) {
       fence_proxy_async();
       issue_step(qlo + G::NS);
     }
+
     if (RB) {
-      // ring threads: warp 0 top row (y0-1), warp 1 bottom row (y0+TY), warp 2 lanes [0,RCOL) left column
-      // (x0-1), lanes [RCOL,2 RCOL) right column (x0+TX); each computes the red ring node of its slot
-      const bool ring = ry < 2 || (ry == 2 && lane < 2 * RCOL);
-      auto ring_pos = [&](int pgl, int& x, int& y) {
-        if (ry < 2) {
-          y = ry == 0 ? y0 - 1 : y0 + TY;
-          x = x0 + 2 * lane + ((y + pgl) & 1);  // x0 even
-        } else if (lane < RCOL) {
-          x = x0 - 1;
-          y = y0 + 2 * lane + ((x + y0 + pgl) & 1);
-        } else {
-          x = x0 + TX;
-          y = y0 + 2 * (lane - RCOL) + ((x + y0 + pgl) & 1);
-        }
-      };
-      T pr1 = (T)0, pr2 = (T)0;  // own red value of planes p-1, p-2
+      T pr1[NR], pr2[NR];  // own red values of planes p-1, p-2 (index m: node kr + 2m of that plane)
+#pragma unroll
+      for (int m = 0; m < NR; m++) pr1[m] = pr2[m] = (T)0;
+      V fprev;  // f(p-1) of the thread's nodes (loaded by the previous plane's red stage)
+#pragma unroll
+      for (int j = 0; j < W; j++) fprev.v[j] = (T)0;
       for (int p = pa - 1; p <= pb; p++) {
         R.wait(N(p));
         if (CORR) {
@@ -414,24 +435,62 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         const T* Up = R.U(N(p));      // u(p+1)
         const T* F0 = R.F(N(p));      // f(p)
         T* PR = PRb(p);
-        up = S.upair(Up, bo);
+        up = svec(Up, bo);
         const int pgl = p + pg0;
         const bool pl_in = pgl >= 1 && pgl <= g.nz - 1;
-        const int kr = (oy + pgl) & 1;  // warp uniform
-        if (NRM && p >= pa && p < pb) acc_norm(U0, F0, um, u0, up, in0, in1);
-        const T pr0 = kr ? red_node<T, ZERO, 1>(S, U0, F0, PR, bo, fo, po, um, u0, up, pl_in && in1)
-                         : red_node<T, ZERO, 0>(S, U0, F0, PR, bo, fo, po, um, u0, up, pl_in && in0);
-        if (ring) {  // red ring node of plane p
-          int x, y;
-          ring_pos(pgl, x, y);
-          const int rb = (y - y0 + 2) * BX + (x - x0 + HX);
-          const T ctr = S.u(U0, rb);
-          const T v = relax(c, ctr, S.u(U0, rb - 1), S.u(U0, rb + 1), S.u(U0, rb - BX), S.u(U0, rb + BX), rzm,
-                            S.u(Up, rb), F0[(y - y0 + 1) * BX + (x - x0 + HX)]);
-          const bool ok = pl_in && x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1;
-          PR[(y - y0 + 1) * PX + (x - x0 + 1)] = ok ? v : ctr;
-          ring_pos(pgl + 1, x, y);  // next plane's node: its z-neighbour below is u(p)
-          rzm = S.u(U0, (y - y0 + 2) * BX + (x - x0 + HX));
+        const int kr = (oy + pgl) & 1;  // warp uniform: red nodes at ox + kr + 2m
+        if (NRM && p >= pa && p < pb) acc_norm(U0, F0, um, u0, up);
+        T pr0[NR];
+        const V fcur = ld_vec(F0 + fo);  // f(p) of the thread's nodes (kept for plane p's black stage)
+        auto red_stage = [&](auto KRc) {
+          constexpr int KR = decltype(KRc)::value;
+          // FP32: 16-B vector loads of the rows above / below (one LDS.128 instead of two
+          // 4-way-conflicted scalars); FP64 (one red node per thread): the scalar is as cheap
+          V dn, upr;
+          if constexpr (W == 4) {
+            dn = svec(U0, bo - BX);
+            upr = svec(U0, bo + BX);
+          } else {
+            dn.v[KR] = su(U0, bo + KR - BX);
+            upr.v[KR] = su(U0, bo + KR + BX);
+          }
+          const T edge = KR == 0 ? su(U0, bo - 1) : su(U0, bo + W);
+          V pv = u0;  // PR row vector: red values at red nodes (black entries are never read)
+#pragma unroll
+          for (int m = 0; m < NR; m++) {
+            const int j = KR + 2 * m;
+            const T ctr = u0.v[j];
+            const T l = j == 0 ? edge : u0.v[j > 0 ? j - 1 : 0];
+            const T r = j == W - 1 ? edge : u0.v[j < W - 1 ? j + 1 : 0];
+            const T v = relax(c, ctr, l, r, dn.v[j], upr.v[j], um.v[j], up.v[j], fcur.v[j]);
+            const T prv = (pl_in && in[j]) ? v : ctr;
+            pv.v[j] = prv;
+            pr0[m] = prv;
+          }
+          if constexpr (sizeof(T) == 8)
+            *reinterpret_cast<double2*>(PR + po) = make_double2(pv.v[0], pv.v[1]);
+          else
+            *reinterpret_cast<float4*>(PR + po) = make_float4(pv.v[0], pv.v[1], pv.v[2], pv.v[3]);
+        };
+        if (kr)
+          red_stage(std::integral_constant<int, 1>());
+        else
+          red_stage(std::integral_constant<int, 0>());
+        if (ring_row || ring_col) {  // red ring nodes of plane p
+#pragma unroll
+          for (int m = 0; m < NR; m++) {
+            if (ring_col && m > 0) break;
+            int x, y;
+            ring_pos(pgl, m, x, y);
+            const int rb = (y - y0 + 2) * BX + (x - x0 + HX);
+            const T ctr = su(U0, rb);
+            const T v = relax(c, ctr, su(U0, rb - 1), su(U0, rb + 1), su(U0, rb - BX), su(U0, rb + BX), rzm[m],
+                              su(Up, rb), F0[(y - y0 + 1) * BX + (x - x0 + HX)]);
+            const bool ok = pl_in && x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1;
+            PR[(y - y0 + 1) * PX + (x - x0 + HX)] = ok ? v : ctr;
+            ring_pos(pgl + 1, m, x, y);  // next plane's node: its z-neighbour below is u(p)
+            rzm[m] = su(U0, (y - y0 + 2) * BX + (x - x0 + HX));
+          }
         }
         __syncthreads();
         // ONESYNC: every thread has finished plane p-2's black update: step p-2 is free
@@ -442,12 +501,39 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         const int bp = p - 1;  // black nodes of plane p-1: they sit where plane p's red nodes are
         if (bp >= pa) {
           const T* P = PRb(bp);
-          const T* Fb = R.F(N(bp));
-          T* orow_b = orow + (long long)bp * g.pstride;
+          auto black_stage = [&](auto KBc) {
+            constexpr int KB = decltype(KBc)::value;
+            V pdn, pup;
+            if constexpr (W == 4) {
+              pdn = ld_vec(P + po - PX);
+              pup = ld_vec(P + po + PX);
+            } else {
+              pdn.v[KB] = P[po + KB - PX];
+              pup.v[KB] = P[po + KB + PX];
+            }
+            const T edge = KB == 0 ? P[po - 1] : P[po + W];
+            const V fb = FKEEP ? fprev : ld_vec(R.F(N(bp)) + fo);
+            // plane bp's red nodes (pr1) sit at (1-KB) + 2m
+            V o;
+#pragma unroll
+            for (int m = 0; m < NR; m++) o.v[(1 - KB) + 2 * m] = pr1[m];
+#pragma unroll
+            for (int m = 0; m < NR; m++) {
+              const int j = KB + 2 * m;
+              const T ctr = um.v[j];
+              // x-1: red of plane bp at j-1 = (1-KB) + 2m' -> m' = m - (1-KB)
+              const T l = (KB == 0 && m == 0) ? edge : pr1[KB == 1 ? m : (m > 0 ? m - 1 : 0)];
+              // x+1: m' = m + KB
+              const T r = (KB == 1 && m == NR - 1) ? edge : pr1[KB == 0 ? m : (m + 1 < NR ? m + 1 : 0)];
+              const T v = relax(c, ctr, l, r, pdn.v[j], pup.v[j], pr2[m], pr0[m], fb.v[j]);
+              o.v[j] = in[j] ? v : ctr;
+            }
+            store_vec(orow + (long long)bp * g.pstride, ox, in, o);
+          };
           if (kr)
-            black_node<T, 1>(c, P, Fb, fo, po, um.y, pr1, pr2, pr0, in0, in1, orow_b, ox);
+            black_stage(std::integral_constant<int, 1>());
           else
-            black_node<T, 0>(c, P, Fb, fo, po, um.x, pr1, pr2, pr0, in0, in1, orow_b, ox);
+            black_stage(std::integral_constant<int, 0>());
         }
         if (!ONESYNC) {
           __syncthreads();
@@ -458,8 +544,12 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         }
         um = u0;
         u0 = up;
-        pr2 = pr1;
-        pr1 = pr0;
+        if (FKEEP) fprev = fcur;
+#pragma unroll
+        for (int m = 0; m < NR; m++) {
+          pr2[m] = pr1[m];
+          pr1[m] = pr0[m];
+        }
       }
     } else {
       for (int p = pa; p < pb; p++) {
@@ -469,15 +559,20 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
           __syncthreads();
         }
         const T* U0 = R.U(N(p - 1));
-        up = S.upair(R.U(N(p)), bo);
-        const Pair<T> fp = ld_pair(R.F(N(p)) + fo);
-        if (MODE == 2 || NRM) acc_norm(U0, R.F(N(p)), um, u0, up, in0, in1);  // r = f - A u, FP64 squares
+        up = svec(R.U(N(p)), bo);
+        if (MODE == 2 || NRM) acc_norm(U0, R.F(N(p)), um, u0, up);  // r = f - A u, FP64 squares
         if (MODE != 2) {
-          const T v0 =
-              relax(c, u0.x, S.u(U0, bo - 1), u0.y, S.u(U0, bo - BX), S.u(U0, bo + BX), um.x, up.x, fp.x);
-          const T v1 =
-              relax(c, u0.y, u0.x, S.u(U0, bo + 2), S.u(U0, bo + 1 - BX), S.u(U0, bo + 1 + BX), um.y, up.y, fp.y);
-          store_pair(orow + (long long)p * g.pstride, ox, in0, in1, in0 ? v0 : u0.x, in1 ? v1 : u0.y);
+          const V fv = ld_vec(R.F(N(p)) + fo), dn = svec(U0, bo - BX), upr = svec(U0, bo + BX);
+          const T el = su(U0, bo - 1), er = su(U0, bo + W);
+          V o;
+#pragma unroll
+          for (int j = 0; j < W; j++) {
+            const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
+            const T r = j == W - 1 ? er : u0.v[j < W - 1 ? j + 1 : 0];
+            const T v = relax(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j], fv.v[j]);
+            o.v[j] = in[j] ? v : u0.v[j];
+          }
+          store_vec(orow + (long long)p * g.pstride, ox, in, o);
         }
         __syncthreads();
         if (tid == 0 && p - 1 + G::NS <= qlast) {
@@ -508,50 +603,54 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
 // ---------------------------------------------------------------------------
 // Fused residual + full-weighting restriction.  Work items are (coarse tile,
 // coarse z-chunk); the fine tile is 2x the coarse tile (x0 = 2 X0).  Per fine
-// plane q: r for every pair of the tile (u column in registers) and the 73
-// low-side ring nodes (row y0-1, column x0-1) into smem; then the 128 coarse
-// nodes form their x- then y-sums of plane q and keep the last three in
+// plane q: r for every node of the tile (u column in registers) and the
+// low-side ring nodes (row y0-1, column x0-1) into smem; then the coarse nodes
+// of the tile form their x- then y-sums of plane q and keep the last three in
 // registers: when q = 2P+1 the z-sum gives f_H(P) (reading 13 order).
 template <typename T>
 __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     k_resid_restrict3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f,
                        Geom gf, Geom gc, Coef<T> c, T* __restrict__ fc, int tiles_x, int ntiles, int zcc,
                        int nitems) {
-  extern __shared__ __align__(128) unsigned char sm[];
   using G = Geo<T>;
-  constexpr int BX = G::BX, HX = G::HX;
+  using V = Vec<T, G::W>;
+  constexpr int W = G::W, TX = G::TX, BX = G::BX, HX = G::HX, PX = G::PX;
+  extern __shared__ __align__(128) unsigned char sm[];
   const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
   T* Rr = reinterpret_cast<T*>(sm + G::PR_OFF);
 
   const int tid = threadIdx.x, lane = tid & 31, ry = tid >> 5;
   const int pgf0 = gf.p_glob0;
-  const int bo = (ry + 2) * BX + 2 * lane + HX;
-  const int fo = (ry + 1) * BX + 2 * lane + HX;
-  const int po = (ry + 1) * PX + 2 * lane + 1;
+  const int bo = (ry + 2) * BX + W * lane + HX;
+  const int fo = (ry + 1) * BX + W * lane + HX;
+  const int po = (ry + 1) * PX + W * lane + HX;
   const T two = (T)2;
   const T scale = (T)(1.0 / 64.0);
+  // coarse node of this thread (tile of TX/2 x TY/2 coarse nodes)
+  constexpr int CNX = TX / 2, CN = (TX / 2) * (TY / 2);
+  const int ccx = tid % CNX, ccy = tid / CNX;
+  const int co = (2 * ccy + 1) * PX + 2 * ccx + HX;  // r offset of fine (2I, 2J)
   uint32_t seq = 0;
   for (int k = blockIdx.x; k < nitems; k += gridDim.x) {
     int tile, Pa, Pb;
     item_of(k, ntiles, zcc, gc.p_lo, gc.p_hi, tile, Pa, Pb);
     const int X0 = (tile % tiles_x) * (TX / 2), Y0 = (tile / tiles_x) * (TY / 2);
     const int x0 = 2 * X0, y0 = 2 * Y0;
-    const int ox = x0 + 2 * lane, oy = y0 + ry;
+    const int ox = x0 + W * lane, oy = y0 + ry;
     const bool rin = oy >= 1 && oy <= gf.ny - 1;
-    const bool in0 = rin && ox >= 1 && ox <= gf.nx - 1;
-    const bool in1 = rin && ox + 1 <= gf.nx - 1;
-    // low-side ring: row y0-1 for x in [x0-1, x0+TX-1] (65 nodes), column x0-1 for y in [y0, y0+TY-1] (TY)
+    bool in[W];
+#pragma unroll
+    for (int j = 0; j < W; j++) in[j] = rin && ox + j >= 1 && ox + j <= gf.nx - 1;
+    // low-side ring: row y0-1 for x in [x0-1, x0+TX-1] (TX+1 nodes), column x0-1 for y in [y0, y0+TY-1]
     const bool has_ring = tid < TX + 1 + TY;
     const int rx = tid < TX + 1 ? x0 - 1 + tid : x0 - 1;
     const int ryy = tid < TX + 1 ? y0 - 1 : y0 + tid - (TX + 1);
     const bool ring_in = rx >= 1 && rx <= gf.nx - 1 && ryy >= 1 && ryy <= gf.ny - 1;
     const int rb = (ryy - y0 + 2) * BX + (rx - x0 + HX);
     const int rf = (ryy - y0 + 1) * BX + (rx - x0 + HX);
-    const int rpo = (ryy - y0 + 1) * PX + (rx - x0 + 1);
-    // coarse node of threads 0..127: warp = coarse row, lane = coarse column
-    const int I = X0 + lane, J = Y0 + ry;
-    const bool cnode = ry < TY / 2 && I >= 1 && I <= gc.nx - 1 && J >= 1 && J <= gc.ny - 1;
-    const int co = (2 * ry + 1) * PX + 2 * lane + 1;  // r offset of fine (2I, 2J)
+    const int rpo = (ryy - y0 + 1) * PX + (rx - x0 + HX);
+    const int I = X0 + ccx, J = Y0 + ccy;
+    const bool cnode = tid < CN && I >= 1 && I <= gc.nx - 1 && J >= 1 && J <= gc.ny - 1;
     T* crow = fc + (long long)J * gc.pitch + I;
 
     const int qf0 = 2 * (Pa + gc.p_glob0) - pgf0;      // fine centre of the first coarse plane
@@ -564,7 +663,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
       for (int q = qlo; q < qlo + G::NS && q <= qlast; q++) R.issue(N(q), &tm_u, &tm_f, x0, y0, q + 1, q, true);
     R.wait(N(qlo));
     R.wait(N(qlo + 1));
-    Pair<T> um = ld_pair(R.U(N(qlo)) + bo), u0 = ld_pair(R.U(N(qlo + 1)) + bo), up;
+    V um = ld_vec(R.U(N(qlo)) + bo), u0 = ld_vec(R.U(N(qlo + 1)) + bo), up;
     T rzm = has_ring ? R.U(N(qlo))[rb] : (T)0;
     __syncthreads();  // step qlo lives on in registers only: refill its slot
     if (tid == 0 && qlo + G::NS <= qlast) {
@@ -577,15 +676,24 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
       const T* U0 = R.U(N(q - 1));
       const T* Up = R.U(N(q));
       const T* F0 = R.F(N(q));
-      up = ld_pair(Up + bo);
+      up = ld_vec(Up + bo);
       const int pgl = q + pgf0;
       const bool pl_in = pgl >= 1 && pgl <= gf.nz - 1;
       {
-        const Pair<T> fp = ld_pair(F0 + fo);
-        const T r0 = sub(fp.x, apply_A(c, u0.x, U0[bo - 1], u0.y, U0[bo - BX], U0[bo + BX], um.x, up.x));
-        const T r1 = sub(fp.y, apply_A(c, u0.y, u0.x, U0[bo + 2], U0[bo + 1 - BX], U0[bo + 1 + BX], um.y, up.y));
-        Rr[po] = pl_in && in0 ? r0 : (T)0;
-        Rr[po + 1] = pl_in && in1 ? r1 : (T)0;
+        const V fv = ld_vec(F0 + fo), dn = ld_vec(U0 + bo - BX), upr = ld_vec(U0 + bo + BX);
+        const T el = U0[bo - 1], er = U0[bo + W];
+        V rv;
+#pragma unroll
+        for (int j = 0; j < W; j++) {
+          const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
+          const T r = j == W - 1 ? er : u0.v[j < W - 1 ? j + 1 : 0];
+          const T rr = sub(fv.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
+          rv.v[j] = pl_in && in[j] ? rr : (T)0;
+        }
+        if constexpr (sizeof(T) == 8)
+          *reinterpret_cast<double2*>(Rr + po) = make_double2(rv.v[0], rv.v[1]);
+        else
+          *reinterpret_cast<float4*>(Rr + po) = make_float4(rv.v[0], rv.v[1], rv.v[2], rv.v[3]);
       }
       if (has_ring) {
         const T uc = U0[rb];
@@ -594,7 +702,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         rzm = uc;
       }
       __syncthreads();
-      if (ry < TY / 2) {
+      if (tid < CN) {
         T tx[3];
 #pragma unroll
         for (int dy = -1; dy <= 1; dy++) {
@@ -642,7 +750,8 @@ static CUresult encode(CUtensorMap* tm, const void* base, const Geom& g, int esz
   if (!cuTensorMapEncodeTiled) return CUDA_ERROR_NOT_FOUND;
   cuuint64_t dims[3] = {(cuuint64_t)(g.nx + 1), (cuuint64_t)g.rows, (cuuint64_t)g.planes};
   cuuint64_t strides[2] = {(cuuint64_t)(g.pitch * esz), (cuuint64_t)(g.pstride * esz)};
-  cuuint32_t box[3] = {(cuuint32_t)(TX + 2 * (16 / esz)), (cuuint32_t)box_rows, 1};
+  const int tx = 32 * (16 / esz);  // Geo<T>::TX
+  cuuint32_t box[3] = {(cuuint32_t)(tx + 2 * (16 / esz)), (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return cuTensorMapEncodeTiled(tm, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                                 const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -732,7 +841,7 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   CUresult e1 = encode(&tu, uin ? uin : f, g, sizeof(T), G::BYU), e2 = encode(&tf, f, g, sizeof(T), G::BYF);
   if (getenv("MG_DEBUG")) fprintf(stderr, "launch_sweep: encode %d %d nx=%d ny=%d rows=%d np=%d\n", (int)e1, (int)e2, g.nx, g.ny, g.rows, g.p_hi - g.p_lo);
   if (e1 != CUDA_SUCCESS || e2 != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  const int tiles_x = (g.nx + TX - 1) / TX, tiles_y = (g.ny + TY - 1) / TY;
+  const int tiles_x = (g.nx + G::TX - 1) / G::TX, tiles_y = (g.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = g.p_hi - g.p_lo;
   auto go = [&](auto kernel) {
@@ -762,7 +871,7 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
 template <typename T>
 int sweep_partials(const Geom& g, bool rbgs) {
   using G = Geo<T>;
-  const int ntiles = ((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
+  const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
   const int np = g.p_hi - g.p_lo;
   const int resident = rbgs ? prepare_kernel(k_sweep3d<T, 1, false, true>, G::SMEM)
                             : prepare_kernel(k_sweep3d<T, 0, false, true>, G::SMEM);
@@ -778,7 +887,7 @@ int sweep_partials(const Geom& g, bool rbgs) {
 template <typename T>
 int norm_partials(const Geom& g) {
   using G = Geo<T>;
-  const int ntiles = ((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
+  const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
   const int np = g.p_hi - g.p_lo;
   const int resident = prepare_kernel(k_sweep3d<T, 2, false>, G::SMEM);
   const int zc = choose_zc(ntiles, np, resident, 2);
@@ -792,7 +901,7 @@ cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f,
   CUtensorMap tu, tf;
   if (encode(&tu, u, g, sizeof(T), G::BYU) != CUDA_SUCCESS || encode(&tf, f, g, sizeof(T), G::BYF) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  const int tiles_x = (g.nx + TX - 1) / TX, tiles_y = (g.ny + TY - 1) / TY;
+  const int tiles_x = (g.nx + G::TX - 1) / G::TX, tiles_y = (g.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = g.p_hi - g.p_lo;
   auto kernel = k_sweep3d<T, 2, false>;
@@ -808,66 +917,90 @@ cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f,
 
 // ---------------------------------------------------------------------------
 // Bi-/trilinear prolongation + correction u += P e, 3D.
-// Pointwise in u, so no staging: thread = fine x-pair (2X, 2X+1) of one row,
-// marching z.  The pair's coarse values after the x- and y-interpolation of a
+// Pointwise in u, so no staging: thread = W fine nodes (2X .. 2X+W-1) of one row,
+// marching z.  The thread's coarse values after the x- and y-interpolation of a
 // coarse plane K, V(K), stay in registers for the 3 fine planes that use it;
 // fine plane z = 2Z+dz gets dz ? (V(Z)+V(Z+1))/2 : V(Z) (reading 13 order).
+// (The default; MG_FLAG_FUSE_PROLONG folds it into the first post-sweep instead.)
 template <typename T>
 __global__ void __launch_bounds__(NT) k_prolong3d(Geom gf, Geom gc, const T* __restrict__ e, T* __restrict__ u,
                                                  int tiles_x, int ntiles, int zc, int nitems) {
+  using G = Geo<T>;
+  using Vt = Vec<T, G::W>;
+  constexpr int W = G::W, NR = G::NRED;
   const int lane = threadIdx.x & 31, ry = threadIdx.x >> 5;
   const T half = (T)0.5;
   for (int k = blockIdx.x; k < nitems; k += gridDim.x) {
     int tile, pa, pb;
     item_of(k, ntiles, zc, gf.p_lo, gf.p_hi, tile, pa, pb);
-    const int x0 = (tile % tiles_x) * TX, y0 = (tile / tiles_x) * TY;
-    const int ox = x0 + 2 * lane, oy = y0 + ry;
+    const int x0 = (tile % tiles_x) * G::TX, y0 = (tile / tiles_x) * TY;
+    const int ox = x0 + W * lane, oy = y0 + ry;
     const bool rin = oy >= 1 && oy <= gf.ny - 1;
-    const bool in0 = rin && ox >= 1 && ox <= gf.nx - 1;
-    const bool in1 = rin && ox + 1 <= gf.nx - 1;
-    if (!(in0 || in1)) continue;
+    bool in[W], any = false;
+#pragma unroll
+    for (int j = 0; j < W; j++) {
+      in[j] = rin && ox + j >= 1 && ox + j <= gf.nx - 1;
+      any = any || in[j];
+    }
+    if (!any) continue;
     const int X = ox >> 1, Y = oy >> 1, dy = oy & 1;
     const T* ec = e + (long long)Y * gc.pitch + X;
-    auto V = [&](int Zg) -> Pair<T> {  // x- then y-interpolated pair of coarse plane Zg (global)
+    auto Vz = [&](int Zg) -> Vt {  // x- then y-interpolated nodes of coarse plane Zg (global)
       const T* p0 = ec + (long long)(Zg - gc.p_glob0) * gc.pstride;
-      const T a0 = __ldg(p0), a1 = __ldg(p0 + 1);
-      Pair<T> v{a0, mul(half, add(a0, a1))};
+      T a[NR + 1];
+#pragma unroll
+      for (int i = 0; i <= NR; i++) a[i] = __ldg(p0 + i);
+      Vt v;
+#pragma unroll
+      for (int i = 0; i < NR; i++) {
+        v.v[2 * i] = a[i];
+        v.v[2 * i + 1] = mul(half, add(a[i], a[i + 1]));
+      }
       if (dy) {
-        const T b0 = __ldg(p0 + gc.pitch), b1 = __ldg(p0 + gc.pitch + 1);
-        const Pair<T> w{b0, mul(half, add(b0, b1))};
-        v = Pair<T>{mul(half, add(v.x, w.x)), mul(half, add(v.y, w.y))};
+#pragma unroll
+        for (int i = 0; i <= NR; i++) a[i] = __ldg(p0 + gc.pitch + i);
+#pragma unroll
+        for (int i = 0; i < NR; i++) {
+          v.v[2 * i] = mul(half, add(v.v[2 * i], a[i]));
+          v.v[2 * i + 1] = mul(half, add(v.v[2 * i + 1], mul(half, add(a[i], a[i + 1]))));
+        }
       }
       return v;
     };
-    T* urow = u + (long long)oy * gf.pitch + ox;
+    T* urow = u + (long long)oy * gf.pitch;
     int Z = (pa + gf.p_glob0) >> 1;
-    Pair<T> A = V(Z), B = A;
+    Vt A = Vz(Z), B = A;
     bool haveB = false;
     for (int z = pa; z < pb; z++) {
       const int zg = z + gf.p_glob0;
       if ((zg >> 1) != Z) {
         Z++;
-        A = haveB ? B : V(Z);
+        A = haveB ? B : Vz(Z);
         haveB = false;
       }
-      Pair<T> v = A;
+      Vt v = A;
       if (zg & 1) {
         if (!haveB) {
-          B = V(Z + 1);
+          B = Vz(Z + 1);
           haveB = true;
         }
-        v = Pair<T>{mul(half, add(A.x, B.x)), mul(half, add(A.y, B.y))};
+#pragma unroll
+        for (int j = 0; j < W; j++) v.v[j] = mul(half, add(A.v[j], B.v[j]));
       }
       T* up = urow + (long long)z * gf.pstride;
-      if (in0 && in1) {
-        const Pair<T> uu = ld_pair(up);
-        typename V2<T>::t o;
-        o.x = add(uu.x, v.x);
-        o.y = add(uu.y, v.y);
-        *reinterpret_cast<typename V2<T>::t*>(up) = o;
+      Vt o;
+      bool all = true;
+#pragma unroll
+      for (int j = 0; j < W; j++) all = all && in[j];
+      if (all) {
+        const Vt uu = ld_vec(up + ox);
+#pragma unroll
+        for (int j = 0; j < W; j++) o.v[j] = add(uu.v[j], v.v[j]);
+        store_vec(up, ox, in, o);
       } else {
-        if (in0) up[0] = add(up[0], v.x);
-        if (in1) up[1] = add(up[1], v.y);
+#pragma unroll
+        for (int j = 0; j < W; j++)
+          if (in[j]) up[ox + j] = add(up[ox + j], v.v[j]);
       }
     }
   }
@@ -875,7 +1008,8 @@ __global__ void __launch_bounds__(NT) k_prolong3d(Geom gf, Geom gc, const T* __r
 
 template <typename T>
 cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cudaStream_t st) {
-  const int tiles_x = (gf.nx + TX - 1) / TX, tiles_y = (gf.ny + TY - 1) / TY;
+  using G = Geo<T>;
+  const int tiles_x = (gf.nx + G::TX - 1) / G::TX, tiles_y = (gf.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = gf.p_hi - gf.p_lo;
   static int resident = 0;
@@ -898,7 +1032,7 @@ cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>&
   CUtensorMap tu, tf;
   if (encode(&tu, u, gf, sizeof(T), G::BYU) != CUDA_SUCCESS || encode(&tf, f, gf, sizeof(T), G::BYF) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  const int tiles_x = (gc.nx + TX / 2 - 1) / (TX / 2), tiles_y = (gc.ny + TY / 2 - 1) / (TY / 2);
+  const int tiles_x = (gc.nx + G::TX / 2 - 1) / (G::TX / 2), tiles_y = (gc.ny + TY / 2 - 1) / (TY / 2);
   const int ntiles = tiles_x * tiles_y;
   const int npc = gc.p_hi - gc.p_lo;
   auto kernel = k_resid_restrict3d<T>;
