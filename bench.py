@@ -220,8 +220,12 @@ def run_mg(args):
     dev = torch.cuda.current_device()
     dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[args.config]
     esz = 8 if dt == "f64" else 4
-    kw = dict(levels=levels, smoother=sm, omega=omega, nu1=nu1, nu2=nu2, dtype=dt, device=dev)
+    kw = dict(levels=levels, smoother=sm, omega=omega, nu1=nu1, nu2=nu2, dtype=dt, device=dev,
+              flags=mgb.FLAG_HOST_LOOP if args.host_loop else 0)
+    # mg_solve runs its loop on the device (one CUDA graph, conditional WHILE node) unless
+    # --host-loop or the slab run spans several ranks (NCCL cannot run in a conditional body)
     slab = world > 1 and args.decomp == "slab"
+    device_loop = not args.host_loop and not slab
     if slab:  # z-slab decomposition of ONE global grid over the ranks (strong scaling), NCCL halos
         S = mgb.distributed_solver(dim, nodes, **kw)
     else:     # N independent replicas (weak scaling)
@@ -272,6 +276,8 @@ def run_mg(args):
     S.profile_enable(False)
     ours = [r for r in recs if not (r["name"].startswith("memset") or r["name"].startswith("nccl"))]
     launches = sum(r["count"] for r in ours) / nprof  # our kernels per step (incl. the norm pipeline)
+    if device_loop:
+        launches += 1  # the loop's check kernel (k_loop_check) per cycle; the profile pass is eager
     tot = sum(r["ms"] for r in recs)
     dom = max(recs, key=lambda r: r["ms"])  # the dominant kernel of the step
     dom_avg_ms = dom["ms"] / dom["count"]
@@ -330,7 +336,8 @@ def run_mg(args):
                        "parallelism": (f"z-slab x{world} (NCCL halos, agglomeration below 8 planes/rank)" if slab
                                        else ("replicas" if world > 1 else "single-gpu")),
                        "l2": "inputs larger than L2 (1.08 GB per array), no flush needed",
-                       "levels": S.levels},
+                       "levels": S.levels,
+                       "driver": "device loop (CUDA graph WHILE node)" if device_loop else "host loop"},
             "residual_reduction_per_step": (rk / r0) ** (1.0 / (args.steps + args.warmup)) if r0 else None,
             "model_bytes_per_step": B, "model_GBps": B / (ms * 1e-3) / 1e9,
             "roofline": roofline, "kernels": breakdown, "cpu_baseline": cpu, "e2e": e2e,
@@ -352,6 +359,7 @@ def main():
     ap.add_argument("--config", default="C3-f64", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--host-loop", action="store_true", help="mg_solve with MG_FLAG_HOST_LOOP (per-cycle sync)")
     ap.add_argument("--decomp", default="slab", choices=["slab", "replicas"],
                     help="N>1: z-slab decomposition of one grid (default) or independent replicas")
     args = ap.parse_args()

@@ -61,6 +61,8 @@ typedef enum { MG_COARSE_DIRECT = 0, MG_COARSE_SWEEPS = 1 } mg_coarse; /* P:191,
 #define MG_FLAG_SLAB 4u       /* slab layout (halos, agglomeration) even with nranks == 1 */
 #define MG_FLAG_FUSE_PROLONG 8u /* fuse prolongation+correction into the first post-sweep (u+Pe formed
                                    in smem); off by default: the sweep is issue-bound, the gain is small */
+#define MG_FLAG_HOST_LOOP 16u   /* mg_solve: host-driven loop (one synchronisation per cycle) instead of
+                                   the on-device loop (one CUDA graph with a conditional WHILE node) */
 
 typedef struct {
     int32_t dim;         /* 2 or 3                                        */
@@ -126,8 +128,14 @@ mg_status mg_residual_norm(mg_solver* s, const void* u, const void* f, double* o
 
 /* Driver loop of the `Application` listing: r0 = norm; repeat
  * { V-cycle; r_k = norm } until r_k <= rtol * r0 or max_cycles.  history (if
- * not NULL) receives max_cycles+1 doubles, history[0] = r0.  Blocking.
- * Returns MG_ERR_NONFINITE if a norm is NaN/Inf. */
+ * not NULL, host memory) receives r_0..r_k (room for max_cycles+1 doubles),
+ * history[0] = r0; *cycles = k.  Blocking.  Returns MG_ERR_NONFINITE if a
+ * norm is NaN/Inf (the loop stops at that cycle).
+ * By default the whole loop runs on the device: one CUDA graph whose WHILE
+ * node repeats {cycle, norm, test} with the stopping test evaluated by a kernel,
+ * one host synchronisation per solve.  MG_FLAG_HOST_LOOP, MG_FLAG_NO_GRAPH,
+ * profiling, or nranks > 1 (NCCL cannot run inside a conditional node) select
+ * the host loop; both give bitwise identical iterates and norms. */
 mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol, int32_t max_cycles,
                    int32_t* cycles, double* history, void* stream);
 

@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libmgb200.so")
 JACOBI, RBGS = 0, 1
 FP64, FP32 = 0, 1
 COARSE_DIRECT, COARSE_SWEEPS = 0, 1
-FLAG_NO_GRAPH, FLAG_BASELINE, FLAG_SLAB, FLAG_FUSE_PROLONG = 1, 2, 4, 8
+FLAG_NO_GRAPH, FLAG_BASELINE, FLAG_SLAB, FLAG_FUSE_PROLONG, FLAG_HOST_LOOP = 1, 2, 4, 8, 16
 
 # every symbol include/mg.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = [

@@ -228,6 +228,9 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
   if (!u || !f || max_cycles < 0 || !(rtol >= 0.0)) return fail(s, MG_ERR_INVALID, "bad argument");
   if (u == f) return fail(s, MG_ERR_INVALID, "u and f must not alias");
   cudaStream_t cs = (cudaStream_t)stream;
+  const bool eager_mode = (s->cfg.flags & MG_FLAG_NO_GRAPH) || s->prof_on;
+  if (!eager_mode && !(s->cfg.flags & MG_FLAG_HOST_LOOP) && plan_loop_supported(s))
+    return plan_solve_device(s, u, f, rtol, max_cycles, cycles, history, cs);
   if (plan_can_split(s)) {
     // pipelined driver loop: head(k) = first sweep of cycle k+1 into the ping-pong buffer
     // + ||f - A u_k|| of its input; tail(k) = the rest of cycle k+1.  u holds u_k

@@ -261,7 +261,13 @@ mg_status plan_build(mg_solver* s) {
     if (hs != 0) return plan_fail(s, MG_ERR_INVALID, "coarsest matrix is not positive definite");
   }
   e = cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap_body, cudaStreamNonBlocking);
   if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamCreate");
+  if (cudaMalloc(&s->d_loop, sizeof(LoopState)) != cudaSuccess ||
+      cudaMallocHost(&s->h_loop, sizeof(LoopState)) != cudaSuccess) {
+    cudaGetLastError();
+    return plan_fail(s, MG_ERR_OOM, "allocation of the driver-loop state failed");
+  }
   // count launches of one cycle with a dry capture
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(s, e, "setup");
@@ -293,6 +299,10 @@ void plan_free(mg_solver* s) {
     cudaEventDestroy(r.b);
   }
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->cap_body) cudaStreamDestroy(s->cap_body);
+  cudaFree(s->d_loop);
+  cudaFree(s->d_hist);
+  if (s->h_loop) cudaFreeHost(s->h_loop);
 }
 
 // ---------------------------------------------------------------- typed schedule
@@ -655,12 +665,14 @@ const Coef<float>& Exec<float>::coef(int l) const {
 }
 
 // ---------------------------------------------------------------- entry points
-// part: 0 whole cycle, 1 head (first sweep + norm of the input into d_norm), 2 tail
+// part: 0 whole cycle, 1 head (first sweep + norm of the input into d_norm), 2 tail,
+// 3 norm of (u, f) into d_norm
 template <typename T>
 static mg_status run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
   Exec<T> x{s, st};
   if (part == 1) return x.head((T*)u, (const T*)f, s->d_norm);
   if (part == 2) return x.tail((T*)u, (const T*)f);
+  if (part == 3) return x.norm(0, (const T*)u, (const T*)f, s->d_norm);
   return x.vcycle((T*)u, (const T*)f);
 }
 

@@ -31,6 +31,17 @@ struct Level {
   void* t = nullptr;      // ping-pong partner of u
 };
 
+// state of the on-device driver loop (loop.cu); written by the host before each solve
+struct LoopState {
+  double rtol;     // in: stopping tolerance (r_k <= rtol * r0)
+  double r0;       // out: initial norm
+  double* hist;    // in: device history buffer (max+1 doubles) or NULL
+  int32_t max;     // in: max_cycles
+  int32_t k;       // out: cycles run
+  int32_t status;  // out: 0 ok, 1 r0 non-finite, 2 r_k non-finite
+  int32_t pad;
+};
+
 struct ProfRec {
   int kind;               // index into the kernel-name table
   int level;
@@ -66,6 +77,11 @@ struct mg_solver {
   double* h_norm = nullptr;  // pinned
   // graphs keyed by (u, f)
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t cap_body = nullptr;   // captures the body of the driver loop's WHILE node
+  mg::LoopState* d_loop = nullptr;
+  mg::LoopState* h_loop = nullptr;   // pinned
+  double* d_hist = nullptr;
+  int64_t hist_cap = 0;
   std::map<std::tuple<void*, const void*, int>, cudaGraphExec_t> graphs;  // (u, f, part)
   // e2e staging
   void* stage_u = nullptr;
@@ -87,10 +103,14 @@ mg_status plan_build(mg_solver* s);
 void plan_free(mg_solver* s);
 mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st);
 mg_status plan_graph_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st);
-// part: 0 whole cycle, 1 head (first sweep + input norm -> d_norm), 2 tail
+// part: 0 whole cycle, 1 head (first sweep + input norm -> d_norm), 2 tail, 3 norm -> d_norm
 mg_status plan_run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st);
 mg_status plan_graph_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st);
 bool plan_can_split(mg_solver* s);
+// on-device driver loop (loop.cu): one graph launch runs the whole mg_solve loop
+bool plan_loop_supported(mg_solver* s);
+mg_status plan_solve_device(mg_solver* s, void* u, const void* f, double rtol, int32_t max_cycles, int32_t* cycles,
+                            double* history, cudaStream_t st);
 mg_status plan_norm(mg_solver* s, int level, const void* u, const void* f, double* out, cudaStream_t st, bool sync);
 mg_status plan_op_smooth(mg_solver* s, int level, const void* uin, const void* f, void* uout, cudaStream_t st);
 mg_status plan_op_residual(mg_solver* s, int level, const void* u, const void* f, void* r, cudaStream_t st);

@@ -1,0 +1,101 @@
+"""On-device driver loop (loop.cu): mg_solve as one CUDA graph
+with a conditional WHILE node against the host-driven loop (MG_FLAG_HOST_LOOP) and
+the oracle's or_solve (the `Application` listing): identical cycle
+counts, bitwise identical iterates and residual histories."""
+import numpy as np
+import pytest
+
+import oracle as orc  # noqa: F401  (make() builds the oracle)
+from paper_1406_5369_b200 import workloads as wl
+
+from test_gpu_parity import make
+
+pytestmark = pytest.mark.gpu
+
+LOOP_CASES = [
+    dict(dim=3, cells=(128, 128, 128), smoother="rbgs"),                  # pipelined split (head/tail)
+    dict(dim=3, cells=(64, 64, 64), smoother="jacobi", nu1=2, nu2=1),    # split, odd sweep count
+    dict(dim=2, cells=(64, 64), levels=5, smoother="jacobi"),            # C1: no split (cycle + norm)
+    dict(dim=3, cells=(64, 64, 64), smoother="rbgs", dtype="f32"),
+    dict(dim=2, cells=(32, 32), levels=1, smoother="rbgs"),               # single level, direct
+    dict(dim=3, cells=(16, 16, 16), levels=2, smoother="rbgs", coarse="sweeps", ncoarse=10),
+]
+
+
+def _flags(name):
+    import paper_1406_5369_b200 as mgb
+    return {"host": mgb.FLAG_HOST_LOOP, "device": 0, "baseline": mgb.FLAG_BASELINE,
+            "slab": mgb.FLAG_SLAB}[name]
+
+
+@pytest.mark.parametrize("case", LOOP_CASES, ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
+def test_device_loop_matches_host_loop_and_oracle(case):
+    case = dict(case)
+    dt = case.get("dtype", "f64")
+    res = {}
+    for mode in ("device", "host"):
+        S, O = make(**case, flags=_flags(mode))
+        u, f = wl.workload("W1", case["dim"], case["cells"], seed=42, dtype=S.np_dtype)
+        du, df = S.from_numpy(u), S.from_numpy(f)
+        k, hist = S.solve(du, df, 1e-10, 40)
+        res[mode] = (k, np.array(hist), S.to_numpy(du))
+    assert res["device"][0] == res["host"][0]
+    assert np.array_equal(res["device"][1], res["host"][1])
+    assert np.array_equal(res["device"][2], res["host"][2])
+    uo, k_or, hist_or = O.solve(u, f, 1e-10, 40)
+    assert res["device"][0] == k_or
+    np.testing.assert_allclose(res["device"][1], hist_or, rtol=1e-12 if dt == "f64" else 1e-5)
+    if dt == "f64":
+        assert np.array_equal(res["device"][2], uo)
+
+
+@pytest.mark.parametrize("variant", ["baseline", "slab"])
+def test_device_loop_other_schedules(variant):
+    """Op-by-op (no split) and slab-layout schedules inside the WHILE body."""
+    case = dict(dim=3, cells=(64, 64, 64), smoother="rbgs")
+    S, O = make(**case, flags=_flags(variant))
+    u, f = wl.workload("W1", 3, (64, 64, 64), seed=5)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    k, hist = S.solve(du, df, 1e-9, 30)
+    uo, k_or, hist_or = O.solve(u, f, 1e-9, 30)
+    assert k == k_or
+    np.testing.assert_allclose(hist, hist_or, rtol=1e-12)
+    assert np.array_equal(S.to_numpy(du), uo)
+
+
+def test_device_loop_stopping_rules_and_graph_reuse():
+    """max_cycles = 0, early stop on rtol, and a cached graph reused with new rtol/max."""
+    S, O = make(3, (64, 64, 64))
+    u, f = wl.workload("W1", 3, (64, 64, 64), seed=42)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    k, hist = S.solve(du, df, 0.0, 0)
+    assert k == 0 and len(hist) == 1 and abs(hist[0] / O.norm(0, u, f) - 1) <= 1e-12
+    assert np.array_equal(S.to_numpy(du), u)
+    k1, h1 = S.solve(du, df, 0.5, 20)          # one V(2,2) cycle reduces the residual by far more than 2x
+    assert k1 == 1
+    u1 = O.vcycle(u, f)
+    assert np.array_equal(S.to_numpy(du), u1)
+    k2, h2 = S.solve(du, df, 0.0, 3)            # same (u, f): same graph, new parameters
+    assert k2 == 3 and h2[0] == h1[1]
+    uo = u1
+    for _ in range(3):
+        uo = O.vcycle(uo, f)
+    assert np.array_equal(S.to_numpy(du), uo)
+
+
+@pytest.mark.parametrize("mode", ["device", "host"])
+def test_nonfinite_initial_residual(mode):
+    import paper_1406_5369_b200 as mgb
+    S, _ = make(3, (32, 32, 32), flags=_flags(mode))
+    u, f = wl.workload("W1", 3, (32, 32, 32), seed=1)
+    f[5, 6, 7] = np.nan
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    with pytest.raises(mgb.MGError) as ei:
+        S.solve(du, df, 1e-10, 5)
+    assert ei.value.status == 6
+    assert np.array_equal(S.to_numpy(du), u)   # no cycle ran
+    # the solver is not poisoned: a clean solve works afterwards
+    f[5, 6, 7] = 0.0
+    df = S.from_numpy(f)
+    k, _ = S.solve(du, df, 0.0, 1)
+    assert k == 1
