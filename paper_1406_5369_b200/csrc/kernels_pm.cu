@@ -33,7 +33,9 @@
 #include <type_traits>
 
 #include "kernels_pm.h"
+#include "kernels_pm2d.h"
 #include "tma.cuh"
+#include "vec.cuh"
 
 namespace mg {
 namespace pm {
@@ -83,48 +85,6 @@ struct Geo {
   static constexpr int RCOL = TY / 2;  // red ring nodes per ring column and plane
   static constexpr int NRING_CORR = 4 * (TX + 4) + 4 * TY;  // box nodes outside the tile that are read
 };
-
-template <typename T, int W>
-struct Vec {
-  T v[W];
-};
-
-template <typename T>
-__device__ __forceinline__ Vec<T, 16 / sizeof(T)> ld_vec(const T* p) {
-  Vec<T, 16 / sizeof(T)> r;
-  if constexpr (sizeof(T) == 8) {
-    const double2 a = *reinterpret_cast<const double2*>(p);
-    r.v[0] = a.x;
-    r.v[1] = a.y;
-  } else {
-    const float4 a = *reinterpret_cast<const float4*>(p);
-    r.v[0] = a.x;
-    r.v[1] = a.y;
-    r.v[2] = a.z;
-    r.v[3] = a.w;
-  }
-  return r;
-}
-
-// store the vector at dst[x..x+W), element k only if ok[k]
-template <typename T>
-__device__ __forceinline__ void store_vec(T* dst, int x, const bool* ok, const Vec<T, 16 / sizeof(T)>& o) {
-  constexpr int W = 16 / sizeof(T);
-  bool all = true;
-#pragma unroll
-  for (int k = 0; k < W; k++) all = all && ok[k];
-  if (all) {
-    if constexpr (sizeof(T) == 8) {
-      *reinterpret_cast<double2*>(dst + x) = make_double2(o.v[0], o.v[1]);
-    } else {
-      *reinterpret_cast<float4*>(dst + x) = make_float4(o.v[0], o.v[1], o.v[2], o.v[3]);
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < W; k++)
-      if (ok[k]) dst[x + k] = o.v[k];
-  }
-}
 
 // A u at a node in the canonical order: D*u - [cx*(l+r) + cy*(d+u) + cz*(m+p)]
 template <typename T>
@@ -745,6 +705,24 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+CUresult encode_tiled(CUtensorMap* tm, bool fp64, int rank, const void* base, const unsigned long long* dims,
+                      const unsigned long long* strides, const unsigned* box) {
+  PFN_cuTensorMapEncodeTiled_v12000 cuTensorMapEncodeTiled = encode_fn();
+  if (!cuTensorMapEncodeTiled) return CUDA_ERROR_NOT_FOUND;
+  cuuint64_t d[5], sd[4];
+  cuuint32_t b[5], estr[5];
+  for (int i = 0; i < rank; i++) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    estr[i] = 1;
+    if (i + 1 < rank) sd[i] = strides[i];
+  }
+  return cuTensorMapEncodeTiled(tm, fp64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                (cuuint32_t)rank, const_cast<void*>(base), d, sd, b, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
 static CUresult encode(CUtensorMap* tm, const void* base, const Geom& g, int esz, int box_rows) {
   PFN_cuTensorMapEncodeTiled_v12000 cuTensorMapEncodeTiled = encode_fn();
   if (!cuTensorMapEncodeTiled) return CUDA_ERROR_NOT_FOUND;
@@ -777,6 +755,7 @@ static CUresult encode_coarse(CUtensorMap* tm, const void* base, const Geom& g, 
 }
 
 bool supported(const Geom& g, int min_nx) {
+  if (!g.three_d) return pm2::supported(g, min_nx);
   return g.three_d && g.nx >= (min_nx < 16 ? 16 : min_nx) && g.ny >= 16 && (g.p_hi - g.p_lo) >= 4;
 }
 
@@ -831,6 +810,10 @@ template <typename T>
 cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
                          int zc_override, cudaStream_t st, double* partial, int* npartial, const T* ecoarse,
                          const Geom* gcoarse) {
+  if (!g.three_d) {
+    if (ecoarse) return cudaErrorInvalidValue;  // fused prolongation: 3D only
+    return pm2::launch_sweep<T>(g, c, rbgs, uin, f, uout, zero_in, st, partial, npartial);
+  }
   const Geom gce = gcoarse ? *gcoarse : Geom{};
   CUtensorMap te;
   memset(&te, 0, sizeof te);
@@ -870,6 +853,7 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
 // upper bound of the partials launch_sweep(..., partial, ...) writes for a level
 template <typename T>
 int sweep_partials(const Geom& g, bool rbgs) {
+  if (!g.three_d) return pm2::sweep_partials<T>(g, rbgs);
   using G = Geo<T>;
   const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
   const int np = g.p_hi - g.p_lo;
@@ -886,6 +870,7 @@ int sweep_partials(const Geom& g, bool rbgs) {
 
 template <typename T>
 int norm_partials(const Geom& g) {
+  if (!g.three_d) return pm2::norm_partials<T>(g);
   using G = Geo<T>;
   const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
   const int np = g.p_hi - g.p_lo;
@@ -897,6 +882,7 @@ int norm_partials(const Geom& g) {
 template <typename T>
 cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f, double* partial, int* npartial,
                         cudaStream_t st) {
+  if (!g.three_d) return pm2::launch_norm<T>(g, c, u, f, partial, npartial, st);
   using G = Geo<T>;
   CUtensorMap tu, tf;
   if (encode(&tu, u, g, sizeof(T), G::BYU) != CUDA_SUCCESS || encode(&tf, f, g, sizeof(T), G::BYF) != CUDA_SUCCESS)
@@ -1008,6 +994,7 @@ __global__ void __launch_bounds__(NT) k_prolong3d(Geom gf, Geom gc, const T* __r
 
 template <typename T>
 cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cudaStream_t st) {
+  if (!gf.three_d) return pm2::launch_prolong<T>(gf, gc, e, u, st);
   using G = Geo<T>;
   const int tiles_x = (gf.nx + G::TX - 1) / G::TX, tiles_y = (gf.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
@@ -1028,6 +1015,7 @@ cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cud
 template <typename T>
 cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>& c, const T* u, const T* f, T* fc,
                                   int zc_override, cudaStream_t st) {
+  if (!gf.three_d) return pm2::launch_resid_restrict<T>(gf, gc, c, u, f, fc, st);
   using G = Geo<T>;
   CUtensorMap tu, tf;
   if (encode(&tu, u, gf, sizeof(T), G::BYU) != CUDA_SUCCESS || encode(&tf, f, gf, sizeof(T), G::BYF) != CUDA_SUCCESS)

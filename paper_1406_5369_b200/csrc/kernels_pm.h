@@ -1,9 +1,16 @@
-// kernels_pm.h — launchers of the TMA plane-marching kernels (3D levels).
+// kernels_pm.h — launchers of the plane-marching kernels: TMA-staged tiles for 3D levels
+// (kernels_pm.cu), warp-marching strips for 2D levels (kernels_pm2d.cu, dispatched here).
 #pragma once
 #include "mg_common.cuh"
 
+#include <cuda.h>
+
 namespace mg {
 namespace pm {
+// cuTensorMapEncodeTiled (through the runtime's driver entry point): element type FP64/FP32,
+// dims/strides (bytes, dims 1..rank-1)/box of a rank-`rank` tensor, no swizzle, zero OOB fill
+CUresult encode_tiled(CUtensorMap* tm, bool fp64, int rank, const void* base, const unsigned long long* dims,
+                      const unsigned long long* strides, const unsigned* box);
 // true when a level is large enough for the plane-marching kernels
 bool supported(const Geom& g, int min_nx);
 // one RBGS (rbgs=true) or Jacobi sweep u_out = S(u_in); zero_in: u_in is taken as 0 (not read)

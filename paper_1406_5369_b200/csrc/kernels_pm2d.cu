@@ -1,0 +1,732 @@
+// kernels_pm2d.cu — warp-marching level operators for 2D levels (sm_100a).
+//
+// A 2D level is [planes = the paper's y][pitch], x fastest (mg_common.cuh).  A
+// warp owns a strip of TX = 32 W columns (lane = one 16-byte vector of W =
+// 16/sizeof(T) nodes) and marches a chunk of rows.  Rows arrive through a
+// warp-private ring of NS shared-memory slots: lane 0 issues, per STEP of RB rows,
+// one 2D TMA box load of u and one of f (cp.async.bulk.tensor.2d, RW = TX + 2W
+// columns from x0 - W, zero-filled outside the array), completing on the slot's
+// mbarrier.  The prefetch costs no registers, and the issue and wait cost is paid
+// once per RB rows.  A lane reads its vector from the slot; its x-neighbours come
+// from the adjacent lanes by warp shuffles (lanes 0 / 31 read the strip-edge nodes
+// from the slot); the rows above and below stay in registers.  No block barriers:
+// the warps of a CTA are independent.  A slot is refilled after the warp's
+// __syncwarp that ends its reads of it.  Warps with consecutive ids take
+// neighbouring strips of the same chunk and the launch is one wave of resident
+// warps (rows split evenly), so strip-edge and chunk-halo re-reads hit L2.
+//
+//  k_jacobi2d          omega-Jacobi sweep, optionally with the residual-norm
+//                      partials of its input; MODE 2: norm partials only
+//  k_rbgs2d            one red-black Gauss-Seidel sweep in ONE pass (listing P:299-305):
+//                      red of row t, then black of row t-1 from the red rows t-2..t,
+//                      all in registers
+//  k_resid_restrict2d  r = f - A u (Alg. 1 line 4) and full weighting:
+//                      read u, f; write f_H (r never leaves registers)
+//  k_prolong2d         u += P e, bilinear
+// Arithmetic is the canonical per-point order of mg_common.cuh with explicitly
+// rounded intrinsics (no FMA): bitwise identical to the op-by-op kernels and the oracle.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#include "kernels_pm.h"
+#include "kernels_pm2d.h"
+#include "tma.cuh"
+#include "vec.cuh"
+
+namespace mg {
+namespace pm2 {
+
+#ifndef MG_PM2_RB
+#define MG_PM2_RB 4
+#endif
+#ifndef MG_PM2_NS
+#define MG_PM2_NS 3
+#endif
+constexpr int WPB = 4;          // warps per CTA
+constexpr int NT = 32 * WPB;
+constexpr int RB = MG_PM2_RB;   // rows per step (one TMA box of u and one of f)
+constexpr int NS = MG_PM2_NS;   // ring slots per warp
+constexpr unsigned FULL = 0xffffffffu;
+
+template <typename T>
+struct G2 {
+  static constexpr int W = 16 / (int)sizeof(T);  // nodes per lane
+  static constexpr int TX = 32 * W;              // strip width (64 FP64 / 128 FP32)
+  static constexpr int NR = W / 2;               // coarse nodes per lane (restriction)
+  static constexpr int RW = TX + 2 * W;          // box row: x in [x0 - W, x0 + TX + W)
+  static constexpr int BOX = RW * RB;            // elements per box
+  static constexpr int BOXB = BOX * (int)sizeof(T);  // 2176 B
+  static constexpr int WARP_BYTES = NS * 2 * BOXB + 128;  // slots (u box, f box) + mbarriers
+  static constexpr int SMEM = WPB * WARP_BYTES;
+};
+
+template <typename T>
+using VT = Vec<T, 16 / sizeof(T)>;
+
+template <typename T>
+__device__ __forceinline__ VT<T> zvec() {
+  VT<T> z;
+#pragma unroll
+  for (int k = 0; k < 16 / (int)sizeof(T); k++) z.v[k] = (T)0;
+  return z;
+}
+
+// 2D operator, canonical order: s = cx*(l+r); s = s + cz*(m+p); A u = D*u - s
+// (m, p: the rows below / above, i.e. the paper's y neighbours on the plane axis)
+template <typename T>
+__device__ __forceinline__ T A2(const Coef<T>& c, T ctr, T l, T r, T m, T p) {
+  T s = mul(c.cx, add(l, r));
+  s = add(s, mul(c.cz, add(m, p)));
+  return sub(mul(c.D, ctr), s);
+}
+// u + wd*(f - A u)
+template <typename T>
+__device__ __forceinline__ T relax2(const Coef<T>& c, T ctr, T l, T r, T m, T p, T f) {
+  return add(ctr, mul(c.wd, sub(f, A2(c, ctr, l, r, m, p))));
+}
+
+// warp gw -> strip and rows [pa, pb) of [lo, hi); consecutive warps: neighbouring strips
+__device__ __forceinline__ void item2(int gw, int nstrips, int nch, int lo, int hi, int& strip, int& pa, int& pb) {
+  strip = gw % nstrips;
+  const int ch = gw / nstrips;
+  const long long n = hi - lo;
+  pa = lo + (int)(n * ch / nch);
+  pb = lo + (int)(n * (ch + 1) / nch);
+}
+
+// left / right x-neighbours of a lane's vector: adjacent lanes, or lx / rx at the strip edges
+template <typename T>
+__device__ __forceinline__ void edges(const VT<T>& v, T lx, T rx, int lane, T& l, T& r) {
+  constexpr int W = G2<T>::W;
+  l = __shfl_up_sync(FULL, v.v[W - 1], 1);
+  r = __shfl_down_sync(FULL, v.v[0], 1);
+  if (lane == 0) l = lx;
+  if (lane == 31) r = rx;
+}
+
+// fixed-order block reduction of the per-thread sums -> partial[blockIdx.x]
+__device__ __forceinline__ void block_partial(double nsum, double* partial) {
+  __shared__ double red[WPB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsum = __dadd_rn(nsum, __shfl_down_sync(FULL, nsum, o));
+  if (lane == 0) red[wid] = nsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < WPB; w++) t = __dadd_rn(t, red[w]);
+    partial[blockIdx.x] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The warp's ring.  A warp marching rows t0 .. tlast uses steps b = -1, 0, 1, ...:
+// step b holds u rows t0 + b RB + 1 .. + RB and (b >= 0) f rows t0 + b RB .. + RB - 1,
+// so row t = t0 + b RB + i reads u(t+1) and f(t) from box row i of step b, and step -1
+// supplies u(t0 - RB + 1 .. t0) for the registers the march starts with.  Step b lives
+// in slot (n0 + b + 1) % NS, mbarrier phase ((n0 + b + 1) / NS) & 1 (n0: steps of the
+// warp's earlier items).
+template <typename T>
+struct WRing {
+  using G = G2<T>;
+  T* buf;
+  uint64_t* bar;
+  uint32_t n0;
+  int t0, x;  // first row of the march, box x start (x0 - W)
+
+  __device__ void init(unsigned char* smem, int wid, int lane) {
+    unsigned char* w = smem + wid * G::WARP_BYTES;
+    buf = reinterpret_cast<T*>(w);
+    bar = reinterpret_cast<uint64_t*>(w + NS * 2 * G::BOXB);
+    n0 = 0;
+    if (lane == 0) {
+      for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+  }
+  __device__ uint32_t N(int b) const { return n0 + (uint32_t)(b + 1); }
+  __device__ T* U(int b) const { return buf + (N(b) % NS) * (2 * G::BOX); }
+  __device__ T* F(int b) const { return U(b) + G::BOX; }
+  __device__ void wait(int b) const { mbar_wait(&bar[N(b) % NS], (N(b) / NS) & 1u); }
+  // lane 0: the loads of step b (u unless !load_u; f when b >= 0)
+  __device__ void issue(int b, const CUtensorMap* tu, const CUtensorMap* tf, bool load_u) const {
+    uint64_t* br = &bar[N(b) % NS];
+    const bool lf = b >= 0;
+    mbar_expect_tx(br, (uint32_t)((load_u ? G::BOXB : 0) + (lf ? G::BOXB : 0)));
+    if (load_u) tma_load_2d(U(b), tu, x, t0 + b * RB + 1, br);
+    if (lf) tma_load_2d(F(b), tf, x, t0 + b * RB, br);
+  }
+  // lane 0: steps -1 .. NS-2 (all slots)
+  __device__ void start(int nsteps, const CUtensorMap* tu, const CUtensorMap* tf, bool load_u) const {
+    for (int b = -1; b < NS - 1 && b < nsteps; b++) issue(b, tu, tf, load_u);
+  }
+  // after the reads of step b: refill its slot with step b + NS
+  __device__ void release(int b, int nsteps, int lane, const CUtensorMap* tu, const CUtensorMap* tf,
+                          bool load_u) const {
+    __syncwarp();
+    if (lane == 0 && b + NS < nsteps) issue(b + NS, tu, tf, load_u);
+  }
+  __device__ void finish(int nsteps) { n0 = N(nsteps - 1) + 1; }
+};
+
+template <typename T>
+__device__ __forceinline__ void prefetch_maps(const CUtensorMap* a, const CUtensorMap* b, int lane) {
+  if (lane == 0) {
+    prefetch_tmap(a);
+    prefetch_tmap(b);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// MODE 0: Jacobi sweep uin -> uout; MODE 2: residual-norm partials only.
+// ZERO: the input iterate is 0 (first sweep after V_H(0, ...)), u not read.
+// NRM (MODE 0): also the norm partials of the sweep's INPUT (fused head sweep).
+template <typename T, int MODE, bool ZERO, bool NRM>
+__global__ void __launch_bounds__(NT) k_jacobi2d(const __grid_constant__ CUtensorMap tm_u,
+                                                 const __grid_constant__ CUtensorMap tm_f, Geom g, Coef<T> c,
+                                                 T* __restrict__ uout, int nstrips, int nch,
+                                                 double* __restrict__ partial) {
+  using V = VT<T>;
+  constexpr int W = G2<T>::W, TX = G2<T>::TX, RW = G2<T>::RW;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WRing<T> R;
+  R.init(smem, wid, lane);
+  prefetch_maps<T>(&tm_u, &tm_f, lane);
+  const int vo = W + W * lane;                // the lane's vector in a box row
+  const int eo = lane == 0 ? W - 1 : W + TX;  // strip-edge node (lane 0: x0-1, lane 31: x0+TX)
+  double nsum = 0.0;
+  for (int gw = blockIdx.x * WPB + wid; gw < nstrips * nch; gw += gridDim.x * WPB) {
+    int strip, pa, pb;
+    item2(gw, nstrips, nch, g.p_lo, g.p_hi, strip, pa, pb);
+    const int x0 = strip * TX, ox = x0 + W * lane;
+    bool in[W];
+#pragma unroll
+    for (int j = 0; j < W; j++) in[j] = ox + j >= 1 && ox + j <= g.nx - 1;
+    const bool okv = ox <= g.nx;
+    R.t0 = pa;
+    R.x = x0 - W;
+    const int nsteps = (pb - 1 - pa) / RB + 1;
+    if (lane == 0) R.start(nsteps, &tm_u, &tm_f, !ZERO);
+    auto urow = [&](const T* row, T& e) -> V {
+      if (ZERO) {
+        e = (T)0;
+        return zvec<T>();
+      }
+      e = row[eo];
+      return ld_vec(row + vo);
+    };
+    T ume, u0s;
+    R.wait(-1);
+    V um = urow(R.U(-1) + (RB - 2) * RW, ume);  // u(pa-1)
+    V u0 = urow(R.U(-1) + (RB - 1) * RW, u0s);  // u(pa)
+    R.release(-1, nsteps, lane, &tm_u, &tm_f, !ZERO);
+    for (int b = 0; b < nsteps; b++) {
+      R.wait(b);
+      const T* Ub = R.U(b);
+      const T* Fb = R.F(b);
+#pragma unroll
+      for (int i = 0; i < RB; i++) {
+        const int p = pa + b * RB + i;
+        if (p >= pb) break;
+        T ups;
+        const V up = urow(Ub + i * RW, ups);
+        const V fv = ld_vec(Fb + i * RW + vo);
+        T l0, r0;
+        edges(u0, u0s, u0s, lane, l0, r0);
+        V o;
+#pragma unroll
+        for (int j = 0; j < W; j++) {
+          const T l = j == 0 ? l0 : u0.v[j > 0 ? j - 1 : 0];
+          const T r = j == W - 1 ? r0 : u0.v[j < W - 1 ? j + 1 : 0];
+          const T rr = sub(fv.v[j], A2(c, u0.v[j], l, r, um.v[j], up.v[j]));
+          if ((MODE == 2 || NRM) && in[j]) nsum = __dadd_rn(nsum, __dmul_rn((double)rr, (double)rr));
+          o.v[j] = in[j] ? add(u0.v[j], mul(c.wd, rr)) : u0.v[j];
+        }
+        if (MODE != 2 && okv) store_vec(uout + (long long)p * g.pstride, ox, in, o);
+        um = u0;
+        u0 = up;
+        u0s = ups;
+      }
+      R.release(b, nsteps, lane, &tm_u, &tm_f, !ZERO);
+    }
+    R.finish(nsteps);
+  }
+  if (MODE == 2 || NRM) block_partial(nsum, partial);
+}
+
+// ---------------------------------------------------------------------------
+// One red-black GS sweep uin -> uout in one pass.  Iteration t computes the red
+// nodes of row t ("post-red" row pr(t): red entries relaxed, black entries old) and
+// then the black nodes of row t-1 from pr(t-2), pr(t-1), pr(t); rows pa-1 and pb get
+// their red nodes only (neighbour chunks' rows, recomputed, never written).  Colour:
+// red = even global i + j (reading 8); strips start at even x, so the colour of a
+// lane's element j in row t is (j + t + p_glob0) & 1, uniform over the warp.
+// Strip-edge (ring) nodes: lane 0 relaxes x0-1, lane 31 x0+TX when they are red.
+template <typename T, bool ZERO, bool NRM>
+__global__ void __launch_bounds__(NT) k_rbgs2d(const __grid_constant__ CUtensorMap tm_u,
+                                               const __grid_constant__ CUtensorMap tm_f, Geom g, Coef<T> c,
+                                               T* __restrict__ uout, int nstrips, int nch,
+                                               double* __restrict__ partial) {
+  using V = VT<T>;
+  constexpr int W = G2<T>::W, TX = G2<T>::TX, NR = G2<T>::NR, RW = G2<T>::RW;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WRing<T> R;
+  R.init(smem, wid, lane);
+  prefetch_maps<T>(&tm_u, &tm_f, lane);
+  const int vo = W + W * lane;
+  // ring node e1 and its outer neighbour e2: lane 0 (x0-1, x0-2), lane 31 (x0+TX, x0+TX+1)
+  const int e1o = lane == 0 ? W - 1 : W + TX, e2o = lane == 0 ? W - 2 : W + TX + 1;
+  double nsum = 0.0;
+  for (int gw = blockIdx.x * WPB + wid; gw < nstrips * nch; gw += gridDim.x * WPB) {
+    int strip, pa, pb;
+    item2(gw, nstrips, nch, g.p_lo, g.p_hi, strip, pa, pb);
+    const int x0 = strip * TX, ox = x0 + W * lane;
+    const int pg0 = g.p_glob0;
+    bool in[W];
+#pragma unroll
+    for (int j = 0; j < W; j++) in[j] = ox + j >= 1 && ox + j <= g.nx - 1;
+    const bool okv = ox <= g.nx;
+    const bool ring_ok = lane == 0 ? x0 - 1 >= 1 : (lane == 31 && x0 + TX <= g.nx - 1);
+    auto plin = [&](int p) {
+      const int pg = p + pg0;
+      return pg >= 1 && pg <= g.nz - 1;
+    };
+    R.t0 = pa - 1;
+    R.x = x0 - W;
+    const int nsteps = (pb - (pa - 1)) / RB + 1;
+    if (lane == 0) R.start(nsteps, &tm_u, &tm_f, !ZERO);
+    auto urow = [&](const T* row, T& e1, T& e2) -> V {
+      if (ZERO) {
+        e1 = e2 = (T)0;
+        return zvec<T>();
+      }
+      e1 = row[e1o];
+      e2 = row[e2o];
+      return ld_vec(row + vo);
+    };
+    T Bx1, Bx2, Cx1, Cx2;
+    R.wait(-1);
+    V B = urow(R.U(-1) + (RB - 2) * RW, Bx1, Bx2);  // u(pa-2) = pr(pa-2) at its black (old) entries
+    V Bo = B;                                       // u_old(t-1) (NRM)
+    V C = urow(R.U(-1) + (RB - 1) * RW, Cx1, Cx2);  // u_old(pa-1)
+    R.release(-1, nsteps, lane, &tm_u, &tm_f, !ZERO);
+    V A = zvec<T>();     // pr(t-2)
+    V Fm1 = zvec<T>();   // f(t-1)
+    T ring_prev = (T)0;  // relaxed ring node of row t-1 (when red)
+    for (int b = 0; b < nsteps; b++) {
+      R.wait(b);
+      const T* Ub = R.U(b);
+      const T* Fb = R.F(b);
+#pragma unroll
+      for (int i = 0; i < RB; i++) {
+        const int t = pa - 1 + b * RB + i;
+        if (t > pb) break;
+        T Dx1, Dx2;
+        const V Dn = urow(Ub + i * RW, Dx1, Dx2);  // u_old(t+1)
+        const V fv = ld_vec(Fb + i * RW + vo);
+        const T fe = Fb[i * RW + e1o];
+        const bool pin = plin(t);
+        T Cl, Cr;
+        edges(C, Cx1, Cx1, lane, Cl, Cr);
+        if (NRM && t >= pa && t < pb) {  // ||f - A u_in||^2 of row t (all old values)
+#pragma unroll
+          for (int j = 0; j < W; j++) {
+            const T l = j == 0 ? Cl : C.v[j > 0 ? j - 1 : 0];
+            const T r = j == W - 1 ? Cr : C.v[j < W - 1 ? j + 1 : 0];
+            const T rr = sub(fv.v[j], A2(c, C.v[j], l, r, Bo.v[j], Dn.v[j]));
+            if (in[j]) nsum = __dadd_rn(nsum, __dmul_rn((double)rr, (double)rr));
+          }
+        }
+        V prT = C;
+        T ring_cur = Cx1;
+        auto body = [&](auto KRc) {
+          constexpr int KR = decltype(KRc)::value;  // red elements of row t: j = KR + 2m
+          if (pin) {
+#pragma unroll
+            for (int m = 0; m < NR; m++) {
+              const int j = KR + 2 * m;
+              const T l = j == 0 ? Cl : C.v[j > 0 ? j - 1 : 0];
+              const T r = j == W - 1 ? Cr : C.v[j < W - 1 ? j + 1 : 0];
+              if (in[j]) prT.v[j] = relax2(c, C.v[j], l, r, B.v[j], Dn.v[j], fv.v[j]);
+            }
+            // ring node: lane 0's x0-1 is red in row t iff KR == 1, lane 31's x0+TX iff KR == 0
+            if (ring_ok && ((lane == 0) == (KR == 1)))
+              ring_cur = lane == 0 ? relax2(c, Cx1, Cx2, C.v[0], Bx1, Dx1, fe)
+                                   : relax2(c, Cx1, C.v[W - 1], Cx2, Bx1, Dx1, fe);
+          }
+          if (t - 1 >= pa) {  // black nodes of row t-1: the same elements j = KR + 2m
+            T Bl, Br;
+            edges(B, ring_prev, ring_prev, lane, Bl, Br);
+            V o = B;
+#pragma unroll
+            for (int m = 0; m < NR; m++) {
+              const int j = KR + 2 * m;
+              const T l = j == 0 ? Bl : B.v[j > 0 ? j - 1 : 0];
+              const T r = j == W - 1 ? Br : B.v[j < W - 1 ? j + 1 : 0];
+              if (in[j]) o.v[j] = relax2(c, B.v[j], l, r, A.v[j], prT.v[j], Fm1.v[j]);
+            }
+            if (okv) store_vec(uout + (long long)(t - 1) * g.pstride, ox, in, o);
+          }
+        };
+        if ((t + pg0) & 1)
+          body(std::integral_constant<int, 1>());
+        else
+          body(std::integral_constant<int, 0>());
+        A = B;
+        B = prT;
+        if (NRM) Bo = C;
+        Bx1 = Cx1;
+        Bx2 = Cx2;
+        C = Dn;
+        Cx1 = Dx1;
+        Cx2 = Dx2;
+        Fm1 = fv;
+        ring_prev = ring_cur;
+      }
+      R.release(b, nsteps, lane, &tm_u, &tm_f, !ZERO);
+    }
+    R.finish(nsteps);
+  }
+  if (NRM) block_partial(nsum, partial);
+}
+
+// ---------------------------------------------------------------------------
+// Fused residual + full weighting.  Warp = a coarse strip (TX/2 coarse nodes = the
+// fine strip x0 .. x0+TX) and a chunk [Pa, Pb) of coarse rows.  Per fine row t: r of
+// the lane's W nodes (lane 0 also r(x0-1)), the x-sums of its NR coarse nodes, and
+// the last three x-sums in registers; fine row 2J+1 completes coarse row J.
+template <typename T>
+__global__ void __launch_bounds__(NT) k_resid_restrict2d(const __grid_constant__ CUtensorMap tm_u,
+                                                         const __grid_constant__ CUtensorMap tm_f, Geom gf, Geom gc,
+                                                         Coef<T> c, T* __restrict__ fc, int nstrips, int nch) {
+  using V = VT<T>;
+  constexpr int W = G2<T>::W, TX = G2<T>::TX, NR = G2<T>::NR, RW = G2<T>::RW;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WRing<T> R;
+  R.init(smem, wid, lane);
+  prefetch_maps<T>(&tm_u, &tm_f, lane);
+  const int vo = W + W * lane;
+  const int e1o = lane == 0 ? W - 1 : W + TX, e2o = lane == 0 ? W - 2 : W + TX + 1;
+  const T two = (T)2, scale = (T)(1.0 / 16.0);
+  for (int gw = blockIdx.x * WPB + wid; gw < nstrips * nch; gw += gridDim.x * WPB) {
+    int strip, Pa, Pb;
+    item2(gw, nstrips, nch, gc.p_lo, gc.p_hi, strip, Pa, Pb);
+    const int x0 = strip * TX, ox = x0 + W * lane;
+    bool in[W];
+#pragma unroll
+    for (int j = 0; j < W; j++) in[j] = ox + j >= 1 && ox + j <= gf.nx - 1;
+    const bool ring_ok = lane == 0 && x0 - 1 >= 1;  // r(x0-1) is an interior residual
+    auto plin = [&](int t) {
+      const int tg = t + gf.p_glob0;
+      return tg >= 1 && tg <= gf.nz - 1;
+    };
+    const int qf0 = 2 * (Pa + gc.p_glob0) - gf.p_glob0;      // fine centre row of coarse row Pa
+    const int qf1 = 2 * (Pb - 1 + gc.p_glob0) - gf.p_glob0;  // ... of coarse row Pb-1
+    const int rlo = qf0 - 1, rhi = qf1 + 1;
+    R.t0 = rlo;
+    R.x = x0 - W;
+    const int nsteps = (rhi - rlo) / RB + 1;
+    if (lane == 0) R.start(nsteps, &tm_u, &tm_f, true);
+    auto urow = [&](const T* row, T& e1, T& e2) -> V {
+      e1 = row[e1o];
+      e2 = row[e2o];
+      return ld_vec(row + vo);
+    };
+    T umx1, umx2, u0x1, u0x2;
+    R.wait(-1);
+    V um = urow(R.U(-1) + (RB - 2) * RW, umx1, umx2);
+    V u0 = urow(R.U(-1) + (RB - 1) * RW, u0x1, u0x2);
+    R.release(-1, nsteps, lane, &tm_u, &tm_f, true);
+    T ty1[NR], ty2[NR];
+#pragma unroll
+    for (int i = 0; i < NR; i++) ty1[i] = ty2[i] = (T)0;
+    const int I0 = ox >> 1;
+    for (int b = 0; b < nsteps; b++) {
+      R.wait(b);
+      const T* Ub = R.U(b);
+      const T* Fb = R.F(b);
+#pragma unroll
+      for (int ii = 0; ii < RB; ii++) {
+        const int t = rlo + b * RB + ii;
+        if (t > rhi) break;
+        T upx1, upx2;
+        const V up = urow(Ub + ii * RW, upx1, upx2);
+        const V fv = ld_vec(Fb + ii * RW + vo);
+        const T fe = Fb[ii * RW + e1o];
+        const bool pin = plin(t);
+        T l0, r0;
+        edges(u0, u0x1, u0x1, lane, l0, r0);
+        V rv;
+#pragma unroll
+        for (int j = 0; j < W; j++) {
+          const T l = j == 0 ? l0 : u0.v[j > 0 ? j - 1 : 0];
+          const T r = j == W - 1 ? r0 : u0.v[j < W - 1 ? j + 1 : 0];
+          const T rr = sub(fv.v[j], A2(c, u0.v[j], l, r, um.v[j], up.v[j]));
+          rv.v[j] = pin && in[j] ? rr : (T)0;
+        }
+        T rx = (T)0;  // lane 0: r(x0-1)
+        if (pin && ring_ok) rx = sub(fe, A2(c, u0x1, u0x2, u0.v[0], umx1, upx1));
+        T rl = __shfl_up_sync(FULL, rv.v[W - 1], 1);
+        if (lane == 0) rl = rx;
+        T tx[NR];
+#pragma unroll
+        for (int i = 0; i < NR; i++) {
+          const T left = i == 0 ? rl : rv.v[i > 0 ? 2 * i - 1 : 0];
+          tx[i] = add(add(left, rv.v[2 * i + 1]), mul(two, rv.v[2 * i]));
+        }
+        const int tg = t + gf.p_glob0;
+        if ((tg & 1) == 1 && t >= qf0 + 1) {  // fine row 2J+1 completes coarse row J
+          const int J = (tg - 1) >> 1;
+          T* crow = fc + (long long)(J - gc.p_glob0) * gc.pstride;
+          if (J >= 1 && J <= gc.nz - 1) {
+#pragma unroll
+            for (int i = 0; i < NR; i++) {
+              const int I = I0 + i;
+              if (I >= 1 && I <= gc.nx - 1) crow[I] = mul(add(add(ty2[i], tx[i]), mul(two, ty1[i])), scale);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < NR; i++) {
+          ty2[i] = ty1[i];
+          ty1[i] = tx[i];
+        }
+        um = u0;
+        umx1 = u0x1;
+        u0 = up;
+        u0x1 = upx1;
+        u0x2 = upx2;
+      }
+      R.release(b, nsteps, lane, &tm_u, &tm_f, true);
+    }
+    R.finish(nsteps);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// u += P e on interior fine nodes.  Fine row z = 2Z + dz gets dz ? (V(Z) + V(Z+1))/2
+// : V(Z), V(K) = coarse row K interpolated along x (reading 13 order: x, then y).
+template <typename T>
+__global__ void __launch_bounds__(NT) k_prolong2d(Geom gf, Geom gc, const T* __restrict__ e, T* __restrict__ u,
+                                                  int nstrips, int nch) {
+  using V = VT<T>;
+  constexpr int W = G2<T>::W, TX = G2<T>::TX, NR = G2<T>::NR;
+  const int lane = threadIdx.x & 31, gw = blockIdx.x * WPB + (threadIdx.x >> 5);
+  if (gw >= nstrips * nch) return;
+  int strip, pa, pb;
+  item2(gw, nstrips, nch, gf.p_lo, gf.p_hi, strip, pa, pb);
+  const int ox = strip * TX + W * lane;
+  bool in[W], any = false, all = true;
+#pragma unroll
+  for (int j = 0; j < W; j++) {
+    in[j] = ox + j >= 1 && ox + j <= gf.nx - 1;
+    any = any || in[j];
+    all = all && in[j];
+  }
+  if (!any) return;
+  const T half = (T)0.5;
+  const int X = ox >> 1;
+  auto Vz = [&](int Zg) -> V {
+    const T* p0 = e + (long long)(Zg - gc.p_glob0) * gc.pstride + X;
+    T a[NR + 1];
+#pragma unroll
+    for (int i = 0; i <= NR; i++) a[i] = X + i <= gc.nx ? __ldg(p0 + i) : (T)0;
+    V v;
+#pragma unroll
+    for (int i = 0; i < NR; i++) {
+      v.v[2 * i] = a[i];
+      v.v[2 * i + 1] = mul(half, add(a[i], a[i + 1]));
+    }
+    return v;
+  };
+  int Z = (pa + gf.p_glob0) >> 1;
+  V Av = Vz(Z), Bv = Av;
+  bool haveB = false;
+  for (int z = pa; z < pb; z++) {
+    const int zg = z + gf.p_glob0;
+    if ((zg >> 1) != Z) {
+      Z++;
+      Av = haveB ? Bv : Vz(Z);
+      haveB = false;
+    }
+    V v = Av;
+    if (zg & 1) {
+      if (!haveB) {
+        Bv = Vz(Z + 1);
+        haveB = true;
+      }
+#pragma unroll
+      for (int j = 0; j < W; j++) v.v[j] = mul(half, add(Av.v[j], Bv.v[j]));
+    }
+    T* up = u + (long long)z * gf.pstride;
+    if (all) {
+      const V uu = ld_vec(up + ox);
+      V o;
+#pragma unroll
+      for (int j = 0; j < W; j++) o.v[j] = add(uu.v[j], v.v[j]);
+      store_vec(up, ox, in, o);
+    } else {
+#pragma unroll
+      for (int j = 0; j < W; j++)
+        if (in[j]) up[ox + j] = add(up[ox + j], v.v[j]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launch geometry: one wave of resident warps; rows split evenly, >= kMinRows per chunk
+constexpr int kMinRows = 16;
+
+template <class K>
+static int resident_warps(K kernel, int smem) {
+  static const void* keys[32];
+  static int vals[32];
+  static int n = 0;
+  for (int i = 0; i < n; i++)
+    if (keys[i] == (const void*)kernel) return vals[i];
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int sms = 0, occ = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, NT, smem);
+  const int r = (occ < 1 ? 1 : occ) * (sms < 1 ? 1 : sms) * WPB;
+  if (n < 32) {
+    keys[n] = (const void*)kernel;
+    vals[n++] = r;
+  }
+  return r;
+}
+
+static void split(int nstrips, int rows, int rw, int& nch, int& nblocks) {
+  nch = rw / nstrips;
+  const int cap = rows / kMinRows;
+  if (nch > cap) nch = cap;
+  if (nch < 1) nch = 1;
+  nblocks = (nstrips * nch + WPB - 1) / WPB;
+}
+
+template <typename T>
+static int strips(const Geom& g) {
+  return (g.nx + G2<T>::TX - 1) / G2<T>::TX;  // covers x in [0, nx): every interior column
+}
+
+// 2D tensor map of a level array: dims (nx+1, planes), box (RW, RB) — OOB reads are zero
+template <typename T>
+static bool encode2d(CUtensorMap* tm, const T* base, const Geom& g) {
+  const unsigned long long dims[2] = {(unsigned long long)(g.nx + 1), (unsigned long long)g.planes};
+  const unsigned long long strides[1] = {(unsigned long long)(g.pstride * sizeof(T))};
+  const unsigned box[2] = {(unsigned)G2<T>::RW, (unsigned)RB};
+  return pm::encode_tiled(tm, sizeof(T) == 8, 2, base, dims, strides, box) == CUDA_SUCCESS;
+}
+
+bool supported(const Geom& g, int min_nx) {
+  return !g.three_d && g.nx >= (min_nx < 16 ? 16 : min_nx) && (g.p_hi - g.p_lo) >= 4;
+}
+
+template <typename T>
+cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
+                         cudaStream_t st, double* partial, int* npartial) {
+  const bool nrm = partial && !zero_in;
+  CUtensorMap tu, tf;
+  if (!encode2d<T>(&tu, uin ? uin : f, g) || !encode2d<T>(&tf, f, g)) return cudaErrorInvalidValue;
+  const int ns = strips<T>(g), smem = G2<T>::SMEM;
+  int nch, nb;
+  auto go = [&](auto kernel) {
+    split(ns, g.p_hi - g.p_lo, resident_warps(kernel, smem), nch, nb);
+    if (npartial) *npartial = nb;
+    kernel<<<nb, NT, smem, st>>>(tu, tf, g, c, uout, ns, nch, partial);
+  };
+  if (rbgs) {
+    if (nrm)
+      go(k_rbgs2d<T, false, true>);
+    else
+      zero_in ? go(k_rbgs2d<T, true, false>) : go(k_rbgs2d<T, false, false>);
+  } else {
+    if (nrm)
+      go(k_jacobi2d<T, 0, false, true>);
+    else
+      zero_in ? go(k_jacobi2d<T, 0, true, false>) : go(k_jacobi2d<T, 0, false, false>);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+int sweep_partials(const Geom& g, bool rbgs) {
+  int nch, nb;
+  const int smem = G2<T>::SMEM;
+  const int rw = rbgs ? resident_warps(k_rbgs2d<T, false, true>, smem)
+                      : resident_warps(k_jacobi2d<T, 0, false, true>, smem);
+  split(strips<T>(g), g.p_hi - g.p_lo, rw, nch, nb);
+  return nb;
+}
+
+template <typename T>
+cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f, double* partial, int* npartial,
+                        cudaStream_t st) {
+  CUtensorMap tu, tf;
+  if (!encode2d<T>(&tu, u, g) || !encode2d<T>(&tf, f, g)) return cudaErrorInvalidValue;
+  auto kernel = k_jacobi2d<T, 2, false, false>;
+  const int ns = strips<T>(g), smem = G2<T>::SMEM;
+  int nch, nb;
+  split(ns, g.p_hi - g.p_lo, resident_warps(kernel, smem), nch, nb);
+  *npartial = nb;
+  kernel<<<nb, NT, smem, st>>>(tu, tf, g, c, nullptr, ns, nch, partial);
+  return cudaGetLastError();
+}
+
+template <typename T>
+int norm_partials(const Geom& g) {
+  int nch, nb;
+  split(strips<T>(g), g.p_hi - g.p_lo, resident_warps(k_jacobi2d<T, 2, false, false>, G2<T>::SMEM), nch, nb);
+  return nb;
+}
+
+template <typename T>
+cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>& c, const T* u, const T* f, T* fc,
+                                  cudaStream_t st) {
+  CUtensorMap tu, tf;
+  if (!encode2d<T>(&tu, u, gf) || !encode2d<T>(&tf, f, gf)) return cudaErrorInvalidValue;
+  auto kernel = k_resid_restrict2d<T>;
+  const int ns = strips<T>(gf), smem = G2<T>::SMEM;
+  int nch, nb;
+  split(ns, gc.p_hi - gc.p_lo, resident_warps(kernel, smem), nch, nb);
+  kernel<<<nb, NT, smem, st>>>(tu, tf, gf, gc, c, fc, ns, nch);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cudaStream_t st) {
+  auto kernel = k_prolong2d<T>;
+  const int ns = strips<T>(gf);
+  int nch, nb;
+  split(ns, gf.p_hi - gf.p_lo, resident_warps(kernel, 0), nch, nb);
+  kernel<<<nb, NT, 0, st>>>(gf, gc, e, u, ns, nch);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool, const double*, const double*,
+                                          double*, bool, cudaStream_t, double*, int*);
+template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
+                                         bool, cudaStream_t, double*, int*);
+template int sweep_partials<double>(const Geom&, bool);
+template int sweep_partials<float>(const Geom&, bool);
+template cudaError_t launch_norm<double>(const Geom&, const Coef<double>&, const double*, const double*, double*,
+                                         int*, cudaStream_t);
+template cudaError_t launch_norm<float>(const Geom&, const Coef<float>&, const float*, const float*, double*, int*,
+                                        cudaStream_t);
+template int norm_partials<double>(const Geom&);
+template int norm_partials<float>(const Geom&);
+template cudaError_t launch_resid_restrict<double>(const Geom&, const Geom&, const Coef<double>&, const double*,
+                                                   const double*, double*, cudaStream_t);
+template cudaError_t launch_resid_restrict<float>(const Geom&, const Geom&, const Coef<float>&, const float*,
+                                                  const float*, float*, cudaStream_t);
+template cudaError_t launch_prolong<double>(const Geom&, const Geom&, const double*, double*, cudaStream_t);
+template cudaError_t launch_prolong<float>(const Geom&, const Geom&, const float*, float*, cudaStream_t);
+
+}  // namespace pm2
+}  // namespace mg

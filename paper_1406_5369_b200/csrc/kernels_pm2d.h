@@ -1,0 +1,26 @@
+// kernels_pm2d.h — launchers of the warp-marching kernels for 2D levels
+// (kernels_pm2d.cu).  Reached through the pm:: launchers, which dispatch on
+// Geom::three_d.
+#pragma once
+#include "mg_common.cuh"
+
+namespace mg {
+namespace pm2 {
+bool supported(const Geom& g, int min_nx);
+template <typename T>
+cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
+                         cudaStream_t st, double* partial, int* npartial);
+template <typename T>
+int sweep_partials(const Geom& g, bool rbgs);
+template <typename T>
+cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f, double* partial, int* npartial,
+                        cudaStream_t st);
+template <typename T>
+int norm_partials(const Geom& g);
+template <typename T>
+cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>& c, const T* u, const T* f, T* fc,
+                                  cudaStream_t st);
+template <typename T>
+cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cudaStream_t st);
+}  // namespace pm2
+}  // namespace mg

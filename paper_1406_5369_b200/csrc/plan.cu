@@ -583,7 +583,7 @@ struct Exec {
         if ((r = exchange(l + 1, cur[l + 1], 1)) != MG_OK) return r;  // e_H neighbour planes (slabs)
         const T* e = cur[l + 1];
         const bool pml = pm(l);
-        if (pml && s->cfg.nu2 >= 1 && (s->cfg.flags & MG_FLAG_FUSE_PROLONG)) {
+        if (pml && L.g.three_d && s->cfg.nu2 >= 1 && (s->cfg.flags & MG_FLAG_FUSE_PROLONG)) {
           // prolongation + correction fused into the first post-sweep: u + P e is formed in
           // shared memory, only S(u + P e) is written
           const bool rb = s->cfg.smoother == MG_RBGS;
