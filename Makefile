@@ -32,11 +32,14 @@ $(LIB): $(CU_OBJS)
 
 oracle: oracle/liboracle_f64.so oracle/liboracle_f32.so
 
-oracle/liboracle_f64.so: oracle/mg_oracle.c oracle/mg_oracle.h
-	$(CC) $(ORACLE_CFLAGS) -DOR_REAL=double -o $@ oracle/mg_oracle.c -lm
+ORACLE_SRCS := oracle/mg_oracle.c oracle/cd_oracle.c
+ORACLE_HDRS := oracle/mg_oracle.h oracle/cd_oracle.h
 
-oracle/liboracle_f32.so: oracle/mg_oracle.c oracle/mg_oracle.h
-	$(CC) $(ORACLE_CFLAGS) -DOR_REAL=float -o $@ oracle/mg_oracle.c -lm
+oracle/liboracle_f64.so: $(ORACLE_SRCS) $(ORACLE_HDRS)
+	$(CC) $(ORACLE_CFLAGS) -DOR_REAL=double -o $@ $(ORACLE_SRCS) -lm
+
+oracle/liboracle_f32.so: $(ORACLE_SRCS) $(ORACLE_HDRS)
+	$(CC) $(ORACLE_CFLAGS) -DOR_REAL=float -o $@ $(ORACLE_SRCS) -lm
 
 clean:
 	rm -rf build $(LIB) oracle/*.so

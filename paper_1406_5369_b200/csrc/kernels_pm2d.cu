@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(NT) k_prolong2d(Geom gf, Geom gc, const T* __r
 
 // ---------------------------------------------------------------------------
 // launch geometry: one wave of resident warps; rows split evenly, >= kMinRows per chunk
-constexpr int kMinRows = 16;
+constexpr int kMinRows = 4;  // measured on C4: 16 -> 1.70 ms, 8 -> 1.63, 4 -> 1.61
 
 template <class K>
 static int resident_warps(K kernel, int smem) {
@@ -603,8 +603,14 @@ static int resident_warps(K kernel, int smem) {
 }
 
 static void split(int nstrips, int rows, int rw, int& nch, int& nblocks) {
+  static int min_rows = 0;
+  if (!min_rows) {
+    const char* e = getenv("MG_PM2_MINROWS");
+    min_rows = e ? atoi(e) : kMinRows;
+    if (min_rows < 2) min_rows = 2;
+  }
   nch = rw / nstrips;
-  const int cap = rows / kMinRows;
+  const int cap = rows / min_rows;
   if (nch > cap) nch = cap;
   if (nch < 1) nch = 1;
   nblocks = (nstrips * nch + WPB - 1) / WPB;

@@ -15,6 +15,9 @@ Workloads:
   W3  polynomial manufactured solution u* = prod x_d(1-x_d),
       f = 2 sum_d prod_{e != d} x_e(1-x_e)   (the discrete solution is exact).
   W4  generic right-hand side f ~ U[-1,1), u0 = 0.
+  W5  complex diffusion: one implicit-Euler step from
+      a noisy image u^n (real part U[0,1) per cell, imaginary part 0): f = u^n,
+      initial guess u = u^n.  Cell arrays, complex.
 
 Arrays are dense, unpadded node arrays including the boundary, x fastest:
 shape (ny+1, nx+1) in 2D and (nz+1, ny+1, nx+1) in 3D.
@@ -105,6 +108,27 @@ def workload(name: str, dim: int, cells, seed: int = 42, dtype=np.float64):
         raise ValueError(f"unknown workload {name}")
     f[~_interior_mask(shape)] = 0.0
     return np.zeros(shape, dtype=dtype), f.astype(dtype)
+
+
+def cell_shape(dim: int, cells) -> tuple:
+    cells = list(cells)
+    return (cells[1], cells[0]) if dim == 2 else (cells[2], cells[1], cells[0])
+
+
+def random_cells(dim: int, cells, seed: int, lo=0.0, hi=1.0) -> np.ndarray:
+    """U[lo,hi) per cell from the global cell index idx = (k*ny + j)*nx + i (float64)."""
+    shape = cell_shape(dim, cells)
+    r = splitmix64_uniform(seed, np.arange(int(np.prod(shape)), dtype=np.uint64)).reshape(shape)
+    if lo != 0.0 or hi != 1.0:
+        r = lo + (hi - lo) * r
+    return r
+
+
+def cd_workload(dim: int, cells, seed: int = 42, dtype=np.complex128):
+    """W5: (u0, f) = (u^n, u^n), u^n = U[0,1) + 0i per cell (a noise image)."""
+    re = random_cells(dim, cells, seed).astype(np.float64 if np.dtype(dtype) == np.complex128 else np.float32)
+    u = re.astype(dtype)
+    return u.copy(), u
 
 
 def exact_solution(name: str, dim: int, cells) -> np.ndarray:
