@@ -47,7 +47,26 @@ WORKLOAD_DESC = {
     "C5": "3D Poisson 7-point 1025^3 nodes, RBGS V(2,2), FP64, W1 seed 42",
     "C1": "2D Poisson 5-point 65^2 nodes, 5 levels, Jacobi(0.8) V(2,2), FP64, W1 seed 42",
 }
+# complex diffusion, FAS on cell-centred grids (the paper's Table 2
+# "Complex Diff." rows: N = 4096^2 cells in 2D, 256^3 in 3D)
+# name: (dim, cells, smoother, nu1, nu2, dtype, omega)
+CD_CONFIGS = {
+    "CD2-f32": (2, 4096, "jacobi", 2, 2, "f32", 0.8),
+    "CD2-gs-f32": (2, 4096, "rbgs", 2, 2, "f32", 1.0),
+    "CD2-f64": (2, 4096, "jacobi", 2, 2, "f64", 0.8),
+    "CD3-f32": (3, 256, "jacobi", 2, 2, "f32", 0.8),
+    "CD3-gs-f32": (3, 256, "rbgs", 2, 2, "f32", 1.0),
+}
+for _k, (_d, _n, _sm, _a, _b, _dt, _om) in CD_CONFIGS.items():
+    WORKLOAD_DESC[_k] = (f"{_d}D complex diffusion (one implicit-Euler step, tau=0.1, theta=pi/30, k=2), "
+                         f"{_n}^{_d} cells, Neumann, FAS V({_a},{_b}) "
+                         f"{'Jacobi(0.8)' if _sm == 'jacobi' else 'RBGS'}, complex {_dt.upper()}, "
+                         f"W5 (noise image u^n ~ U[0,1) seed 42, f = u^n)")
 METRIC = "V(2,2)-cycle unknowns/s (one cycle + residual norm per step)"
+
+
+def is_cd(name):
+    return name in CD_CONFIGS
 
 
 def dist_env():
@@ -72,6 +91,37 @@ def model_bytes_per_step(S, esz):
     for c in S.level_cells(0):
         n0 *= c + 1
     return total + 2 * n0 * esz
+
+
+def l2_note(array_bytes):
+    if array_bytes > 126e6:
+        return f"inputs larger than L2 ({array_bytes / 1e9:.3f} GB per array), no flush needed"
+    return (f"inputs L2-resident ({array_bytes / 1e6:.1f} MB per array < 126 MB L2): no flush; this config "
+            "measures the L2-resident regime")
+
+
+def cd_model_bytes_per_step(S, esz):
+    """Complex diffusion, op-by-op FAS schedule (kernels_cd.cu), complex words s = 2 esz per cell:
+    per level l < L-1: g field 2, Jacobi sweep 4 (read u, g, f; write u) x (nu1+nu2) [RBGS: 2 colour
+    passes of 2.5 each], u^ = R u 1 + 2/2^d, coarse g 2/2^d, FAS rhs 3 + 3/2^d, prolongation 2 + 2/2^d;
+    coarsest: g 2 + ncoarse sweeps; + the norm pass (2 words of level 0)."""
+    s = 2 * esz
+    sweep = 4.0 if S.cfg.smoother == 0 else 5.0
+    nu = S.cfg.nu1 + S.cfg.nu2
+    q = 2.0 ** -S.dim
+    total = 0.0
+    for l in range(S.levels):
+        n = 1
+        for c in S.level_cells(l):
+            n *= c
+        if l < S.levels - 1:
+            total += n * s * (2 + sweep * nu + (1 + 2 * q) + 2 * q + (3 + 3 * q) + (2 + 2 * q))
+        else:
+            total += n * s * (2 + sweep * S.cfg.ncoarse)
+    n0 = 1
+    for c in S.level_cells(0):
+        n0 *= c
+    return total + 2 * n0 * s
 
 
 class ClockSampler:
@@ -154,6 +204,8 @@ def oracle_step_time(cfgname, max_seconds=30.0):
 
     import oracle as orc
     from paper_1406_5369_b200 import workloads as wl
+    if is_cd(cfgname):
+        return cd_oracle_step_time(cfgname, max_seconds)
     dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[cfgname]
     cells = (nodes - 1,) * dim
     # full size when it fits the budget, else the largest power-of-two grid that does
@@ -176,6 +228,43 @@ def oracle_step_time(cfgname, max_seconds=30.0):
     raise RuntimeError("unreachable")
 
 
+class _CdStepper:
+    """Adapter so the reference arm can step the complex-diffusion oracle like the Poisson one."""
+
+    def __init__(self, O):
+        self.O = O
+
+    def vcycle_inplace(self, u, f):
+        u[...] = self.O.cycle(u, f)
+
+    def norm(self, l, u, f):
+        return self.O.norm(l, u, f)
+
+
+def cd_oracle_step_time(cfgname, max_seconds):
+    import numpy as np
+
+    from oracle.cd import CDConfig, CDOracle, JACOBI, RBGS
+    from paper_1406_5369_b200 import workloads as wl
+    dim, n0, sm, nu1, nu2, dt, omega = CD_CONFIGS[cfgname]
+    cdt = np.complex128 if dt == "f64" else np.complex64
+    for n in [n0, n0 // 2, n0 // 4, n0 // 8]:
+        cells = (n,) * dim
+        O = CDOracle(CDConfig(dim=dim, cells=cells, smoother=RBGS if sm == "rbgs" else JACOBI, omega=omega,
+                              nu1=nu1, nu2=nu2), cdt)
+        u, f = wl.cd_workload(dim, cells, 42, cdt)
+        t0 = time.perf_counter()
+        u = O.cycle(u, f)
+        O.norm(0, u, f)
+        t = time.perf_counter() - t0
+        if t <= max_seconds or n == n0 // 8:
+            desc = (f"one FAS V({nu1},{nu2})-cycle + nonlinear residual norm of the CPU oracle (plain C, -O2 "
+                    f"-ffp-contract=off, one thread) on {'x'.join(str(c) for c in cells)} cells, W5 seed 42"
+                    + ("" if n == n0 else f" (reduced from {n0}^{dim} to fit the CPU time budget)"))
+            return t, n ** dim, desc, 1, (_CdStepper(O), u, f)
+    raise RuntimeError("unreachable")
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -191,11 +280,13 @@ def run_reference(args):
         O.norm(0, u, f)
     dt = (time.perf_counter() - t0) / args.steps
     val = unk / dt
-    dim, nodes, *_ = CONFIGS[args.config]
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "unknowns/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": CONFIGS[args.config][5], "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": (("c" if is_cd(args.config) else "") + (CD_CONFIGS[args.config][5] if is_cd(args.config)
+                                                          else CONFIGS[args.config][5])),
+        "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC[args.config], "parallelism": "cpu-oracle",
                    "l2": "inputs larger than L2 (CPU run)"},
         "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": threads, "kind": "oracle", "sample": desc},
@@ -218,13 +309,20 @@ def run_mg(args):
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[args.config]
+    cd = is_cd(args.config)
+    if cd:  # complex diffusion: `nodes` are cells, FAS with ncoarse sweeps on the coarsest level
+        dim, nodes, sm, nu1, nu2, dt, omega = CD_CONFIGS[args.config]
+        levels = 0
+    else:
+        dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[args.config]
     esz = 8 if dt == "f64" else 4
     kw = dict(levels=levels, smoother=sm, omega=omega, nu1=nu1, nu2=nu2, dtype=dt, device=dev,
               flags=mgb.FLAG_HOST_LOOP if args.host_loop else 0)
+    if cd:
+        kw.update(problem="complex_diffusion", coarse="sweeps")
     # mg_solve runs its loop on the device (one CUDA graph, conditional WHILE node) unless
     # --host-loop or the slab run spans several ranks (NCCL cannot run in a conditional body)
-    slab = world > 1 and args.decomp == "slab"
+    slab = world > 1 and args.decomp == "slab" and not cd
     device_loop = not args.host_loop and not slab
     if slab:  # z-slab decomposition of ONE global grid over the ranks (strong scaling), NCCL halos
         S = mgb.distributed_solver(dim, nodes, **kw)
@@ -235,8 +333,10 @@ def run_mg(args):
     f = S.empty()
     with torch.cuda.stream(stream):
         S.workload_fill(u, 42, stream=stream)
+        if cd:  # W5: f = u^n = the initial iterate
+            S.workload_fill(f, 42, stream=stream)
     torch.cuda.synchronize()
-    unk = interior_unknowns(dim, nodes)
+    unk = nodes ** dim if cd else interior_unknowns(dim, nodes)
 
     # K steps = the library's driver loop mg_solve(rtol=0, max_cycles=K): K V-cycles, each
     # followed by the residual norm (pipelined into the next cycle's first sweep; the
@@ -289,7 +389,7 @@ def run_mg(args):
         "alg_bytes_per_launch": dom["bytes"], "avg_launch_ms": dom_avg_ms,
         "share_of_step": dom["ms"] / tot if tot else None,
     }
-    B = model_bytes_per_step(S, esz)
+    B = cd_model_bytes_per_step(S, esz) if cd else model_bytes_per_step(S, esz)
     breakdown = sorted(({"kernel": r["name"], "ms_per_step": r["ms"] / nprof, "launches_per_step": r["count"] / nprof,
                          "GBps": (r["bytes"] * r["count"] / (r["ms"] * 1e-3) / 1e9) if r["ms"] else None}
                         for r in recs), key=lambda d: -d["ms_per_step"])[:8]
@@ -331,11 +431,13 @@ def run_mg(args):
         line = {
             "metric": METRIC, "value": unk_total / (ms * 1e-3), "unit": "unknowns/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
-            "config": {"workload": WORKLOAD_DESC[args.config], "grid_nodes": nodes, "dim": dim,
+            "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": ("c" if cd else "") + dt,
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC[args.config], ("grid_cells" if cd else "grid_nodes"): nodes,
+                       "dim": dim,
                        "parallelism": (f"z-slab x{world} (NCCL halos, agglomeration below 8 planes/rank)" if slab
                                        else ("replicas" if world > 1 else "single-gpu")),
-                       "l2": "inputs larger than L2 (1.08 GB per array), no flush needed",
+                       "l2": l2_note(S.shape[0] * S.shape[1] * S.shape[2] * esz * (2 if cd else 1)),
                        "levels": S.levels,
                        "driver": "device loop (CUDA graph WHILE node)" if device_loop else "host loop"},
             "residual_reduction_per_step": (rk / r0) ** (1.0 / (args.steps + args.warmup)) if r0 else None,
@@ -356,7 +458,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mg", choices=["mg", "reference"])
-    ap.add_argument("--config", default="C3-f64", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C3-f64", choices=sorted(CONFIGS) + sorted(CD_CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-loop", action="store_true", help="mg_solve with MG_FLAG_HOST_LOOP (per-cycle sync)")

@@ -54,6 +54,18 @@ typedef enum {
 typedef enum { MG_JACOBI = 0, MG_RBGS = 1 } mg_smoother;      /* P:224 */
 typedef enum { MG_FP64 = 0, MG_FP32 = 1 } mg_dtype;           /* Table 1 P:350 */
 typedef enum { MG_COARSE_DIRECT = 0, MG_COARSE_SWEEPS = 1 } mg_coarse; /* P:191, P:281 */
+/* The problem (Table 1 "Operator", P:347-352):
+ *  MG_PROBLEM_POISSON: A = -sum a_d d^2/dx_d^2 on a NODE-based grid, Dirichlet data in
+ *    u's boundary nodes, correction-scheme V-cycle (Alg. 1).
+ *  MG_PROBLEM_COMPLEX_DIFFUSION: one implicit-Euler step of nonlinear isotropic complex
+ *    diffusion u - tau div(g(Im u) grad u) = f, g = e^{i theta}/(1 + (Im u/(kappa theta))^2)
+ *    (Eqs. 2-3, P:521-535), averaged finite differences on a CELL-centred grid with
+ *    Neumann (zero-flux) boundaries, FAS V-cycle with lagged diffusivity, cell-average
+ *    restriction and constant interpolation (P:534; DESIGN.md §11).  Arrays hold COMPLEX
+ *    values, (re, im) interleaved, of the precision `dtype`; nodes[d] then counts CELLS
+ *    (the unknowns) per axis; there are no boundary entries; coarse must be
+ *    MG_COARSE_SWEEPS (ncoarse sweeps on the coarsest level); nranks must be 1. */
+typedef enum { MG_PROBLEM_POISSON = 0, MG_PROBLEM_COMPLEX_DIFFUSION = 1 } mg_problem;
 
 /* flags */
 #define MG_FLAG_NO_GRAPH 1u   /* launch eagerly instead of replaying a CUDA graph   */
@@ -85,12 +97,18 @@ typedef struct {
                             rank, e.g. broadcast with torch.distributed), else NULL.
                             mg_create is then collective: all ranks must call it.      */
     uint32_t flags;      /* MG_FLAG_*                                                   */
-    int32_t pm_min_nx;   /* smallest x-extent (cells) of a 3D level that uses the plane-
+    int32_t pm_min_nx;   /* smallest x-extent (cells) of a level that uses the plane-
                             marching kernels; 0 => 128.  Smaller levels use one thread per
                             node.  Results are bitwise identical either way.              */
+    int32_t problem;     /* mg_problem (default MG_PROBLEM_POISSON)                     */
+    double tau;          /* complex diffusion: implicit-Euler time step (default 0.1)    */
+    double theta;        /* complex diffusion: angle of Eq. 3 (default pi/30)            */
+    double kappa;        /* complex diffusion: scaling k of Eq. 3 (default 2); the paper
+                            gives no values (S:372)                                        */
 } mg_config;
 
-/* Fill `cfg` with the defaults above for a `dim`-D grid of `nodes` per axis. */
+/* Fill `cfg` with the defaults above for a `dim`-D grid of `nodes` per axis
+ * (complex diffusion: set problem, coarse = MG_COARSE_SWEEPS and nodes = cells). */
 void mg_config_default(mg_config* cfg, int32_t dim, int64_t nodes);
 
 /* Validate `cfg`, build the level hierarchy (h_l = 2^l h, re-discretised
@@ -117,13 +135,14 @@ mg_status mg_partition(const mg_config* cfg, int32_t level, int64_t* first_plane
 mg_status mg_level_layout(const mg_solver* s, int32_t level, int64_t shape[3]);
 int32_t mg_num_levels(const mg_solver* s);
 
-/* One V(nu1,nu2)-cycle of Alg. 1 (P:187-219), in place on u, asynchronous on
- * `stream`.  Replays a cached CUDA graph for this (u, f) unless
+/* One V(nu1,nu2)-cycle of Alg. 1 (P:187-219) — for complex diffusion one FAS
+ * V-cycle (S:431-439) — in place on u, asynchronous on `stream`.  Replays a cached CUDA graph for this (u, f) unless
  * MG_FLAG_NO_GRAPH. */
 mg_status mg_vcycle(mg_solver* s, void* u, const void* f, void* stream);
 
 /* ||f - A u||_2 over interior nodes, unscaled (L2Residual, P:266-274; S:543),
- * FP64 accumulation, deterministic reduction order.  Blocking. */
+ * FP64 accumulation, deterministic reduction order.  Blocking.  Complex diffusion:
+ * the nonlinear residual ||f - A(u) u||_2 with the diffusivity evaluated from u. */
 mg_status mg_residual_norm(mg_solver* s, const void* u, const void* f, double* out, void* stream);
 
 /* Driver loop of the `Application` listing (P:264-276): r0 = norm; repeat
@@ -147,7 +166,12 @@ mg_status mg_vcycle_host(mg_solver* s, void* u_host, const void* f_host, int32_t
                          double* norm_out, void* stream);
 
 /* ---- per-operation entry points (one step of Alg. 1 each, for parity tests).
- * Arrays use mg_level_layout(level).  Asynchronous unless stated. */
+ * Arrays use mg_level_layout(level).  Asynchronous unless stated.
+ * Complex diffusion: mg_op_smooth freezes the diffusivity at g(u_in) (lagged) and
+ * sweeps once; mg_op_residual gives f - A(g(u)) u; mg_op_restrict is the cell average;
+ * mg_op_prolong_correct adds the parent cell's value (constant interpolation);
+ * mg_op_norm is the nonlinear residual norm; mg_op_coarse_solve is not available
+ * (MG_ERR_INVALID: the FAS coarsest level is ncoarse sweeps). */
 /* one sweep of the configured smoother S_h (P:224, listing P:299-305):
  * u_out = S(u_in); u_out may equal u_in.  Boundary nodes of u_out := u_in's. */
 mg_status mg_op_smooth(mg_solver* s, int32_t level, const void* u_in, const void* f, void* u_out, void* stream);

@@ -24,6 +24,7 @@ JACOBI, RBGS = 0, 1
 FP64, FP32 = 0, 1
 COARSE_DIRECT, COARSE_SWEEPS = 0, 1
 FLAG_NO_GRAPH, FLAG_BASELINE, FLAG_SLAB, FLAG_FUSE_PROLONG, FLAG_HOST_LOOP = 1, 2, 4, 8, 16
+PROBLEM_POISSON, PROBLEM_COMPLEX_DIFFUSION = 0, 1
 
 # every symbol include/mg.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = [
@@ -55,6 +56,10 @@ class MGConfig(ctypes.Structure):
         ("nccl_id", ctypes.c_void_p),
         ("flags", ctypes.c_uint32),
         ("pm_min_nx", ctypes.c_int32),
+        ("problem", ctypes.c_int32),
+        ("tau", ctypes.c_double),
+        ("theta", ctypes.c_double),
+        ("kappa", ctypes.c_double),
     ]
 
 
@@ -121,8 +126,14 @@ def _torch():
     return torch
 
 
+def _problem_code(problem):
+    return PROBLEM_COMPLEX_DIFFUSION if problem in ("complex_diffusion", "cd", PROBLEM_COMPLEX_DIFFUSION) \
+        else PROBLEM_POISSON
+
+
 def make_config(dim, nodes, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, coarse="direct", ncoarse=10,
-                dtype="f64", device=0, coeff=(1.0, 1.0, 1.0), h=None, flags=0, rank=0, nranks=1, pm_min_nx=0):
+                dtype="f64", device=0, coeff=(1.0, 1.0, 1.0), h=None, flags=0, rank=0, nranks=1, pm_min_nx=0,
+                problem="poisson", tau=None, theta=None, kappa=None):
     """Build an mg_config (argument marshalling only)."""
     lib = load_library()
     if isinstance(nodes, int):
@@ -144,6 +155,13 @@ def make_config(dim, nodes, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2,
     c.rank, c.nranks = rank, nranks
     c.flags = flags
     c.pm_min_nx = pm_min_nx
+    c.problem = _problem_code(problem)
+    if tau is not None:
+        c.tau = float(tau)
+    if theta is not None:
+        c.theta = float(theta)
+    if kappa is not None:
+        c.kappa = float(kappa)
     return c
 
 
@@ -184,7 +202,9 @@ class Solver:
 
     def __init__(self, dim, nodes, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, coarse="direct",
                  ncoarse=10, dtype="f64", device=0, coeff=(1.0, 1.0, 1.0), h=None, flags=0, rank=0, nranks=1,
-                 nccl_id=None, pm_min_nx=0):
+                 nccl_id=None, pm_min_nx=0, problem="poisson", tau=None, theta=None, kappa=None):
+        """problem="complex_diffusion": `nodes` are CELLS per axis, arrays are complex
+        (torch complex64 / complex128), coarse defaults to "sweeps" (FAS)."""
         lib = load_library()
         self.lib = lib
         if isinstance(nodes, int):
@@ -208,6 +228,16 @@ class Solver:
         c.nccl_id = ctypes.cast(ctypes.c_char_p(nccl_id), ctypes.c_void_p) if nccl_id is not None else None
         c.flags = flags
         c.pm_min_nx = pm_min_nx
+        c.problem = _problem_code(problem)
+        self.complex = c.problem == PROBLEM_COMPLEX_DIFFUSION
+        if self.complex and coarse == "direct":
+            c.coarse = COARSE_SWEEPS
+        if tau is not None:
+            c.tau = float(tau)
+        if theta is not None:
+            c.theta = float(theta)
+        if kappa is not None:
+            c.kappa = float(kappa)
         self.cfg = c
         self.dim = dim
         self.nodes = tuple(int(n) for n in nodes[:dim])
@@ -218,6 +248,11 @@ class Solver:
         self.h = h_
         self.levels = lib.mg_num_levels(self.h)
         torch = _torch()
+        if self.complex:
+            self.torch_dtype = torch.complex128 if c.dtype == FP64 else torch.complex64
+            self.np_dtype = np.complex128 if c.dtype == FP64 else np.complex64
+            self.first_plane, self.owned_planes, self.distributed, self.halo = 0, self.shape[0], False, 0
+            return
         self.torch_dtype = torch.float64 if c.dtype == FP64 else torch.float32
         self.np_dtype = np.float64 if c.dtype == FP64 else np.float32
         self.first_plane, self.owned_planes, self.distributed, self.halo = partition(
@@ -263,6 +298,8 @@ class Solver:
         return tuple(s)
 
     def level_cells(self, level):
+        if self.complex:
+            return tuple(n >> level for n in self.nodes)
         return tuple((n - 1) >> level for n in self.nodes)
 
     def empty(self, level=0):
@@ -278,6 +315,9 @@ class Solver:
         a = np.asarray(a, dtype=self.np_dtype)
         if self.dim == 2:
             a = a[:, None, :]
+        if self.complex:  # cell array, no boundary entries
+            host[:, :, : a.shape[2]] = a
+            return torch.from_numpy(host).to(f"cuda:{self.cfg.device}")
         g0 = self.first_plane - self.halo if (level == 0 and self.distributed) else 0
         for i in range(P):
             gp = g0 + i
@@ -287,7 +327,7 @@ class Solver:
 
     def to_numpy(self, t, level=0):
         """Device tensor -> dense node array; in slab mode the rank's OWNED planes only."""
-        nx = self.level_cells(level)[0] + 1
+        nx = self.level_cells(level)[0] + (0 if self.complex else 1)
         a = t.detach().cpu().numpy()
         if level == 0 and self.distributed:
             a = a[self.halo: self.halo + self.owned_planes]

@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -63,6 +64,48 @@ extern "C" void mg_config_default(mg_config* c, int32_t dim, int64_t nodes) {
   c->nranks = 1;
   c->nccl_id = nullptr;
   c->flags = 0;
+  c->problem = MG_PROBLEM_POISSON;
+  c->tau = 0.1;  // complex diffusion defaults (the paper gives none)
+  c->theta = M_PI / 30.0;
+  c->kappa = 2.0;
+}
+
+// complex diffusion (cell-centred FAS): nodes[d] are cells; coarsest level has 2 cells
+// along the shortest axis (< 3 unknowns per direction)
+static mg_status validate_cd(const mg_config* c, int* levels_out) {
+  mg_solver* s = nullptr;
+  if (c->smoother != MG_JACOBI && c->smoother != MG_RBGS) return fail(s, MG_ERR_INVALID, "bad smoother");
+  if (!(c->omega > 0.0 && c->omega < 2.0)) return fail(s, MG_ERR_INVALID, "omega must be in (0,2) (S:46)");
+  if (c->nu1 < 0 || c->nu2 < 0) return fail(s, MG_ERR_INVALID, "nu1, nu2 must be >= 0");
+  if (c->coarse != MG_COARSE_SWEEPS || c->ncoarse < 1)
+    return fail(s, MG_ERR_INVALID, "complex diffusion needs coarse = MG_COARSE_SWEEPS, ncoarse >= 1 (FAS, S:437)");
+  if (c->dtype != MG_FP64 && c->dtype != MG_FP32) return fail(s, MG_ERR_INVALID, "bad dtype");
+  if (c->nranks != 1) return fail(s, MG_ERR_INVALID, "complex diffusion runs on one rank (nranks = 1)");
+  if (c->flags & (MG_FLAG_SLAB | MG_FLAG_FUSE_PROLONG))
+    return fail(s, MG_ERR_INVALID, "MG_FLAG_SLAB / MG_FLAG_FUSE_PROLONG do not apply to complex diffusion");
+  if (!(c->tau > 0.0) || !(c->theta > 0.0 && c->theta < M_PI / 2) || !(c->kappa > 0.0))
+    return fail(s, MG_ERR_INVALID, "need tau > 0, theta in (0, pi/2), kappa > 0 (S:303)");
+  int64_t mincells = INT64_MAX;
+  for (int d = 0; d < c->dim; d++) {
+    const int64_t n = c->nodes[d];
+    if (n < 1 || n > (1ll << 30)) return fail(s, MG_ERR_INVALID, "cells[%d] out of range", d);
+    if (c->h[d] < 0.0) return fail(s, MG_ERR_INVALID, "h[%d] < 0", d);
+    if (n < mincells) mincells = n;
+  }
+  int L = c->levels;
+  if (L < 0) return fail(s, MG_ERR_INVALID, "levels < 0");
+  if (L == 0) {
+    L = 1;
+    while ((mincells >> L) >= 2 && ((mincells >> L) << L) == mincells) L++;
+  }
+  for (int d = 0; d < c->dim; d++) {
+    const int64_t n = c->nodes[d];
+    if (L - 1 >= 62 || (n % (1ll << (L - 1))) != 0 || (n >> (L - 1)) < 1)
+      return fail(s, MG_ERR_NOT_COARSENABLE, "cells[%d] = %lld not divisible by 2^(levels-1) = 2^%d", d,
+                  (long long)n, L - 1);
+  }
+  *levels_out = L;
+  return MG_OK;
 }
 
 // ------------------------------------------------------------------ creation
@@ -70,6 +113,8 @@ static mg_status validate(const mg_config* c, int* levels_out) {
   mg_solver* s = nullptr;
   if (!c) return fail(s, MG_ERR_INVALID, "config is NULL");
   if (c->dim != 2 && c->dim != 3) return fail(s, MG_ERR_INVALID, "dim must be 2 or 3 (got %d)", c->dim);
+  if (c->problem == MG_PROBLEM_COMPLEX_DIFFUSION) return validate_cd(c, levels_out);
+  if (c->problem != MG_PROBLEM_POISSON) return fail(s, MG_ERR_INVALID, "bad problem %d", c->problem);
   if (c->smoother != MG_JACOBI && c->smoother != MG_RBGS) return fail(s, MG_ERR_INVALID, "bad smoother");
   if (!(c->omega > 0.0 && c->omega < 2.0)) return fail(s, MG_ERR_INVALID, "omega must be in (0,2) (S:46)");
   if (c->nu1 < 0 || c->nu2 < 0) return fail(s, MG_ERR_INVALID, "nu1, nu2 must be >= 0");
@@ -118,6 +163,7 @@ extern "C" mg_status mg_partition(const mg_config* cfg, int32_t level, int64_t* 
   int L = 0;
   mg_status st = validate(cfg, &L);
   if (st != MG_OK) return st;
+  if (cfg->problem != MG_PROBLEM_POISSON) return fail(nullptr, MG_ERR_INVALID, "complex diffusion is not decomposed");
   if (level < 0 || level >= L) return fail(nullptr, MG_ERR_INVALID, "level %d out of range", level);
   mg::Partition pt;
   std::string perr;
@@ -294,7 +340,7 @@ extern "C" mg_status mg_vcycle_host(mg_solver* s, void* u_host, const void* f_ho
   if (!u_host || !f_host || ncycles < 0) return fail(s, MG_ERR_INVALID, "bad argument");
   cudaStream_t cs = (cudaStream_t)stream;
   const Level& lv = s->lv[0];
-  size_t bytes = lv.elems * s->esz;
+  size_t bytes = lv.elems * s->esz * (s->cfg.problem == MG_PROBLEM_COMPLEX_DIFFUSION ? 2 : 1);
   if (!s->stage_u) {
     if (cudaMalloc(&s->stage_u, bytes) != cudaSuccess || cudaMalloc(&s->stage_f, bytes) != cudaSuccess) {
       cudaGetLastError();

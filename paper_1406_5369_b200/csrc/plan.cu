@@ -39,6 +39,15 @@ enum Kind {
   K_SWEEP_NORM,
   K_TAIL,
   K_SWEEP_CORR,
+  K_CD_GFIELD,
+  K_CD_JACOBI,
+  K_CD_RBGS,
+  K_CD_RESTRICT,
+  K_CD_FAS_RHS,
+  K_CD_PROLONG,
+  K_CD_NORM,
+  K_CD_RESIDUAL,
+  K_CD_COPY,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -46,7 +55,10 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "norm_final",    "coarse_direct", "memset",       "add_interior",
                                        "rbgs_fused",    "jacobi_pm",     "resid_restrict",
                                        "nccl_halo",     "nccl_allgather", "sweep+norm",
-                                       "coarse_tail",   "prolong+sweep"};
+                                       "coarse_tail",   "prolong+sweep",
+                                       "cd_gfield",     "cd_jacobi",     "cd_rbgs_colour", "cd_restrict",
+                                       "cd_fas_rhs",    "cd_prolong",    "cd_norm_partial", "cd_residual",
+                                       "cd_copy"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -109,6 +121,32 @@ static dim3 rows_grid(const Geom& g) {
   return dim3((unsigned)((q + 1) / 2));
 }
 
+static mg_status cd_build(mg_solver* s);
+static mg_status alloc_common(mg_solver* s, int np);
+
+// norm partials / scalar, capture streams, driver-loop state (both problems)
+static mg_status alloc_common(mg_solver* s, int np) {
+  s->n_partial_cap = np;
+  if (cudaMalloc(&s->d_partial, sizeof(double) * np) != cudaSuccess ||
+      cudaMalloc(&s->d_norm, sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&s->d_rank_sums, sizeof(double) * s->cfg.nranks) != cudaSuccess ||
+      cudaMallocHost(&s->h_norm, sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return plan_fail(s, MG_ERR_OOM, "allocation of norm buffers failed");
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap_body, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamCreate");
+  if (cudaMalloc(&s->d_loop, sizeof(LoopState)) != cudaSuccess ||
+      cudaMallocHost(&s->h_loop, sizeof(LoopState)) != cudaSuccess) {
+    cudaGetLastError();
+    return plan_fail(s, MG_ERR_OOM, "allocation of the driver-loop state failed");
+  }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(s, e, "setup");
+  return MG_OK;
+}
+
 // ---------------------------------------------------------------- build / free
 mg_status plan_build(mg_solver* s) {
   const mg_config& c = s->cfg;
@@ -122,6 +160,7 @@ mg_status plan_build(mg_solver* s) {
              major);
     return plan_fail(s, MG_ERR_CUDA, buf);
   }
+  if (c.problem == MG_PROBLEM_COMPLEX_DIFFUSION) return cd_build(s);
   const int esz = (int)s->esz;
   const int64_t align = 128 / esz;
   {
@@ -228,14 +267,6 @@ mg_status plan_build(mg_solver* s) {
     int a = s->esz == 8 ? pm::sweep_partials<double>(s->lv[0].g, rb) : pm::sweep_partials<float>(s->lv[0].g, rb);
     if (a > np) np = a;
   }
-  s->n_partial_cap = np;
-  if (cudaMalloc(&s->d_partial, sizeof(double) * np) != cudaSuccess ||
-      cudaMalloc(&s->d_norm, sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&s->d_rank_sums, sizeof(double) * c.nranks) != cudaSuccess ||
-      cudaMallocHost(&s->h_norm, sizeof(double)) != cudaSuccess) {
-    cudaGetLastError();
-    return plan_fail(s, MG_ERR_OOM, "allocation of norm buffers failed");
-  }
   // coarsest-level direct solve: factor once (reading 3)
   Level& C = s->lv[s->L - 1];
   int m = (C.g.nx - 1) * (C.g.three_d ? C.g.ny - 1 : 1) * (C.g.nz - 1);
@@ -260,18 +291,7 @@ mg_status plan_build(mg_solver* s) {
     if (e != cudaSuccess) return cuda_fail(s, e, "coarse Cholesky factorisation");
     if (hs != 0) return plan_fail(s, MG_ERR_INVALID, "coarsest matrix is not positive definite");
   }
-  e = cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap_body, cudaStreamNonBlocking);
-  if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamCreate");
-  if (cudaMalloc(&s->d_loop, sizeof(LoopState)) != cudaSuccess ||
-      cudaMallocHost(&s->h_loop, sizeof(LoopState)) != cudaSuccess) {
-    cudaGetLastError();
-    return plan_fail(s, MG_ERR_OOM, "allocation of the driver-loop state failed");
-  }
-  // count launches of one cycle with a dry capture
-  e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) return cuda_fail(s, e, "setup");
-  return MG_OK;
+  return alloc_common(s, np);
 }
 
 void plan_free(mg_solver* s) {
@@ -283,6 +303,8 @@ void plan_free(mg_solver* s) {
     cudaFree(L.f);
     cudaFree(L.r);
     cudaFree(L.t);
+    cudaFree(L.uh);
+    cudaFree(L.gd);
   }
   s->lv.clear();
   cudaFree(s->d_chol);
@@ -669,6 +691,205 @@ const Coef<float>& Exec<float>::coef(int l) const {
   return s->lv[l].c32;
 }
 
+
+// ================================================================ complex diffusion (FAS)
+// One implicit-Euler step of nonlinear complex diffusion on a cell-centred grid, FAS
+// V-cycle with lagged diffusivity (oracle/cd_oracle.c), kernels in
+// kernels_cd.cu.  Level l: cells n_d >> l, h_l = 2^l h, w_d = tau / h_{l,d}^2.
+static bool is_cd(const mg_solver* s) { return s->cfg.problem == MG_PROBLEM_COMPLEX_DIFFUSION; }
+
+static mg_status cd_build(mg_solver* s) {
+  const mg_config& c = s->cfg;
+  const int esz = (int)s->esz;
+  const int64_t align = 128 / (2 * esz);  // complex elements per 128 B
+  s->lv.resize(s->L);
+  int np = 1;
+  for (int l = 0; l < s->L; l++) {
+    Level& L = s->lv[l];
+    int64_t n[3];
+    double w[3] = {0, 0, 0};
+    for (int d = 0; d < 3; d++) {
+      n[d] = d < c.dim ? c.nodes[d] >> l : 1;
+      const double h0 = c.h[d] > 0.0 ? c.h[d] : (d < c.dim ? 1.0 / (double)c.nodes[d] : 0.0);
+      const double h = std::ldexp(h0, l);
+      if (d < c.dim) w[d] = c.tau / (h * h);
+    }
+    Geom& g = L.g;
+    g.three_d = c.dim == 3;
+    g.nx = (int)n[0];
+    g.ny = c.dim == 3 ? (int)n[1] : 0;
+    g.nz = c.dim == 3 ? (int)n[2] : (int)n[1];
+    g.rows = c.dim == 3 ? g.ny : 1;
+    g.planes = g.nz;
+    g.p_lo = 0;
+    g.p_hi = g.nz;
+    g.p_glob0 = 0;
+    g.pitch = (g.nx + align - 1) / align * align;
+    g.pstride = g.pitch * g.rows;
+    L.gown = g;
+    // coefficients in double, cast once: x, in-plane y (3D), plane axis (3D z, 2D y)
+    const double wx = w[0], wy = c.dim == 3 ? w[1] : 0.0, wz = c.dim == 3 ? w[2] : w[1];
+    const double kth = c.kappa * c.theta, ct = std::cos(c.theta), sn = std::sin(c.theta);
+    L.cd64 = CdCoef<double>{{wx, wy, wz}, c.omega, kth, ct, sn};
+    L.cd32 = CdCoef<float>{{(float)wx, (float)wy, (float)wz}, (float)c.omega, (float)kth, (float)ct, (float)sn};
+    L.shape[0] = g.planes;
+    L.shape[1] = g.rows;
+    L.shape[2] = g.pitch;
+    L.elems = (size_t)L.shape[0] * L.shape[1] * L.shape[2];
+    const size_t bytes = L.elems * 2 * esz;
+    void** bufs[5] = {&L.u, &L.f, &L.uh, &L.gd, &L.t};
+    for (int b = 0; b < 5; b++) {
+      if (l == 0 && (b < 3)) continue;  // level 0 u, f are the caller's; no u^ on level 0
+      if (cudaMalloc(bufs[b], bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return plan_fail(s, MG_ERR_OOM, "device allocation of level buffers failed");
+      }
+      cudaError_t e = cudaMemset(*bufs[b], 0, bytes);
+      if (e != cudaSuccess) return cuda_fail(s, e, "cudaMemset");
+    }
+    const int a = cd_norm_partials(g);
+    if (a > np) np = a;
+  }
+  return alloc_common(s, np);
+}
+
+template <typename T>
+struct CdExec {
+  mg_solver* s;
+  cudaStream_t st;
+  const CdCoef<T>& cc(int l) const;
+  double cw(int l) const {  // one complex word per cell of level l
+    const Geom& g = s->lv[l].g;
+    return (double)g.nx * (g.three_d ? g.ny : 1) * g.nz * 2.0 * sizeof(T);
+  }
+  const Geom& G(int l) const { return s->lv[l].g; }
+  T* gd(int l) const { return (T*)s->lv[l].gd; }
+
+  mg_status gfield(int l, const T* u) {
+    return launch(s, st, K_CD_GFIELD, l, 2 * cw(l), [&] { return cd_launch_gfield<T>(G(l), cc(l), u, gd(l), st); });
+  }
+  // one sweep with the frozen g of level l; Jacobi ping-pongs cur <-> oth
+  mg_status smooth(int l, T*& cur, T*& oth, const T* f) {
+    if (s->cfg.smoother == MG_JACOBI) {
+      T* in = cur;
+      T* out = oth;
+      mg_status r = launch(s, st, K_CD_JACOBI, l, 4 * cw(l),
+                           [&] { return cd_launch_jacobi<T>(G(l), cc(l), gd(l), in, f, out, st); });
+      std::swap(cur, oth);
+      return r;
+    }
+    for (int colour = 0; colour < 2; colour++) {
+      T* u = cur;
+      mg_status r = launch(s, st, K_CD_RBGS, l, 2.5 * cw(l),
+                           [&] { return cd_launch_rbgs<T>(G(l), cc(l), gd(l), u, f, colour, st); });
+      if (r != MG_OK) return r;
+    }
+    return MG_OK;
+  }
+  mg_status copy(int l, const T* src, T* dst) {
+    const Geom& g = G(l);
+    const size_t w = (size_t)g.nx * 2 * sizeof(T), p = (size_t)g.pitch * 2 * sizeof(T);
+    return launch(s, st, K_CD_COPY, l, 2 * cw(l), [&] {
+      return cudaMemcpy2DAsync(dst, p, src, p, w, (size_t)g.rows * g.planes, cudaMemcpyDeviceToDevice, st);
+    });
+  }
+  // FAS V-cycle at level l; g_ready: g of level l already built from cur[l]
+  mg_status rec(int l, std::vector<T*>& cur, std::vector<T*>& oth, const T* f, bool g_ready) {
+    mg_status r;
+    if (!g_ready && (r = gfield(l, cur[l])) != MG_OK) return r;  // lagged diffusivity, frozen in the cycle
+    if (l == s->L - 1) {
+      for (int k = 0; k < s->cfg.ncoarse; k++)
+        if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+      return MG_OK;
+    }
+    for (int k = 0; k < s->cfg.nu1; k++)
+      if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+    Level& C = s->lv[l + 1];
+    T* uh = (T*)C.uh;
+    T* fc = (T*)C.f;
+    const T* ul = cur[l];
+    T* uc = cur[l + 1];
+    // u^_H = R u_h, u_H = u^_H
+    if ((r = launch(s, st, K_CD_RESTRICT, l, cw(l) + 2 * cw(l + 1),
+                    [&] { return cd_launch_restrict<T>(G(l), G(l + 1), ul, uh, uc, st); })) != MG_OK)
+      return r;
+    if ((r = gfield(l + 1, uh)) != MG_OK) return r;  // coarse operator from the restricted lagged solution
+    // f_H = A_H(u^_H) u^_H + R (f_h - A_h u_h)
+    if ((r = launch(s, st, K_CD_FAS_RHS, l, 3 * cw(l) + 3 * cw(l + 1), [&] {
+           return cd_launch_fas_rhs<T>(G(l), G(l + 1), cc(l), cc(l + 1), gd(l), ul, f, gd(l + 1), uh, fc, st);
+         })) != MG_OK)
+      return r;
+    if ((r = rec(l + 1, cur, oth, fc, true)) != MG_OK) return r;
+    // u_h += P (u_H - u^_H)
+    const T* ucn = cur[l + 1];
+    T* ulw = cur[l];
+    if ((r = launch(s, st, K_CD_PROLONG, l, 2 * cw(l) + 2 * cw(l + 1),
+                    [&] { return cd_launch_prolong<T>(G(l), G(l + 1), ucn, uh, ulw, st); })) != MG_OK)
+      return r;
+    for (int k = 0; k < s->cfg.nu2; k++)
+      if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+    return MG_OK;
+  }
+  mg_status vcycle(T* u0, const T* f0) {
+    std::vector<T*> cur(s->L), oth(s->L);
+    for (int l = 0; l < s->L; l++) {
+      cur[l] = l == 0 ? u0 : (T*)s->lv[l].u;
+      oth[l] = (T*)s->lv[l].t;
+    }
+    mg_status r = rec(0, cur, oth, f0, false);
+    if (r != MG_OK) return r;
+    if (cur[0] != u0) return copy(0, cur[0], u0);
+    return MG_OK;
+  }
+  mg_status norm(int l, const T* u, const T* f, double* out_dev) {
+    int np = 0;
+    mg_status r = launch(s, st, K_CD_NORM, l, 2 * cw(l), [&] {
+      return cd_launch_norm_partial<T>(G(l), cc(l), u, f, s->d_partial, &np, st);
+    });
+    if (r != MG_OK) return r;
+    return launch(s, st, K_NORM_FINAL, l, 8.0 * np, [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });
+  }
+  mg_status op_smooth(int l, const T* uin, const T* f, T* uout) {
+    mg_status r = gfield(l, uin);
+    if (r != MG_OK) return r;
+    if (s->cfg.smoother == MG_JACOBI) {
+      T* dst = uin == uout ? (T*)s->lv[l].t : uout;
+      if ((r = launch(s, st, K_CD_JACOBI, l, 4 * cw(l),
+                      [&] { return cd_launch_jacobi<T>(G(l), cc(l), gd(l), uin, f, dst, st); })) != MG_OK)
+        return r;
+      return dst == uout ? MG_OK : copy(l, dst, uout);
+    }
+    if (uin != uout && (r = copy(l, uin, uout)) != MG_OK) return r;
+    T* cur = uout;
+    T* oth = nullptr;
+    return smooth(l, cur, oth, f);
+  }
+  mg_status op_residual(int l, const T* u, const T* f, T* res) {
+    mg_status r = gfield(l, u);
+    if (r != MG_OK) return r;
+    return launch(s, st, K_CD_RESIDUAL, l, 3 * cw(l),
+                  [&] { return cd_launch_residual<T>(G(l), cc(l), gd(l), u, f, res, st); });
+  }
+};
+template <>
+const CdCoef<double>& CdExec<double>::cc(int l) const {
+  return s->lv[l].cd64;
+}
+template <>
+const CdCoef<float>& CdExec<float>::cc(int l) const {
+  return s->lv[l].cd32;
+}
+
+static mg_status cd_run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
+  if (part == 1 || part == 2) return plan_fail(s, MG_ERR_INVALID, "complex diffusion cycles are not split");
+  if (s->esz == 8) {
+    CdExec<double> x{s, st};
+    return part == 3 ? x.norm(0, (const double*)u, (const double*)f, s->d_norm) : x.vcycle((double*)u, (const double*)f);
+  }
+  CdExec<float> x{s, st};
+  return part == 3 ? x.norm(0, (const float*)u, (const float*)f, s->d_norm) : x.vcycle((float*)u, (const float*)f);
+}
+
 // ---------------------------------------------------------------- entry points
 // part: 0 whole cycle, 1 head (first sweep + norm of the input into d_norm), 2 tail,
 // 3 norm of (u, f) into d_norm
@@ -683,7 +904,8 @@ static mg_status run_part(mg_solver* s, int part, void* u, const void* f, cudaSt
 
 mg_status plan_run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
   s->launch_counter = 0;
-  mg_status r = s->esz == 8 ? run_part<double>(s, part, u, f, st) : run_part<float>(s, part, u, f, st);
+  mg_status r = is_cd(s) ? cd_run_part(s, part, u, f, st)
+                         : s->esz == 8 ? run_part<double>(s, part, u, f, st) : run_part<float>(s, part, u, f, st);
   if (part == 0) s->launches_per_cycle = s->launch_counter;
   return r;
 }
@@ -693,6 +915,7 @@ mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st)
 }
 
 bool plan_can_split(mg_solver* s) {
+  if (is_cd(s)) return false;
   return s->esz == 8 ? Exec<double>{s, 0}.can_split() : Exec<float>{s, 0}.can_split();
 }
 
@@ -727,7 +950,9 @@ mg_status plan_graph_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t s
 }
 
 mg_status plan_norm(mg_solver* s, int level, const void* u, const void* f, double* out, cudaStream_t st, bool sync) {
-  mg_status r = s->esz == 8 ? Exec<double>{s, st}.norm(level, (const double*)u, (const double*)f, s->d_norm)
+  mg_status r = is_cd(s) ? (s->esz == 8 ? CdExec<double>{s, st}.norm(level, (const double*)u, (const double*)f, s->d_norm)
+                                        : CdExec<float>{s, st}.norm(level, (const float*)u, (const float*)f, s->d_norm))
+              : s->esz == 8 ? Exec<double>{s, st}.norm(level, (const double*)u, (const double*)f, s->d_norm)
                             : Exec<float>{s, st}.norm(level, (const float*)u, (const float*)f, s->d_norm);
   if (r != MG_OK) return r;
   cudaError_t e = cudaMemcpyAsync(s->h_norm, s->d_norm, sizeof(double), cudaMemcpyDeviceToHost, st);
@@ -768,11 +993,17 @@ static mg_status op_smooth_T(mg_solver* s, int l, const T* uin, const T* f, T* u
 }
 
 mg_status plan_op_smooth(mg_solver* s, int l, const void* uin, const void* f, void* uout, cudaStream_t st) {
+  if (is_cd(s))
+    return s->esz == 8 ? CdExec<double>{s, st}.op_smooth(l, (const double*)uin, (const double*)f, (double*)uout)
+                       : CdExec<float>{s, st}.op_smooth(l, (const float*)uin, (const float*)f, (float*)uout);
   if (s->esz == 8) return op_smooth_T<double>(s, l, (const double*)uin, (const double*)f, (double*)uout, st);
   return op_smooth_T<float>(s, l, (const float*)uin, (const float*)f, (float*)uout, st);
 }
 
 mg_status plan_op_residual(mg_solver* s, int l, const void* u, const void* f, void* r, cudaStream_t st) {
+  if (is_cd(s))
+    return s->esz == 8 ? CdExec<double>{s, st}.op_residual(l, (const double*)u, (const double*)f, (double*)r)
+                       : CdExec<float>{s, st}.op_residual(l, (const float*)u, (const float*)f, (float*)r);
   const Level& L = s->lv[l];
   return launch(s, st, K_RESIDUAL, l, 0, [&] {
     return s->esz == 8 ? launch_residual<double>(L.g, L.c64, (const double*)u, (const double*)f, (double*)r, st)
@@ -781,6 +1012,12 @@ mg_status plan_op_residual(mg_solver* s, int l, const void* u, const void* f, vo
 }
 
 mg_status plan_op_restrict(mg_solver* s, int l, const void* r, void* fc, cudaStream_t st) {
+  if (is_cd(s))
+    return launch(s, st, K_CD_RESTRICT, l, 0, [&] {
+      const Geom &gf = s->lv[l].g, &gc = s->lv[l + 1].g;
+      return s->esz == 8 ? cd_launch_restrict<double>(gf, gc, (const double*)r, (double*)fc, nullptr, st)
+                         : cd_launch_restrict<float>(gf, gc, (const float*)r, (float*)fc, nullptr, st);
+    });
   const Level& F = s->lv[l];
   const Level& C = s->lv[l + 1];
   cudaError_t e = cudaMemsetAsync(fc, 0, C.elems * s->esz, st);
@@ -792,6 +1029,12 @@ mg_status plan_op_restrict(mg_solver* s, int l, const void* r, void* fc, cudaStr
 }
 
 mg_status plan_op_prolong(mg_solver* s, int l, const void* e, void* u, cudaStream_t st) {
+  if (is_cd(s))
+    return launch(s, st, K_CD_PROLONG, l, 0, [&] {
+      const Geom &gf = s->lv[l].g, &gc = s->lv[l + 1].g;
+      return s->esz == 8 ? cd_launch_prolong<double>(gf, gc, (const double*)e, nullptr, (double*)u, st)
+                         : cd_launch_prolong<float>(gf, gc, (const float*)e, nullptr, (float*)u, st);
+    });
   const Level& F = s->lv[l];
   const Level& C = s->lv[l + 1];
   return launch(s, st, K_PROLONG, l, 0, [&] {
@@ -818,11 +1061,19 @@ static mg_status op_coarse_T(mg_solver* s, const T* f, T* e, cudaStream_t st) {
 }
 
 mg_status plan_op_coarse(mg_solver* s, const void* f, void* e, cudaStream_t st) {
+  if (is_cd(s)) return plan_fail(s, MG_ERR_INVALID, "complex diffusion: the FAS coarsest level is ncoarse sweeps");
   if (s->esz == 8) return op_coarse_T<double>(s, (const double*)f, (double*)e, st);
   return op_coarse_T<float>(s, (const float*)f, (float*)e, st);
 }
 
 mg_status plan_workload_fill(mg_solver* s, void* dst, uint64_t seed, double lo, double hi, cudaStream_t st) {
+  if (is_cd(s)) {
+    const Geom& g = s->lv[0].g;
+    cudaError_t e = s->esz == 8 ? cd_launch_fill<double>(g, (double*)dst, seed, lo, hi, st)
+                                : cd_launch_fill<float>(g, (float*)dst, seed, lo, hi, st);
+    if (e != cudaSuccess) return cuda_fail(s, e, "workload_fill");
+    return MG_OK;
+  }
   const Level& L = s->lv[0];
   cudaError_t e = s->esz == 8 ? launch_workload_fill<double>(L.g, seed, lo, hi, (double*)dst, st)
                               : launch_workload_fill<float>(L.g, seed, lo, hi, (float*)dst, st);

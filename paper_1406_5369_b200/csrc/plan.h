@@ -11,6 +11,7 @@
 #include "mg.h"
 #include "mg_common.cuh"
 #include "partition.h"
+#include "kernels_cd.h"
 
 typedef struct ncclComm* ncclComm_t;
 
@@ -29,6 +30,11 @@ struct Level {
   void* f = nullptr;      // library-owned right-hand side (levels >= 1)
   void* r = nullptr;      // residual scratch (op-by-op schedule)
   void* t = nullptr;      // ping-pong partner of u
+  // complex diffusion (cell-centred FAS): restricted lagged solution u^ and diffusivity g
+  void* uh = nullptr;
+  void* gd = nullptr;
+  CdCoef<double> cd64{};
+  CdCoef<float> cd32{};
 };
 
 // state of the on-device driver loop (loop.cu); written by the host before each solve

@@ -57,6 +57,15 @@ def test_config_defaults():
     lib.mg_config_default(ctypes.byref(c), 3, 513)
     assert (c.dim, list(c.nodes), c.levels, c.smoother, c.omega, c.nu1, c.nu2, c.coarse, c.ncoarse) == \
         (3, [513, 513, 513], 0, mgb.RBGS, 1.0, 2, 2, mgb.COARSE_DIRECT, 10)
+    assert (c.problem, c.tau, c.kappa) == (mgb.PROBLEM_POISSON, 0.1, 2.0) and abs(c.theta - 3.141592653589793 / 30) < 1e-16
+
+
+def test_complex_diffusion_config_valid_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    st, h, msg = _create(problem=1, nodes=16, coarse=1)
+    assert st == 4 and "no CPU fallback" in msg
 
 
 @pytest.mark.parametrize("kw,status", [
@@ -69,6 +78,14 @@ def test_config_defaults():
     (dict(nodes=18), 2),                          # 17 cells: not coarsenable
     (dict(nodes=17, levels=6), 2),                # 16 cells, 6 levels -> coarsest has 0 interior nodes
     (dict(nodes3=(17, 33, 10)), 2),               # 9 cells along z
+    # complex diffusion (problem 1): nodes are cells; FAS needs SWEEPS; one rank; Eq. 3 parameters
+    (dict(problem=1, nodes=16), 1),               # coarse = DIRECT (the default) is rejected
+    (dict(problem=1, nodes=16, coarse=1, nranks=2), 1),
+    (dict(problem=1, nodes=16, coarse=1, theta=2.0), 1),
+    (dict(problem=1, nodes=16, coarse=1, tau=0.0), 1),
+    (dict(problem=1, nodes=16, coarse=1, kappa=-1.0), 1),
+    (dict(problem=1, nodes3=(16, 16, 12), coarse=1, levels=4), 2),  # 12 cells not divisible by 8
+    (dict(problem=2), 1),
 ])
 def test_create_rejects_bad_config(kw, status):
     st, h, msg = _create(**kw)
