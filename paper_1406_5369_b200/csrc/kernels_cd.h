@@ -40,11 +40,32 @@ cudaError_t cd_launch_prolong(const Geom& gf, const Geom& gc, const T* uc, const
 template <typename T>
 cudaError_t cd_launch_residual(const Geom& g, const CdCoef<T>& c, const T* gd, const T* u, const T* f, T* r,
                                cudaStream_t st);
-// partial sums of |f - A(g(u)) u|^2 (g evaluated from u on the fly), one double per block
+// partial sums of |f - A(g(u)) u|^2, one double per block; g read from gd (which must hold
+// g(u)) or, when gd == nullptr, evaluated from u on the fly
 template <typename T>
-cudaError_t cd_launch_norm_partial(const Geom& g, const CdCoef<T>& c, const T* u, const T* f, double* partial,
-                                   int* npartial, cudaStream_t st);
+cudaError_t cd_launch_norm_partial(const Geom& g, const CdCoef<T>& c, const T* gd, const T* u, const T* f,
+                                   double* partial, int* npartial, cudaStream_t st);
 int cd_norm_partials(const Geom& g);
+// The coarse tail of the FAS cycle: levels lt..L-1 (k = 0 .. nl-1) in ONE single-CTA launch
+// (latency-bound levels; every pass of the recursion separated by __syncthreads).
+constexpr int kCdTailMax = 12;
+constexpr int kCdTailCells = 4096;  // the top tail level has at most this many cells
+template <typename T>
+struct CdTail {
+  int nl;
+  int rbgs, nu1, nu2, ncoarse;
+  int g_ready;  // the top level's g field is already g(u_top)
+  Geom g[kCdTailMax];
+  CdCoef<T> c[kCdTailMax];
+  T* u[kCdTailMax];
+  T* f[kCdTailMax];
+  T* uh[kCdTailMax];
+  T* gd[kCdTailMax];
+  T* t[kCdTailMax];
+};
+template <typename T>
+cudaError_t cd_launch_tail(const CdTail<T>& p, cudaStream_t st);
+
 // W5 inputs: re = lo + (hi-lo) U[0,1)(global cell index), im = 0
 template <typename T>
 cudaError_t cd_launch_fill(const Geom& g, T* dst, uint64_t seed, double lo, double hi, cudaStream_t st);

@@ -48,6 +48,7 @@ enum Kind {
   K_CD_NORM,
   K_CD_RESIDUAL,
   K_CD_COPY,
+  K_CD_TAIL,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -58,7 +59,7 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "coarse_tail",   "prolong+sweep",
                                        "cd_gfield",     "cd_jacobi",     "cd_rbgs_colour", "cd_restrict",
                                        "cd_fas_rhs",    "cd_prolong",    "cd_norm_partial", "cd_residual",
-                                       "cd_copy"};
+                                       "cd_copy",       "cd_tail"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -793,9 +794,41 @@ struct CdExec {
       return cudaMemcpy2DAsync(dst, p, src, p, w, (size_t)g.rows * g.planes, cudaMemcpyDeviceToDevice, st);
     });
   }
+  // first level of the single-CTA coarse tail (kernels_cd.cu): <= kCdTailCells cells; L if none
+  int tail_level() const {
+    if (s->cfg.flags & MG_FLAG_BASELINE) return s->L;
+    for (int l = 0; l < s->L; l++) {
+      const Geom& g = G(l);
+      if ((long long)g.nx * (g.three_d ? g.ny : 1) * g.nz <= kCdTailCells && s->L - l <= kCdTailMax) return l;
+    }
+    return s->L;
+  }
+  mg_status run_tail(int lt, std::vector<T*>& cur, std::vector<T*>& oth, const T* f_top, bool g_ready) {
+    CdTail<T> P{};
+    P.nl = s->L - lt;
+    P.rbgs = s->cfg.smoother == MG_RBGS;
+    P.nu1 = s->cfg.nu1;
+    P.nu2 = s->cfg.nu2;
+    P.ncoarse = s->cfg.ncoarse;
+    P.g_ready = g_ready;
+    double bytes = 0;
+    for (int k = 0; k < P.nl; k++) {
+      Level& L = s->lv[lt + k];
+      P.g[k] = L.g;
+      P.c[k] = cc(lt + k);
+      P.u[k] = cur[lt + k];
+      P.t[k] = oth[lt + k];
+      P.f[k] = k == 0 ? const_cast<T*>(f_top) : (T*)L.f;
+      P.uh[k] = (T*)L.uh;
+      P.gd[k] = gd(lt + k);
+      bytes += cw(lt + k) * (2 + 4.0 * (P.nu1 + P.nu2) + 10);
+    }
+    return launch(s, st, K_CD_TAIL, lt, bytes, [&] { return cd_launch_tail<T>(P, st); });
+  }
   // FAS V-cycle at level l; g_ready: g of level l already built from cur[l]
   mg_status rec(int l, std::vector<T*>& cur, std::vector<T*>& oth, const T* f, bool g_ready) {
     mg_status r;
+    if (l == tail_level()) return run_tail(l, cur, oth, f, g_ready);  // the result lands in cur[l]
     if (!g_ready && (r = gfield(l, cur[l])) != MG_OK) return r;  // lagged diffusivity, frozen in the cycle
     if (l == s->L - 1) {
       for (int k = 0; k < s->cfg.ncoarse; k++)
@@ -830,21 +863,29 @@ struct CdExec {
       if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
     return MG_OK;
   }
-  mg_status vcycle(T* u0, const T* f0) {
+  // g_ready: lv[0].gd already holds g(u0) (the head computed it for the norm)
+  mg_status vcycle(T* u0, const T* f0, bool g_ready = false) {
     std::vector<T*> cur(s->L), oth(s->L);
     for (int l = 0; l < s->L; l++) {
       cur[l] = l == 0 ? u0 : (T*)s->lv[l].u;
       oth[l] = (T*)s->lv[l].t;
     }
-    mg_status r = rec(0, cur, oth, f0, false);
+    mg_status r = rec(0, cur, oth, f0, g_ready);
     if (r != MG_OK) return r;
     if (cur[0] != u0) return copy(0, cur[0], u0);
     return MG_OK;
   }
-  mg_status norm(int l, const T* u, const T* f, double* out_dev) {
+  // pipelined driver loop (mg_solve): head = g(u_k) for the next cycle + ||f - A(g(u_k)) u_k||
+  // from the stored field; tail = the cycle with g ready
+  mg_status head(const T* u0, const T* f0, double* out_dev) {
+    mg_status r = gfield(0, u0);
+    if (r != MG_OK) return r;
+    return norm(0, u0, f0, out_dev, gd(0));
+  }
+  mg_status norm(int l, const T* u, const T* f, double* out_dev, const T* gstored = nullptr) {
     int np = 0;
-    mg_status r = launch(s, st, K_CD_NORM, l, 2 * cw(l), [&] {
-      return cd_launch_norm_partial<T>(G(l), cc(l), u, f, s->d_partial, &np, st);
+    mg_status r = launch(s, st, K_CD_NORM, l, (gstored ? 3 : 2) * cw(l), [&] {
+      return cd_launch_norm_partial<T>(G(l), cc(l), gstored, u, f, s->d_partial, &np, st);
     });
     if (r != MG_OK) return r;
     return launch(s, st, K_NORM_FINAL, l, 8.0 * np, [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });
@@ -880,14 +921,19 @@ const CdCoef<float>& CdExec<float>::cc(int l) const {
   return s->lv[l].cd32;
 }
 
-static mg_status cd_run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
-  if (part == 1 || part == 2) return plan_fail(s, MG_ERR_INVALID, "complex diffusion cycles are not split");
-  if (s->esz == 8) {
-    CdExec<double> x{s, st};
-    return part == 3 ? x.norm(0, (const double*)u, (const double*)f, s->d_norm) : x.vcycle((double*)u, (const double*)f);
+template <typename T>
+static mg_status cd_run_part_T(mg_solver* s, int part, T* u, const T* f, cudaStream_t st) {
+  CdExec<T> x{s, st};
+  switch (part) {
+    case 1: return x.head(u, f, s->d_norm);
+    case 2: return x.vcycle(u, f, true);
+    case 3: return x.norm(0, u, f, s->d_norm);
+    default: return x.vcycle(u, f);
   }
-  CdExec<float> x{s, st};
-  return part == 3 ? x.norm(0, (const float*)u, (const float*)f, s->d_norm) : x.vcycle((float*)u, (const float*)f);
+}
+static mg_status cd_run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
+  return s->esz == 8 ? cd_run_part_T<double>(s, part, (double*)u, (const double*)f, st)
+                     : cd_run_part_T<float>(s, part, (float*)u, (const float*)f, st);
 }
 
 // ---------------------------------------------------------------- entry points
@@ -915,7 +961,7 @@ mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st)
 }
 
 bool plan_can_split(mg_solver* s) {
-  if (is_cd(s)) return false;
+  if (is_cd(s)) return true;  // head = g(u_k) + norm from the stored field, tail = the cycle
   return s->esz == 8 ? Exec<double>{s, 0}.can_split() : Exec<float>{s, 0}.can_split();
 }
 
