@@ -61,7 +61,7 @@ typedef enum { MG_COARSE_DIRECT = 0, MG_COARSE_SWEEPS = 1 } mg_coarse; /* P:191,
  *    diffusion u - tau div(g(Im u) grad u) = f, g = e^{i theta}/(1 + (Im u/(kappa theta))^2)
  *    (Eqs. 2-3), averaged finite differences on a CELL-centred grid with
  *    Neumann (zero-flux) boundaries, FAS V-cycle with lagged diffusivity, cell-average
- *    restriction and constant interpolation (P:534; DESIGN.md §11).  Arrays hold COMPLEX
+ *    restriction and constant interpolation (P:534; DESIGN.md §10).  Arrays hold COMPLEX
  *    values, (re, im) interleaved, of the precision `dtype`; nodes[d] then counts CELLS
  *    (the unknowns) per axis; there are no boundary entries; coarse must be
  *    MG_COARSE_SWEEPS (ncoarse sweeps on the coarsest level); nranks must be 1. */
