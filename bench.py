@@ -188,12 +188,14 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def ncu_traffic(kernel):
+def ncu_traffic(config, kernel):
+    """DRAM bytes per launch of `kernel` in bench config `config` from one committed ncu --set full
+    capture (profiles/ncu_traffic.json), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
-    return d.get(kernel)
+    return d.get(f"{config}:{kernel}")
 
 
 # --------------------------------------------------------------------- oracle (CPU) legs
@@ -385,7 +387,7 @@ def run_mg(args):
     achieved = dom["bytes"] / (dom_avg_ms * 1e-3) / 1e9
     roofline = {
         "bound": "hbm", "kernel": dom["name"], "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": ncu_traffic(dom["name"]), "peak_source": peak_src,
+        "frac": achieved / peak, "traffic": ncu_traffic(args.config, dom["name"]), "peak_source": peak_src,
         "alg_bytes_per_launch": dom["bytes"], "avg_launch_ms": dom_avg_ms,
         "share_of_step": dom["ms"] / tot if tot else None,
     }
