@@ -14,7 +14,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
-JACOBI, RBGS = 0, 1
+JACOBI, RBGS, GS_LEX = 0, 1, 2
 COARSE_DIRECT, COARSE_SWEEPS = 0, 1
 
 
@@ -88,6 +88,7 @@ def _load(dtype):
     lib.or_residual.argtypes = [C, ctypes.c_int, P, P, P]
     lib.or_jacobi.argtypes = [C, ctypes.c_int, P, P, P]
     lib.or_rbgs.argtypes = [C, ctypes.c_int, P, P]
+    lib.or_gs_lex.argtypes = [C, ctypes.c_int, P, P]
     lib.or_smooth.argtypes = [C, ctypes.c_int, P, P, P]
     lib.or_restrict.argtypes = [C, ctypes.c_int, P, P]
     lib.or_prolong_correct.argtypes = [C, ctypes.c_int, P, P]
@@ -160,8 +161,15 @@ class Oracle:
         self.lib.or_rbgs(ctypes.byref(self._c), l, self._chk(u, l), self._chk(f, l))
         return u
 
+    def gs_lex(self, l, u, f):
+        u = u.copy()
+        self.lib.or_gs_lex(ctypes.byref(self._c), l, self._chk(u, l), self._chk(f, l))
+        return u
+
     def smooth(self, l, u, f):
-        return self.jacobi(l, u, f) if self.cfg.smoother == JACOBI else self.rbgs(l, u, f)
+        if self.cfg.smoother == JACOBI:
+            return self.jacobi(l, u, f)
+        return self.gs_lex(l, u, f) if self.cfg.smoother == GS_LEX else self.rbgs(l, u, f)
 
     def restrict(self, l, r):
         fc = np.empty(self.shape(l + 1), self.dtype)

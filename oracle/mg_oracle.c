@@ -151,11 +151,29 @@ void or_rbgs(const or_config* cfg, int l, real* u, const real* f) {
     rbgs_colour(cfg, &L, u, f, 1); /* black */
 }
 
+/* Lexicographic omega-Gauss-Seidel sweep (Table 1 "omega-Gauss-Seidel", P:351;
+ * S:416 "order lex -> one nest, row-major"): interior nodes in row-major order
+ * (x fastest, then y, then z), in place, each reading the latest values:
+ * u(x) = u(x) + (omega/D)(f - A u)(x).  Sequential by definition. */
+void or_gs_lex(const or_config* cfg, int l, real* u, const real* f) {
+    lvl L = level_of(cfg, l);
+    int nx = L.nx, ny = L.ny;
+    for (int k = L.kmin; k <= L.kmax; k++)
+        for (int j = 1; j < ny; j++)
+            for (int i = 1; i < nx; i++) {
+                int64_t p = IDX(i, j, k);
+                real r = point_residual(cfg->dim, u, p, L.sy, L.sz, L.cx, L.cy, L.cz, L.D, f[p]);
+                u[p] = u[p] + L.wd * r;
+            }
+}
+
 /* one sweep of the configured smoother S_h (Alg. 1 lines 3 and 7) */
 void or_smooth(const or_config* cfg, int l, real* u, const real* f, real* tmp) {
     if (cfg->smoother == OR_JACOBI) {
         or_jacobi(cfg, l, u, f, tmp);
         memcpy(u, tmp, sizeof(real) * or_level_nodes(cfg, l));
+    } else if (cfg->smoother == OR_GS_LEX) {
+        or_gs_lex(cfg, l, u, f);
     } else {
         or_rbgs(cfg, l, u, f);
     }

@@ -31,6 +31,7 @@ typedef OR_REAL real;
 
 #define OR_JACOBI 0
 #define OR_RBGS 1
+#define OR_GS_LEX 2
 #define OR_COARSE_DIRECT 0
 #define OR_COARSE_SWEEPS 1
 
@@ -40,7 +41,7 @@ typedef struct {
     int levels;       /* L >= 1; level 0 finest, level L-1 coarsest  */
     double a[3];      /* A = -sum_d a_d d^2/dx_d^2 ; Poisson: a = 1  */
     double h[3];      /* fine spacing per axis; unit domain: 1/n[d]  */
-    int smoother;     /* OR_JACOBI | OR_RBGS                         */
+    int smoother;     /* OR_JACOBI | OR_RBGS | OR_GS_LEX (Table 1)    */
     double omega;     /* damping                              */
     int nu1, nu2;     /* pre/post smoothing steps (Alg. 1)        */
     int coarse;       /* OR_COARSE_DIRECT | OR_COARSE_SWEEPS  */
@@ -56,6 +57,7 @@ int64_t or_level_nodes(const or_config* cfg, int l);
 void or_residual(const or_config* cfg, int l, const real* u, const real* f, real* r);
 void or_jacobi(const or_config* cfg, int l, const real* u_in, const real* f, real* u_out);
 void or_rbgs(const or_config* cfg, int l, real* u, const real* f);
+void or_gs_lex(const or_config* cfg, int l, real* u, const real* f);
 void or_smooth(const or_config* cfg, int l, real* u, const real* f, real* tmp);
 void or_restrict(const or_config* cfg, int l, const real* r_fine, real* f_coarse);
 void or_prolong_correct(const or_config* cfg, int l, const real* e_coarse, real* u_fine);

@@ -92,6 +92,13 @@ def rbgs(A, D, omega, u, f, cells):
     return u
 
 
+def gs_lex(A, D, omega, u, f):
+    """Lexicographic SOR written as a matrix iteration: with A = D - L - U (L strictly
+    lower in lex order), u' = u + omega (D - omega L)^-1 (f - A u)."""
+    L = -np.tril(A, -1)
+    return u + omega * np.linalg.solve(np.diag(np.full(A.shape[0], D)) - omega * L, f - A @ u)
+
+
 def interior(a: np.ndarray) -> np.ndarray:
     return a[(slice(1, -1),) * a.ndim].reshape(-1).astype(np.float64)
 
@@ -125,6 +132,8 @@ class DenseMG:
     def smooth(self, l, u, f):
         if self.smoother == "jacobi":
             return jacobi(self.A[l], self.D[l], self.omega, u, f)
+        if self.smoother == "gs_lex":
+            return gs_lex(self.A[l], self.D[l], self.omega, u, f)
         return rbgs(self.A[l], self.D[l], self.omega, u, f, self.cells[l])
 
     def vcycle(self, u, f, l=0):

@@ -18,9 +18,9 @@ GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "survey_
 
 
 def cfg(dim, cells, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, coarse=orc.COARSE_DIRECT, ncoarse=10):
-    sm = orc.RBGS if smoother == "rbgs" else orc.JACOBI
+    sm = {"rbgs": orc.RBGS, "gs_lex": orc.GS_LEX}.get(smoother, orc.JACOBI)
     if omega is None:
-        omega = 1.0 if sm == orc.RBGS else 0.8
+        omega = 0.8 if sm == orc.JACOBI else 1.0
     return orc.Config(dim=dim, cells=tuple(cells), levels=levels, smoother=sm, omega=omega,
                       nu1=nu1, nu2=nu2, coarse=coarse, ncoarse=ncoarse)
 
@@ -106,6 +106,32 @@ def test_rbgs_equals_dense(dim, cells, omega):
     out = O.rbgs(0, u, f)
     ref = dense.rbgs(A, D, omega, dense.interior(u), dense.interior(f), list(cells))
     np.testing.assert_allclose(dense.interior(out), ref, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("dim,cells", SMALL)
+@pytest.mark.parametrize("omega", [1.0, 1.2])
+def test_gs_lex_equals_dense_sor(dim, cells, omega):
+    """Lexicographic omega-GS (Table 1, S:416 'order lex') = the SOR matrix iteration
+    u + omega (D - omega L)^-1 (f - A u), L the strictly lower part in row-major order."""
+    O = orc.Oracle(cfg(dim, cells, levels=1, smoother="gs_lex", omega=omega))
+    u, f = rnd(O.shape(0), 25), rnd(O.shape(0), 26)
+    c, D, _ = dense.coeffs(list(cells), 0)
+    A = dense.assemble_A(list(cells), c)
+    out = O.gs_lex(0, u, f)
+    ref = dense.gs_lex(A, D, omega, dense.interior(u), dense.interior(f))
+    np.testing.assert_allclose(dense.interior(out), ref, rtol=1e-13, atol=1e-13)
+
+
+def test_gs_lex_last_node_residual_zero():
+    """omega = 1: the last node in lexicographic order has no later neighbour, so its
+    residual is exactly solved away (to rounding) by the sweep."""
+    for dim, cells in [(2, (8, 6)), (3, (4, 6, 4))]:
+        O = orc.Oracle(cfg(dim, cells, levels=1, smoother="gs_lex", omega=1.0))
+        u, f = rnd(O.shape(0), 27), rnd(O.shape(0), 28)
+        out = O.gs_lex(0, u, f)
+        r = O.residual(0, out, f)
+        last = (-2,) * dim
+        assert abs(r[last]) <= 1e-12 * np.abs(f).max() * 4 * cells[0] ** 2, r[last]
 
 
 def test_rbgs_black_residual_zero_and_single_unknown_exact():
@@ -247,6 +273,8 @@ DENSE_CASES = [
     (3, (8, 8, 8), 2, "rbgs", 1.0, 2, 2),
     (3, (8, 8, 8), 3, "jacobi", 0.8, 2, 2),
     (3, (8, 8, 16), 3, "rbgs", 1.0, 2, 1),
+    (2, (16, 8), 3, "gs_lex", 1.0, 2, 2),
+    (3, (8, 8, 8), 2, "gs_lex", 1.15, 1, 1),
 ]
 
 
