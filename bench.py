@@ -38,6 +38,8 @@ CONFIGS = {
     "C4": (2, 8193, "jacobi", 3, 3, "f32", 0, 0.8),
     "C5": (3, 1025, "rbgs", 2, 2, "f64", 0, 1.0),
     "C1": (2, 65, "jacobi", 2, 2, "f64", 5, 0.8),
+    # smoother variant: lexicographic omega-GS, one launch per hyperplane
+    "C2-lex": (3, 129, "gs_lex", 2, 2, "f64", 0, 1.0),
 }
 WORKLOAD_DESC = {
     "C3-f64": "3D Poisson 7-point 513^3 nodes, RBGS V(2,2), FP64, W1 (f=0, u0~U[0,1) seed 42)",
@@ -46,6 +48,7 @@ WORKLOAD_DESC = {
     "C4": "2D Poisson 5-point 8193^2 nodes, Jacobi(0.8) V(3,3), FP32, W1 seed 42",
     "C5": "3D Poisson 7-point 1025^3 nodes, RBGS V(2,2), FP64, W1 seed 42",
     "C1": "2D Poisson 5-point 65^2 nodes, 5 levels, Jacobi(0.8) V(2,2), FP64, W1 seed 42",
+    "C2-lex": "3D Poisson 7-point 129^3 nodes, lexicographic GS V(2,2), FP64, W1 seed 42",
 }
 # complex diffusion, FAS on cell-centred grids (the paper's Table 2
 # "Complex Diff." rows: N = 4096^2 cells in 2D, 256^3 in 3D)
@@ -215,7 +218,7 @@ def oracle_step_time(cfgname, max_seconds=30.0):
     for n in [nodes - 1, (nodes - 1) // 2, (nodes - 1) // 4]:
         cells = (n,) * dim
         c = orc.Config(dim=dim, cells=cells, levels=levels if n == nodes - 1 else 0,
-                       smoother=orc.RBGS if sm == "rbgs" else orc.JACOBI, omega=omega, nu1=nu1, nu2=nu2)
+                       smoother={"rbgs": orc.RBGS, "gs_lex": orc.GS_LEX}.get(sm, orc.JACOBI), omega=omega, nu1=nu1, nu2=nu2)
         O = orc.Oracle(c, npdt)
         u, f = wl.workload("W1", dim, cells, seed=42, dtype=npdt)
         t0 = time.perf_counter()

@@ -51,7 +51,9 @@ typedef enum {
     MG_ERR_POISONED = 8          /* an earlier CUDA/NCCL error poisoned it    */
 } mg_status;
 
-typedef enum { MG_JACOBI = 0, MG_RBGS = 1 } mg_smoother;
+/* omega-Jacobi, red-black GS, lexicographic omega-GS (Table 1, "order lex";
+ * one hyperplane i+j+k = s at a time on the GPU, nranks = 1, Poisson only) */
+typedef enum { MG_JACOBI = 0, MG_RBGS = 1, MG_GS_LEX = 2 } mg_smoother;
 typedef enum { MG_FP64 = 0, MG_FP32 = 1 } mg_dtype;           /* Table 1 */
 typedef enum { MG_COARSE_DIRECT = 0, MG_COARSE_SWEEPS = 1 } mg_coarse;
 /* The problem (Table 1 "Operator"):

@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmgb200.so")
 
-JACOBI, RBGS = 0, 1
+JACOBI, RBGS, GS_LEX = 0, 1, 2
 FP64, FP32 = 0, 1
 COARSE_DIRECT, COARSE_SWEEPS = 0, 1
 FLAG_NO_GRAPH, FLAG_BASELINE, FLAG_SLAB, FLAG_FUSE_PROLONG, FLAG_HOST_LOOP = 1, 2, 4, 8, 16
@@ -126,6 +126,10 @@ def _torch():
     return torch
 
 
+def _smoother_code(smoother):
+    return {"rbgs": RBGS, RBGS: RBGS, "gs_lex": GS_LEX, GS_LEX: GS_LEX}.get(smoother, JACOBI)
+
+
 def _problem_code(problem):
     return PROBLEM_COMPLEX_DIFFUSION if problem in ("complex_diffusion", "cd", PROBLEM_COMPLEX_DIFFUSION) \
         else PROBLEM_POISSON
@@ -145,8 +149,8 @@ def make_config(dim, nodes, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2,
         c.coeff[d] = float(coeff[d])
         c.h[d] = 0.0 if h is None or d >= dim else float(h[d])
     c.levels = levels
-    c.smoother = RBGS if smoother in ("rbgs", RBGS) else JACOBI
-    c.omega = float(omega) if omega is not None else (1.0 if c.smoother == RBGS else 0.8)
+    c.smoother = _smoother_code(smoother)
+    c.omega = float(omega) if omega is not None else (0.8 if c.smoother == JACOBI else 1.0)
     c.nu1, c.nu2 = nu1, nu2
     c.coarse = COARSE_DIRECT if coarse in ("direct", COARSE_DIRECT) else COARSE_SWEEPS
     c.ncoarse = ncoarse
@@ -216,8 +220,8 @@ class Solver:
             c.coeff[d] = float(coeff[d])
             c.h[d] = 0.0 if h is None or d >= dim else float(h[d])
         c.levels = levels
-        c.smoother = RBGS if smoother in ("rbgs", RBGS) else JACOBI
-        c.omega = float(omega) if omega is not None else (1.0 if c.smoother == RBGS else 0.8)
+        c.smoother = _smoother_code(smoother)
+        c.omega = float(omega) if omega is not None else (0.8 if c.smoother == JACOBI else 1.0)
         c.nu1, c.nu2 = nu1, nu2
         c.coarse = COARSE_DIRECT if coarse in ("direct", COARSE_DIRECT) else COARSE_SWEEPS
         c.ncoarse = ncoarse

@@ -115,7 +115,10 @@ static mg_status validate(const mg_config* c, int* levels_out) {
   if (c->dim != 2 && c->dim != 3) return fail(s, MG_ERR_INVALID, "dim must be 2 or 3 (got %d)", c->dim);
   if (c->problem == MG_PROBLEM_COMPLEX_DIFFUSION) return validate_cd(c, levels_out);
   if (c->problem != MG_PROBLEM_POISSON) return fail(s, MG_ERR_INVALID, "bad problem %d", c->problem);
-  if (c->smoother != MG_JACOBI && c->smoother != MG_RBGS) return fail(s, MG_ERR_INVALID, "bad smoother");
+  if (c->smoother != MG_JACOBI && c->smoother != MG_RBGS && c->smoother != MG_GS_LEX)
+    return fail(s, MG_ERR_INVALID, "bad smoother");
+  if (c->smoother == MG_GS_LEX && (c->nranks > 1 || (c->flags & MG_FLAG_SLAB)))
+    return fail(s, MG_ERR_INVALID, "the lexicographic smoother is sequential across the domain: nranks = 1, no MG_FLAG_SLAB");
   if (!(c->omega > 0.0 && c->omega < 2.0)) return fail(s, MG_ERR_INVALID, "omega must be in (0,2) (S:46)");
   if (c->nu1 < 0 || c->nu2 < 0) return fail(s, MG_ERR_INVALID, "nu1, nu2 must be >= 0");
   if (c->coarse != MG_COARSE_DIRECT && c->coarse != MG_COARSE_SWEEPS) return fail(s, MG_ERR_INVALID, "bad coarse");

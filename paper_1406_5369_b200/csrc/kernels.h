@@ -11,6 +11,12 @@ template <typename T>
 cudaError_t launch_jacobi(const Geom& g, const Coef<T>& c, const T* uin, const T* f, T* uout, cudaStream_t st);
 template <typename T>
 cudaError_t launch_rbgs_colour(const Geom& g, const Coef<T>& c, T* u, const T* f, int colour, cudaStream_t st);
+// one hyperplane i + j + global plane = s of a lexicographic omega-GS sweep (in place)
+template <typename T>
+cudaError_t launch_gs_lex_plane(const Geom& g, const Coef<T>& c, T* u, const T* f, int s, cudaStream_t st);
+// first / last hyperplane index of a level's interior
+inline int gs_lex_smin(const Geom& g) { return 1 + (g.three_d ? 1 : 0) + g.p_lo + g.p_glob0; }
+inline int gs_lex_smax(const Geom& g) { return (g.nx - 1) + (g.three_d ? g.ny - 1 : 0) + g.p_hi - 1 + g.p_glob0; }
 template <typename T>
 cudaError_t launch_residual(const Geom& g, const Coef<T>& c, const T* u, const T* f, T* r, cudaStream_t st);
 template <typename T>

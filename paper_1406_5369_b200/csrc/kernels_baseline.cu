@@ -82,6 +82,24 @@ __global__ void __launch_bounds__(BX* BY) k_rbgs_colour(Geom g, Coef<T> c, T* __
   u[p] = add(u[p], mul(c.wd, r));
 }
 
+// ---- lexicographic omega-GS (Table 1; "order lex"): one hyperplane
+// i + j + global plane = s per launch.  Every node's lower neighbours lie on the
+// previous hyperplane (already new), its upper ones on the next (still old), so
+// the sweep over s = min..max reproduces the row-major sequential sweep exactly.
+template <typename T>
+__global__ void __launch_bounds__(256) k_gs_lex_plane(Geom g, Coef<T> c, T* __restrict__ u,
+                                                      const T* __restrict__ f, int s) {
+  const int nj = g.three_d ? g.ny - 1 : 1;
+  const int q = blockIdx.x * 256 + threadIdx.x;
+  if (q >= nj * (g.p_hi - g.p_lo)) return;
+  const int j = g.three_d ? 1 + q % nj : 0;
+  const int pl = g.p_lo + q / nj;
+  const int i = s - j - (pl + g.p_glob0);
+  if (i < 1 || i > g.nx - 1) return;
+  const long long p = lin(g, i, j, pl);
+  u[p] = add(u[p], mul(c.wd, point_residual(u, p, g, c, f[p])));
+}
+
 // ---- residual r = f - A u (Alg. 1 line 4) ----------------------------------
 template <typename T>
 __global__ void __launch_bounds__(BX* BY) k_residual(Geom g, Coef<T> c, const T* __restrict__ u,
@@ -365,6 +383,13 @@ cudaError_t launch_rbgs_colour(const Geom& g, const Coef<T>& c, T* u, const T* f
   return cudaGetLastError();
 }
 template <typename T>
+cudaError_t launch_gs_lex_plane(const Geom& g, const Coef<T>& c, T* u, const T* f, int s, cudaStream_t st) {
+  const int n = (g.three_d ? g.ny - 1 : 1) * (g.p_hi - g.p_lo);
+  if (n <= 0) return cudaSuccess;
+  k_gs_lex_plane<T><<<(n + 255) / 256, 256, 0, st>>>(g, c, u, f, s);
+  return cudaGetLastError();
+}
+template <typename T>
 cudaError_t launch_residual(const Geom& g, const Coef<T>& c, const T* u, const T* f, T* r, cudaStream_t st) {
   if (empty(g)) return cudaSuccess;
   k_residual<T><<<grid_of(g), dim3(BX, BY), 0, st>>>(g, c, u, f, r);
@@ -434,6 +459,7 @@ cudaError_t launch_workload_fill(const Geom& g, uint64_t seed, double lo, double
 #define MG_INST(T)                                                                                           \
   template cudaError_t launch_jacobi<T>(const Geom&, const Coef<T>&, const T*, const T*, T*, cudaStream_t);  \
   template cudaError_t launch_rbgs_colour<T>(const Geom&, const Coef<T>&, T*, const T*, int, cudaStream_t);  \
+  template cudaError_t launch_gs_lex_plane<T>(const Geom&, const Coef<T>&, T*, const T*, int, cudaStream_t); \
   template cudaError_t launch_residual<T>(const Geom&, const Coef<T>&, const T*, const T*, T*, cudaStream_t); \
   template cudaError_t launch_restrict<T>(const Geom&, const Geom&, const T*, T*, cudaStream_t);             \
   template cudaError_t launch_prolong_correct<T>(const Geom&, const Geom&, const T*, T*, cudaStream_t);      \

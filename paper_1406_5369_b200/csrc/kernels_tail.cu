@@ -59,6 +59,24 @@ __device__ void zero_level(const Geom& g, T* u) {
 template <typename T>
 __device__ T* sweep(const Geom& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f) {
   const int n = interior_count(g);
+  if (rbgs == 2) {  // lexicographic omega-GS: hyperplanes i + j + global plane = s in order
+    const int nj = g.three_d ? g.ny - 1 : 1;
+    const int m = nj * (g.p_hi - g.p_lo);
+    const int smin = 1 + (g.three_d ? 1 : 0) + g.p_lo + g.p_glob0;
+    const int smax = (g.nx - 1) + (g.three_d ? g.ny - 1 : 0) + g.p_hi - 1 + g.p_glob0;
+    for (int s = smin; s <= smax; s++) {
+      for (int q = gtid(); q < m; q += gstride()) {
+        const int j = g.three_d ? 1 + q % nj : 0;
+        const int pl = g.p_lo + q / nj;
+        const int i = s - j - (pl + g.p_glob0);
+        if (i < 1 || i > g.nx - 1) continue;
+        const long long p = lin(g, i, j, pl);
+        u[p] = add(u[p], mul(c.wd, point_residual(u, p, g, c, f[p])));
+      }
+      pass_sync();
+    }
+    return u;
+  }
   if (rbgs) {
     for (int colour = 0; colour < 2; colour++) {
       for (int q = gtid(); q < n; q += gstride()) {

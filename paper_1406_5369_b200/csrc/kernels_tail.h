@@ -9,7 +9,7 @@ constexpr int kTailMax = 12;  // levels handled by one tail launch
 template <typename T>
 struct TailParams {
   int nl;          // tail levels (index 0 = the top tail level lt)
-  int rbgs;        // smoother: 1 red-black GS, 0 Jacobi
+  int rbgs;        // smoother: 1 red-black GS, 0 Jacobi, 2 lexicographic GS
   int nu1, nu2;
   int sweeps;      // coarsest: 1 = ncoarse sweeps, 0 = direct
   int ncoarse;

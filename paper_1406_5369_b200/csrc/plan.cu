@@ -49,6 +49,7 @@ enum Kind {
   K_CD_RESIDUAL,
   K_CD_COPY,
   K_CD_TAIL,
+  K_GS_LEX,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -59,7 +60,7 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "coarse_tail",   "prolong+sweep",
                                        "cd_gfield",     "cd_jacobi",     "cd_rbgs_colour", "cd_restrict",
                                        "cd_fas_rhs",    "cd_prolong",    "cd_norm_partial", "cd_residual",
-                                       "cd_copy",       "cd_tail"};
+                                       "cd_copy",       "cd_tail",       "gs_lex_plane"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -337,7 +338,7 @@ struct Exec {
   double w(int l) const { return nodes_of(s->lv[l]) * sizeof(T); }  // one word per node of level l
 
   bool pm(int l) const {
-    return !(s->cfg.flags & MG_FLAG_BASELINE) && pm::supported(s->lv[l].g, s->cfg.pm_min_nx ? s->cfg.pm_min_nx : 128);
+    return !(s->cfg.flags & MG_FLAG_BASELINE) && s->cfg.smoother != MG_GS_LEX && pm::supported(s->lv[l].g, s->cfg.pm_min_nx ? s->cfg.pm_min_nx : 128);
   }
   // First level of the single-CTA coarse tail (levels >= lt run in one launch): the
   // first non-distributed level whose interior has <= 48K nodes.  L if none / disabled.
@@ -360,7 +361,7 @@ struct Exec {
   mg_status run_tail(int lt, T* u_top, const T* f_top) {
     TailParams<T> P{};
     P.nl = s->L - lt;
-    P.rbgs = s->cfg.smoother == MG_RBGS;
+    P.rbgs = s->cfg.smoother == MG_RBGS ? 1 : (s->cfg.smoother == MG_GS_LEX ? 2 : 0);
     P.nu1 = s->cfg.nu1;
     P.nu2 = s->cfg.nu2;
     P.sweeps = s->cfg.coarse == MG_COARSE_SWEEPS;
@@ -455,6 +456,16 @@ struct Exec {
       r = launch(s, st, K_JACOBI, l, 3 * w(l), [&] { return launch_jacobi<T>(L.g, coef(l), cur, f, other, st); });
       std::swap(cur, other);
       return r;
+    }
+    if (s->cfg.smoother == MG_GS_LEX) {  // one launch per hyperplane (nranks == 1)
+      const int a = gs_lex_smin(L.g), b = gs_lex_smax(L.g);
+      T* u = cur;
+      for (int hp = a; hp <= b; hp++) {
+        mg_status r = launch(s, st, K_GS_LEX, l, 3 * w(l) / (b - a + 1),
+                             [&] { return launch_gs_lex_plane<T>(L.g, coef(l), u, f, hp, st); });
+        if (r != MG_OK) return r;
+      }
+      return MG_OK;
     }
     for (int colour = 0; colour < 2; colour++) {
       mg_status r = exchange(l, cur, 1);

@@ -86,6 +86,8 @@ def test_complex_diffusion_config_valid_without_gpu_fails_loudly():
     (dict(problem=1, nodes=16, coarse=1, kappa=-1.0), 1),
     (dict(problem=1, nodes3=(16, 16, 12), coarse=1, levels=4), 2),  # 12 cells not divisible by 8
     (dict(problem=2), 1),
+    (dict(smoother=2, nranks=2), 1),              # lexicographic GS is sequential: one rank only
+    (dict(problem=1, nodes=16, coarse=1, smoother=2), 1),  # ... and Poisson only
 ])
 def test_create_rejects_bad_config(kw, status):
     st, h, msg = _create(**kw)

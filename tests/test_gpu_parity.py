@@ -20,11 +20,12 @@ def make(dim, cells, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, dtype=
          ncoarse=10, flags=0, pm_min_nx=16):
     import paper_1406_5369_b200 as mgb
     if omega is None:
-        omega = 1.0 if smoother == "rbgs" else 0.8
+        omega = 0.8 if smoother == "jacobi" else 1.0
     S = mgb.Solver(dim, tuple(c + 1 for c in cells), levels=levels, smoother=smoother, omega=omega, nu1=nu1,
                    nu2=nu2, coarse=coarse, ncoarse=ncoarse, dtype=dtype, flags=flags, pm_min_nx=pm_min_nx)
     O = orc.Oracle(orc.Config(dim=dim, cells=tuple(cells), levels=S.levels,
-                              smoother=orc.RBGS if smoother == "rbgs" else orc.JACOBI, omega=omega, nu1=nu1,
+                              smoother={"rbgs": orc.RBGS, "gs_lex": orc.GS_LEX}.get(smoother, orc.JACOBI),
+                              omega=omega, nu1=nu1,
                               nu2=nu2, coarse=orc.COARSE_DIRECT if coarse == "direct" else orc.COARSE_SWEEPS,
                               ncoarse=ncoarse),
                    np.float64 if dtype == "f64" else np.float32)

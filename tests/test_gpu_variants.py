@@ -50,3 +50,47 @@ def test_sor_rb_iteration_parity_and_faster():
         np.testing.assert_allclose(hist, hist_or, rtol=1e-12)
         counts[omega] = k
     assert counts[1.15] <= counts[1.0], counts
+
+
+LEX_CASES = [
+    dict(dim=2, cells=(64, 64)),                       # whole cycle in the coarse tail
+    dict(dim=2, cells=(256, 128), nu1=1, nu2=1),        # per-hyperplane kernels above the tail
+    dict(dim=3, cells=(32, 32, 32), omega=1.2),
+    dict(dim=3, cells=(64, 64, 32)),
+    dict(dim=2, cells=(128, 128), dtype="f32"),
+]
+
+
+@pytest.mark.parametrize("case", LEX_CASES, ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
+def test_gs_lex_cycle_parity(case):
+    """Lexicographic omega-GS (Table 1): hyperplane-ordered on the GPU, equal to
+    the oracle's sequential row-major sweep bit for bit."""
+    case = dict(case)
+    dt = case.get("dtype", "f64")
+    S, O = make(**case, smoother="gs_lex", pm_min_nx=0)
+    u, f = wl.workload("W4", case["dim"], case["cells"], seed=31, dtype=S.np_dtype)
+    u = u + wl.random_interior(case["dim"], case["cells"], 5, S.np_dtype)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    uo = u.copy()
+    for k in range(2):
+        S.vcycle(du, df)
+        O.vcycle_inplace(uo, f)
+        got = S.to_numpy(du)
+        assert relerr(got, uo) <= TOL[dt], (k, relerr(got, uo))
+        assert np.array_equal(got, uo)
+
+
+def test_gs_lex_per_op_and_solve():
+    S, O = make(2, (96, 64), levels=4, smoother="gs_lex")
+    u = wl.random_interior(2, (96, 64), 8, np.float64, -1, 1)
+    f = wl.random_interior(2, (96, 64), 9, np.float64, -1, 1)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    out = S.empty(0)
+    S.op_smooth(0, du, df, out)
+    assert np.array_equal(S.to_numpy(out), O.smooth(0, u, f))
+    u1, f1 = wl.workload("W1", 2, (96, 64), seed=42)
+    d1, g1 = S.from_numpy(u1), S.from_numpy(f1)
+    k, hist = S.solve(d1, g1, 1e-10, 40)
+    _, k_or, hist_or = O.solve(u1, f1, 1e-10, 40)
+    assert k == k_or
+    np.testing.assert_allclose(hist, hist_or, rtol=1e-12)
