@@ -399,7 +399,9 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         const int pgl = p + pg0;
         const bool pl_in = pgl >= 1 && pgl <= g.nz - 1;
         const int kr = (oy + pgl) & 1;  // warp uniform: red nodes at ox + kr + 2m
-        if (NRM && p >= pa && p < pb) acc_norm(U0, F0, um, u0, up);
+        // NRM: ||f - A u_in||^2 of plane p; the red nodes' residuals come from the red stage below
+        // (the same operands), only the black nodes' are computed separately
+        const bool nrm_here = NRM && p >= pa && p < pb;
         T pr0[NR];
         const V fcur = ld_vec(F0 + fo);  // f(p) of the thread's nodes (kept for plane p's black stage)
         auto red_stage = [&](auto KRc) {
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
           // FP32: 16-B vector loads of the rows above / below (one LDS.128 instead of two
           // 4-way-conflicted scalars); FP64 (one red node per thread): the scalar is as cheap
           V dn, upr;
-          if constexpr (W == 4) {
+          if constexpr (W == 4 || NRM) {
             dn = svec(U0, bo - BX);
             upr = svec(U0, bo + BX);
           } else {
@@ -415,6 +417,20 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
             upr.v[KR] = su(U0, bo + KR + BX);
           }
           const T edge = KR == 0 ? su(U0, bo - 1) : su(U0, bo + W);
+          if constexpr (NRM) {
+            if (nrm_here) {  // black nodes of plane p: residual of the old iterate
+              const T oedge = KR == 0 ? su(U0, bo + W) : su(U0, bo - 1);
+#pragma unroll
+              for (int m = 0; m < NR; m++) {
+                const int j = (1 - KR) + 2 * m;
+                const T l = j == 0 ? oedge : u0.v[j > 0 ? j - 1 : 0];
+                const T r = j == W - 1 ? oedge : u0.v[j < W - 1 ? j + 1 : 0];
+                const double rr =
+                    (double)sub(fcur.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
+                if (in[j]) nsum = __dadd_rn(nsum, __dmul_rn(rr, rr));
+              }
+            }
+          }
           V pv = u0;  // PR row vector: red values at red nodes (black entries are never read)
 #pragma unroll
           for (int m = 0; m < NR; m++) {
@@ -422,7 +438,10 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
             const T ctr = u0.v[j];
             const T l = j == 0 ? edge : u0.v[j > 0 ? j - 1 : 0];
             const T r = j == W - 1 ? edge : u0.v[j < W - 1 ? j + 1 : 0];
-            const T v = relax(c, ctr, l, r, dn.v[j], upr.v[j], um.v[j], up.v[j], fcur.v[j]);
+            // relax() written out: the residual doubles as the red node's norm term
+            const T res = sub(fcur.v[j], apply_A(c, ctr, l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
+            const T v = add(ctr, mul(c.wd, res));
+            if (NRM && nrm_here && in[j]) nsum = __dadd_rn(nsum, __dmul_rn((double)res, (double)res));
             const T prv = (pl_in && in[j]) ? v : ctr;
             pv.v[j] = prv;
             pr0[m] = prv;
@@ -520,7 +539,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         }
         const T* U0 = R.U(N(p - 1));
         up = svec(R.U(N(p)), bo);
-        if (MODE == 2 || NRM) acc_norm(U0, R.F(N(p)), um, u0, up);  // r = f - A u, FP64 squares
+        if (MODE == 2) acc_norm(U0, R.F(N(p)), um, u0, up);  // r = f - A u, FP64 squares
         if (MODE != 2) {
           const V fv = ld_vec(R.F(N(p)) + fo), dn = svec(U0, bo - BX), upr = svec(U0, bo + BX);
           const T el = su(U0, bo - 1), er = su(U0, bo + W);
@@ -529,7 +548,10 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
           for (int j = 0; j < W; j++) {
             const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
             const T r = j == W - 1 ? er : u0.v[j < W - 1 ? j + 1 : 0];
-            const T v = relax(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j], fv.v[j]);
+            // relax() written out: with NRM the residual is also the norm term of the input
+            const T res = sub(fv.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
+            const T v = add(u0.v[j], mul(c.wd, res));
+            if (NRM && in[j]) nsum = __dadd_rn(nsum, __dmul_rn((double)res, (double)res));
             o.v[j] = in[j] ? v : u0.v[j];
           }
           store_vec(orow + (long long)p * g.pstride, ox, in, o);
