@@ -138,6 +138,11 @@ static mg_status alloc_common(mg_solver* s, int np) {
   }
   cudaError_t e = cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap_body, cudaStreamNonBlocking);
+  if (e == cudaSuccess && s->comm) {  // halo exchanges overlapped with interior sweeps
+    e = cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
+  }
   if (e != cudaSuccess) return cuda_fail(s, e, "cudaStreamCreate");
   if (cudaMalloc(&s->d_loop, sizeof(LoopState)) != cudaSuccess ||
       cudaMallocHost(&s->h_loop, sizeof(LoopState)) != cudaSuccess) {
@@ -324,6 +329,9 @@ void plan_free(mg_solver* s) {
   }
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   if (s->cap_body) cudaStreamDestroy(s->cap_body);
+  if (s->comm_stream) cudaStreamDestroy(s->comm_stream);
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   cudaFree(s->d_loop);
   cudaFree(s->d_hist);
   if (s->h_loop) cudaFreeHost(s->h_loop);
@@ -395,7 +403,8 @@ struct Exec {
 
   // Slab halo exchange of a distributed level: my h top owned planes
   // go to rank+1's lower halo, my h bottom owned planes to rank-1's upper halo.
-  mg_status exchange(int l, T* buf, int h) {
+  mg_status exchange(int l, T* buf, int h) { return exchange_on(l, buf, h, st); }
+  mg_status exchange_on(int l, T* buf, int h, cudaStream_t st) {
     const Level& L = s->lv[l];
     if (!L.dist || !s->comm) return MG_OK;
     const int H = s->pt.H, P = s->pt.P, rk = s->pt.rank;
@@ -434,15 +443,43 @@ struct Exec {
     const Level& L = s->lv[l];
     if (pm(l)) {
       const bool rb = s->cfg.smoother == MG_RBGS;
-      if (!zero_in) {
-        mg_status r = exchange(l, cur, rb ? 2 : 1);
-        if (r != MG_OK) return r;
-      }
       T* in = cur;
       T* out = other;
-      mg_status r = launch(s, st, rb ? K_SWEEP_RBGS : K_SWEEP_JACOBI, l, (zero_in ? 2 : 3) * w(l), [&] {
-        return pm::launch_sweep<T>(L.g, coef(l), rb, zero_in ? nullptr : in, f, out, zero_in, zc(l), st);
-      });
+      const Kind kind = rb ? K_SWEEP_RBGS : K_SWEEP_JACOBI;
+      const int B = rb ? 2 : 1;  // planes next to the slab faces that read halo planes
+      auto sweep_range = [&](int lo, int hi) {
+        Geom gr = L.g;
+        gr.p_lo = lo;
+        gr.p_hi = hi;
+        return launch(s, st, kind, l, (zero_in ? 2 : 3) * w(l) * (hi - lo) / (L.g.p_hi - L.g.p_lo), [&] {
+          return pm::launch_sweep<T>(gr, coef(l), rb, zero_in ? nullptr : in, f, out, zero_in, zc(l), st);
+        });
+      };
+      mg_status r;
+      if (!zero_in && L.dist && L.g.p_hi - L.g.p_lo >= 2 * B + 8) {
+        // slab: the halo exchange runs on the comm stream while the interior planes, which
+        // read no halo, are swept; then the B planes next to each face.  The
+        // plane ranges split the same per-plane arithmetic: bitwise identical to one launch.
+        const int lo = L.g.p_lo, hi = L.g.p_hi;
+        if (s->comm) {
+          cudaError_t e = cudaEventRecord(s->ev_fork, st);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(s->comm_stream, s->ev_fork, 0);
+          if (e != cudaSuccess) return cuda_fail(s, e, "halo fork");
+          if ((r = exchange_on(l, in, B, s->comm_stream)) != MG_OK) return r;
+          e = cudaEventRecord(s->ev_join, s->comm_stream);
+          if (e != cudaSuccess) return cuda_fail(s, e, "halo join");
+        }
+        if ((r = sweep_range(lo + B, hi - B)) != MG_OK) return r;
+        if (s->comm) {
+          cudaError_t e = cudaStreamWaitEvent(st, s->ev_join, 0);
+          if (e != cudaSuccess) return cuda_fail(s, e, "halo join");
+        }
+        if ((r = sweep_range(lo, lo + B)) != MG_OK || (r = sweep_range(hi - B, hi)) != MG_OK) return r;
+        std::swap(cur, other);
+        return MG_OK;
+      }
+      if (!zero_in && (r = exchange(l, cur, B)) != MG_OK) return r;
+      r = sweep_range(L.g.p_lo, L.g.p_hi);
       std::swap(cur, other);
       return r;
     }

@@ -84,6 +84,8 @@ struct mg_solver {
   // graphs keyed by (u, f)
   cudaStream_t cap_stream = nullptr;
   cudaStream_t cap_body = nullptr;   // captures the body of the driver loop's WHILE node
+  cudaStream_t comm_stream = nullptr;  // slab halo exchanges overlapped with interior sweeps
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   mg::LoopState* d_loop = nullptr;
   mg::LoopState* h_loop = nullptr;   // pinned
   double* d_hist = nullptr;
