@@ -167,6 +167,17 @@ mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol, int32_t ma
 mg_status mg_vcycle_host(mg_solver* s, void* u_host, const void* f_host, int32_t ncycles,
                          double* norm_out, void* stream);
 
+/* End-to-end for a stream of `nbatch` independent problems in HOST memory (pinned):
+ * problem b copies f_in[b] and u_in[b] to the device, runs `ncycles` cycles, computes
+ * its residual norm into norms[b] (may be NULL) and copies u back to u_out[b] (u_out[b]
+ * may equal u_in[b]).  Copies and compute are pipelined over two library-owned staging
+ * sets and two copy streams: the H2D of problem b+1 and the D2H of problem b-1 overlap
+ * problem b's cycles (PCIe is full duplex).  Blocking; the host buffers of all problems
+ * must stay valid and unaliased across problems until it returns. */
+mg_status mg_vcycle_host_batch(mg_solver* s, const void* const* u_in, void* const* u_out,
+                               const void* const* f_in, int32_t nbatch, int32_t ncycles,
+                               double* norms, void* stream);
+
 /* ---- per-operation entry points (one step of Alg. 1 each, for parity tests).
  * Arrays use mg_level_layout(level).  Asynchronous unless stated.
  * Complex diffusion: mg_op_smooth freezes the diffusivity at g(u_in) (lagged) and

@@ -29,7 +29,7 @@ PROBLEM_POISSON, PROBLEM_COMPLEX_DIFFUSION = 0, 1
 # every symbol include/mg.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = [
     "mg_config_default", "mg_create", "mg_layout", "mg_level_layout", "mg_num_levels", "mg_vcycle",
-    "mg_residual_norm", "mg_solve", "mg_vcycle_host", "mg_op_smooth", "mg_op_residual", "mg_op_restrict",
+    "mg_residual_norm", "mg_solve", "mg_vcycle_host", "mg_vcycle_host_batch", "mg_op_smooth", "mg_op_residual", "mg_op_restrict",
     "mg_op_prolong_correct", "mg_op_coarse_solve", "mg_op_norm", "mg_workload_fill",
     "mg_launches_per_cycle", "mg_profile_enable", "mg_profile_read", "mg_error_string", "mg_destroy",
     "mg_partition", "mg_nccl_unique_id",
@@ -94,6 +94,7 @@ def load_library():
     lib.mg_residual_norm.argtypes = [P, P, P, pD, P]
     lib.mg_solve.argtypes = [P, P, P, D, I32, ctypes.POINTER(I32), pD, P]
     lib.mg_vcycle_host.argtypes = [P, P, P, I32, pD, P]
+    lib.mg_vcycle_host_batch.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), I32, I32, pD, P]
     lib.mg_op_smooth.argtypes = [P, I32, P, P, P, P]
     lib.mg_op_residual.argtypes = [P, I32, P, P, P, P]
     lib.mg_op_restrict.argtypes = [P, I32, P, P, P]
@@ -360,6 +361,16 @@ class Solver:
                                           ctypes.c_void_p(f_host.data_ptr()), int(ncycles), ctypes.byref(out),
                                           self._stream(stream)))
         return out.value
+
+    def vcycle_host_batch(self, u_in, u_out, f_in, ncycles=1, stream=None):
+        """Pipelined end-to-end over independent problems held in host (pinned) tensors:
+        lists u_in, u_out, f_in of equal length; returns the residual norm of each problem."""
+        n = len(u_in)
+        arr = lambda ts: (ctypes.c_void_p * n)(*[t.data_ptr() for t in ts])
+        norms = (ctypes.c_double * n)()
+        self._chk(self.lib.mg_vcycle_host_batch(self.h, arr(u_in), arr(u_out), arr(f_in), n, int(ncycles), norms,
+                                                self._stream(stream)))
+        return list(norms)
 
     # ---- per-operation entry points
     def op_smooth(self, level, u_in, f, u_out, stream=None):

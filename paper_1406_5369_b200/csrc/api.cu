@@ -366,6 +366,70 @@ extern "C" mg_status mg_vcycle_host(mg_solver* s, void* u_host, const void* f_ho
   return MG_OK;
 }
 
+extern "C" mg_status mg_vcycle_host_batch(mg_solver* s, const void* const* u_in, void* const* u_out,
+                                          const void* const* f_in, int32_t nbatch, int32_t ncycles, double* norms,
+                                          void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  if (!u_in || !u_out || !f_in || nbatch < 0 || ncycles < 0) return fail(s, MG_ERR_INVALID, "bad argument");
+  for (int b = 0; b < nbatch; b++)
+    if (!u_in[b] || !u_out[b] || !f_in[b]) return fail(s, MG_ERR_INVALID, "NULL host buffer of problem %d", b);
+  cudaStream_t cs = (cudaStream_t)stream;
+  const Level& lv = s->lv[0];
+  const size_t bytes = lv.elems * s->esz * (s->cfg.problem == MG_PROBLEM_COMPLEX_DIFFUSION ? 2 : 1);
+  if (!s->h2d_stream) {
+    for (int k = 0; k < 2; k++) {
+      if (cudaMalloc(&s->bstage_u[k], bytes) != cudaSuccess || cudaMalloc(&s->bstage_f[k], bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(s, MG_ERR_OOM, "staging allocation failed");
+      }
+      CK(cudaEventCreateWithFlags(&s->ev_h2d[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&s->ev_comp[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&s->ev_d2h[k], cudaEventDisableTiming));
+    }
+    CK(cudaStreamCreateWithFlags(&s->h2d_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->d2h_stream, cudaStreamNonBlocking));
+  }
+  if (norms && nbatch > s->h_norms_cap) {
+    if (s->h_norms) cudaFreeHost(s->h_norms);
+    s->h_norms = nullptr;
+    s->h_norms_cap = 0;
+    CK(cudaMallocHost(&s->h_norms, sizeof(double) * nbatch));
+    s->h_norms_cap = nbatch;
+  }
+  // the pipeline starts after everything already queued on the caller's stream
+  CK(cudaEventRecord(s->ev_comp[0], cs));
+  CK(cudaStreamWaitEvent(s->h2d_stream, s->ev_comp[0], 0));
+  for (int b = 0; b < nbatch; b++) {
+    const int k = b & 1;
+    void* su = s->bstage_u[k];
+    void* sf = s->bstage_f[k];
+    // H2D of problem b into set k once problem b-2 (same set) has been copied out
+    if (b >= 2) CK(cudaStreamWaitEvent(s->h2d_stream, s->ev_d2h[k], 0));
+    CK(cudaMemcpyAsync(sf, f_in[b], bytes, cudaMemcpyHostToDevice, s->h2d_stream));
+    CK(cudaMemcpyAsync(su, u_in[b], bytes, cudaMemcpyHostToDevice, s->h2d_stream));
+    CK(cudaEventRecord(s->ev_h2d[k], s->h2d_stream));
+    // cycles + norm on the caller's stream
+    CK(cudaStreamWaitEvent(cs, s->ev_h2d[k], 0));
+    for (int c = 0; c < ncycles; c++)
+      if ((st = mg_vcycle(s, su, sf, stream)) != MG_OK) return st;
+    if (norms) {
+      if ((st = plan_norm(s, 0, su, sf, nullptr, cs, false)) != MG_OK) return st;  // -> d_norm
+      CK(cudaMemcpyAsync(s->h_norms + b, s->d_norm, sizeof(double), cudaMemcpyDeviceToHost, cs));
+    }
+    CK(cudaEventRecord(s->ev_comp[k], cs));
+    // D2H of the result on the other copy engine
+    CK(cudaStreamWaitEvent(s->d2h_stream, s->ev_comp[k], 0));
+    CK(cudaMemcpyAsync(u_out[b], su, bytes, cudaMemcpyDeviceToHost, s->d2h_stream));
+    CK(cudaEventRecord(s->ev_d2h[k], s->d2h_stream));
+  }
+  CK(cudaStreamSynchronize(s->d2h_stream));
+  CK(cudaStreamSynchronize(cs));
+  if (norms)
+    for (int b = 0; b < nbatch; b++) norms[b] = s->h_norms[b];
+  return MG_OK;
+}
+
 // ------------------------------------------------------------------ per-op entry points
 #define LEVEL_CHECK(l)                                                                        \
   do {                                                                                        \

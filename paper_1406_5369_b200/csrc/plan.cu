@@ -323,6 +323,16 @@ void plan_free(mg_solver* s) {
   if (s->h_norm) cudaFreeHost(s->h_norm);
   cudaFree(s->stage_u);
   cudaFree(s->stage_f);
+  for (int k = 0; k < 2; k++) {
+    cudaFree(s->bstage_u[k]);
+    cudaFree(s->bstage_f[k]);
+    if (s->ev_h2d[k]) cudaEventDestroy(s->ev_h2d[k]);
+    if (s->ev_comp[k]) cudaEventDestroy(s->ev_comp[k]);
+    if (s->ev_d2h[k]) cudaEventDestroy(s->ev_d2h[k]);
+  }
+  if (s->h2d_stream) cudaStreamDestroy(s->h2d_stream);
+  if (s->d2h_stream) cudaStreamDestroy(s->d2h_stream);
+  if (s->h_norms) cudaFreeHost(s->h_norms);
   for (auto& r : s->prof) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);

@@ -91,9 +91,15 @@ struct mg_solver {
   double* d_hist = nullptr;
   int64_t hist_cap = 0;
   std::map<std::tuple<void*, const void*, int>, cudaGraphExec_t> graphs;  // (u, f, part)
-  // e2e staging
+  // e2e staging (mg_vcycle_host), and the double-buffered pipeline of mg_vcycle_host_batch
   void* stage_u = nullptr;
   void* stage_f = nullptr;
+  void* bstage_u[2] = {nullptr, nullptr};
+  void* bstage_f[2] = {nullptr, nullptr};
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  double* h_norms = nullptr;  // pinned, batch norms
+  int h_norms_cap = 0;
   // instrumentation
   int64_t launches_per_cycle = 0;
   int64_t launch_counter = 0;

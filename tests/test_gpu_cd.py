@@ -136,3 +136,16 @@ def test_cd_vcycle_host_e2e():
     ref = O.cycle(O.cycle(u, f), f)
     assert np.array_equal(S.to_numpy(hu.cuda()), ref)
     assert abs(n / O.norm(0, ref, f) - 1) <= 1e-12
+
+
+def test_cd_vcycle_host_batch():
+    S, O = make(2, (256, 128), smoother="rbgs")
+    ins = [wl.cd_workload(2, (256, 128), seed=s) for s in (3, 4)]
+    hu = [S.from_numpy(u).cpu().pin_memory() for u, _ in ins]
+    hf = [S.from_numpy(f).cpu().pin_memory() for _, f in ins]
+    ho = [h.clone().pin_memory() for h in hu]
+    norms = S.vcycle_host_batch(hu, ho, hf, 2)
+    for b, (u, f) in enumerate(ins):
+        ref = O.cycle(O.cycle(u, f), f)
+        assert np.array_equal(S.to_numpy(ho[b].cuda()), ref)
+        assert abs(norms[b] / O.norm(0, ref, f) - 1) <= 1e-12

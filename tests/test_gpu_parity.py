@@ -291,3 +291,23 @@ def test_fused_prolongation_sweep_parity(dt):
             assert relerr(got, uo) <= TOL[dt]
             if dt == "f64":
                 assert np.array_equal(got, uo)
+
+
+def test_vcycle_host_batch_pipeline():
+    """mg_vcycle_host_batch: independent problems from pinned host buffers, pipelined copies;
+    each result equals the oracle's cycle of that problem (in != out and in-place)."""
+    S, O = make(3, (64, 64, 64))
+    probs = [wl.workload("W4", 3, (64, 64, 64), seed=s) for s in (1, 2, 3)]
+    hu = [S.from_numpy(u + wl.random_interior(3, (64, 64, 64), 10 + i)).cpu().pin_memory()
+          for i, (u, _) in enumerate(probs)]
+    hf = [S.from_numpy(f).cpu().pin_memory() for _, f in probs]
+    refs = [O.vcycle(S.to_numpy(h.cuda()), f) for h, (_, f) in zip(hu, probs)]
+    ho = [h.clone().pin_memory() for h in hu]
+    norms = S.vcycle_host_batch(hu, ho, hf, 1)
+    for b in range(3):
+        assert np.array_equal(S.to_numpy(ho[b].cuda()), refs[b]), b
+        assert abs(norms[b] / O.norm(0, refs[b], probs[b][1]) - 1) < 1e-12
+    norms2 = S.vcycle_host_batch(hu, hu, hf, 1)  # in place
+    for b in range(3):
+        assert np.array_equal(S.to_numpy(hu[b].cuda()), refs[b]), b
+        assert norms2[b] == norms[b]
