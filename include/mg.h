@@ -107,6 +107,11 @@ typedef struct {
     double theta;        /* complex diffusion: angle of Eq. 3 (default pi/30)            */
     double kappa;        /* complex diffusion: scaling k of Eq. 3 (default 2); the paper
                             gives no values                                        */
+    void* loopback;      /* nranks > 1 without NCCL: a group from mg_loopback_group_create
+                            shared by `nranks` solvers of THIS process on the same device,
+                            each driven by its own host thread (the collectives rendezvous
+                            on the host and copy device-to-device); requires
+                            MG_FLAG_NO_GRAPH.  For testing the multi-rank path on one GPU. */
 } mg_config;
 
 /* Fill `cfg` with the defaults above for a `dim`-D grid of `nodes` per axis
@@ -217,6 +222,11 @@ mg_status mg_profile_enable(mg_solver* s, int32_t on);
  * (may exceed cap; only min(n,cap) written).  Synchronises the device. */
 int32_t mg_profile_read(mg_solver* s, int32_t cap, const char** names, double* ms,
                         int64_t* count, double* bytes);
+
+/* Loopback group of `nranks` ranks for mg_config.loopback (see there); destroy it after
+ * every solver of the group has been destroyed. */
+mg_status mg_loopback_group_create(int32_t nranks, void** group);
+void mg_loopback_group_destroy(void* group);
 
 /* Host-only: write a fresh 128-byte ncclUniqueId into out (rank 0 calls it and
  * broadcasts the bytes to the other ranks before mg_create). */

@@ -29,7 +29,8 @@ PROBLEM_POISSON, PROBLEM_COMPLEX_DIFFUSION = 0, 1
 # every symbol include/mg.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = [
     "mg_config_default", "mg_create", "mg_layout", "mg_level_layout", "mg_num_levels", "mg_vcycle",
-    "mg_residual_norm", "mg_solve", "mg_vcycle_host", "mg_vcycle_host_batch", "mg_op_smooth", "mg_op_residual", "mg_op_restrict",
+    "mg_residual_norm", "mg_solve", "mg_vcycle_host", "mg_vcycle_host_batch", "mg_loopback_group_create",
+    "mg_loopback_group_destroy", "mg_op_smooth", "mg_op_residual", "mg_op_restrict",
     "mg_op_prolong_correct", "mg_op_coarse_solve", "mg_op_norm", "mg_workload_fill",
     "mg_launches_per_cycle", "mg_profile_enable", "mg_profile_read", "mg_error_string", "mg_destroy",
     "mg_partition", "mg_nccl_unique_id",
@@ -60,6 +61,7 @@ class MGConfig(ctypes.Structure):
         ("tau", ctypes.c_double),
         ("theta", ctypes.c_double),
         ("kappa", ctypes.c_double),
+        ("loopback", ctypes.c_void_p),
     ]
 
 
@@ -94,6 +96,9 @@ def load_library():
     lib.mg_residual_norm.argtypes = [P, P, P, pD, P]
     lib.mg_solve.argtypes = [P, P, P, D, I32, ctypes.POINTER(I32), pD, P]
     lib.mg_vcycle_host.argtypes = [P, P, P, I32, pD, P]
+    lib.mg_loopback_group_create.argtypes = [I32, ctypes.POINTER(P)]
+    lib.mg_loopback_group_destroy.argtypes = [P]
+    lib.mg_loopback_group_destroy.restype = None
     lib.mg_vcycle_host_batch.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), I32, I32, pD, P]
     lib.mg_op_smooth.argtypes = [P, I32, P, P, P, P]
     lib.mg_op_residual.argtypes = [P, I32, P, P, P, P]
@@ -180,6 +185,26 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class LoopbackGroup:
+    """mg_loopback_group_create: `nranks` solvers of this process on one device, each driven
+    by its own host thread and stream, exchanging halos by device copies (tests of the
+    multi-rank path on one GPU; solvers need flags=FLAG_NO_GRAPH)."""
+
+    def __init__(self, nranks):
+        self.lib = load_library()
+        h = ctypes.c_void_p()
+        st = self.lib.mg_loopback_group_create(int(nranks), ctypes.byref(h))
+        if st != 0:
+            raise MGError(st, self.lib.mg_error_string(None).decode())
+        self.handle = h.value
+        self.nranks = nranks
+
+    def close(self):
+        if self.handle:
+            self.lib.mg_loopback_group_destroy(ctypes.c_void_p(self.handle))
+            self.handle = None
+
+
 def distributed_solver(dim, nodes, **kw):
     """Collective: one Solver per rank of the default torch.distributed group, z-slab
     decomposed over NCCL (the unique id is broadcast through torch.distributed)."""
@@ -207,7 +232,7 @@ class Solver:
 
     def __init__(self, dim, nodes, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, coarse="direct",
                  ncoarse=10, dtype="f64", device=0, coeff=(1.0, 1.0, 1.0), h=None, flags=0, rank=0, nranks=1,
-                 nccl_id=None, pm_min_nx=0, problem="poisson", tau=None, theta=None, kappa=None):
+                 nccl_id=None, pm_min_nx=0, problem="poisson", tau=None, theta=None, kappa=None, loopback=None):
         """problem="complex_diffusion": `nodes` are CELLS per axis, arrays are complex
         (torch complex64 / complex128), coarse defaults to "sweeps" (FAS)."""
         lib = load_library()
@@ -234,6 +259,8 @@ class Solver:
         c.flags = flags
         c.pm_min_nx = pm_min_nx
         c.problem = _problem_code(problem)
+        c.loopback = loopback.handle if isinstance(loopback, LoopbackGroup) else loopback
+        self._loopback = loopback  # keep the group alive while this rank exists
         self.complex = c.problem == PROBLEM_COMPLEX_DIFFUSION
         if self.complex and coarse == "direct":
             c.coarse = COARSE_SWEEPS

@@ -188,7 +188,14 @@ extern "C" mg_status mg_create(const mg_config* cfg, mg_solver** out) {
   int L = 0;
   mg_status st = validate(cfg, &L);
   if (st != MG_OK) return st;
-  if (cfg->nranks > 1 && !cfg->nccl_id) return fail(nullptr, MG_ERR_INVALID, "nranks > 1 needs nccl_id (ncclUniqueId)");
+  if (cfg->nranks > 1 && !cfg->nccl_id && !cfg->loopback)
+    return fail(nullptr, MG_ERR_INVALID, "nranks > 1 needs nccl_id (ncclUniqueId) or a loopback group");
+  if (cfg->nranks > 1 && cfg->loopback) {
+    if (mg::loop_group_size(static_cast<mg::LoopGroup*>(cfg->loopback)) != cfg->nranks)
+      return fail(nullptr, MG_ERR_INVALID, "loopback group size != nranks");
+    if (!(cfg->flags & MG_FLAG_NO_GRAPH))
+      return fail(nullptr, MG_ERR_INVALID, "the loopback transport needs MG_FLAG_NO_GRAPH (eager launches)");
+  }
   int ndev = 0;
   cudaError_t ce = cudaGetDeviceCount(&ndev);
   if (ce != cudaSuccess || ndev == 0)
@@ -497,6 +504,14 @@ extern "C" int32_t mg_profile_read(mg_solver* s, int32_t cap, const char** names
 
 // used by plan.cu for error reporting
 mg_status mg::plan_fail(mg_solver* s, mg_status st, const char* msg) { return fail(s, st, "%s", msg); }
+
+extern "C" mg_status mg_loopback_group_create(int32_t nranks, void** group) {
+  if (!group || nranks < 1) return fail(nullptr, MG_ERR_INVALID, "bad argument");
+  *group = mg::loop_group_create(nranks);
+  return MG_OK;
+}
+
+extern "C" void mg_loopback_group_destroy(void* group) { mg::loop_group_destroy(static_cast<mg::LoopGroup*>(group)); }
 
 extern "C" mg_status mg_nccl_unique_id(void* out128) {
   if (!out128) return fail(nullptr, MG_ERR_INVALID, "out is NULL");

@@ -46,7 +46,7 @@ static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   return plan_fail(s, MG_ERR_CUDA, buf);
 }
 
-bool plan_loop_supported(mg_solver* s) { return s->comm == nullptr; }
+bool plan_loop_supported(mg_solver* s) { return !comm_active(s); }
 
 // Capture: [head | norm] -> init -> WHILE { [tail + head | cycle + norm] -> check }.
 static mg_status build_loop_graph(mg_solver* s, void* u, const void* f, cudaGraphExec_t* out) {

@@ -138,7 +138,7 @@ static mg_status alloc_common(mg_solver* s, int np) {
   }
   cudaError_t e = cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->cap_body, cudaStreamNonBlocking);
-  if (e == cudaSuccess && s->comm) {  // halo exchanges overlapped with interior sweeps
+  if (e == cudaSuccess && comm_active(s)) {  // halo exchanges overlapped with interior sweeps
     e = cudaStreamCreateWithFlags(&s->comm_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
@@ -175,7 +175,14 @@ mg_status plan_build(mg_solver* s) {
     mg_status ps = compute_partition(&c, s->L, &s->pt, &perr);
     if (ps != MG_OK) return plan_fail(s, ps, perr.c_str());
   }
-  if (c.nranks > 1) {  // NCCL communicator over NVLink (unique id broadcast by the caller)
+  if (c.nranks > 1 && c.loopback) {  // loopback transport: ranks of this process on this device
+    s->loop = static_cast<LoopGroup*>(c.loopback);
+    if (cudaEventCreateWithFlags(&s->lb_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->lb_done, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return plan_fail(s, MG_ERR_CUDA, "loopback events");
+    }
+  } else if (c.nranks > 1) {  // NCCL communicator over NVLink (unique id broadcast by the caller)
     ncclUniqueId id;
     memcpy(&id, c.nccl_id, sizeof id);
     ncclResult_t nr = ncclCommInitRank(&s->comm, c.nranks, id, c.rank);
@@ -320,6 +327,8 @@ void plan_free(mg_solver* s) {
   cudaFree(s->d_norm);
   cudaFree(s->d_rank_sums);
   if (s->comm) ncclCommDestroy(s->comm);
+  if (s->lb_ready) cudaEventDestroy(s->lb_ready);
+  if (s->lb_done) cudaEventDestroy(s->lb_done);
   if (s->h_norm) cudaFreeHost(s->h_norm);
   cudaFree(s->stage_u);
   cudaFree(s->stage_f);
@@ -409,43 +418,29 @@ struct Exec {
     return e ? atoi(e) : 0;
   }
 
-  static ncclDataType_t nccl_type() { return sizeof(T) == 8 ? ncclDouble : ncclFloat; }
 
   // Slab halo exchange of a distributed level: my h top owned planes
   // go to rank+1's lower halo, my h bottom owned planes to rank-1's upper halo.
   mg_status exchange(int l, T* buf, int h) { return exchange_on(l, buf, h, st); }
   mg_status exchange_on(int l, T* buf, int h, cudaStream_t st) {
     const Level& L = s->lv[l];
-    if (!L.dist || !s->comm) return MG_OK;
-    const int H = s->pt.H, P = s->pt.P, rk = s->pt.rank;
+    if (!L.dist || !comm_active(s)) return MG_OK;
+    const int H = s->pt.H;
     const size_t ps = (size_t)L.g.pstride;
     const int owned = L.g.planes - 2 * H;
-    return launch(s, st, K_HALO, l, 2.0 * h * ps * sizeof(T), [&] {
-      ncclResult_t nr = ncclGroupStart();
-      if (rk < P - 1 && nr == ncclSuccess) {
-        nr = ncclSend(buf + (size_t)(H + owned - h) * ps, h * ps, nccl_type(), rk + 1, s->comm, st);
-        if (nr == ncclSuccess) nr = ncclRecv(buf + (size_t)(H + owned) * ps, h * ps, nccl_type(), rk + 1, s->comm, st);
-      }
-      if (rk > 0 && nr == ncclSuccess) {
-        nr = ncclSend(buf + (size_t)H * ps, h * ps, nccl_type(), rk - 1, s->comm, st);
-        if (nr == ncclSuccess) nr = ncclRecv(buf + (size_t)(H - h) * ps, h * ps, nccl_type(), rk - 1, s->comm, st);
-      }
-      ncclResult_t ne = ncclGroupEnd();
-      return (nr == ncclSuccess && ne == ncclSuccess) ? cudaSuccess : cudaErrorUnknown;
-    });
+    return launch(s, st, K_HALO, l, 2.0 * h * ps * sizeof(T),
+                  [&] { return comm_halo(s, buf, ps * sizeof(T), H, owned, h, st); });
   }
 
   // Agglomeration: every rank restricted into its own planes of the full first
   // undistributed level; all-gather the equal chunks (the top boundary plane stays 0).
   mg_status allgather_level(int l, T* buf) {
     const Level& L = s->lv[l];
-    if (!s->comm) return MG_OK;
+    if (!comm_active(s)) return MG_OK;
     const size_t ps = (size_t)L.g.pstride;
     const size_t chunk = (size_t)(s->pt.n[l] / s->pt.P) * ps;
-    return launch(s, st, K_ALLGATHER, l, (double)chunk * s->pt.P * sizeof(T), [&] {
-      ncclResult_t nr = ncclAllGather(buf + (size_t)s->pt.rank * chunk, buf, chunk, nccl_type(), s->comm, st);
-      return nr == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
-    });
+    return launch(s, st, K_ALLGATHER, l, (double)chunk * s->pt.P * sizeof(T),
+                  [&] { return comm_allgather(s, buf, chunk * sizeof(T), st); });
   }
 
   // one sweep; zero_in: the iterate is known to be 0 (first sweep after V_H(0,...))
@@ -471,7 +466,7 @@ struct Exec {
         // read no halo, are swept; then the B planes next to each face.  The
         // plane ranges split the same per-plane arithmetic: bitwise identical to one launch.
         const int lo = L.g.p_lo, hi = L.g.p_hi;
-        if (s->comm) {
+        if (comm_active(s)) {
           cudaError_t e = cudaEventRecord(s->ev_fork, st);
           if (e == cudaSuccess) e = cudaStreamWaitEvent(s->comm_stream, s->ev_fork, 0);
           if (e != cudaSuccess) return cuda_fail(s, e, "halo fork");
@@ -480,7 +475,7 @@ struct Exec {
           if (e != cudaSuccess) return cuda_fail(s, e, "halo join");
         }
         if ((r = sweep_range(lo + B, hi - B)) != MG_OK) return r;
-        if (s->comm) {
+        if (comm_active(s)) {
           cudaError_t e = cudaStreamWaitEvent(st, s->ev_join, 0);
           if (e != cudaSuccess) return cuda_fail(s, e, "halo join");
         }
@@ -711,7 +706,11 @@ struct Exec {
     const Level& L = s->lv[l];
     int np = norm_num_partials<T>(L.g);
     const bool pml = pm(l);
-    mg_status r = launch(s, st, K_NORM_PARTIAL, l, 2 * w(l), [&] {
+    // slabs: the residual of the owned face planes reads the neighbours' planes, and the
+    // cycle's last sweep left u's halo planes stale (halos are library scratch)
+    mg_status r = exchange(l, const_cast<T*>(u), 1);
+    if (r != MG_OK) return r;
+    r = launch(s, st, K_NORM_PARTIAL, l, 2 * w(l), [&] {
       return pml ? pm::launch_norm<T>(L.g, coef(l), u, f, s->d_partial, &np, st)
                  : launch_norm_partial<T>(L.g, coef(l), u, f, s->d_partial, st);
     });
@@ -731,10 +730,9 @@ struct Exec {
     if ((r = launch(s, st, K_NORM_FINAL, l, 8.0 * np,
                     [&] { return launch_norm_final(s->d_partial, np, mine, st, false); })) != MG_OK)
       return r;
-    if (s->comm && (r = launch(s, st, K_ALLGATHER, l, 8.0 * s->pt.P, [&] {
-                      ncclResult_t nr = ncclAllGather(mine, s->d_rank_sums, 1, ncclDouble, s->comm, st);
-                      return nr == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
-                    })) != MG_OK)
+    if (comm_active(s) && (r = launch(s, st, K_ALLGATHER, l, 8.0 * s->pt.P, [&] {
+                             return comm_allgather(s, s->d_rank_sums, sizeof(double), st);
+                           })) != MG_OK)
       return r;
     return launch(s, st, K_NORM_FINAL, l, 8.0 * s->pt.P,
                   [&] { return launch_norm_combine(s->d_rank_sums, s->pt.P, out_dev, st); });

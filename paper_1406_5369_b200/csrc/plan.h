@@ -12,6 +12,7 @@
 #include "mg_common.cuh"
 #include "partition.h"
 #include "kernels_cd.h"
+#include "comm.h"
 
 typedef struct ncclComm* ncclComm_t;
 
@@ -75,6 +76,8 @@ struct mg_solver {
   // slab decomposition / NCCL
   mg::Partition pt;
   ncclComm_t comm = nullptr;
+  mg::LoopGroup* loop = nullptr;  // loopback transport (ranks of one process on one device; tests)
+  cudaEvent_t lb_ready = nullptr, lb_done = nullptr;
   double* d_rank_sums = nullptr;  // per-rank sums of r^2 (all-gathered)
   // norm
   double* d_partial = nullptr;
