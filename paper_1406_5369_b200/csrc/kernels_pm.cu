@@ -807,12 +807,18 @@ static int prepare_kernel(K kernel, int smem) {
 // to balance SMs; the halo re-loads of short chunks mostly hit L2.  So: among
 // chunk lengths >= 16 planes, minimise (ceil(waves)/waves) * (1 + halo/(2 zc))
 // plus a small penalty below 8 waves.
-static int choose_zc(long long ntiles, int np, int resident, int halo) {
+// L2-resident levels (three arrays < 48 MB) may use chunks down to 4 planes: their halo
+// re-reads are L2 hits, and 16-plane chunks leave most of the GPU idle on 129^3.
+static int min_zc_for(const Geom& g, size_t esz) {
+  return (double)g.planes * (double)g.pstride * (double)esz * 3.0 < 48e6 ? 4 : 16;
+}
+
+static int choose_zc(long long ntiles, int np, int resident, int halo, int min_zc = 16) {
   int best = np;
   double best_cost = 1e300;
   for (int c = 1; c <= 256 && c <= np; c++) {
     const int zc = (np + c - 1) / c;
-    if (zc < 16 && c > 1) break;
+    if (zc < min_zc && c > 1) break;
     const int chunks = (np + zc - 1) / zc;
     const long long items = ntiles * chunks;
     const double wx = (double)items / resident;
@@ -851,7 +857,7 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   const int np = g.p_hi - g.p_lo;
   auto go = [&](auto kernel) {
     const int resident = prepare_kernel(kernel, ecoarse ? G::SMEM_CORR : G::SMEM);
-    const int zc = zc_override > 0 ? zc_override : choose_zc(ntiles, np, resident, rbgs ? 4 : 2);
+    const int zc = zc_override > 0 ? zc_override : choose_zc(ntiles, np, resident, rbgs ? 4 : 2, min_zc_for(g, sizeof(T)));
     const int nitems = ntiles * ((np + zc - 1) / zc);
     if (getenv("MG_DEBUG"))
       fprintf(stderr, "launch_sweep: resident=%d zc=%d nitems=%d smem=%d\n", resident, zc, nitems, G::SMEM);
@@ -883,7 +889,7 @@ int sweep_partials(const Geom& g, bool rbgs) {
                             : prepare_kernel(k_sweep3d<T, 0, false, true>, G::SMEM);
   int best = 0;
   for (int halo : {2, 4}) {
-    const int zc = choose_zc(ntiles, np, resident, halo);
+    const int zc = choose_zc(ntiles, np, resident, halo, min_zc_for(g, sizeof(T)));
     const int n = ntiles * ((np + zc - 1) / zc);
     if (n > best) best = n;
   }
@@ -897,7 +903,7 @@ int norm_partials(const Geom& g) {
   const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
   const int np = g.p_hi - g.p_lo;
   const int resident = prepare_kernel(k_sweep3d<T, 2, false>, G::SMEM);
-  const int zc = choose_zc(ntiles, np, resident, 2);
+  const int zc = choose_zc(ntiles, np, resident, 2, min_zc_for(g, sizeof(T)));
   return ntiles * ((np + zc - 1) / zc);
 }
 
@@ -914,7 +920,7 @@ cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f,
   const int np = g.p_hi - g.p_lo;
   auto kernel = k_sweep3d<T, 2, false>;
   const int resident = prepare_kernel(kernel, G::SMEM);
-  const int zc = choose_zc(ntiles, np, resident, 2);
+  const int zc = choose_zc(ntiles, np, resident, 2, min_zc_for(g, sizeof(T)));
   const int nitems = ntiles * ((np + zc - 1) / zc);
   *npartial = nitems;
   CUtensorMap te;
@@ -1028,7 +1034,7 @@ cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cud
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_prolong3d<T>, NT, 0);
     resident = (occ < 1 ? 1 : occ) * (sms < 1 ? 1 : sms);
   }
-  const int zc = choose_zc(ntiles, np, resident, 0);
+  const int zc = choose_zc(ntiles, np, resident, 0, min_zc_for(gf, sizeof(T)));
   const int nitems = ntiles * ((np + zc - 1) / zc);
   k_prolong3d<T><<<nitems, NT, 0, st>>>(gf, gc, e, u, tiles_x, ntiles, zc, nitems);
   return cudaGetLastError();
@@ -1047,7 +1053,7 @@ cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>&
   const int npc = gc.p_hi - gc.p_lo;
   auto kernel = k_resid_restrict3d<T>;
   const int resident = prepare_kernel(kernel, G::SMEM);
-  const int zcc = zc_override > 0 ? zc_override : choose_zc(ntiles, npc, resident, 2);
+  const int zcc = zc_override > 0 ? zc_override : choose_zc(ntiles, npc, resident, 2, min_zc_for(gf, sizeof(T)));
   const int nitems = ntiles * ((npc + zcc - 1) / zcc);
   kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, gf, gc, c, fc, tiles_x, ntiles, zcc, nitems);
   return cudaGetLastError();
