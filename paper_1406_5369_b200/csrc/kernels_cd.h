@@ -66,6 +66,12 @@ struct CdTail {
 template <typename T>
 cudaError_t cd_launch_tail(const CdTail<T>& p, cudaStream_t st);
 
+// 2D warp-marching Jacobi sweep (kernels_cd2d.cu), bitwise equal to cd_launch_jacobi
+bool cd2d_supported(const Geom& g);
+template <typename T>
+cudaError_t cd2d_launch_jacobi(const Geom& g, const CdCoef<T>& c, const T* gd, const T* uin, const T* f, T* uout,
+                               cudaStream_t st);
+
 // W5 inputs: re = lo + (hi-lo) U[0,1)(global cell index), im = 0
 template <typename T>
 cudaError_t cd_launch_fill(const Geom& g, T* dst, uint64_t seed, double lo, double hi, cudaStream_t st);

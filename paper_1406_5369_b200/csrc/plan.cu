@@ -830,8 +830,11 @@ struct CdExec {
     if (s->cfg.smoother == MG_JACOBI) {
       T* in = cur;
       T* out = oth;
-      mg_status r = launch(s, st, K_CD_JACOBI, l, 4 * cw(l),
-                           [&] { return cd_launch_jacobi<T>(G(l), cc(l), gd(l), in, f, out, st); });
+      const bool marching = !(s->cfg.flags & MG_FLAG_BASELINE) && cd2d_supported(G(l));
+      mg_status r = launch(s, st, K_CD_JACOBI, l, 4 * cw(l), [&] {
+        return marching ? cd2d_launch_jacobi<T>(G(l), cc(l), gd(l), in, f, out, st)
+                        : cd_launch_jacobi<T>(G(l), cc(l), gd(l), in, f, out, st);
+      });
       std::swap(cur, oth);
       return r;
     }

@@ -41,6 +41,8 @@ CASES = [
     dict(dim=3, cells=(16, 32, 8), smoother="jacobi"),
     dict(dim=3, cells=(32, 32, 32), smoother="rbgs", dtype="f32"),
     dict(dim=2, cells=(256, 256), smoother="rbgs", omega=1.15),
+    dict(dim=2, cells=(200, 48), levels=3, smoother="jacobi", dtype="f32"),  # ragged warp strips
+    dict(dim=2, cells=(200, 48), levels=3, smoother="jacobi"),
 ]
 
 
