@@ -599,7 +599,8 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
   constexpr int W = G::W, TX = G::TX, BX = G::BX, HX = G::HX, PX = G::PX;
   extern __shared__ __align__(128) unsigned char sm[];
   const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
-  T* Rr = reinterpret_cast<T*>(sm + G::PR_OFF);
+  // r planes alternate between two smem buffers: one barrier per fine plane
+  T* const Rr2 = reinterpret_cast<T*>(sm + G::PR_OFF);
 
   const int tid = threadIdx.x, lane = tid & 31, ry = tid >> 5;
   const int pgf0 = gf.p_glob0;
@@ -658,6 +659,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
       const T* U0 = R.U(N(q - 1));
       const T* Up = R.U(N(q));
       const T* F0 = R.F(N(q));
+      T* Rr = Rr2 + (size_t)(q & 1) * (G::PB / sizeof(T));
       up = ld_vec(Up + bo);
       const int pgl = q + pgf0;
       const bool pl_in = pgl >= 1 && pgl <= gf.nz - 1;
@@ -684,6 +686,12 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         rzm = uc;
       }
       __syncthreads();
+      // every thread is past plane q-1's coarse sums and plane q's residuals: step q-1
+      // (u(q), f(q-1)) is consumed, and Rr of plane q-1 may be overwritten next plane
+      if (tid == 0 && q - 1 + G::NS <= qlast) {
+        fence_proxy_async();
+        R.issue(N(q - 1 + G::NS), &tm_u, &tm_f, x0, y0, q + G::NS, q - 1 + G::NS, true);
+      }
       if (tid < CN) {
         T tx[3];
 #pragma unroll
@@ -698,11 +706,6 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         }
         ty2 = ty1;
         ty1 = ty0;
-      }
-      __syncthreads();
-      if (tid == 0 && q - 1 + G::NS <= qlast) {
-        fence_proxy_async();
-        R.issue(N(q - 1 + G::NS), &tm_u, &tm_f, x0, y0, q + G::NS, q - 1 + G::NS, true);
       }
       um = u0;
       u0 = up;
@@ -985,36 +988,49 @@ __global__ void __launch_bounds__(NT) k_prolong3d(Geom gf, Geom gc, const T* __r
     int Z = (pa + gf.p_glob0) >> 1;
     Vt A = Vz(Z), B = A;
     bool haveB = false;
-    for (int z = pa; z < pb; z++) {
-      const int zg = z + gf.p_glob0;
-      if ((zg >> 1) != Z) {
-        Z++;
-        A = haveB ? B : Vz(Z);
-        haveB = false;
-      }
-      Vt v = A;
-      if (zg & 1) {
-        if (!haveB) {
-          B = Vz(Z + 1);
-          haveB = true;
-        }
+    bool all = true;
 #pragma unroll
-        for (int j = 0; j < W; j++) v.v[j] = mul(half, add(A.v[j], B.v[j]));
-      }
-      T* up = urow + (long long)z * gf.pstride;
-      Vt o;
-      bool all = true;
-#pragma unroll
-      for (int j = 0; j < W; j++) all = all && in[j];
+    for (int j = 0; j < W; j++) all = all && in[j];
+    // KZ planes per iteration: their u vectors are loaded before any store (more bytes in
+    // flight per thread; the compiler cannot reorder loads of u across stores to u)
+    constexpr int KZ = 4;
+    for (int z0 = pa; z0 < pb; z0 += KZ) {
+      Vt uu[KZ];
       if (all) {
-        const Vt uu = ld_vec(up + ox);
 #pragma unroll
-        for (int j = 0; j < W; j++) o.v[j] = add(uu.v[j], v.v[j]);
-        store_vec(up, ox, in, o);
-      } else {
+        for (int k = 0; k < KZ; k++)
+          if (z0 + k < pb) uu[k] = ld_vec(urow + (long long)(z0 + k) * gf.pstride + ox);
+      }
 #pragma unroll
-        for (int j = 0; j < W; j++)
-          if (in[j]) up[ox + j] = add(up[ox + j], v.v[j]);
+      for (int k = 0; k < KZ; k++) {
+        const int z = z0 + k;
+        if (z >= pb) break;
+        const int zg = z + gf.p_glob0;
+        if ((zg >> 1) != Z) {
+          Z++;
+          A = haveB ? B : Vz(Z);
+          haveB = false;
+        }
+        Vt v = A;
+        if (zg & 1) {
+          if (!haveB) {
+            B = Vz(Z + 1);
+            haveB = true;
+          }
+#pragma unroll
+          for (int j = 0; j < W; j++) v.v[j] = mul(half, add(A.v[j], B.v[j]));
+        }
+        T* up = urow + (long long)z * gf.pstride;
+        if (all) {
+          Vt o;
+#pragma unroll
+          for (int j = 0; j < W; j++) o.v[j] = add(uu[k].v[j], v.v[j]);
+          store_vec(up, ox, in, o);
+        } else {
+#pragma unroll
+          for (int j = 0; j < W; j++)
+            if (in[j]) up[ox + j] = add(up[ox + j], v.v[j]);
+        }
       }
     }
   }
