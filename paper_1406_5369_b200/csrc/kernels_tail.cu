@@ -139,6 +139,39 @@ __device__ void restrict_fw(const Geom& gf, const Geom& gc, const T* r, T* fc) {
   pass_sync();
 }
 
+// the first sweep from a zero iterate (V_H(0, ...)) without a zeroing pass: Jacobi writes
+// t = 0 + wd (f - A 0) = 0 + wd f; RBGS's red pass writes 0 + wd f at red nodes and 0 at black
+// nodes (the black pass then runs as usual).  With A 0 = D*0 - 0 = +0 and f - (+0) = f the
+// values are bitwise those of a sweep over a zeroed array.
+template <typename T>
+__device__ T* sweep_from_zero(const Geom& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f) {
+  const int n = interior_count(g);
+  const T zero = (T)0;
+  if (!rbgs) {
+    for (int q = gtid(); q < n; q += gstride()) {
+      const Idx d = interior_node(g, q);
+      const long long p = lin(g, d.i, d.j, d.pl);
+      t[p] = add(zero, mul(c.wd, sub(f[p], zero)));
+    }
+    pass_sync();
+    return t;
+  }
+  for (int q = gtid(); q < n; q += gstride()) {  // red pass (colour 0) + zero black nodes
+    const Idx d = interior_node(g, q);
+    const long long p = lin(g, d.i, d.j, d.pl);
+    u[p] = ((d.i + d.j + d.pl + g.p_glob0) & 1) == 0 ? add(zero, mul(c.wd, sub(f[p], zero))) : zero;
+  }
+  pass_sync();
+  for (int q = gtid(); q < n; q += gstride()) {  // black pass
+    const Idx d = interior_node(g, q);
+    if (((d.i + d.j + d.pl + g.p_glob0) & 1) != 1) continue;
+    const long long p = lin(g, d.i, d.j, d.pl);
+    u[p] = add(u[p], mul(c.wd, point_residual(u, p, g, c, f[p])));
+  }
+  pass_sync();
+  return u;
+}
+
 // u += P e, separable x -> y -> plane axis
 template <typename T>
 __device__ void prolong(const Geom& gf, const Geom& gc, const T* e, T* u) {
@@ -173,14 +206,19 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   for (int k = 0; k < P.nl; k++) cur[k] = P.u[k];
   for (int k = 0; k < P.nl - 1; k++) {
     const Geom& g = P.g[k];
-    if (k > 0 || P.zero_first) {  // V_H(0, ...)
+    const bool zero = k > 0 || P.zero_first;  // V_H(0, ...)
+    const bool fold = zero && P.nu1 > 0 && P.rbgs != 2;  // the zero guess folded into the first sweep
+    if (zero && !fold) {
       zero_level(g, cur[k]);
       pass_sync();
     }
     for (int s = 0; s < P.nu1; s++) {
-      T* nxt = sweep(g, P.c[k], P.rbgs, cur[k], cur[k] == P.u[k] ? P.t[k] : P.u[k], P.f[k]);
-      cur[k] = nxt;
+      T* oth = cur[k] == P.u[k] ? P.t[k] : P.u[k];
+      cur[k] = (s == 0 && fold) ? sweep_from_zero(g, P.c[k], P.rbgs, cur[k], oth, P.f[k])
+                                : sweep(g, P.c[k], P.rbgs, cur[k], oth, P.f[k]);
     }
+    // separate residual and restriction passes: measured faster than one fused pass whose
+    // coarse threads each evaluate 3^d fine residuals (latency-bound serial chains)
     residual(g, P.c[k], cur[k], P.f[k], P.r[k]);
     restrict_fw(g, P.g[k + 1], P.r[k], P.f[k + 1]);
   }
@@ -188,13 +226,20 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   {
     const int k = P.nl - 1;
     const Geom& g = P.g[k];
-    if (P.nl > 1 || P.zero_first) {
+    const bool zero = P.nl > 1 || P.zero_first;
+    // DIRECT writes every interior node, so its zero guess needs no pass; SWEEPS folds it
+    // into the first sweep (lexicographic GS zeroes first)
+    const bool fold = zero && P.sweeps && P.ncoarse > 0 && P.rbgs != 2;
+    if (zero && P.sweeps && !fold) {
       zero_level(g, cur[k]);
       pass_sync();
     }
     if (P.sweeps) {
-      for (int s = 0; s < P.ncoarse; s++)
-        cur[k] = sweep(g, P.c[k], P.rbgs, cur[k], cur[k] == P.u[k] ? P.t[k] : P.u[k], P.f[k]);
+      for (int s = 0; s < P.ncoarse; s++) {
+        T* oth = cur[k] == P.u[k] ? P.t[k] : P.u[k];
+        cur[k] = (s == 0 && fold) ? sweep_from_zero(g, P.c[k], P.rbgs, cur[k], oth, P.f[k])
+                                  : sweep(g, P.c[k], P.rbgs, cur[k], oth, P.f[k]);
+      }
     } else if (gtid() == 0) {
       // same loop order as k_coarse_direct / the oracle
       const int jlo = g.three_d ? 1 : 0, jhi = g.three_d ? g.ny - 1 : 0;
