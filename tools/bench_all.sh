@@ -1,6 +1,6 @@
 # every bench config once (default settings) -> gpurun_out/bench_all/<config>.json
 mkdir -p gpurun_out/bench_all
-for c in C3-f64 C3-f32 C5 C2 C4 C1 CD2-f32 CD2-gs-f32 CD2-f64 CD3-f32 CD3-gs-f32; do
+for c in C3-f64 C3-f32 C5 C2 C4 C1 C2-lex CD2-f32 CD2-gs-f32 CD2-f64 CD3-f32 CD3-gs-f32; do
   timeout 600 python bench.py --config $c > gpurun_out/bench_all/$c.json 2> gpurun_out/bench_all/$c.err
   python - <<PY
 import json
