@@ -15,6 +15,7 @@
 #include "kernels.h"
 #include "kernels_cd.h"
 #include "cd_common.cuh"
+#include "launch_util.h"
 
 namespace mg {
 
@@ -277,8 +278,7 @@ __global__ void __launch_bounds__(NB) k_cd_fill(Geom g, T* __restrict__ dst, uin
 }
 
 int grid_for(long long n) {
-  static int sms = 0;
-  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int sms = sm_count();
   const long long b = (n + NB - 1) / NB;
   const long long cap = (long long)(sms > 0 ? sms : 148) * 8;  // 8 x 256 threads per SM
   return (int)(b < cap ? (b < 1 ? 1 : b) : cap);

@@ -17,6 +17,7 @@
 #include "cd_common.cuh"
 #include "kernels_cd.h"
 #include "kernels_pm.h"
+#include "launch_util.h"
 #include "tma.cuh"
 #include "vec.cuh"
 
@@ -224,21 +225,7 @@ __global__ void __launch_bounds__(NT) k_cd_jacobi2d(const __grid_constant__ CUte
 // ---------------------------------------------------------------------------
 template <class K>
 static int resident_warps(K kernel, int smem) {
-  static const void* keys[8];
-  static int vals[8];
-  static int n = 0;
-  for (int i = 0; i < n; i++)
-    if (keys[i] == (const void*)kernel) return vals[i];
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int sms = 0, occ = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, NT, smem);
-  const int r = (occ < 1 ? 1 : occ) * (sms < 1 ? 1 : sms) * WPB;
-  if (n < 8) {
-    keys[n] = (const void*)kernel;
-    vals[n++] = r;
-  }
-  return r;
+  return resident_ctas((const void*)kernel, NT, smem) * WPB;
 }
 
 // complex level array viewed as reals: dims (2 nx, planes), box (RW, RB), zero OOB fill

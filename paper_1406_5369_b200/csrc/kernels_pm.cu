@@ -34,6 +34,7 @@
 
 #include "kernels_pm.h"
 #include "kernels_pm2d.h"
+#include "launch_util.h"
 #include "tma.cuh"
 #include "vec.cuh"
 
@@ -719,14 +720,14 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
 // cuTensorMapEncodeTiled through the runtime's driver entry point, so that the
 // library does not link libcuda (it must load on GPU-less hosts for the ABI tests).
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {  // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 
@@ -788,21 +789,7 @@ bool supported(const Geom& g, int min_nx) {
 // number of CTAs the device keeps resident (cached per kernel).
 template <class K>
 static int prepare_kernel(K kernel, int smem) {
-  static const void* keys[32];
-  static int vals[32];
-  static int n = 0;
-  for (int i = 0; i < n; i++)
-    if (keys[i] == (const void*)kernel) return vals[i];
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int sms = 0, occ = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, NT, smem);
-  const int r = (occ < 1 ? 1 : occ) * (sms < 1 ? 1 : sms);
-  if (n < 32) {
-    keys[n] = (const void*)kernel;
-    vals[n++] = r;
-  }
-  return r;
+  return resident_ctas((const void*)kernel, NT, smem);
 }
 
 // z-chunk size.  Measured on the 513^3 RBGS sweep (tools/scan_zc.py): what
@@ -1043,13 +1030,7 @@ cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cud
   const int tiles_x = (gf.nx + G::TX - 1) / G::TX, tiles_y = (gf.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = gf.p_hi - gf.p_lo;
-  static int resident = 0;
-  if (!resident) {
-    int sms = 0, occ = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_prolong3d<T>, NT, 0);
-    resident = (occ < 1 ? 1 : occ) * (sms < 1 ? 1 : sms);
-  }
+  const int resident = resident_ctas((const void*)k_prolong3d<T>, NT, 0);
   const int zc = choose_zc(ntiles, np, resident, 0, min_zc_for(gf, sizeof(T)));
   const int nitems = ntiles * ((np + zc - 1) / zc);
   k_prolong3d<T><<<nitems, NT, 0, st>>>(gf, gc, e, u, tiles_x, ntiles, zc, nitems);

@@ -32,6 +32,7 @@
 
 #include "kernels_pm.h"
 #include "kernels_pm2d.h"
+#include "launch_util.h"
 #include "tma.cuh"
 #include "vec.cuh"
 
@@ -585,30 +586,15 @@ constexpr int kMinRows = 4;  // measured on C4: 16 -> 1.70 ms, 8 -> 1.63, 4 -> 1
 
 template <class K>
 static int resident_warps(K kernel, int smem) {
-  static const void* keys[32];
-  static int vals[32];
-  static int n = 0;
-  for (int i = 0; i < n; i++)
-    if (keys[i] == (const void*)kernel) return vals[i];
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int sms = 0, occ = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, NT, smem);
-  const int r = (occ < 1 ? 1 : occ) * (sms < 1 ? 1 : sms) * WPB;
-  if (n < 32) {
-    keys[n] = (const void*)kernel;
-    vals[n++] = r;
-  }
-  return r;
+  return resident_ctas((const void*)kernel, NT, smem) * WPB;
 }
 
 static void split(int nstrips, int rows, int rw, int& nch, int& nblocks) {
-  static int min_rows = 0;
-  if (!min_rows) {
+  static const int min_rows = [] {  // tuning knob MG_PM2_MINROWS (thread-safe one-time read)
     const char* e = getenv("MG_PM2_MINROWS");
-    min_rows = e ? atoi(e) : kMinRows;
-    if (min_rows < 2) min_rows = 2;
-  }
+    const int v = e ? atoi(e) : kMinRows;
+    return v < 2 ? 2 : v;
+  }();
   nch = rw / nstrips;
   const int cap = rows / min_rows;
   if (nch > cap) nch = cap;

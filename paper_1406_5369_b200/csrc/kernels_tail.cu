@@ -295,9 +295,9 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
 
 template <typename T>
 cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
-  static int cluster = 0;  // 16 CTAs (non-portable) where allowed, else the portable 8
-  if (!cluster) {
-    cluster = 8;
+  // 16 CTAs (non-portable) where allowed, else the portable 8 (thread-safe one-time probe)
+  static const int cluster = [] {
+    int c = 8;
     if (cudaFuncSetAttribute(k_tail<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3(16);
@@ -310,10 +310,11 @@ cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
       q.attrs = &a;
       q.numAttrs = 1;
       int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, k_tail<T>, &q) == cudaSuccess && n >= 1) cluster = 16;
+      if (cudaOccupancyMaxActiveClusters(&n, k_tail<T>, &q) == cudaSuccess && n >= 1) c = 16;
     }
     cudaGetLastError();
-  }
+    return c;
+  }();
   // tiny tails (a few thousand nodes, e.g. the whole 65^2 C1 hierarchy) run faster on one CTA
   const Geom& g0 = p.g[0];
   const long long top = (long long)(g0.nx - 1) * (g0.three_d ? g0.ny - 1 : 1) * (g0.p_hi - g0.p_lo);

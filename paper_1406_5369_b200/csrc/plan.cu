@@ -372,11 +372,10 @@ struct Exec {
   int tail_level() const {
     if (s->cfg.flags & MG_FLAG_BASELINE) return s->L;
     const int first = s->pt.slab ? s->pt.la : 0;
-    static long long tail_max = 0;
-    if (!tail_max) {
+    static const long long tail_max = [] {  // tuning knob MG_TAIL_MAX (thread-safe one-time read)
       const char* e = getenv("MG_TAIL_MAX");
-      tail_max = e ? atoll(e) : 48 * 1024;
-    }
+      return e ? atoll(e) : 48ll * 1024;
+    }();
     for (int l = first; l < s->L; l++) {
       const Geom& g = s->lv[l].g;
       const long long n = (long long)(g.nx - 1) * (g.three_d ? g.ny - 1 : 1) * (g.nz - 1);
