@@ -72,6 +72,13 @@ template <typename T>
 cudaError_t cd2d_launch_jacobi(const Geom& g, const CdCoef<T>& c, const T* gd, const T* uin, const T* f, T* uout,
                                cudaStream_t st);
 
+// its residual-norm variant (g = g(u) stored): partial sums of |f - A u|^2, one per CTA
+template <typename T>
+int cd2d_norm_partials(const Geom& g);
+template <typename T>
+cudaError_t cd2d_launch_norm(const Geom& g, const CdCoef<T>& c, const T* gd, const T* u, const T* f,
+                             double* partial, int* npartial, cudaStream_t st);
+
 // W5 inputs: re = lo + (hi-lo) U[0,1)(global cell index), im = 0
 template <typename T>
 cudaError_t cd_launch_fill(const Geom& g, T* dst, uint64_t seed, double lo, double hi, cudaStream_t st);

@@ -111,11 +111,15 @@ struct Ring {
   __device__ void finish(int nsteps) { n0 = N(nsteps - 1) + 1; }
 };
 
-template <typename T>
+// NORM: instead of the sweep, the partial sums of |f - A(g) u|^2 (FP64), one per CTA in a
+// fixed order (the nonlinear residual norm of the head, with g = g(u) stored)
+template <typename T, bool NORM>
 __global__ void __launch_bounds__(NT) k_cd_jacobi2d(const __grid_constant__ CUtensorMap tm_u,
                                                     const __grid_constant__ CUtensorMap tm_g,
                                                     const __grid_constant__ CUtensorMap tm_f, Geom g, CdCoef<T> c,
-                                                    T* __restrict__ uout, int nstrips, int nch) {
+                                                    T* __restrict__ uout, int nstrips, int nch,
+                                                    double* __restrict__ partial) {
+  double nsum = 0.0;
   using V = VT<T>;
   using GG = G<T>;
   constexpr int CW = GG::CW, TX = GG::TX, RW = GG::RW;
@@ -188,9 +192,26 @@ __global__ void __launch_bounds__(NT) k_cd_jacobi2d(const __grid_constant__ CUte
           const C2<T> diag = {add((T)1, acc_a.re), acc_a.im};
           const C2<T> du = cmul(diag, uc);
           const C2<T> fc = cell(fv, j);
-          const C2<T> z = cdiv(C2<T>{sub(fc.re, sub(du.re, acc_s.re)), sub(fc.im, sub(du.im, acc_s.im))}, diag);
-          o.v[2 * j] = add(uc.re, mul(c.omega, z.re));
-          o.v[2 * j + 1] = add(uc.im, mul(c.omega, z.im));
+          const C2<T> res = {sub(fc.re, sub(du.re, acc_s.re)), sub(fc.im, sub(du.im, acc_s.im))};
+          if constexpr (NORM) {
+            if (ci < g.nx) {
+              const double rr = (double)res.re, ri = (double)res.im;
+              nsum = __dadd_rn(nsum, __dadd_rn(__dmul_rn(rr, rr), __dmul_rn(ri, ri)));
+            }
+          } else {
+            const C2<T> z = cdiv(res, diag);
+            o.v[2 * j] = add(uc.re, mul(c.omega, z.re));
+            o.v[2 * j + 1] = add(uc.im, mul(c.omega, z.im));
+          }
+        }
+        if (NORM) {
+          um = u0;
+          gm = g0;
+          u0 = up;
+          g0 = gp;
+          u0e = upe;
+          g0e = gpe;
+          continue;
         }
         T* orow = uout + (long long)t * g.pstride * 2;
         bool all = true;
@@ -220,6 +241,18 @@ __global__ void __launch_bounds__(NT) k_cd_jacobi2d(const __grid_constant__ CUte
     }
     R.finish(nsteps);
   }
+  if constexpr (NORM) {  // fixed-order block reduction -> partial[blockIdx.x]
+    __shared__ double red[WPB];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nsum = __dadd_rn(nsum, __shfl_down_sync(FULL, nsum, o));
+    if (lane == 0) red[wid] = nsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < WPB; w++) tot = __dadd_rn(tot, red[w]);
+      partial[blockIdx.x] = tot;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -241,20 +274,48 @@ static bool encode(CUtensorMap* tm, const T* base, const Geom& g) {
 
 bool cd2d_supported(const Geom& g) { return !g.three_d && g.nx >= 64 && g.nz >= 8; }
 
+namespace {
+template <typename T>
+int cd2d_grid(const Geom& g, int& ns, int& nch) {
+  using namespace cd2;
+  ns = (g.nx + G<T>::TX - 1) / G<T>::TX;
+  const int rw = resident_warps(k_cd_jacobi2d<T, false>, G<T>::SMEM);
+  nch = rw / ns;
+  if (nch > g.nz / 4) nch = g.nz / 4;
+  if (nch < 1) nch = 1;
+  return (ns * nch + WPB - 1) / WPB;
+}
+}  // namespace
+
 template <typename T>
 cudaError_t cd2d_launch_jacobi(const Geom& g, const CdCoef<T>& c, const T* gd, const T* uin, const T* f, T* uout,
                                cudaStream_t st) {
   using namespace cd2;
   CUtensorMap tu, tg, tf;
   if (!encode<T>(&tu, uin, g) || !encode<T>(&tg, gd, g) || !encode<T>(&tf, f, g)) return cudaErrorInvalidValue;
-  const int ns = (g.nx + G<T>::TX - 1) / G<T>::TX;
-  const int smem = G<T>::SMEM;
-  const int rw = resident_warps(k_cd_jacobi2d<T>, smem);
-  int nch = rw / ns;
-  if (nch > g.nz / 4) nch = g.nz / 4;
-  if (nch < 1) nch = 1;
-  const int nb = (ns * nch + WPB - 1) / WPB;
-  k_cd_jacobi2d<T><<<nb, NT, smem, st>>>(tu, tg, tf, g, c, uout, ns, nch);
+  int ns, nch;
+  const int nb = cd2d_grid<T>(g, ns, nch);
+  k_cd_jacobi2d<T, false><<<nb, NT, G<T>::SMEM, st>>>(tu, tg, tf, g, c, uout, ns, nch, nullptr);
+  return cudaGetLastError();
+}
+
+template <typename T>
+int cd2d_norm_partials(const Geom& g) {
+  int ns, nch;
+  return cd2d_grid<T>(g, ns, nch);
+}
+
+template <typename T>
+cudaError_t cd2d_launch_norm(const Geom& g, const CdCoef<T>& c, const T* gd, const T* u, const T* f,
+                             double* partial, int* npartial, cudaStream_t st) {
+  using namespace cd2;
+  CUtensorMap tu, tg, tf;
+  if (!encode<T>(&tu, u, g) || !encode<T>(&tg, gd, g) || !encode<T>(&tf, f, g)) return cudaErrorInvalidValue;
+  int ns, nch;
+  const int nb = cd2d_grid<T>(g, ns, nch);
+  *npartial = nb;
+  resident_warps(k_cd_jacobi2d<T, true>, G<T>::SMEM);  // opt in to the shared-memory size
+  k_cd_jacobi2d<T, true><<<nb, NT, G<T>::SMEM, st>>>(tu, tg, tf, g, c, nullptr, ns, nch, partial);
   return cudaGetLastError();
 }
 
@@ -262,5 +323,11 @@ template cudaError_t cd2d_launch_jacobi<float>(const Geom&, const CdCoef<float>&
                                                const float*, float*, cudaStream_t);
 template cudaError_t cd2d_launch_jacobi<double>(const Geom&, const CdCoef<double>&, const double*, const double*,
                                                 const double*, double*, cudaStream_t);
+template int cd2d_norm_partials<float>(const Geom&);
+template int cd2d_norm_partials<double>(const Geom&);
+template cudaError_t cd2d_launch_norm<float>(const Geom&, const CdCoef<float>&, const float*, const float*,
+                                             const float*, double*, int*, cudaStream_t);
+template cudaError_t cd2d_launch_norm<double>(const Geom&, const CdCoef<double>&, const double*, const double*,
+                                              const double*, double*, int*, cudaStream_t);
 
 }  // namespace mg

@@ -803,8 +803,12 @@ static mg_status cd_build(mg_solver* s) {
       cudaError_t e = cudaMemset(*bufs[b], 0, bytes);
       if (e != cudaSuccess) return cuda_fail(s, e, "cudaMemset");
     }
-    const int a = cd_norm_partials(g);
+    int a = cd_norm_partials(g);
     if (a > np) np = a;
+    if (cd2d_supported(g)) {
+      a = esz == 8 ? cd2d_norm_partials<double>(g) : cd2d_norm_partials<float>(g);
+      if (a > np) np = a;
+    }
   }
   return alloc_common(s, np);
 }
@@ -942,8 +946,10 @@ struct CdExec {
   }
   mg_status norm(int l, const T* u, const T* f, double* out_dev, const T* gstored = nullptr) {
     int np = 0;
+    const bool marching = gstored && !(s->cfg.flags & MG_FLAG_BASELINE) && cd2d_supported(G(l));
     mg_status r = launch(s, st, K_CD_NORM, l, (gstored ? 3 : 2) * cw(l), [&] {
-      return cd_launch_norm_partial<T>(G(l), cc(l), gstored, u, f, s->d_partial, &np, st);
+      return marching ? cd2d_launch_norm<T>(G(l), cc(l), gstored, u, f, s->d_partial, &np, st)
+                      : cd_launch_norm_partial<T>(G(l), cc(l), gstored, u, f, s->d_partial, &np, st);
     });
     if (r != MG_OK) return r;
     return launch(s, st, K_NORM_FINAL, l, 8.0 * np, [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });
