@@ -1016,7 +1016,10 @@ mg_status plan_run_part(mg_solver* s, int part, void* u, const void* f, cudaStre
   s->launch_counter = 0;
   mg_status r = is_cd(s) ? cd_run_part(s, part, u, f, st)
                          : s->esz == 8 ? run_part<double>(s, part, u, f, st) : run_part<float>(s, part, u, f, st);
+  // launches of one cycle: the whole cycle, or head + tail of the pipelined split
   if (part == 0) s->launches_per_cycle = s->launch_counter;
+  if (part == 1) s->head_launches = s->launch_counter;
+  if (part == 2) s->launches_per_cycle = s->head_launches + s->launch_counter;
   return r;
 }
 
