@@ -57,6 +57,7 @@ CD_CONFIGS = {
     "CD2-f32": (2, 4096, "jacobi", 2, 2, "f32", 0.8),
     "CD2-gs-f32": (2, 4096, "rbgs", 2, 2, "f32", 1.0),
     "CD2-f64": (2, 4096, "jacobi", 2, 2, "f64", 0.8),
+    "CD2-gs-f64": (2, 4096, "rbgs", 2, 2, "f64", 1.0),
     "CD3-f32": (3, 256, "jacobi", 2, 2, "f32", 0.8),
     "CD3-gs-f32": (3, 256, "rbgs", 2, 2, "f32", 1.0),
 }
