@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <initializer_list>
 #include <map>
 #include <string>
 #include <vector>
@@ -258,6 +259,15 @@ static mg_status guard(mg_solver* s) {
 
 static bool aligned(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// device arrays: non-NULL and 16-byte aligned (TMA boxes and vector accesses need it)
+static mg_status check_arrays(mg_solver* s, std::initializer_list<const void*> ps) {
+  for (const void* p : ps) {
+    if (!p) return fail(s, MG_ERR_INVALID, "NULL array argument");
+    if (!aligned(p)) return fail(s, MG_ERR_LAYOUT, "device arrays must be 16-byte aligned");
+  }
+  return MG_OK;
+}
+
 extern "C" mg_status mg_vcycle(mg_solver* s, void* u, const void* f, void* stream) {
   mg_status st = guard(s);
   if (st != MG_OK) return st;
@@ -273,7 +283,8 @@ extern "C" mg_status mg_vcycle(mg_solver* s, void* u, const void* f, void* strea
 extern "C" mg_status mg_residual_norm(mg_solver* s, const void* u, const void* f, double* out, void* stream) {
   mg_status st = guard(s);
   if (st != MG_OK) return st;
-  if (!u || !f || !out) return fail(s, MG_ERR_INVALID, "NULL argument");
+  if (!out) return fail(s, MG_ERR_INVALID, "NULL argument");
+  if ((st = check_arrays(s, {u, f})) != MG_OK) return st;
   return plan_norm(s, 0, u, f, out, (cudaStream_t)stream, true);
 }
 
@@ -281,7 +292,8 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
                               double* history, void* stream) {
   mg_status st = guard(s);
   if (st != MG_OK) return st;
-  if (!u || !f || max_cycles < 0 || !(rtol >= 0.0)) return fail(s, MG_ERR_INVALID, "bad argument");
+  if (max_cycles < 0 || !(rtol >= 0.0)) return fail(s, MG_ERR_INVALID, "bad argument");
+  if ((st = check_arrays(s, {u, f})) != MG_OK) return st;
   if (u == f) return fail(s, MG_ERR_INVALID, "u and f must not alias");
   cudaStream_t cs = (cudaStream_t)stream;
   const bool eager_mode = (s->cfg.flags & MG_FLAG_NO_GRAPH) || s->prof_on;
@@ -448,6 +460,7 @@ extern "C" mg_status mg_op_smooth(mg_solver* s, int32_t level, const void* u_in,
   mg_status st = guard(s);
   if (st != MG_OK) return st;
   LEVEL_CHECK(level);
+  if ((st = check_arrays(s, {u_in, f, u_out})) != MG_OK) return st;
   return plan_op_smooth(s, level, u_in, f, u_out, (cudaStream_t)stream);
 }
 extern "C" mg_status mg_op_residual(mg_solver* s, int32_t level, const void* u, const void* f, void* r,
@@ -455,23 +468,27 @@ extern "C" mg_status mg_op_residual(mg_solver* s, int32_t level, const void* u, 
   mg_status st = guard(s);
   if (st != MG_OK) return st;
   LEVEL_CHECK(level);
+  if ((st = check_arrays(s, {u, f, r})) != MG_OK) return st;
   return plan_op_residual(s, level, u, f, r, (cudaStream_t)stream);
 }
 extern "C" mg_status mg_op_restrict(mg_solver* s, int32_t level, const void* r, void* fc, void* stream) {
   mg_status st = guard(s);
   if (st != MG_OK) return st;
   LEVEL_CHECK(level + 1);
+  if ((st = check_arrays(s, {r, fc})) != MG_OK) return st;
   return plan_op_restrict(s, level, r, fc, (cudaStream_t)stream);
 }
 extern "C" mg_status mg_op_prolong_correct(mg_solver* s, int32_t level, const void* e, void* u, void* stream) {
   mg_status st = guard(s);
   if (st != MG_OK) return st;
   LEVEL_CHECK(level + 1);
+  if ((st = check_arrays(s, {e, u})) != MG_OK) return st;
   return plan_op_prolong(s, level, e, u, (cudaStream_t)stream);
 }
 extern "C" mg_status mg_op_coarse_solve(mg_solver* s, const void* f, void* e, void* stream) {
   mg_status st = guard(s);
   if (st != MG_OK) return st;
+  if ((st = check_arrays(s, {f, e})) != MG_OK) return st;
   return plan_op_coarse(s, f, e, (cudaStream_t)stream);
 }
 extern "C" mg_status mg_op_norm(mg_solver* s, int32_t level, const void* u, const void* f, double* out,
@@ -479,13 +496,15 @@ extern "C" mg_status mg_op_norm(mg_solver* s, int32_t level, const void* u, cons
   mg_status st = guard(s);
   if (st != MG_OK) return st;
   LEVEL_CHECK(level);
+  if (!out) return fail(s, MG_ERR_INVALID, "NULL argument");
+  if ((st = check_arrays(s, {u, f})) != MG_OK) return st;
   return plan_norm(s, level, u, f, out, (cudaStream_t)stream, true);
 }
 
 extern "C" mg_status mg_workload_fill(mg_solver* s, void* dst, uint64_t seed, double lo, double hi, void* stream) {
   mg_status st = guard(s);
   if (st != MG_OK) return st;
-  if (!dst) return fail(s, MG_ERR_INVALID, "dst is NULL");
+  if ((st = check_arrays(s, {dst})) != MG_OK) return st;
   return plan_workload_fill(s, dst, seed, lo, hi, (cudaStream_t)stream);
 }
 

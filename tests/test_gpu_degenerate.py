@@ -53,3 +53,22 @@ def test_zero_residual_stops_after_one_cycle():
     du, df = S.empty(), S.empty()
     k, hist = S.solve(du, df, 1e-10, 10)
     assert k == 1 and hist == [0.0, 0.0]
+
+
+def test_bad_arguments_fail_without_poisoning():
+    """Misaligned or NULL device arrays are rejected up front (MG_ERR_LAYOUT / MG_ERR_INVALID)
+    and leave the solver usable."""
+    import ctypes
+    import paper_1406_5369_b200 as mgb
+    S, O = make(3, (32, 32, 32))
+    u, f = wl.workload("W1", 3, (32, 32, 32), seed=42)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    bad = ctypes.c_void_p(du.data_ptr() + 8)
+    out = ctypes.c_double()
+    assert S.lib.mg_residual_norm(S.h, bad, S._p(df), ctypes.byref(out), None) == 7
+    assert S.lib.mg_vcycle(S.h, bad, S._p(df), None) == 7
+    k = ctypes.c_int32()
+    assert S.lib.mg_solve(S.h, None, S._p(df), 0.0, 1, ctypes.byref(k), None, None) == 1
+    assert S.lib.mg_op_smooth(S.h, 0, S._p(du), bad, S._p(du), None) == 7
+    S.vcycle(du, df)  # still usable
+    assert np.array_equal(S.to_numpy(du), O.vcycle(u, f))
