@@ -394,7 +394,13 @@ def run_mg(args):
         "frac": achieved / peak, "traffic": ncu_traffic(args.config, dom["name"]), "peak_source": peak_src,
         "alg_bytes_per_launch": dom["bytes"], "avg_launch_ms": dom_avg_ms,
         "share_of_step": dom["ms"] / tot if tot else None,
+        "timing": ("per-kernel CUDA events on the solver stream, separate instrumented eager pass of the same "
+                   "kernels (the timed region replays a CUDA graph)"),
     }
+    array_bytes = S.shape[0] * S.shape[1] * S.shape[2] * esz * (2 if cd else 1)
+    if array_bytes * 3 < 126e6:  # L2-resident sizes
+        roofline["note"] = ("L2-resident grid (three arrays < 126 MB L2): the HBM fraction is not meaningful; "
+                            "the step is bound by launch and barrier latency")
     B = cd_model_bytes_per_step(S, esz) if cd else model_bytes_per_step(S, esz)
     breakdown = sorted(({"kernel": r["name"], "ms_per_step": r["ms"] / nprof, "launches_per_step": r["count"] / nprof,
                          "GBps": (r["bytes"] * r["count"] / (r["ms"] * 1e-3) / 1e9) if r["ms"] else None}
