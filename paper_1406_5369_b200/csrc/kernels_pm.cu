@@ -1025,7 +1025,7 @@ __global__ void __launch_bounds__(NT) k_prolong3d(Geom gf, Geom gc, const T* __r
 
 template <typename T>
 cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cudaStream_t st) {
-  if (!gf.three_d) return pm2::launch_prolong<T>(gf, gc, e, u, st);
+  if (!gf.three_d) return pm2::launch_prolong<T>(gf, gc, e, u, u, st);
   using G = Geo<T>;
   const int tiles_x = (gf.nx + G::TX - 1) / G::TX, tiles_y = (gf.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;

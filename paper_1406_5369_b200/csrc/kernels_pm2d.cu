@@ -22,7 +22,7 @@
 //                      all in registers
 //  k_resid_restrict2d  r = f - A u (Alg. 1 line 4) and full weighting:
 //                      read u, f; write f_H (r never leaves registers)
-//  k_prolong2d         u += P e, bilinear
+//  k_prolong2d         uout = uin + P e, bilinear
 // Arithmetic is the canonical per-point order of mg_common.cuh with explicitly
 // rounded intrinsics (no FMA): bitwise identical to the op-by-op kernels and the oracle.
 #include <cstdio>
@@ -257,6 +257,113 @@ __global__ void __launch_bounds__(NT) k_jacobi2d(const __grid_constant__ CUtenso
     R.finish(nsteps);
   }
   if (MODE == 2 || NRM) block_partial(nsum, partial);
+}
+
+// ---------------------------------------------------------------------------
+// K omega-Jacobi sweeps in ONE pass (temporal blocking in registers; 2 <= K <= W + 1).
+// Stage k (k = 1..K) is the k-th sweep; at iteration t stage k relaxes row t-k+1 from
+// stage k-1's rows t-k .. t-k+2, kept in a 3-row register window per stage.  Strips
+// OVERLAP: a warp covers TX columns from x0 but only its lanes 1..30 store (columns
+// x0+W .. x0+TX-W-1), so the strip stride is TX - 2W.  A stage-k value is exact at least
+// K-1 <= W columns inside the strip's box, hence exact on every stored column; the outer
+// lanes' values are used only as neighbours of values that are discarded.  No lane-divergent
+// edge code.  Every value is a single sweep's canonical arithmetic: bitwise equal to K
+// launches of k_jacobi2d.  u, f read once, u^(K) written once: 3 words for K sweeps.
+// ZERO: the input iterate is 0 (first sweeps after V_H(0, ...)), u not read.
+template <typename T, int K, bool ZERO>
+__global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUtensorMap tm_u,
+                                                   const __grid_constant__ CUtensorMap tm_f, Geom g, Coef<T> c,
+                                                   T* __restrict__ uout, int nstrips, int nch) {
+  using V = VT<T>;
+  constexpr int W = G2<T>::W, TX = G2<T>::TX, RW = G2<T>::RW, SX = TX - 2 * W;
+  static_assert(K >= 2 && K <= W + 1, "overlap W columns per side");
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WRing<T> R;
+  R.init(smem, wid, lane);
+  prefetch_maps<T>(&tm_u, &tm_f, lane);
+  const int vo = W + W * lane;                // the lane's vector in a box row
+  const int eo = lane == 0 ? W - 1 : W + TX;  // the column beyond the strip (stage-0 neighbour)
+  const bool stores = lane >= 1 && lane <= 30;
+  for (int gw = blockIdx.x * WPB + wid; gw < nstrips * nch; gw += gridDim.x * WPB) {
+    int strip, pa, pb;
+    item2(gw, nstrips, nch, g.p_lo, g.p_hi, strip, pa, pb);
+    const int x0 = strip * SX - W, ox = x0 + W * lane;
+    bool in[W], any = false;
+#pragma unroll
+    for (int j = 0; j < W; j++) {
+      in[j] = ox + j >= 1 && ox + j <= g.nx - 1;
+      any = any || in[j];
+    }
+    const int ts = pa - K + 1, te = pb + K - 2;  // stage-1 rows (= iterations)
+    R.t0 = ts;
+    R.x = x0 - W;
+    const int nsteps = (te - ts) / RB + 1;
+    if (lane == 0) R.start(nsteps, &tm_u, &tm_f, !ZERO);
+    auto urow = [&](const T* r, T& e) -> V {
+      if (ZERO) {
+        e = (T)0;
+        return zvec<T>();
+      }
+      e = r[eo];
+      return ld_vec(r + vo);
+    };
+    // window slot of a row: (row - ts + 1) mod 3; S[k][slot] stage k, e0[slot] stage-0 edge
+    V S[K + 1][3];
+    T e0[3];
+    V Fw[3];
+    R.wait(-1);
+    S[0][0] = urow(R.U(-1) + (RB - 2) * RW, e0[0]);  // row ts-1
+    S[0][1] = urow(R.U(-1) + (RB - 1) * RW, e0[1]);  // row ts
+    R.release(-1, nsteps, lane, &tm_u, &tm_f, !ZERO);
+    auto iter = [&](auto PHc, int t, const T* ur, const T* fr) {
+      constexpr int PH = decltype(PHc)::value;
+      S[0][(PH + 2) % 3] = urow(ur, e0[(PH + 2) % 3]);  // stage 0, row t+1
+      Fw[(PH + 1) % 3] = ld_vec(fr + vo);               // f, row t
+#pragma unroll
+      for (int k = 1; k <= K; k++) {
+        const int sm = (PH - k + 1 + 6) % 3, s0 = (PH - k + 2 + 6) % 3, sp = (PH - k + 6) % 3;
+        const V& P0 = S[k - 1][s0];
+        const int rg = t - k + 1 + g.p_glob0;
+        const bool rin = rg >= 1 && rg <= g.nz - 1;
+        T l0 = __shfl_up_sync(FULL, P0.v[W - 1], 1), r0 = __shfl_down_sync(FULL, P0.v[0], 1);
+        if (k == 1) {  // the box supplies the stage-0 columns beyond the strip; later stages'
+          if (lane == 0) l0 = e0[s0];  // out-of-strip neighbours only feed discarded values
+          if (lane == 31) r0 = e0[s0];
+        }
+        V o;
+#pragma unroll
+        for (int j = 0; j < W; j++) {
+          const T l = j == 0 ? l0 : P0.v[j > 0 ? j - 1 : 0];
+          const T r = j == W - 1 ? r0 : P0.v[j < W - 1 ? j + 1 : 0];
+          const T ctr = P0.v[j];
+          o.v[j] = (rin && in[j]) ? add(ctr, mul(c.wd, sub(Fw[s0].v[j], A2(c, ctr, l, r, S[k - 1][sm].v[j],
+                                                                           S[k - 1][sp].v[j]))))
+                                  : ctr;
+        }
+        S[k][s0] = o;
+      }
+      const int ro = t - K + 1;  // the stage-K row of this iteration
+      if (stores && any && ro >= pa && ro < pb) store_vec(uout + (long long)ro * g.pstride, ox, in, S[K][(PH - K + 8) % 3]);
+    };
+    for (int b = 0; b < nsteps; b++) {
+      R.wait(b);
+      const T* Ub = R.U(b);
+      const T* Fb = R.F(b);
+#pragma unroll
+      for (int i = 0; i < RB; i++) {
+        const int t = ts + b * RB + i;
+        if (t > te) break;
+        switch ((t - ts) % 3) {
+          case 0: iter(std::integral_constant<int, 0>(), t, Ub + i * RW, Fb + i * RW); break;
+          case 1: iter(std::integral_constant<int, 1>(), t, Ub + i * RW, Fb + i * RW); break;
+          default: iter(std::integral_constant<int, 2>(), t, Ub + i * RW, Fb + i * RW); break;
+        }
+      }
+      R.release(b, nsteps, lane, &tm_u, &tm_f, !ZERO);
+    }
+    R.finish(nsteps);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -511,10 +618,12 @@ __global__ void __launch_bounds__(NT) k_resid_restrict2d(const __grid_constant__
 }
 
 // ---------------------------------------------------------------------------
-// u += P e on interior fine nodes.  Fine row z = 2Z + dz gets dz ? (V(Z) + V(Z+1))/2
-// : V(Z), V(K) = coarse row K interpolated along x (reading 13 order: x, then y).
+// uout = uin + P e on interior fine nodes (uout == uin: in place; out of place, uout's
+// boundary must already hold the Dirichlet data).  Fine row z = 2Z + dz gets
+// dz ? (V(Z) + V(Z+1))/2 : V(Z), V(K) = coarse row K interpolated along x (reading 13
+// order: x, then y).
 template <typename T>
-__global__ void __launch_bounds__(NT) k_prolong2d(Geom gf, Geom gc, const T* __restrict__ e, T* __restrict__ u,
+__global__ void __launch_bounds__(NT) k_prolong2d(Geom gf, Geom gc, const T* __restrict__ e, const T* uin, T* uout,
                                                   int nstrips, int nch) {
   using V = VT<T>;
   constexpr int W = G2<T>::W, TX = G2<T>::TX, NR = G2<T>::NR;
@@ -565,17 +674,18 @@ __global__ void __launch_bounds__(NT) k_prolong2d(Geom gf, Geom gc, const T* __r
 #pragma unroll
       for (int j = 0; j < W; j++) v.v[j] = mul(half, add(Av.v[j], Bv.v[j]));
     }
-    T* up = u + (long long)z * gf.pstride;
+    const T* ui = uin + (long long)z * gf.pstride;
+    T* uo = uout + (long long)z * gf.pstride;
     if (all) {
-      const V uu = ld_vec(up + ox);
+      const V uu = ld_vec(ui + ox);
       V o;
 #pragma unroll
       for (int j = 0; j < W; j++) o.v[j] = add(uu.v[j], v.v[j]);
-      store_vec(up, ox, in, o);
+      store_vec(uo, ox, in, o);
     } else {
 #pragma unroll
       for (int j = 0; j < W; j++)
-        if (in[j]) up[ox + j] = add(up[ox + j], v.v[j]);
+        if (in[j]) uo[ox + j] = add(ui[ox + j], v.v[j]);
     }
   }
 }
@@ -648,6 +758,29 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
 }
 
 template <typename T>
+cudaError_t launch_jacobi_k(const Geom& g, const Coef<T>& c, int K, const T* uin, const T* f, T* uout, bool zero_in,
+                            cudaStream_t st) {
+  CUtensorMap tu, tf;
+  if (!encode2d<T>(&tu, uin ? uin : f, g) || !encode2d<T>(&tf, f, g)) return cudaErrorInvalidValue;
+  // overlapping strips of stride TX - 2W covering the columns 0 .. nx
+  const int ns = (g.nx + 1 + (G2<T>::TX - 2 * G2<T>::W) - 1) / (G2<T>::TX - 2 * G2<T>::W);
+  const int smem = G2<T>::SMEM;
+  int nch, nb;
+  auto go = [&](auto kernel) {
+    split(ns, g.p_hi - g.p_lo, resident_warps(kernel, smem), nch, nb);
+    kernel<<<nb, NT, smem, st>>>(tu, tf, g, c, uout, ns, nch);
+  };
+  if (K == 2)
+    zero_in ? go(k_jacobi2d_k<T, 2, true>) : go(k_jacobi2d_k<T, 2, false>);
+  else if constexpr (G2<T>::W >= 3) {
+    zero_in ? go(k_jacobi2d_k<T, 3, true>) : go(k_jacobi2d_k<T, 3, false>);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
 int sweep_partials(const Geom& g, bool rbgs) {
   int nch, nb;
   const int smem = G2<T>::SMEM;
@@ -692,12 +825,12 @@ cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>&
 }
 
 template <typename T>
-cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cudaStream_t st) {
+cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, const T* uin, T* uout, cudaStream_t st) {
   auto kernel = k_prolong2d<T>;
   const int ns = strips<T>(gf);
   int nch, nb;
   split(ns, gf.p_hi - gf.p_lo, resident_warps(kernel, 0), nch, nb);
-  kernel<<<nb, NT, 0, st>>>(gf, gc, e, u, ns, nch);
+  kernel<<<nb, NT, 0, st>>>(gf, gc, e, uin, uout, ns, nch);
   return cudaGetLastError();
 }
 
@@ -705,6 +838,10 @@ template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool
                                           double*, bool, cudaStream_t, double*, int*);
 template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
                                          bool, cudaStream_t, double*, int*);
+template cudaError_t launch_jacobi_k<double>(const Geom&, const Coef<double>&, int, const double*, const double*,
+                                             double*, bool, cudaStream_t);
+template cudaError_t launch_jacobi_k<float>(const Geom&, const Coef<float>&, int, const float*, const float*, float*,
+                                            bool, cudaStream_t);
 template int sweep_partials<double>(const Geom&, bool);
 template int sweep_partials<float>(const Geom&, bool);
 template cudaError_t launch_norm<double>(const Geom&, const Coef<double>&, const double*, const double*, double*,
@@ -717,8 +854,9 @@ template cudaError_t launch_resid_restrict<double>(const Geom&, const Geom&, con
                                                    const double*, double*, cudaStream_t);
 template cudaError_t launch_resid_restrict<float>(const Geom&, const Geom&, const Coef<float>&, const float*,
                                                   const float*, float*, cudaStream_t);
-template cudaError_t launch_prolong<double>(const Geom&, const Geom&, const double*, double*, cudaStream_t);
-template cudaError_t launch_prolong<float>(const Geom&, const Geom&, const float*, float*, cudaStream_t);
+template cudaError_t launch_prolong<double>(const Geom&, const Geom&, const double*, const double*, double*,
+                                            cudaStream_t);
+template cudaError_t launch_prolong<float>(const Geom&, const Geom&, const float*, const float*, float*, cudaStream_t);
 
 }  // namespace pm2
 }  // namespace mg

@@ -12,6 +12,10 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
                          cudaStream_t st, double* partial, int* npartial);
 template <typename T>
 int sweep_partials(const Geom& g, bool rbgs);
+// K (2, or 3 in FP32) omega-Jacobi sweeps in one pass: bitwise equal to K single sweeps
+template <typename T>
+cudaError_t launch_jacobi_k(const Geom& g, const Coef<T>& c, int K, const T* uin, const T* f, T* uout, bool zero_in,
+                            cudaStream_t st);
 template <typename T>
 cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f, double* partial, int* npartial,
                         cudaStream_t st);
@@ -20,7 +24,8 @@ int norm_partials(const Geom& g);
 template <typename T>
 cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>& c, const T* u, const T* f, T* fc,
                                   cudaStream_t st);
+// uout = uin + P e (in place when uout == uin; out of place, uout's boundary holds the data)
 template <typename T>
-cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cudaStream_t st);
+cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, const T* uin, T* uout, cudaStream_t st);
 }  // namespace pm2
 }  // namespace mg

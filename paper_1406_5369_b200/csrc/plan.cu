@@ -12,6 +12,7 @@
 #include "kernels.h"
 #include "partition.h"
 #include "kernels_pm.h"
+#include "kernels_pm2d.h"
 #include "kernels_tail.h"
 #include <cstdlib>
 #include "plan.h"
@@ -50,6 +51,7 @@ enum Kind {
   K_CD_COPY,
   K_CD_TAIL,
   K_GS_LEX,
+  K_SWEEP_JACOBI_K,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -60,7 +62,7 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "coarse_tail",   "prolong+sweep",
                                        "cd_gfield",     "cd_jacobi",     "cd_rbgs_colour", "cd_restrict",
                                        "cd_fas_rhs",    "cd_prolong",    "cd_norm_partial", "cd_residual",
-                                       "cd_copy",       "cd_tail",       "gs_lex_plane"};
+                                       "cd_copy",       "cd_tail",       "gs_lex_plane",  "jacobi_pm_xK"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -518,6 +520,43 @@ struct Exec {
     return MG_OK;
   }
 
+  // n sweeps; 2D plane-marching Jacobi levels (not slab-distributed) run them K at a time in
+  // one pass (k_jacobi2d_k: K = 3 in FP32, 2 in FP64), bitwise equal to n single sweeps
+  // 2D omega-Jacobi on a marching level: n sweeps run as passes of up to 3 (FP32) / 2 (FP64)
+  // fused sweeps (pm2::launch_jacobi_k, temporal blocking; bitwise equal to single sweeps)
+  bool kfusable(int l) const {
+    static const bool off = getenv("MG_NO_KFUSE") != nullptr;
+    const Level& L = s->lv[l];
+    return !off && pm(l) && !L.g.three_d && s->cfg.smoother == MG_JACOBI && !L.dist;
+  }
+  int passes(int l, int n) const {
+    const int kmax = sizeof(T) == 4 ? 3 : 2;
+    return kfusable(l) ? (n + kmax - 1) / kmax : n;
+  }
+
+  mg_status smooth_n(int l, T*& cur, T*& other, const T* f, int n, bool zero_in) {
+    const Level& L = s->lv[l];
+    const int p = passes(l, n);
+    mg_status r = MG_OK;
+    for (int k = 0, i = 0; k < n; i++) {
+      const int K = n / p + (i < n % p ? 1 : 0);
+      if (K >= 2) {
+        T* in = cur;
+        T* out = other;
+        const bool z = zero_in && k == 0;
+        if ((r = launch(s, st, K_SWEEP_JACOBI_K, l, (z ? 2 : 3) * w(l), [&] {
+               return pm2::launch_jacobi_k<T>(L.g, coef(l), K, z ? nullptr : in, f, out, z, st);
+             })) != MG_OK)
+          return r;
+        std::swap(cur, other);
+      } else if ((r = smooth(l, cur, other, f, zero_in && k == 0)) != MG_OK) {
+        return r;
+      }
+      k += K;
+    }
+    return r;
+  }
+
   mg_status memset0(int l, T* p) {
     return launch(s, st, K_MEMSET, l, w(l),
                   [&] { return cudaMemsetAsync(p, 0, s->lv[l].elems * sizeof(T), st); });
@@ -615,8 +654,10 @@ struct Exec {
         const T* f = l == 0 ? f0 : (const T*)L.f;
         // V_H(0, ...): the zero guess is folded into the first sweep (bitwise identical)
         if (l > 0 && s->cfg.nu1 == 0 && (r = memset0(l, cur[l])) != MG_OK) return r;
-        for (int k = (after_head && l == 0) ? 1 : 0; k < s->cfg.nu1; k++)
-          if ((r = smooth(l, cur[l], oth[l], f, l > 0 && k == 0)) != MG_OK) return r;
+        {
+          const int k0 = (after_head && l == 0) ? 1 : 0;
+          if ((r = smooth_n(l, cur[l], oth[l], f, s->cfg.nu1 - k0, l > 0 && k0 == 0)) != MG_OK) return r;
+        }
         T* res = (T*)L.r;
         T* fc = (T*)s->lv[l + 1].f;
         const Level& C = s->lv[l + 1];
@@ -680,13 +721,19 @@ struct Exec {
             if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
           continue;
         }
+        // level 0: the ping-pong buffers swap once per pass; when fused passes change the
+        // parity of the sweep count, the prolongation writes out of place (same traffic) so
+        // the cycle still ends in u without a copy-back
+        const int n0 = s->cfg.nu1 - (after_head ? 1 : 0);
+        const bool flip = l == 0 && kfusable(0) && ((passes(0, n0) + passes(0, s->cfg.nu2) - n0 - s->cfg.nu2) & 1);
         if ((r = launch(s, st, K_PROLONG, l, 2 * w(l) + w(l + 1), [&] {
-               return pml ? pm::launch_prolong<T>(L.g, s->lv[l + 1].g, e, cur[l], st)
-                          : launch_prolong_correct<T>(L.g, s->lv[l + 1].g, e, cur[l], st);
+               return flip ? pm2::launch_prolong<T>(L.g, s->lv[l + 1].g, e, cur[l], oth[l], st)
+                      : pml ? pm::launch_prolong<T>(L.g, s->lv[l + 1].g, e, cur[l], st)
+                            : launch_prolong_correct<T>(L.g, s->lv[l + 1].g, e, cur[l], st);
              })) != MG_OK)
           return r;
-        for (int k = 0; k < s->cfg.nu2; k++)
-          if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+        if (flip) std::swap(cur[l], oth[l]);
+        if ((r = smooth_n(l, cur[l], oth[l], f, s->cfg.nu2, false)) != MG_OK) return r;
       }
     }
     if (cur[0] != u0) {
