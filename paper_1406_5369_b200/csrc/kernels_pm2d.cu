@@ -129,18 +129,24 @@ __device__ __forceinline__ void block_partial(double nsum, double* partial) {
 // supplies u(t0 - RB + 1 .. t0) for the registers the march starts with.  Step b lives
 // in slot (n0 + b + 1) % NS, mbarrier phase ((n0 + b + 1) / NS) & 1 (n0: steps of the
 // warp's earlier items).
-template <typename T>
+template <typename T, int RBR = RB>
 struct WRing {
-  using G = G2<T>;
+  struct G {  // G2<T> with RBR rows per box; slots 128-B aligned (TMA destinations)
+    static constexpr int BOXB = G2<T>::RW * RBR * (int)sizeof(T);
+    static constexpr int SLOTB = (BOXB + 127) / 128 * 128;
+    static constexpr int BOX = SLOTB / (int)sizeof(T);  // slot stride in elements
+  };
+  static constexpr int WARP_BYTES = NS * 2 * G::SLOTB + 128;
+  static constexpr int SMEM = WPB * WARP_BYTES;
   T* buf;
   uint64_t* bar;
   uint32_t n0;
   int t0, x;  // first row of the march, box x start (x0 - W)
 
   __device__ void init(unsigned char* smem, int wid, int lane) {
-    unsigned char* w = smem + wid * G::WARP_BYTES;
+    unsigned char* w = smem + wid * WARP_BYTES;
     buf = reinterpret_cast<T*>(w);
-    bar = reinterpret_cast<uint64_t*>(w + NS * 2 * G::BOXB);
+    bar = reinterpret_cast<uint64_t*>(w + NS * 2 * G::SLOTB);
     n0 = 0;
     if (lane == 0) {
       for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
@@ -157,8 +163,8 @@ struct WRing {
     uint64_t* br = &bar[N(b) % NS];
     const bool lf = b >= 0;
     mbar_expect_tx(br, (uint32_t)((load_u ? G::BOXB : 0) + (lf ? G::BOXB : 0)));
-    if (load_u) tma_load_2d(U(b), tu, x, t0 + b * RB + 1, br);
-    if (lf) tma_load_2d(F(b), tf, x, t0 + b * RB, br);
+    if (load_u) tma_load_2d(U(b), tu, x, t0 + b * RBR + 1, br);
+    if (lf) tma_load_2d(F(b), tf, x, t0 + b * RBR, br);
   }
   // lane 0: steps -1 .. NS-2 (all slots)
   __device__ void start(int nsteps, const CUtensorMap* tu, const CUtensorMap* tf, bool load_u) const {
@@ -270,21 +276,26 @@ __global__ void __launch_bounds__(NT) k_jacobi2d(const __grid_constant__ CUtenso
 // edge code.  Every value is a single sweep's canonical arithmetic: bitwise equal to K
 // launches of k_jacobi2d.  u, f read once, u^(K) written once: 3 words for K sweeps.
 // ZERO: the input iterate is 0 (first sweeps after V_H(0, ...)), u not read.
-template <typename T, int K, bool ZERO>
+// NRM: also the norm partials of the INPUT's residual f - A u, from stage 1 on the nodes
+// the warp stores (fused head of the pipelined solve: sweep + ||r|| of its input).
+template <typename T, int K, bool ZERO, bool NRM>
 __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUtensorMap tm_u,
                                                    const __grid_constant__ CUtensorMap tm_f, Geom g, Coef<T> c,
-                                                   T* __restrict__ uout, int nstrips, int nch) {
+                                                   T* __restrict__ uout, int nstrips, int nch,
+                                                   double* __restrict__ partial) {
   using V = VT<T>;
   constexpr int W = G2<T>::W, TX = G2<T>::TX, RW = G2<T>::RW, SX = TX - 2 * W;
   static_assert(K >= 2 && K <= W + 1, "overlap W columns per side");
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WRing<T> R;
+  constexpr int R3 = 3;  // rows per box = the window period: a row's window slots are static
+  WRing<T, R3> R;
   R.init(smem, wid, lane);
   prefetch_maps<T>(&tm_u, &tm_f, lane);
   const int vo = W + W * lane;                // the lane's vector in a box row
   const int eo = lane == 0 ? W - 1 : W + TX;  // the column beyond the strip (stage-0 neighbour)
   const bool stores = lane >= 1 && lane <= 30;
+  double nsum = 0.0;
   for (int gw = blockIdx.x * WPB + wid; gw < nstrips * nch; gw += gridDim.x * WPB) {
     int strip, pa, pb;
     item2(gw, nstrips, nch, g.p_lo, g.p_hi, strip, pa, pb);
@@ -298,7 +309,7 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
     const int ts = pa - K + 1, te = pb + K - 2;  // stage-1 rows (= iterations)
     R.t0 = ts;
     R.x = x0 - W;
-    const int nsteps = (te - ts) / RB + 1;
+    const int nsteps = (te - ts) / R3 + 1;
     if (lane == 0) R.start(nsteps, &tm_u, &tm_f, !ZERO);
     auto urow = [&](const T* r, T& e) -> V {
       if (ZERO) {
@@ -313,8 +324,8 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
     T e0[3];
     V Fw[3];
     R.wait(-1);
-    S[0][0] = urow(R.U(-1) + (RB - 2) * RW, e0[0]);  // row ts-1
-    S[0][1] = urow(R.U(-1) + (RB - 1) * RW, e0[1]);  // row ts
+    S[0][0] = urow(R.U(-1) + 1 * RW, e0[0]);  // row ts-1
+    S[0][1] = urow(R.U(-1) + 2 * RW, e0[1]);  // row ts
     R.release(-1, nsteps, lane, &tm_u, &tm_f, !ZERO);
     auto iter = [&](auto PHc, int t, const T* ur, const T* fr) {
       constexpr int PH = decltype(PHc)::value;
@@ -337,33 +348,32 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
           const T l = j == 0 ? l0 : P0.v[j > 0 ? j - 1 : 0];
           const T r = j == W - 1 ? r0 : P0.v[j < W - 1 ? j + 1 : 0];
           const T ctr = P0.v[j];
-          o.v[j] = (rin && in[j]) ? add(ctr, mul(c.wd, sub(Fw[s0].v[j], A2(c, ctr, l, r, S[k - 1][sm].v[j],
-                                                                           S[k - 1][sp].v[j]))))
-                                  : ctr;
+          const T rr = sub(Fw[s0].v[j], A2(c, ctr, l, r, S[k - 1][sm].v[j], S[k - 1][sp].v[j]));
+          o.v[j] = selv(rin && in[j], add(ctr, mul(c.wd, rr)), ctr);
+          if (NRM && k == 1) {  // stage 1 row t: the input's residual on the stored nodes
+            const double q = __dmul_rn((double)rr, (double)rr);
+            nsum = __dadd_rn(nsum, (stores && rin && in[j] && t >= pa && t < pb) ? q : 0.0);
+          }
         }
         S[k][s0] = o;
       }
       const int ro = t - K + 1;  // the stage-K row of this iteration
       if (stores && any && ro >= pa && ro < pb) store_vec(uout + (long long)ro * g.pstride, ox, in, S[K][(PH - K + 8) % 3]);
     };
+    // rows past te (in the last box) compute values that are never stored
     for (int b = 0; b < nsteps; b++) {
       R.wait(b);
       const T* Ub = R.U(b);
       const T* Fb = R.F(b);
-#pragma unroll
-      for (int i = 0; i < RB; i++) {
-        const int t = ts + b * RB + i;
-        if (t > te) break;
-        switch ((t - ts) % 3) {
-          case 0: iter(std::integral_constant<int, 0>(), t, Ub + i * RW, Fb + i * RW); break;
-          case 1: iter(std::integral_constant<int, 1>(), t, Ub + i * RW, Fb + i * RW); break;
-          default: iter(std::integral_constant<int, 2>(), t, Ub + i * RW, Fb + i * RW); break;
-        }
-      }
+      const int t = ts + b * R3;
+      iter(std::integral_constant<int, 0>(), t, Ub, Fb);
+      iter(std::integral_constant<int, 1>(), t + 1, Ub + RW, Fb + RW);
+      iter(std::integral_constant<int, 2>(), t + 2, Ub + 2 * RW, Fb + 2 * RW);
       R.release(b, nsteps, lane, &tm_u, &tm_f, !ZERO);
     }
     R.finish(nsteps);
   }
+  if (NRM) block_partial(nsum, partial);
 }
 
 // ---------------------------------------------------------------------------
@@ -718,11 +728,18 @@ static int strips(const Geom& g) {
 }
 
 // 2D tensor map of a level array: dims (nx+1, planes), box (RW, RB) — OOB reads are zero
+// overlapping strips of the fused Jacobi passes: stride TX - 2W covering the columns 0 .. nx
 template <typename T>
-static bool encode2d(CUtensorMap* tm, const T* base, const Geom& g) {
+static int kstrips(const Geom& g) {
+  constexpr int SX = G2<T>::TX - 2 * G2<T>::W;
+  return (g.nx + 1 + SX - 1) / SX;
+}
+
+template <typename T>
+static bool encode2d(CUtensorMap* tm, const T* base, const Geom& g, int rows = RB) {
   const unsigned long long dims[2] = {(unsigned long long)(g.nx + 1), (unsigned long long)g.planes};
   const unsigned long long strides[1] = {(unsigned long long)(g.pstride * sizeof(T))};
-  const unsigned box[2] = {(unsigned)G2<T>::RW, (unsigned)RB};
+  const unsigned box[2] = {(unsigned)G2<T>::RW, (unsigned)rows};
   return pm::encode_tiled(tm, sizeof(T) == 8, 2, base, dims, strides, box) == CUDA_SUCCESS;
 }
 
@@ -759,24 +776,33 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
 
 template <typename T>
 cudaError_t launch_jacobi_k(const Geom& g, const Coef<T>& c, int K, const T* uin, const T* f, T* uout, bool zero_in,
-                            cudaStream_t st) {
+                            cudaStream_t st, double* partial, int* npartial) {
   CUtensorMap tu, tf;
-  if (!encode2d<T>(&tu, uin ? uin : f, g) || !encode2d<T>(&tf, f, g)) return cudaErrorInvalidValue;
-  // overlapping strips of stride TX - 2W covering the columns 0 .. nx
-  const int ns = (g.nx + 1 + (G2<T>::TX - 2 * G2<T>::W) - 1) / (G2<T>::TX - 2 * G2<T>::W);
-  const int smem = G2<T>::SMEM;
+  if (!encode2d<T>(&tu, uin ? uin : f, g, 3) || !encode2d<T>(&tf, f, g, 3)) return cudaErrorInvalidValue;
+  if (partial && zero_in) return cudaErrorInvalidValue;
+  const int ns = kstrips<T>(g);
+  const int smem = WRing<T, 3>::SMEM;
   int nch, nb;
   auto go = [&](auto kernel) {
     split(ns, g.p_hi - g.p_lo, resident_warps(kernel, smem), nch, nb);
-    kernel<<<nb, NT, smem, st>>>(tu, tf, g, c, uout, ns, nch);
+    kernel<<<nb, NT, smem, st>>>(tu, tf, g, c, uout, ns, nch, partial);
+  };
+  auto goK = [&](auto Kc) {
+    constexpr int KK = decltype(Kc)::value;
+    if (partial)
+      go(k_jacobi2d_k<T, KK, false, true>);
+    else
+      zero_in ? go(k_jacobi2d_k<T, KK, true, false>) : go(k_jacobi2d_k<T, KK, false, false>);
   };
   if (K == 2)
-    zero_in ? go(k_jacobi2d_k<T, 2, true>) : go(k_jacobi2d_k<T, 2, false>);
+    goK(std::integral_constant<int, 2>());
   else if constexpr (G2<T>::W >= 3) {
-    zero_in ? go(k_jacobi2d_k<T, 3, true>) : go(k_jacobi2d_k<T, 3, false>);
+    if (K != 3) return cudaErrorInvalidValue;
+    goK(std::integral_constant<int, 3>());
   } else {
     return cudaErrorInvalidValue;
   }
+  if (npartial) *npartial = nb;
   return cudaGetLastError();
 }
 
@@ -787,6 +813,17 @@ int sweep_partials(const Geom& g, bool rbgs) {
   const int rw = rbgs ? resident_warps(k_rbgs2d<T, false, true>, smem)
                       : resident_warps(k_jacobi2d<T, 0, false, true>, smem);
   split(strips<T>(g), g.p_hi - g.p_lo, rw, nch, nb);
+  if (!rbgs) {  // the fused head (k_jacobi2d_k NRM, K = 2 or 3)
+    int nb2;
+    split(kstrips<T>(g), g.p_hi - g.p_lo, resident_warps(k_jacobi2d_k<T, 2, false, true>, WRing<T, 3>::SMEM), nch,
+          nb2);
+    nb = nb2 > nb ? nb2 : nb;
+    if constexpr (G2<T>::W >= 3) {
+      split(kstrips<T>(g), g.p_hi - g.p_lo, resident_warps(k_jacobi2d_k<T, 3, false, true>, WRing<T, 3>::SMEM), nch,
+            nb2);
+      nb = nb2 > nb ? nb2 : nb;
+    }
+  }
   return nb;
 }
 
@@ -839,9 +876,9 @@ template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool
 template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
                                          bool, cudaStream_t, double*, int*);
 template cudaError_t launch_jacobi_k<double>(const Geom&, const Coef<double>&, int, const double*, const double*,
-                                             double*, bool, cudaStream_t);
+                                             double*, bool, cudaStream_t, double*, int*);
 template cudaError_t launch_jacobi_k<float>(const Geom&, const Coef<float>&, int, const float*, const float*, float*,
-                                            bool, cudaStream_t);
+                                            bool, cudaStream_t, double*, int*);
 template int sweep_partials<double>(const Geom&, bool);
 template int sweep_partials<float>(const Geom&, bool);
 template cudaError_t launch_norm<double>(const Geom&, const Coef<double>&, const double*, const double*, double*,

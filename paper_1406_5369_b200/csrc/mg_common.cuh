@@ -24,6 +24,17 @@ __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, 
 __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+// c ? a : b as one selp: both operands are computed, no branch around an expensive a
+__device__ __forceinline__ float selv(bool c, float a, float b) {
+  float r;
+  asm("{.reg .pred p; setp.ne.u32 p, %3, 0; selp.f32 %0, %1, %2, p;}" : "=f"(r) : "f"(a), "f"(b), "r"((unsigned)c));
+  return r;
+}
+__device__ __forceinline__ double selv(bool c, double a, double b) {
+  double r;
+  asm("{.reg .pred p; setp.ne.u32 p, %3, 0; selp.f64 %0, %1, %2, p;}" : "=d"(r) : "d"(a), "d"(b), "r"((unsigned)c));
+  return r;
+}
 
 // Geometry of one level on this rank.
 struct Geom {

@@ -52,6 +52,7 @@ enum Kind {
   K_CD_TAIL,
   K_GS_LEX,
   K_SWEEP_JACOBI_K,
+  K_SWEEP_NORM_K,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -62,7 +63,8 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "coarse_tail",   "prolong+sweep",
                                        "cd_gfield",     "cd_jacobi",     "cd_rbgs_colour", "cd_restrict",
                                        "cd_fas_rhs",    "cd_prolong",    "cd_norm_partial", "cd_residual",
-                                       "cd_copy",       "cd_tail",       "gs_lex_plane",  "jacobi_pm_xK"};
+                                       "cd_copy",       "cd_tail",       "gs_lex_plane",  "jacobi_pm_xK",
+                                       "jacobi_pm_xK+norm"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -605,11 +607,26 @@ struct Exec {
     const bool rb = s->cfg.smoother == MG_RBGS;
     int np = 0;
     T* t0 = (T*)L.t;
+    const int hk = head_sweeps();
+    if (hk > 1) {  // fused Jacobi passes: the head is the first pass, up to 3 sweeps
+      if ((r = launch(s, st, K_SWEEP_NORM_K, 0, 3 * w(0), [&] {
+             return pm2::launch_jacobi_k<T>(L.g, coef(0), hk, u0, f0, t0, false, st, s->d_partial, &np);
+           })) != MG_OK)
+        return r;
+      return norm_finish(0, np, out_dev);
+    }
     if ((r = launch(s, st, K_SWEEP_NORM, 0, 3 * w(0), [&] {
            return pm::launch_sweep<T>(L.g, coef(0), rb, u0, f0, t0, false, zc(0), st, s->d_partial, &np);
          })) != MG_OK)
       return r;
     return norm_finish(0, np, out_dev);
+  }
+
+  // level-0 pre-sweeps the head runs: the first fused pass, else one sweep
+  int head_sweeps() const {
+    if (!kfusable(0)) return 1;
+    const int n = s->cfg.nu1, p = passes(0, n);
+    return n / p + (n % p ? 1 : 0);
   }
 
   mg_status vcycle(T* u0, const T* f0) { return vcycle_impl(u0, f0, false); }
@@ -655,7 +672,7 @@ struct Exec {
         // V_H(0, ...): the zero guess is folded into the first sweep (bitwise identical)
         if (l > 0 && s->cfg.nu1 == 0 && (r = memset0(l, cur[l])) != MG_OK) return r;
         {
-          const int k0 = (after_head && l == 0) ? 1 : 0;
+          const int k0 = (after_head && l == 0) ? head_sweeps() : 0;
           if ((r = smooth_n(l, cur[l], oth[l], f, s->cfg.nu1 - k0, l > 0 && k0 == 0)) != MG_OK) return r;
         }
         T* res = (T*)L.r;
@@ -724,8 +741,9 @@ struct Exec {
         // level 0: the ping-pong buffers swap once per pass; when fused passes change the
         // parity of the sweep count, the prolongation writes out of place (same traffic) so
         // the cycle still ends in u without a copy-back
-        const int n0 = s->cfg.nu1 - (after_head ? 1 : 0);
-        const bool flip = l == 0 && kfusable(0) && ((passes(0, n0) + passes(0, s->cfg.nu2) - n0 - s->cfg.nu2) & 1);
+        const int hk = after_head ? head_sweeps() : 0, n0 = s->cfg.nu1 - hk;
+        const bool flip = l == 0 && kfusable(0) &&
+                          (((hk ? 1 : 0) + passes(0, n0) + passes(0, s->cfg.nu2) - s->cfg.nu1 - s->cfg.nu2) & 1);
         if ((r = launch(s, st, K_PROLONG, l, 2 * w(l) + w(l + 1), [&] {
                return flip ? pm2::launch_prolong<T>(L.g, s->lv[l + 1].g, e, cur[l], oth[l], st)
                       : pml ? pm::launch_prolong<T>(L.g, s->lv[l + 1].g, e, cur[l], st)
