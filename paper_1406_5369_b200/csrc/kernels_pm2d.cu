@@ -278,11 +278,15 @@ __global__ void __launch_bounds__(NT) k_jacobi2d(const __grid_constant__ CUtenso
 // ZERO: the input iterate is 0 (first sweeps after V_H(0, ...)), u not read.
 // NRM: also the norm partials of the INPUT's residual f - A u, from stage 1 on the nodes
 // the warp stores (fused head of the pipelined solve: sweep + ||r|| of its input).
-template <typename T, int K, bool ZERO, bool NRM>
+// CORR: the input is u + P e (Alg. 1 line 6): stage 0 of every row is
+// corrected in registers as it arrives, in k_prolong2d's order (x, then y, then the add),
+// so the corrected iterate never makes an HBM round trip (prolongation fused into the
+// first post-smoothing pass; e read from L2/HBM once, a quarter word per node).
+template <typename T, int K, bool ZERO, bool NRM, bool CORR>
 __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUtensorMap tm_u,
                                                    const __grid_constant__ CUtensorMap tm_f, Geom g, Coef<T> c,
                                                    T* __restrict__ uout, int nstrips, int nch,
-                                                   double* __restrict__ partial) {
+                                                   double* __restrict__ partial, const T* __restrict__ ec, Geom gc) {
   using V = VT<T>;
   constexpr int W = G2<T>::W, TX = G2<T>::TX, RW = G2<T>::RW, SX = TX - 2 * W;
   static_assert(K >= 2 && K <= W + 1, "overlap W columns per side");
@@ -319,6 +323,57 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
       e = r[eo];
       return ld_vec(r + vo);
     };
+    // ---- CORR: coarse rows interpolated along x at the lane's columns (V) and at its
+    // strip-edge column (lanes 0 / 31); cA = V(cz), cB = V(cz + 1).  Rows advance by one, so
+    // cz advances by at most one per row: one refill site, predicated loads, no branches
+    const int X = ox >> 1, xe = lane == 0 ? x0 - 1 : x0 + TX, Xe = xe >> 1;
+    const bool ein = xe >= 1 && xe <= g.nx - 1, eok = (lane == 0 || lane == 31) && ein;
+    bool xok[W / 2 + 1];
+#pragma unroll
+    for (int i = 0; i <= W / 2; i++) xok[i] = X + i >= 0 && X + i <= gc.nx;
+    const T half = (T)0.5;
+    auto Vrow = [&](int Z, T& es) -> V {
+      const bool rok = Z >= 0 && Z <= gc.nz;
+      const T* p0 = ec + (long long)((rok ? Z : gc.p_glob0) - gc.p_glob0) * gc.pstride;
+      T a[W / 2 + 1];
+#pragma unroll
+      for (int i = 0; i <= W / 2; i++) a[i] = (rok && xok[i]) ? __ldg(p0 + X + i) : (T)0;
+      V v;
+#pragma unroll
+      for (int i = 0; i < W / 2; i++) {
+        v.v[2 * i] = a[i];
+        v.v[2 * i + 1] = mul(half, add(a[i], a[i + 1]));
+      }
+      const T e1 = (rok && eok) ? __ldg(p0 + Xe) : (T)0;
+      const T e2 = (rok && eok && (xe & 1)) ? __ldg(p0 + Xe + 1) : (T)0;
+      es = (xe & 1) ? mul(half, add(e1, e2)) : e1;
+      return v;
+    };
+    int cz = 0;
+    V cA, cB;
+    T eA = (T)0, eB = (T)0;
+    if (CORR) {  // prime: cB = V(Z(ts - 1)), so the first row's advance makes it cA
+      cz = ((ts - 1 + g.p_glob0) >> 1) - 1;
+      cB = Vrow(cz + 1, eB);
+    }
+    auto correct = [&](V& v, T& es, int row) {  // stage 0 of local row `row` += P e
+      const int zg = row + g.p_glob0, Z = zg >> 1;
+      if (Z != cz) {
+        cA = cB;
+        eA = eB;
+        cB = Vrow(Z + 1, eB);
+        cz = Z;
+      }
+      const bool zin = zg >= 1 && zg <= g.nz - 1;
+      const bool odd = zg & 1;
+#pragma unroll
+      for (int j = 0; j < W; j++) {
+        const T pv = odd ? mul(half, add(cA.v[j], cB.v[j])) : cA.v[j];
+        v.v[j] = selv(zin && in[j], add(v.v[j], pv), v.v[j]);
+      }
+      const T pe = odd ? mul(half, add(eA, eB)) : eA;
+      es = selv(zin && ein, add(es, pe), es);
+    };
     // window slot of a row: (row - ts + 1) mod 3; S[k][slot] stage k, e0[slot] stage-0 edge
     V S[K + 1][3];
     T e0[3];
@@ -326,10 +381,15 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
     R.wait(-1);
     S[0][0] = urow(R.U(-1) + 1 * RW, e0[0]);  // row ts-1
     S[0][1] = urow(R.U(-1) + 2 * RW, e0[1]);  // row ts
+    if (CORR) {
+      correct(S[0][0], e0[0], ts - 1);
+      correct(S[0][1], e0[1], ts);
+    }
     R.release(-1, nsteps, lane, &tm_u, &tm_f, !ZERO);
     auto iter = [&](auto PHc, int t, const T* ur, const T* fr) {
       constexpr int PH = decltype(PHc)::value;
       S[0][(PH + 2) % 3] = urow(ur, e0[(PH + 2) % 3]);  // stage 0, row t+1
+      if (CORR) correct(S[0][(PH + 2) % 3], e0[(PH + 2) % 3], t + 1);
       Fw[(PH + 1) % 3] = ld_vec(fr + vo);               // f, row t
 #pragma unroll
       for (int k = 1; k <= K; k++) {
@@ -351,8 +411,8 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
           const T rr = sub(Fw[s0].v[j], A2(c, ctr, l, r, S[k - 1][sm].v[j], S[k - 1][sp].v[j]));
           o.v[j] = selv(rin && in[j], add(ctr, mul(c.wd, rr)), ctr);
           if (NRM && k == 1) {  // stage 1 row t: the input's residual on the stored nodes
-            const double q = __dmul_rn((double)rr, (double)rr);
-            nsum = __dadd_rn(nsum, (stores && rin && in[j] && t >= pa && t < pb) ? q : 0.0);
+            const double d = selv(stores && rin && in[j] && t >= pa && t < pb, (double)rr, 0.0);
+            nsum = __fma_rn(d, d, nsum);  // FP32 rr: d*d is exact, = dadd(nsum, dmul(d, d))
           }
         }
         S[k][s0] = o;
@@ -776,23 +836,26 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
 
 template <typename T>
 cudaError_t launch_jacobi_k(const Geom& g, const Coef<T>& c, int K, const T* uin, const T* f, T* uout, bool zero_in,
-                            cudaStream_t st, double* partial, int* npartial) {
+                            cudaStream_t st, double* partial, int* npartial, const T* e, const Geom* gc) {
   CUtensorMap tu, tf;
   if (!encode2d<T>(&tu, uin ? uin : f, g, 3) || !encode2d<T>(&tf, f, g, 3)) return cudaErrorInvalidValue;
-  if (partial && zero_in) return cudaErrorInvalidValue;
+  if ((partial && zero_in) || (e && (zero_in || partial || !gc))) return cudaErrorInvalidValue;
   const int ns = kstrips<T>(g);
   const int smem = WRing<T, 3>::SMEM;
+  const Geom gcv = gc ? *gc : g;
   int nch, nb;
   auto go = [&](auto kernel) {
     split(ns, g.p_hi - g.p_lo, resident_warps(kernel, smem), nch, nb);
-    kernel<<<nb, NT, smem, st>>>(tu, tf, g, c, uout, ns, nch, partial);
+    kernel<<<nb, NT, smem, st>>>(tu, tf, g, c, uout, ns, nch, partial, e, gcv);
   };
   auto goK = [&](auto Kc) {
     constexpr int KK = decltype(Kc)::value;
     if (partial)
-      go(k_jacobi2d_k<T, KK, false, true>);
+      go(k_jacobi2d_k<T, KK, false, true, false>);
+    else if (e)
+      go(k_jacobi2d_k<T, KK, false, false, true>);
     else
-      zero_in ? go(k_jacobi2d_k<T, KK, true, false>) : go(k_jacobi2d_k<T, KK, false, false>);
+      zero_in ? go(k_jacobi2d_k<T, KK, true, false, false>) : go(k_jacobi2d_k<T, KK, false, false, false>);
   };
   if (K == 2)
     goK(std::integral_constant<int, 2>());
@@ -815,11 +878,11 @@ int sweep_partials(const Geom& g, bool rbgs) {
   split(strips<T>(g), g.p_hi - g.p_lo, rw, nch, nb);
   if (!rbgs) {  // the fused head (k_jacobi2d_k NRM, K = 2 or 3)
     int nb2;
-    split(kstrips<T>(g), g.p_hi - g.p_lo, resident_warps(k_jacobi2d_k<T, 2, false, true>, WRing<T, 3>::SMEM), nch,
+    split(kstrips<T>(g), g.p_hi - g.p_lo, resident_warps(k_jacobi2d_k<T, 2, false, true, false>, WRing<T, 3>::SMEM), nch,
           nb2);
     nb = nb2 > nb ? nb2 : nb;
     if constexpr (G2<T>::W >= 3) {
-      split(kstrips<T>(g), g.p_hi - g.p_lo, resident_warps(k_jacobi2d_k<T, 3, false, true>, WRing<T, 3>::SMEM), nch,
+      split(kstrips<T>(g), g.p_hi - g.p_lo, resident_warps(k_jacobi2d_k<T, 3, false, true, false>, WRing<T, 3>::SMEM), nch,
             nb2);
       nb = nb2 > nb ? nb2 : nb;
     }
@@ -876,9 +939,9 @@ template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool
 template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
                                          bool, cudaStream_t, double*, int*);
 template cudaError_t launch_jacobi_k<double>(const Geom&, const Coef<double>&, int, const double*, const double*,
-                                             double*, bool, cudaStream_t, double*, int*);
+                                             double*, bool, cudaStream_t, double*, int*, const double*, const Geom*);
 template cudaError_t launch_jacobi_k<float>(const Geom&, const Coef<float>&, int, const float*, const float*, float*,
-                                            bool, cudaStream_t, double*, int*);
+                                            bool, cudaStream_t, double*, int*, const float*, const Geom*);
 template int sweep_partials<double>(const Geom&, bool);
 template int sweep_partials<float>(const Geom&, bool);
 template cudaError_t launch_norm<double>(const Geom&, const Coef<double>&, const double*, const double*, double*,

@@ -53,6 +53,7 @@ enum Kind {
   K_GS_LEX,
   K_SWEEP_JACOBI_K,
   K_SWEEP_NORM_K,
+  K_PROLONG_JACOBI_K,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -64,7 +65,7 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "cd_gfield",     "cd_jacobi",     "cd_rbgs_colour", "cd_restrict",
                                        "cd_fas_rhs",    "cd_prolong",    "cd_norm_partial", "cd_residual",
                                        "cd_copy",       "cd_tail",       "gs_lex_plane",  "jacobi_pm_xK",
-                                       "jacobi_pm_xK+norm"};
+                                       "jacobi_pm_xK+norm", "prolong+jacobi_xK"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -622,12 +623,13 @@ struct Exec {
     return norm_finish(0, np, out_dev);
   }
 
-  // level-0 pre-sweeps the head runs: the first fused pass, else one sweep
-  int head_sweeps() const {
-    if (!kfusable(0)) return 1;
-    const int n = s->cfg.nu1, p = passes(0, n);
-    return n / p + (n % p ? 1 : 0);
+  // sweeps in the first of the passes(l, n) passes (smooth_n's split); 1 when not fusable
+  int first_k(int l, int n) const {
+    const int p = passes(l, n);
+    return p > 0 ? n / p + (n % p ? 1 : 0) : 0;
   }
+  // level-0 pre-sweeps the head runs: the first fused pass, else one sweep
+  int head_sweeps() const { return kfusable(0) ? first_k(0, s->cfg.nu1) : 1; }
 
   mg_status vcycle(T* u0, const T* f0) { return vcycle_impl(u0, f0, false); }
   mg_status tail(T* u0, const T* f0) { return vcycle_impl(u0, f0, true); }
@@ -744,6 +746,21 @@ struct Exec {
         const int hk = after_head ? head_sweeps() : 0, n0 = s->cfg.nu1 - hk;
         const bool flip = l == 0 && kfusable(0) &&
                           (((hk ? 1 : 0) + passes(0, n0) + passes(0, s->cfg.nu2) - s->cfg.nu1 - s->cfg.nu2) & 1);
+        const int k1 = first_k(l, s->cfg.nu2);
+        if (kfusable(l) && !flip && k1 >= 2) {
+          // prolongation + correction fused into the first post-smoothing pass: u + P e is
+          // formed in registers, only the pass's result is written (cur[l] is not modified)
+          const T* in = cur[l];
+          T* out = oth[l];
+          const Geom gcg = s->lv[l + 1].g;
+          if ((r = launch(s, st, K_PROLONG_JACOBI_K, l, 3 * w(l) + w(l + 1), [&] {
+                 return pm2::launch_jacobi_k<T>(L.g, coef(l), k1, in, f, out, false, st, nullptr, nullptr, e, &gcg);
+               })) != MG_OK)
+            return r;
+          std::swap(cur[l], oth[l]);
+          if ((r = smooth_n(l, cur[l], oth[l], f, s->cfg.nu2 - k1, false)) != MG_OK) return r;
+          continue;
+        }
         if ((r = launch(s, st, K_PROLONG, l, 2 * w(l) + w(l + 1), [&] {
                return flip ? pm2::launch_prolong<T>(L.g, s->lv[l + 1].g, e, cur[l], oth[l], st)
                       : pml ? pm::launch_prolong<T>(L.g, s->lv[l + 1].g, e, cur[l], st)
