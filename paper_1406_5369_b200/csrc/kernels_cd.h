@@ -78,6 +78,14 @@ int cd2d_norm_partials(const Geom& g);
 template <typename T>
 cudaError_t cd2d_launch_norm(const Geom& g, const CdCoef<T>& c, const T* gd, const T* u, const T* f,
                              double* partial, int* npartial, cudaStream_t st);
+// K (1..3 FP32, 1..2 FP64) omega-Jacobi sweeps with the frozen g in one pass (temporal
+// blocking), bitwise equal to K cd2d_launch_jacobi sweeps; partial != nullptr: also the
+// partials of |f - A(g) uin|^2 (*npartial of them, at most cd2d_kpartials)
+template <typename T>
+cudaError_t cd2d_launch_jacobi_k(const Geom& g, const CdCoef<T>& c, int K, const T* gd, const T* uin, const T* f,
+                                 T* uout, cudaStream_t st, double* partial = nullptr, int* npartial = nullptr);
+template <typename T>
+int cd2d_kpartials(const Geom& g);
 
 // W5 inputs: re = lo + (hi-lo) U[0,1)(global cell index), im = 0
 template <typename T>

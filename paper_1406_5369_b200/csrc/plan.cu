@@ -54,6 +54,8 @@ enum Kind {
   K_SWEEP_JACOBI_K,
   K_SWEEP_NORM_K,
   K_PROLONG_JACOBI_K,
+  K_CD_JACOBI_K,
+  K_CD_JACOBI_K_NORM,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -65,7 +67,8 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "cd_gfield",     "cd_jacobi",     "cd_rbgs_colour", "cd_restrict",
                                        "cd_fas_rhs",    "cd_prolong",    "cd_norm_partial", "cd_residual",
                                        "cd_copy",       "cd_tail",       "gs_lex_plane",  "jacobi_pm_xK",
-                                       "jacobi_pm_xK+norm", "prolong+jacobi_xK"};
+                                       "jacobi_pm_xK+norm", "prolong+jacobi_xK",
+                                       "cd_jacobi_xK",  "cd_jacobi_xK+norm"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -890,6 +893,8 @@ static mg_status cd_build(mg_solver* s) {
     if (cd2d_supported(g)) {
       a = esz == 8 ? cd2d_norm_partials<double>(g) : cd2d_norm_partials<float>(g);
       if (a > np) np = a;
+      a = esz == 8 ? cd2d_kpartials<double>(g) : cd2d_kpartials<float>(g);  // fused head pass
+      if (a > np) np = a;
     }
   }
   return alloc_common(s, np);
@@ -928,6 +933,53 @@ struct CdExec {
       mg_status r = launch(s, st, K_CD_RBGS, l, 2.5 * cw(l),
                            [&] { return cd_launch_rbgs<T>(G(l), cc(l), gd(l), u, f, colour, st); });
       if (r != MG_OK) return r;
+    }
+    return MG_OK;
+  }
+  // Jacobi on a 2D marching level: n sweeps as passes of up to kmax fused sweeps
+  // (cd2d_launch_jacobi_k, temporal blocking; bitwise equal to single sweeps).  Measured on
+  // CD2: the complex sweep is already issue-bound alone, so K = 2 passes
+  // are SLOWER than two single sweeps (0.37 vs 0.25 ms at 4096^2 FP32); kmax defaults to 1
+  // and the fused kernel serves the solve's head (first sweep + the input's norm in one
+  // pass).  MG_CD_KMAX = 2 / 3 re-enables multi-sweep passes.
+  bool kfusable(int l) const {
+    static const bool off = getenv("MG_NO_KFUSE") != nullptr;
+    return !off && s->cfg.smoother == MG_JACOBI && !(s->cfg.flags & MG_FLAG_BASELINE) && cd2d_supported(G(l));
+  }
+  int kmax() const {
+    static const int env = getenv("MG_CD_KMAX") ? atoi(getenv("MG_CD_KMAX")) : 1;
+    const int cap = sizeof(T) == 4 ? 3 : 2;
+    return env < 1 ? 1 : (env > cap ? cap : env);
+  }
+  int passes(int l, int n) const { return kfusable(l) ? (n + kmax() - 1) / kmax() : n; }
+  int first_k(int l, int n) const {
+    const int p = passes(l, n);
+    return p > 0 ? n / p + (n % p ? 1 : 0) : 0;
+  }
+  // level-0 pre-sweeps the solve's head runs (its first pass, with the input's norm)
+  int head_sweeps() const {
+    return (kfusable(0) && s->L > 1 && tail_level() > 0 && s->cfg.nu1 >= 1) ? first_k(0, s->cfg.nu1) : 0;
+  }
+  // n sweeps in p passes (p = 0: passes(l, n))
+  mg_status smooth_n(int l, T*& cur, T*& oth, const T* f, int n, int p = 0) {
+    if (!kfusable(l)) {
+      for (int k = 0; k < n; k++) {
+        mg_status r = smooth(l, cur, oth, f);
+        if (r != MG_OK) return r;
+      }
+      return MG_OK;
+    }
+    if (p <= 0) p = passes(l, n);
+    for (int k = 0, i = 0; k < n; i++) {
+      const int K = n / p + (i < n % p ? 1 : 0);
+      T* in = cur;
+      T* out = oth;
+      mg_status r = K == 1 ? smooth(l, cur, oth, f) : launch(s, st, K_CD_JACOBI_K, l, 4 * cw(l), [&] {
+        return cd2d_launch_jacobi_k<T>(G(l), cc(l), K, gd(l), in, f, out, st);
+      });
+      if (r != MG_OK) return r;
+      if (K > 1) std::swap(cur, oth);
+      k += K;
     }
     return MG_OK;
   }
@@ -970,17 +1022,13 @@ struct CdExec {
     return launch(s, st, K_CD_TAIL, lt, bytes, [&] { return cd_launch_tail<T>(P, st); });
   }
   // FAS V-cycle at level l; g_ready: g of level l already built from cur[l]
-  mg_status rec(int l, std::vector<T*>& cur, std::vector<T*>& oth, const T* f, bool g_ready) {
+  // skip: level-0 pre-sweeps the head already ran
+  mg_status rec(int l, std::vector<T*>& cur, std::vector<T*>& oth, const T* f, bool g_ready, int skip = 0) {
     mg_status r;
     if (l == tail_level()) return run_tail(l, cur, oth, f, g_ready);  // the result lands in cur[l]
     if (!g_ready && (r = gfield(l, cur[l])) != MG_OK) return r;  // lagged diffusivity, frozen in the cycle
-    if (l == s->L - 1) {
-      for (int k = 0; k < s->cfg.ncoarse; k++)
-        if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
-      return MG_OK;
-    }
-    for (int k = 0; k < s->cfg.nu1; k++)
-      if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+    if (l == s->L - 1) return smooth_n(l, cur[l], oth[l], f, s->cfg.ncoarse);
+    if ((r = smooth_n(l, cur[l], oth[l], f, s->cfg.nu1 - skip)) != MG_OK) return r;
     Level& C = s->lv[l + 1];
     T* uh = (T*)C.uh;
     T* fc = (T*)C.f;
@@ -1003,18 +1051,27 @@ struct CdExec {
     if ((r = launch(s, st, K_CD_PROLONG, l, 2 * cw(l) + 2 * cw(l + 1),
                     [&] { return cd_launch_prolong<T>(G(l), G(l + 1), ucn, uh, ulw, st); })) != MG_OK)
       return r;
-    for (int k = 0; k < s->cfg.nu2; k++)
-      if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
-    return MG_OK;
+    // level 0: when fused passes change the ping-pong parity, one more post pass keeps the
+    // result in u (no copy-back)
+    int p2 = 0;
+    if (l == 0 && kfusable(0)) {
+      const int nu1 = s->cfg.nu1, nu2 = s->cfg.nu2;
+      p2 = passes(0, nu2);
+      if ((((skip ? 1 : 0) + passes(0, nu1 - skip) + p2 - nu1 - nu2) & 1) && p2 < nu2) p2++;
+    }
+    return smooth_n(l, cur[l], oth[l], f, s->cfg.nu2, p2);
   }
-  // g_ready: lv[0].gd already holds g(u0) (the head computed it for the norm)
-  mg_status vcycle(T* u0, const T* f0, bool g_ready = false) {
+  // g_ready: lv[0].gd already holds g(u0) (the head computed it for the norm); after_head:
+  // the head also ran the first level-0 pre-smoothing pass (u0 -> lv[0].t)
+  mg_status vcycle(T* u0, const T* f0, bool g_ready = false, bool after_head = false) {
     std::vector<T*> cur(s->L), oth(s->L);
     for (int l = 0; l < s->L; l++) {
       cur[l] = l == 0 ? u0 : (T*)s->lv[l].u;
       oth[l] = (T*)s->lv[l].t;
     }
-    mg_status r = rec(0, cur, oth, f0, g_ready);
+    const int hk = after_head ? head_sweeps() : 0;
+    if (hk > 0) std::swap(cur[0], oth[0]);
+    mg_status r = rec(0, cur, oth, f0, g_ready, hk);
     if (r != MG_OK) return r;
     if (cur[0] != u0) return copy(0, cur[0], u0);
     return MG_OK;
@@ -1024,7 +1081,16 @@ struct CdExec {
   mg_status head(const T* u0, const T* f0, double* out_dev) {
     mg_status r = gfield(0, u0);
     if (r != MG_OK) return r;
-    return norm(0, u0, f0, out_dev, gd(0));
+    const int hk = head_sweeps();
+    if (hk == 0) return norm(0, u0, f0, out_dev, gd(0));
+    // the first pre-smoothing pass also accumulates ||f - A(g(u0)) u0||: one pass instead of two
+    int np = 0;
+    T* t0 = (T*)s->lv[0].t;
+    if ((r = launch(s, st, K_CD_JACOBI_K_NORM, 0, 4 * cw(0), [&] {
+           return cd2d_launch_jacobi_k<T>(G(0), cc(0), hk, gd(0), u0, f0, t0, st, s->d_partial, &np);
+         })) != MG_OK)
+      return r;
+    return launch(s, st, K_NORM_FINAL, 0, 8.0 * np, [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });
   }
   mg_status norm(int l, const T* u, const T* f, double* out_dev, const T* gstored = nullptr) {
     int np = 0;
@@ -1072,7 +1138,7 @@ static mg_status cd_run_part_T(mg_solver* s, int part, T* u, const T* f, cudaStr
   CdExec<T> x{s, st};
   switch (part) {
     case 1: return x.head(u, f, s->d_norm);
-    case 2: return x.vcycle(u, f, true);
+    case 2: return x.vcycle(u, f, true, true);
     case 3: return x.norm(0, u, f, s->d_norm);
     default: return x.vcycle(u, f);
   }
