@@ -473,10 +473,14 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
           }
         }
         __syncthreads();
-        // ONESYNC: every thread has finished plane p-2's black update: step p-2 is free
-        if (ONESYNC && tid == 0 && p >= pa && p - 2 + G::NS <= qlast) {
+        // ONESYNC: every thread has finished plane p-2's black update: step p-2 is free.
+        // FKEEP (f(p-1) kept in registers for the black stage): step p-1 (u(p), f(p-1)) is
+        // read only by plane p's red stage, so it is free here already — one plane deeper
+        // prefetch with the same NS slots
+        constexpr int LAG = FKEEP ? 1 : 2;
+        if (ONESYNC && tid == 0 && p >= pa - 2 + LAG && p - LAG + G::NS <= qlast) {
           fence_proxy_async();
-          issue_step(p - 2 + G::NS);
+          issue_step(p - LAG + G::NS);
         }
         const int bp = p - 1;  // black nodes of plane p-1: they sit where plane p's red nodes are
         if (bp >= pa) {
