@@ -984,7 +984,10 @@ __global__ void __launch_bounds__(NT) k_prolong3d(Geom gf, Geom gc, const T* __r
     for (int j = 0; j < W; j++) all = all && in[j];
     // KZ planes per iteration: their u vectors are loaded before any store (more bytes in
     // flight per thread; the compiler cannot reorder loads of u across stores to u)
-    constexpr int KZ = 4;
+#ifndef MG_PROLONG_KZ
+#define MG_PROLONG_KZ 4  // measured: 8 spills and is slower (C3 L0 0.46 vs 0.43 ms)
+#endif
+    constexpr int KZ = MG_PROLONG_KZ;
     for (int z0 = pa; z0 < pb; z0 += KZ) {
       Vt uu[KZ];
       if (all) {
