@@ -697,12 +697,19 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         fence_proxy_async();
         R.issue(N(q - 1 + G::NS), &tm_u, &tm_f, x0, y0, q + G::NS, q - 1 + G::NS, true);
       }
-      if (tid < CN) {
+      if (tid < CN) {  // whole warps: CN = 256 (FP64) / 512 (FP32)
+        // x-sums r(2I-1) + r(2I+1) + 2 r(2I): (r(2I), r(2I+1)) is one aligned pair load and
+        // r(2I-1) the left lane's second element (lane 0 loads it) — 5 smem wavefronts per
+        // warp and row instead of 12 for three strided scalars; same values, same order
+        using P2 = std::conditional_t<sizeof(T) == 8, double2, float2>;
         T tx[3];
 #pragma unroll
         for (int dy = -1; dy <= 1; dy++) {
           const T* row = Rr + co + dy * PX;
-          tx[dy + 1] = add(add(row[-1], row[1]), mul(two, row[0]));
+          const P2 pr = *reinterpret_cast<const P2*>(row);
+          T left = __shfl_up_sync(0xffffffffu, pr.y, 1);
+          if (lane == 0) left = row[-1];
+          tx[dy + 1] = add(add(left, pr.y), mul(two, pr.x));
         }
         const T ty0 = add(add(tx[0], tx[2]), mul(two, tx[1]));
         if (cnode && (pgl & 1) == 1 && q >= qf0 + 1) {  // fine plane 2P+1 completes coarse plane P
