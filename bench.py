@@ -294,7 +294,7 @@ def run_reference(args):
                                                           else CONFIGS[args.config][5])),
         "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC[args.config], "parallelism": "cpu-oracle",
-                   "l2": "inputs larger than L2 (CPU run)"},
+                   "l2": "CPU run on the host cores (the GPU L2 flush rule does not apply)"},
         "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": threads, "kind": "oracle", "sample": desc},
         "e2e": {"value": val, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -218,7 +218,8 @@ int64_t mg_launches_per_cycle(const mg_solver* s);
 mg_status mg_profile_enable(mg_solver* s, int32_t on);
 /* Per-kernel timing since enable: for entry i (< n), names[i] points to a static string
  * "<kernel>@L<level>", ms[i] = summed device time, count[i] = launches,
- * bytes[i] = ALGORITHMIC bytes per launch.  Returns the number of entries
+ * bytes[i] = mean ALGORITHMIC bytes per launch (launches of one kernel may
+ * differ, e.g. a zero-guess first sweep does not read u).  Returns the number of entries
  * (may exceed cap; only min(n,cap) written).  Synchronises the device. */
 int32_t mg_profile_read(mg_solver* s, int32_t cap, const char** names, double* ms,
                         int64_t* count, double* bytes);

@@ -1355,10 +1355,11 @@ static void prof_drain(mg_solver* s) {
     for (auto& p : s->prof_done)
       if (p.name == name) sum = &p;
     if (!sum) {
-      s->prof_done.push_back(ProfSum{name, 0, r.bytes, 0});
+      s->prof_done.push_back(ProfSum{name, 0, 0, 0});
       sum = &s->prof_done.back();
     }
     sum->ms += ms;
+    sum->bytes += r.bytes;  // summed: launches of one kind can differ (zero-guess sweeps skip u)
     sum->count++;
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -1382,7 +1383,7 @@ int plan_profile_read(mg_solver* s, int cap, const char** names, double* ms, int
     if (names) names[i] = s->prof_done[i].name.c_str();
     if (ms) ms[i] = s->prof_done[i].ms;
     if (count) count[i] = s->prof_done[i].count;
-    if (bytes) bytes[i] = s->prof_done[i].bytes;
+    if (bytes) bytes[i] = s->prof_done[i].count ? s->prof_done[i].bytes / s->prof_done[i].count : 0.0;
   }
   return n;
 }
