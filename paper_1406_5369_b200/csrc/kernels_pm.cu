@@ -851,21 +851,21 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   using G = Geo<T>;
   CUtensorMap tu, tf;
   CUresult e1 = encode(&tu, uin ? uin : f, g, sizeof(T), G::BYU), e2 = encode(&tf, f, g, sizeof(T), G::BYF);
-  if (getenv("MG_DEBUG")) fprintf(stderr, "launch_sweep: encode %d %d nx=%d ny=%d rows=%d np=%d\n", (int)e1, (int)e2, g.nx, g.ny, g.rows, g.p_hi - g.p_lo);
+  static const bool debug = getenv("MG_DEBUG") != nullptr;  // thread-safe one-time read
+  if (debug)
+    fprintf(stderr, "launch_sweep: encode %d %d nx=%d ny=%d rows=%d np=%d\n", (int)e1, (int)e2, g.nx, g.ny, g.rows,
+            g.p_hi - g.p_lo);
   if (e1 != CUDA_SUCCESS || e2 != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const int tiles_x = (g.nx + G::TX - 1) / G::TX, tiles_y = (g.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = g.p_hi - g.p_lo;
   auto go = [&](auto kernel) {
-    const int resident = prepare_kernel(kernel, ecoarse ? G::SMEM_CORR : G::SMEM);
+    const int smem = ecoarse ? G::SMEM_CORR : G::SMEM;
+    const int resident = prepare_kernel(kernel, smem);
     const int zc = zc_override > 0 ? zc_override : choose_zc(ntiles, np, resident, rbgs ? 4 : 2, min_zc_for(g, sizeof(T)));
     const int nitems = ntiles * ((np + zc - 1) / zc);
-    if (getenv("MG_DEBUG"))
-      fprintf(stderr, "launch_sweep: resident=%d zc=%d nitems=%d smem=%d\n", resident, zc, nitems, G::SMEM);
+    if (debug) fprintf(stderr, "launch_sweep: resident=%d zc=%d nitems=%d smem=%d\n", resident, zc, nitems, smem);
     if (npartial) *npartial = nitems;
-    const int smem = ecoarse ? G::SMEM_CORR : G::SMEM;
-    const int resident2 = ecoarse ? prepare_kernel(kernel, smem) : resident;
-    (void)resident2;
     kernel<<<nitems, NT, smem, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial, te, gce);
   };
   if (ecoarse)

@@ -421,8 +421,8 @@ struct Exec {
 
   // z-chunk override for tuning (MG_ZC); 0 = the launcher's own choice
   int zc(int) const {
-    const char* e = getenv("MG_ZC");
-    return e ? atoi(e) : 0;
+    static const int v = getenv("MG_ZC") ? atoi(getenv("MG_ZC")) : 0;  // thread-safe one-time read
+    return v;
   }
 
 
