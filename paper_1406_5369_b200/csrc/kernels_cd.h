@@ -87,6 +87,18 @@ cudaError_t cd2d_launch_jacobi_k(const Geom& g, const CdCoef<T>& c, int K, const
 template <typename T>
 int cd2d_kpartials(const Geom& g);
 
+// 3D plane-marching Jacobi sweep and stored-g residual norm (kernels_cd3d.cu), bitwise equal to
+// cd_launch_jacobi / the partials of cd_launch_norm_partial's sum
+bool cd3d_supported(const Geom& g);
+template <typename T>
+cudaError_t cd3d_launch_jacobi(const Geom& g, const CdCoef<T>& c, const T* gd, const T* uin, const T* f, T* uout,
+                               cudaStream_t st);
+template <typename T>
+int cd3d_norm_partials(const Geom& g);
+template <typename T>
+cudaError_t cd3d_launch_norm(const Geom& g, const CdCoef<T>& c, const T* gd, const T* u, const T* f,
+                             double* partial, int* npartial, cudaStream_t st);
+
 // W5 inputs: re = lo + (hi-lo) U[0,1)(global cell index), im = 0
 template <typename T>
 cudaError_t cd_launch_fill(const Geom& g, T* dst, uint64_t seed, double lo, double hi, cudaStream_t st);

@@ -896,6 +896,10 @@ static mg_status cd_build(mg_solver* s) {
       a = esz == 8 ? cd2d_kpartials<double>(g) : cd2d_kpartials<float>(g);  // fused head pass
       if (a > np) np = a;
     }
+    if (cd3d_supported(g)) {
+      a = esz == 8 ? cd3d_norm_partials<double>(g) : cd3d_norm_partials<float>(g);
+      if (a > np) np = a;
+    }
   }
   return alloc_common(s, np);
 }
@@ -920,10 +924,12 @@ struct CdExec {
     if (s->cfg.smoother == MG_JACOBI) {
       T* in = cur;
       T* out = oth;
-      const bool marching = !(s->cfg.flags & MG_FLAG_BASELINE) && cd2d_supported(G(l));
+      const bool opt = !(s->cfg.flags & MG_FLAG_BASELINE);
+      const bool m2 = opt && cd2d_supported(G(l)), m3 = opt && cd3d_supported(G(l));
       mg_status r = launch(s, st, K_CD_JACOBI, l, 4 * cw(l), [&] {
-        return marching ? cd2d_launch_jacobi<T>(G(l), cc(l), gd(l), in, f, out, st)
-                        : cd_launch_jacobi<T>(G(l), cc(l), gd(l), in, f, out, st);
+        return m2   ? cd2d_launch_jacobi<T>(G(l), cc(l), gd(l), in, f, out, st)
+               : m3 ? cd3d_launch_jacobi<T>(G(l), cc(l), gd(l), in, f, out, st)
+                    : cd_launch_jacobi<T>(G(l), cc(l), gd(l), in, f, out, st);
       });
       std::swap(cur, oth);
       return r;
@@ -1094,10 +1100,12 @@ struct CdExec {
   }
   mg_status norm(int l, const T* u, const T* f, double* out_dev, const T* gstored = nullptr) {
     int np = 0;
-    const bool marching = gstored && !(s->cfg.flags & MG_FLAG_BASELINE) && cd2d_supported(G(l));
+    const bool opt = gstored && !(s->cfg.flags & MG_FLAG_BASELINE);
+    const bool m2 = opt && cd2d_supported(G(l)), m3 = opt && cd3d_supported(G(l));
     mg_status r = launch(s, st, K_CD_NORM, l, (gstored ? 3 : 2) * cw(l), [&] {
-      return marching ? cd2d_launch_norm<T>(G(l), cc(l), gstored, u, f, s->d_partial, &np, st)
-                      : cd_launch_norm_partial<T>(G(l), cc(l), gstored, u, f, s->d_partial, &np, st);
+      return m2   ? cd2d_launch_norm<T>(G(l), cc(l), gstored, u, f, s->d_partial, &np, st)
+             : m3 ? cd3d_launch_norm<T>(G(l), cc(l), gstored, u, f, s->d_partial, &np, st)
+                  : cd_launch_norm_partial<T>(G(l), cc(l), gstored, u, f, s->d_partial, &np, st);
     });
     if (r != MG_OK) return r;
     return launch(s, st, K_NORM_FINAL, l, 8.0 * np, [&] { return launch_norm_final(s->d_partial, np, out_dev, st); });

@@ -43,6 +43,10 @@ CASES = [
     dict(dim=2, cells=(256, 256), smoother="rbgs", omega=1.15),
     dict(dim=2, cells=(200, 48), levels=3, smoother="jacobi", dtype="f32"),  # ragged warp strips
     dict(dim=2, cells=(200, 48), levels=3, smoother="jacobi"),
+    # 3D plane-marching Jacobi (kernels_cd3d.cu): tiles ragged in x (32 / 64 cells) and y (8 rows)
+    dict(dim=3, cells=(72, 44, 20), levels=2, smoother="jacobi"),
+    dict(dim=3, cells=(100, 36, 16), levels=2, smoother="jacobi", dtype="f32"),
+    dict(dim=3, cells=(64, 64, 64), smoother="jacobi", dtype="f32"),
 ]
 
 
