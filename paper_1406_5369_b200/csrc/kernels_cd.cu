@@ -14,6 +14,9 @@
 // so the iterates are bitwise those of the oracle.
 #include "kernels.h"
 #include "kernels_cd.h"
+#include <cstdint>
+#include <type_traits>
+
 #include "cd_common.cuh"
 #include "launch_util.h"
 
@@ -296,9 +299,41 @@ long long host_cells(const Geom& g) { return (long long)g.nx * (g.three_d ? g.ny
 
 }  // namespace
 
+// g over the whole pitched array, one 16-byte vector (16 / (2 sizeof T) cells) per thread and
+// step: the per-cell function is that of k_cd_gfield (bitwise); pitch cells beyond nx get a
+// harmless value that nothing reads (every kernel bounds its faces by nx)
+template <typename T>
+__global__ void __launch_bounds__(NB) k_cd_gfield_vec(Geom g, CdCoef<T> c, const T* __restrict__ u,
+                                                      T* __restrict__ gd, long long nvec) {
+  constexpr int CW = 16 / (2 * (int)sizeof(T));
+  using V = std::conditional_t<sizeof(T) == 8, double2, float4>;
+  for (long long q = (long long)blockIdx.x * NB + threadIdx.x; q < nvec; q += (long long)gridDim.x * NB) {
+    const V uv = reinterpret_cast<const V*>(u)[q];
+    const T* ur = reinterpret_cast<const T*>(&uv);
+    V gv;
+    T* gr = reinterpret_cast<T*>(&gv);
+#pragma unroll
+    for (int j = 0; j < CW; j++) {
+      const C2<T> d = diffusivity(c, ur[2 * j + 1]);
+      gr[2 * j] = d.re;
+      gr[2 * j + 1] = d.im;
+    }
+    reinterpret_cast<V*>(gd)[q] = gv;
+  }
+}
+
 template <typename T>
 cudaError_t cd_launch_gfield(const Geom& g, const CdCoef<T>& c, const T* u, T* gd, cudaStream_t s) {
-  k_cd_gfield<T><<<grid_rows(g, g.nx), NB, 0, s>>>(g, c, u, gd);
+  constexpr int CW = 16 / (2 * (int)sizeof(T));
+  const long long cells = (long long)g.pstride * g.planes;
+  if (cells % CW == 0 && ((uintptr_t)u & 15) == 0 && ((uintptr_t)gd & 15) == 0) {
+    const long long nvec = cells / CW;
+    const long long want = (nvec + NB - 1) / NB;
+    const int nb = (int)(want < 148LL * 16 ? want : 148LL * 16);
+    k_cd_gfield_vec<T><<<nb, NB, 0, s>>>(g, c, u, gd, nvec);
+  } else {
+    k_cd_gfield<T><<<grid_rows(g, g.nx), NB, 0, s>>>(g, c, u, gd);
+  }
   return cudaGetLastError();
 }
 template <typename T>
