@@ -153,7 +153,9 @@ mg_status mg_vcycle(mg_solver* s, void* u, const void* f, void* stream);
 mg_status mg_residual_norm(mg_solver* s, const void* u, const void* f, double* out, void* stream);
 
 /* Driver loop of the `Application` listing: r0 = norm; repeat
- * { V-cycle; r_k = norm } until r_k <= rtol * r0 or max_cycles.  history (if
+ * { V-cycle; r_k = norm } until r_k <= rtol * r0 or max_cycles.  rtol < 0 turns
+ * the residual test off: exactly max_cycles cycles (a fixed-work loop that does not
+ * stop when an iterate reaches an exact solution); NaN rtol is MG_ERR_INVALID.  history (if
  * not NULL, host memory) receives r_0..r_k (room for max_cycles+1 doubles),
  * history[0] = r0; *cycles = k.  Blocking.  Returns MG_ERR_NONFINITE if a
  * norm is NaN/Inf (the loop stops at that cycle).

@@ -292,7 +292,8 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
                               double* history, void* stream) {
   mg_status st = guard(s);
   if (st != MG_OK) return st;
-  if (max_cycles < 0 || !(rtol >= 0.0)) return fail(s, MG_ERR_INVALID, "bad argument");
+  if (max_cycles < 0 || std::isnan(rtol)) return fail(s, MG_ERR_INVALID, "bad argument");
+  const bool test_on = rtol >= 0.0;  // rtol < 0: exactly max_cycles cycles (no residual test)
   if ((st = check_arrays(s, {u, f})) != MG_OK) return st;
   if (u == f) return fail(s, MG_ERR_INVALID, "u and f must not alias");
   cudaStream_t cs = (cudaStream_t)stream;
@@ -326,7 +327,7 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
         if (cycles) *cycles = k;
         return fail(s, MG_ERR_NONFINITE, "residual norm not finite after cycle %d (S:535)", k);
       }
-      if (rk <= rtol * r0) break;
+      if (test_on && rk <= rtol * r0) break;
     }
     if (cycles) *cycles = k;
     return MG_OK;
@@ -349,7 +350,7 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
       if (cycles) *cycles = k;
       return fail(s, MG_ERR_NONFINITE, "residual norm not finite after cycle %d (S:535)", k);
     }
-    if (rk <= rtol * r0) break;
+    if (test_on && rk <= rtol * r0) break;
   }
   if (cycles) *cycles = k;
   return MG_OK;

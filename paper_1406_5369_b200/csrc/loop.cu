@@ -36,7 +36,7 @@ __global__ void k_loop_check(const double* __restrict__ d_norm, LoopState* st, c
   st->k = k;
   if (st->hist) st->hist[k] = rk;
   if (!fin) st->status = 2;
-  const bool done = !fin || k >= st->max || rk <= st->rtol * st->r0;
+  const bool done = !fin || k >= st->max || (st->rtol >= 0.0 && rk <= st->rtol * st->r0);  // rtol < 0: no test
   cudaGraphSetConditional(h, done ? 0u : 1u);
 }
 

@@ -99,3 +99,21 @@ def test_nonfinite_initial_residual(mode):
     df = S.from_numpy(f)
     k, _ = S.solve(du, df, 0.0, 1)
     assert k == 1
+
+
+@pytest.mark.parametrize("host", [False, True], ids=["device", "host"])
+def test_negative_rtol_runs_exactly_max_cycles(host):
+    """rtol < 0 switches the residual test off (mg.h): a solve from the exact solution
+    (u = f = 0, r0 = 0) runs every requested cycle, while rtol = 0 stops after one
+    (r1 = 0 <= 0 * r0).  The bench relies on it: W1 (f = 0) decays ~10x per cycle and
+    reaches an exact zero after a few hundred cycles.  NaN rtol is rejected."""
+    import paper_1406_5369_b200 as mgb
+    flags = mgb.FLAG_HOST_LOOP if host else 0
+    S, _ = make(3, (32, 32, 32), smoother="rbgs", flags=flags)
+    u, f = S.empty(), S.empty()
+    k, hist = S.solve(u, f, 0.0, 7)
+    assert k == 1 and hist[0] == 0.0 and hist[1] == 0.0
+    k, hist = S.solve(u, f, -1.0, 7)
+    assert k == 7 and len(hist) == 8 and all(h == 0.0 for h in hist)
+    with pytest.raises(mgb.MGError):
+        S.solve(u, f, float("nan"), 3)
