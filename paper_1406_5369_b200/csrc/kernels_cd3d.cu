@@ -218,7 +218,7 @@ template <typename T, bool NORM>
 static void grid_of(const Geom& g, int& tiles_x, int& ntiles, int& zc, int& nitems, int& nb) {
   tiles_x = (g.nx + G<T>::TX - 1) / G<T>::TX;
   ntiles = tiles_x * ((g.ny + TY - 1) / TY);
-  const int resident = resident_ctas((const void*)k_cd_jacobi3d<T, NORM>, NT, G<T>::SMEM) * sm_count();
+  const int resident = resident_ctas((const void*)k_cd_jacobi3d<T, NORM>, NT, G<T>::SMEM);  // whole GPU
   int nch = resident / ntiles;
   if (nch < 1) nch = 1;
   if (nch > g.nz / 4) nch = g.nz / 4 > 0 ? g.nz / 4 : 1;
