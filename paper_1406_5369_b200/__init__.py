@@ -316,6 +316,34 @@ class Solver:
     def _p(t):
         return ctypes.c_void_p(t.data_ptr())
 
+    def _dev(self, t, level=0, what="array"):
+        """Device pointer of a caller array after checking what the C ABI cannot: a CUDA tensor on
+        the solver's device, the solver's dtype, contiguous, of the level's layout (mg.h) — a raw
+        pointer to anything else would be read and written out of bounds."""
+        torch = _torch()
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{what}: expected a torch.Tensor, got {type(t).__name__}")
+        if t.device.type != "cuda" or (t.device.index or 0) != self.cfg.device:
+            raise ValueError(f"{what}: expected a tensor on cuda:{self.cfg.device}, got {t.device}")
+        if t.dtype != self.torch_dtype:
+            raise TypeError(f"{what}: expected dtype {self.torch_dtype}, got {t.dtype}")
+        want = self.shape if level == 0 else self.level_shape(level)
+        if tuple(t.shape) != tuple(want):
+            raise ValueError(f"{what}: expected shape {tuple(want)} (level {level} layout), got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what}: expected a contiguous tensor")
+        return ctypes.c_void_p(t.data_ptr())
+
+    def _host(self, t, what="host array"):
+        """Host pointer of a level-0 host array (dense layout, the solver's dtype)."""
+        torch = _torch()
+        if not isinstance(t, torch.Tensor) or t.device.type != "cpu":
+            raise TypeError(f"{what}: expected a CPU torch.Tensor")
+        if t.dtype != self.torch_dtype or tuple(t.shape) != tuple(self.shape) or not t.is_contiguous():
+            raise ValueError(f"{what}: expected a contiguous {self.torch_dtype} tensor of shape {tuple(self.shape)}, "
+                             f"got {t.dtype} {tuple(t.shape)}")
+        return t.data_ptr()
+
     # ---- layout
     @property
     def shape(self):
@@ -367,25 +395,26 @@ class Solver:
 
     # ---- the method
     def vcycle(self, u, f, stream=None):
-        self._chk(self.lib.mg_vcycle(self.h, self._p(u), self._p(f), self._stream(stream)))
+        self._chk(self.lib.mg_vcycle(self.h, self._dev(u, 0, "u"), self._dev(f, 0, "f"), self._stream(stream)))
 
     def residual_norm(self, u, f, stream=None):
         out = ctypes.c_double()
-        self._chk(self.lib.mg_residual_norm(self.h, self._p(u), self._p(f), ctypes.byref(out), self._stream(stream)))
+        self._chk(self.lib.mg_residual_norm(self.h, self._dev(u, 0, "u"), self._dev(f, 0, "f"), ctypes.byref(out),
+                                            self._stream(stream)))
         return out.value
 
     def solve(self, u, f, rtol, max_cycles, stream=None):
         hist = (ctypes.c_double * (max_cycles + 1))()
         k = ctypes.c_int32()
-        self._chk(self.lib.mg_solve(self.h, self._p(u), self._p(f), float(rtol), int(max_cycles), ctypes.byref(k),
+        self._chk(self.lib.mg_solve(self.h, self._dev(u, 0, "u"), self._dev(f, 0, "f"), float(rtol), int(max_cycles), ctypes.byref(k),
                                     hist, self._stream(stream)))
         return k.value, list(hist)[: k.value + 1]
 
     def vcycle_host(self, u_host, f_host, ncycles=1, stream=None):
         """End-to-end through the C ABI with host (pinned) tensors; returns the residual norm."""
         out = ctypes.c_double()
-        self._chk(self.lib.mg_vcycle_host(self.h, ctypes.c_void_p(u_host.data_ptr()),
-                                          ctypes.c_void_p(f_host.data_ptr()), int(ncycles), ctypes.byref(out),
+        self._chk(self.lib.mg_vcycle_host(self.h, ctypes.c_void_p(self._host(u_host, "u_host")),
+                                          ctypes.c_void_p(self._host(f_host, "f_host")), int(ncycles), ctypes.byref(out),
                                           self._stream(stream)))
         return out.value
 
@@ -393,7 +422,9 @@ class Solver:
         """Pipelined end-to-end over independent problems held in host (pinned) tensors:
         lists u_in, u_out, f_in of equal length; returns the residual norm of each problem."""
         n = len(u_in)
-        arr = lambda ts: (ctypes.c_void_p * n)(*[t.data_ptr() for t in ts])
+        if not (len(u_out) == len(f_in) == n):
+            raise ValueError("u_in, u_out and f_in must have equal lengths")
+        arr = lambda ts: (ctypes.c_void_p * n)(*[self._host(t) for t in ts])
         norms = (ctypes.c_double * n)()
         self._chk(self.lib.mg_vcycle_host_batch(self.h, arr(u_in), arr(u_out), arr(f_in), n, int(ncycles), norms,
                                                 self._stream(stream)))
@@ -401,28 +432,34 @@ class Solver:
 
     # ---- per-operation entry points
     def op_smooth(self, level, u_in, f, u_out, stream=None):
-        self._chk(self.lib.mg_op_smooth(self.h, level, self._p(u_in), self._p(f), self._p(u_out),
+        self._chk(self.lib.mg_op_smooth(self.h, level, self._dev(u_in, level, "u_in"), self._dev(f, level, "f"),
+                                        self._dev(u_out, level, "u_out"),
                                         self._stream(stream)))
 
     def op_residual(self, level, u, f, r, stream=None):
-        self._chk(self.lib.mg_op_residual(self.h, level, self._p(u), self._p(f), self._p(r), self._stream(stream)))
+        self._chk(self.lib.mg_op_residual(self.h, level, self._dev(u, level, "u"), self._dev(f, level, "f"),
+                                          self._dev(r, level, "r"), self._stream(stream)))
 
     def op_restrict(self, level, r, fc, stream=None):
-        self._chk(self.lib.mg_op_restrict(self.h, level, self._p(r), self._p(fc), self._stream(stream)))
+        self._chk(self.lib.mg_op_restrict(self.h, level, self._dev(r, level, "r"), self._dev(fc, level + 1, "fc"),
+                                          self._stream(stream)))
 
     def op_prolong_correct(self, level, e, u, stream=None):
-        self._chk(self.lib.mg_op_prolong_correct(self.h, level, self._p(e), self._p(u), self._stream(stream)))
+        self._chk(self.lib.mg_op_prolong_correct(self.h, level, self._dev(e, level + 1, "e"), self._dev(u, level, "u"),
+                                                 self._stream(stream)))
 
     def op_coarse_solve(self, f, e, stream=None):
-        self._chk(self.lib.mg_op_coarse_solve(self.h, self._p(f), self._p(e), self._stream(stream)))
+        self._chk(self.lib.mg_op_coarse_solve(self.h, self._dev(f, self.levels - 1, "f"), self._dev(e, self.levels - 1, "e"),
+                                              self._stream(stream)))
 
     def op_norm(self, level, u, f, stream=None):
         out = ctypes.c_double()
-        self._chk(self.lib.mg_op_norm(self.h, level, self._p(u), self._p(f), ctypes.byref(out), self._stream(stream)))
+        self._chk(self.lib.mg_op_norm(self.h, level, self._dev(u, level, "u"), self._dev(f, level, "f"), ctypes.byref(out),
+                                      self._stream(stream)))
         return out.value
 
     def workload_fill(self, dst, seed, lo=0.0, hi=1.0, stream=None):
-        self._chk(self.lib.mg_workload_fill(self.h, self._p(dst), ctypes.c_uint64(seed), float(lo), float(hi),
+        self._chk(self.lib.mg_workload_fill(self.h, self._dev(dst, 0, "dst"), ctypes.c_uint64(seed), float(lo), float(hi),
                                             self._stream(stream)))
 
     # ---- instrumentation

@@ -72,3 +72,28 @@ def test_bad_arguments_fail_without_poisoning():
     assert S.lib.mg_op_smooth(S.h, 0, S._p(du), bad, S._p(du), None) == 7
     S.vcycle(du, df)  # still usable
     assert np.array_equal(S.to_numpy(du), O.vcycle(u, f))
+
+
+def test_binding_rejects_bad_tensors():
+    """The Python binding checks what a raw pointer cannot carry (device, dtype, layout
+    shape, contiguity) before the C ABI sees it: no kernel ever touches a wrong-sized array."""
+    import torch
+    from test_gpu_parity import make
+    S, _ = make(3, (32, 32, 32), smoother="rbgs")
+    u, f = S.empty(), S.empty()
+    bad = [
+        (u.cpu(), TypeError, ValueError),                     # host tensor
+        (u.float(), TypeError, ValueError),                   # wrong dtype
+        (u[:, :, :-8], ValueError, TypeError),                # wrong shape
+        (u.transpose(0, 2).contiguous(), ValueError, TypeError),
+        (torch.empty_strided(u.shape, (1, u.shape[0], u.shape[0] * u.shape[1]), dtype=u.dtype, device=u.device),
+         ValueError, TypeError),                              # non-contiguous
+    ]
+    for t, *errs in bad:
+        with pytest.raises(tuple(errs)):
+            S.vcycle(t, f)
+        with pytest.raises(tuple(errs)):
+            S.solve(u, t, 0.0, 1)
+    with pytest.raises(ValueError):
+        S.op_restrict(0, S.empty(0), S.empty(0))  # fc must have the level-1 layout
+    S.vcycle(u, f)  # the solver is still usable
