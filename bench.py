@@ -203,11 +203,20 @@ def ncu_traffic(config, kernel):
 
 
 # --------------------------------------------------------------------- oracle (CPU) legs
+def _host_threads_for_oracle():
+    """torchrun exports OMP_NUM_THREADS=1 to every rank; the oracle leg runs on rank 0 alone and
+    is meant to use the host's cores (as at N=1), so lift that default before the oracle's
+    OpenMP runtime is first loaded (it reads the variable once, at load time)."""
+    if os.environ.get("TORCHELASTIC_RUN_ID") is not None and os.environ.get("OMP_NUM_THREADS") == "1":
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
+
+
 def oracle_step_time(cfgname, max_seconds=30.0):
     """Time the CPU oracle, as it stands, on one V-cycle + norm of the workload.
     Returns (seconds per step, unknowns per step, sample description, threads)."""
     import numpy as np
 
+    _host_threads_for_oracle()
     import oracle as orc
     from paper_1406_5369_b200 import workloads as wl
     if is_cd(cfgname):

@@ -48,3 +48,18 @@ def test_product_arm_contract():
     c = d["clocks"]
     assert c["sm_mhz"] > 0 and c["sm_max_mhz"] > 0 and isinstance(c["reasons"], list)
     assert "workload" in d["config"] and "l2" in d["config"]
+
+
+def test_reference_arm_under_torchrun():
+    """N > 1: rank 0 alone prints ONE line, the other rank exits 0; the oracle keeps the host's
+    cores although torchrun exports OMP_NUM_THREADS=1 to every rank."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29561", os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--config", "C1", "--gpus", "2", "--steps", "2", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+    assert d["cpu_baseline"]["cores"] == (os.cpu_count() or 1)
