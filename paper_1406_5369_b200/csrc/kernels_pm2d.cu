@@ -282,14 +282,22 @@ __global__ void __launch_bounds__(NT) k_jacobi2d(const __grid_constant__ CUtenso
 // corrected in registers as it arrives, in k_prolong2d's order (x, then y, then the add),
 // so the corrected iterate never makes an HBM round trip (prolongation fused into the
 // first post-smoothing pass; e read from L2/HBM once, a quarter word per node).
-template <typename T, int K, bool ZERO, bool NRM, bool CORR>
+// RR (K <= W-1): also r = f - A u^(K) of the pass's result (Alg. 1 line 4) and its full
+// weighting into the coarse f — k_resid_restrict2d's values and order — as one
+// more stage: r of row t-K from the stage-K window, its x-sums (lane shuffles), the last
+// three in registers, fine row 2J+1 completing coarse row J.  The march runs 2 rows further
+// on each side so r is exact on rows pa-1 .. pb; each coarse row is written by the chunk
+// holding its centre row 2J, each coarse column by the lane storing fine column 2I.
+template <typename T, int K, bool ZERO, bool NRM, bool CORR, bool RR = false>
 __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUtensorMap tm_u,
                                                    const __grid_constant__ CUtensorMap tm_f, Geom g, Coef<T> c,
                                                    T* __restrict__ uout, int nstrips, int nch,
-                                                   double* __restrict__ partial, const T* __restrict__ ec, Geom gc) {
+                                                   double* __restrict__ partial, const T* __restrict__ ec, Geom gc,
+                                                   T* __restrict__ fcout) {
   using V = VT<T>;
-  constexpr int W = G2<T>::W, TX = G2<T>::TX, RW = G2<T>::RW, SX = TX - 2 * W;
+  constexpr int W = G2<T>::W, TX = G2<T>::TX, RW = G2<T>::RW, SX = TX - 2 * W, NRC = W / 2;
   static_assert(K >= 2 && K <= W + 1, "overlap W columns per side");
+  static_assert(!RR || K <= W - 1, "r of the stored columns needs u^(K) one column further in");
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int R3 = 3;  // rows per box = the window period: a row's window slots are static
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
       in[j] = ox + j >= 1 && ox + j <= g.nx - 1;
       any = any || in[j];
     }
-    const int ts = pa - K + 1, te = pb + K - 2;  // stage-1 rows (= iterations)
+    const int ts = pa - K + 1 - (RR ? 2 : 0), te = pb + K - 2 + (RR ? 2 : 0);  // stage-1 rows (= iterations)
     R.t0 = ts;
     R.x = x0 - W;
     const int nsteps = (te - ts) / R3 + 1;
@@ -378,6 +386,11 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
     V S[K + 1][3];
     T e0[3];
     V Fw[3];
+    V Fold;                      // RR with K = 3: f of row t-3 (its window slot is reused by row t)
+    T ty1[NRC], ty2[NRC];        // RR: x-sums of the two previous residual rows
+#pragma unroll
+    for (int i = 0; i < NRC; i++) ty1[i] = ty2[i] = (T)0;
+    const T two = (T)2, scale = (T)(1.0 / 16.0);
     R.wait(-1);
     S[0][0] = urow(R.U(-1) + 1 * RW, e0[0]);  // row ts-1
     S[0][1] = urow(R.U(-1) + 2 * RW, e0[1]);  // row ts
@@ -390,6 +403,7 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
       constexpr int PH = decltype(PHc)::value;
       S[0][(PH + 2) % 3] = urow(ur, e0[(PH + 2) % 3]);  // stage 0, row t+1
       if (CORR) correct(S[0][(PH + 2) % 3], e0[(PH + 2) % 3], t + 1);
+      if (RR && K == 3) Fold = Fw[(PH + 1) % 3];        // f, row t-3
       Fw[(PH + 1) % 3] = ld_vec(fr + vo);               // f, row t
 #pragma unroll
       for (int k = 1; k <= K; k++) {
@@ -419,6 +433,44 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
       }
       const int ro = t - K + 1;  // the stage-K row of this iteration
       if (stores && any && ro >= pa && ro < pb) store_vec(uout + (long long)ro * g.pstride, ox, in, S[K][(PH - K + 8) % 3]);
+      if constexpr (RR) {  // residual of row t-K from stage-K rows t-K-1 .. t-K+1, restriction
+        constexpr int s0 = (PH - K + 1 + 9) % 3, sm = (PH - K + 9) % 3, sp = (PH - K + 2 + 9) % 3;
+        const V& P0 = S[K][s0];
+        const V& Fr = K == 3 ? Fold : Fw[(PH + 3 - K + 1) % 3];
+        const int rg = t - K + g.p_glob0;
+        const bool rin = rg >= 1 && rg <= g.nz - 1;
+        const T l0 = __shfl_up_sync(FULL, P0.v[W - 1], 1), r0 = __shfl_down_sync(FULL, P0.v[0], 1);
+        V rv;
+#pragma unroll
+        for (int j = 0; j < W; j++) {
+          const T l = j == 0 ? l0 : P0.v[j > 0 ? j - 1 : 0];
+          const T r = j == W - 1 ? r0 : P0.v[j < W - 1 ? j + 1 : 0];
+          rv.v[j] = selv(rin && in[j], sub(Fr.v[j], A2(c, P0.v[j], l, r, S[K][sm].v[j], S[K][sp].v[j])), (T)0);
+        }
+        const T rl = __shfl_up_sync(FULL, rv.v[W - 1], 1);  // r(ox - 1): exact for lanes 1..30
+        T tx[NRC];
+#pragma unroll
+        for (int i = 0; i < NRC; i++) {
+          const T left = i == 0 ? rl : rv.v[i > 0 ? 2 * i - 1 : 0];
+          tx[i] = add(add(left, rv.v[2 * i + 1]), mul(two, rv.v[2 * i]));
+        }
+        if ((rg & 1) == 1) {  // fine row 2J+1 completes coarse row J
+          const int J = (rg - 1) >> 1, cr = 2 * J - g.p_glob0;  // the centre row, local
+          if (stores && cr >= pa && cr < pb && J >= 1 && J <= gc.nz - 1) {
+            T* crow = fcout + (long long)(J - gc.p_glob0) * gc.pstride;
+#pragma unroll
+            for (int i = 0; i < NRC; i++) {
+              const int I = (ox >> 1) + i;
+              if (I >= 1 && I <= gc.nx - 1) crow[I] = mul(add(add(ty2[i], tx[i]), mul(two, ty1[i])), scale);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < NRC; i++) {
+          ty2[i] = ty1[i];
+          ty1[i] = tx[i];
+        }
+      }
     };
     // rows past te (in the last box) compute values that are never stored
     for (int b = 0; b < nsteps; b++) {
@@ -835,21 +887,36 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
 }
 
 template <typename T>
+bool rr_fusable(int K) {
+  return K >= 2 && K <= G2<T>::W - 1;
+}
+
+template <typename T>
 cudaError_t launch_jacobi_k(const Geom& g, const Coef<T>& c, int K, const T* uin, const T* f, T* uout, bool zero_in,
-                            cudaStream_t st, double* partial, int* npartial, const T* e, const Geom* gc) {
+                            cudaStream_t st, double* partial, int* npartial, const T* e, const Geom* gc, T* fc) {
   CUtensorMap tu, tf;
   if (!encode2d<T>(&tu, uin ? uin : f, g, 3) || !encode2d<T>(&tf, f, g, 3)) return cudaErrorInvalidValue;
-  if ((partial && zero_in) || (e && (zero_in || partial || !gc))) return cudaErrorInvalidValue;
+  if ((partial && zero_in) || (e && (zero_in || partial || !gc)) || (fc && (e || !gc || !rr_fusable<T>(K))))
+    return cudaErrorInvalidValue;
   const int ns = kstrips<T>(g);
   const int smem = WRing<T, 3>::SMEM;
   const Geom gcv = gc ? *gc : g;
   int nch, nb;
   auto go = [&](auto kernel) {
     split(ns, g.p_hi - g.p_lo, resident_warps(kernel, smem), nch, nb);
-    kernel<<<nb, NT, smem, st>>>(tu, tf, g, c, uout, ns, nch, partial, e, gcv);
+    kernel<<<nb, NT, smem, st>>>(tu, tf, g, c, uout, ns, nch, partial, e, gcv, fc);
   };
   auto goK = [&](auto Kc) {
     constexpr int KK = decltype(Kc)::value;
+    if constexpr (KK <= G2<T>::W - 1) {  // RR variants (FP32: K = 2, 3)
+      if (fc) {
+        if (partial)
+          go(k_jacobi2d_k<T, KK, false, true, false, true>);
+        else
+          zero_in ? go(k_jacobi2d_k<T, KK, true, false, false, true>) : go(k_jacobi2d_k<T, KK, false, false, false, true>);
+        return;
+      }
+    }
     if (partial)
       go(k_jacobi2d_k<T, KK, false, true, false>);
     else if (e)
@@ -880,6 +947,16 @@ int sweep_partials(const Geom& g, bool rbgs) {
     int nb2;
     split(kstrips<T>(g), g.p_hi - g.p_lo, resident_warps(k_jacobi2d_k<T, 2, false, true, false>, WRing<T, 3>::SMEM), nch,
           nb2);
+    nb = nb2 > nb ? nb2 : nb;
+    if constexpr (G2<T>::W >= 3) {  // the head with the fused residual + restriction
+      split(kstrips<T>(g), g.p_hi - g.p_lo,
+            resident_warps(k_jacobi2d_k<T, 2, false, true, false, true>, WRing<T, 3>::SMEM), nch, nb2);
+      nb = nb2 > nb ? nb2 : nb;
+    }
+    if constexpr (G2<T>::W >= 4) {
+      split(kstrips<T>(g), g.p_hi - g.p_lo,
+            resident_warps(k_jacobi2d_k<T, 3, false, true, false, true>, WRing<T, 3>::SMEM), nch, nb2);
+    }
     nb = nb2 > nb ? nb2 : nb;
     if constexpr (G2<T>::W >= 3) {
       split(kstrips<T>(g), g.p_hi - g.p_lo, resident_warps(k_jacobi2d_k<T, 3, false, true, false>, WRing<T, 3>::SMEM), nch,
@@ -939,9 +1016,12 @@ template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool
 template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
                                          bool, cudaStream_t, double*, int*);
 template cudaError_t launch_jacobi_k<double>(const Geom&, const Coef<double>&, int, const double*, const double*,
-                                             double*, bool, cudaStream_t, double*, int*, const double*, const Geom*);
+                                             double*, bool, cudaStream_t, double*, int*, const double*, const Geom*,
+                                             double*);
 template cudaError_t launch_jacobi_k<float>(const Geom&, const Coef<float>&, int, const float*, const float*, float*,
-                                            bool, cudaStream_t, double*, int*, const float*, const Geom*);
+                                            bool, cudaStream_t, double*, int*, const float*, const Geom*, float*);
+template bool rr_fusable<double>(int);
+template bool rr_fusable<float>(int);
 template int sweep_partials<double>(const Geom&, bool);
 template int sweep_partials<float>(const Geom&, bool);
 template cudaError_t launch_norm<double>(const Geom&, const Coef<double>&, const double*, const double*, double*,

@@ -56,6 +56,7 @@ enum Kind {
   K_PROLONG_JACOBI_K,
   K_CD_JACOBI_K,
   K_CD_JACOBI_K_NORM,
+  K_SWEEP_RR_K,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -68,7 +69,7 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "cd_fas_rhs",    "cd_prolong",    "cd_norm_partial", "cd_residual",
                                        "cd_copy",       "cd_tail",       "gs_lex_plane",  "jacobi_pm_xK",
                                        "jacobi_pm_xK+norm", "prolong+jacobi_xK",
-                                       "cd_jacobi_xK",  "cd_jacobi_xK+norm"};
+                                       "cd_jacobi_xK",  "cd_jacobi_xK+norm", "jacobi_xK+resid_restrict"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -540,7 +541,9 @@ struct Exec {
     return kfusable(l) ? (n + kmax - 1) / kmax : n;
   }
 
-  mg_status smooth_n(int l, T*& cur, T*& other, const T* f, int n, bool zero_in) {
+  // rr_fc != nullptr: the LAST pass also writes the restriction of its result's residual
+  // into rr_fc (level l+1) when it can (rr_last(l, n)); the caller skips its own then
+  mg_status smooth_n(int l, T*& cur, T*& other, const T* f, int n, bool zero_in, T* rr_fc = nullptr) {
     const Level& L = s->lv[l];
     const int p = passes(l, n);
     mg_status r = MG_OK;
@@ -550,9 +553,13 @@ struct Exec {
         T* in = cur;
         T* out = other;
         const bool z = zero_in && k == 0;
-        if ((r = launch(s, st, K_SWEEP_JACOBI_K, l, (z ? 2 : 3) * w(l), [&] {
-               return pm2::launch_jacobi_k<T>(L.g, coef(l), K, z ? nullptr : in, f, out, z, st);
-             })) != MG_OK)
+        T* fcl = (rr_fc && k + K == n) ? rr_fc : nullptr;
+        const Geom gcg = s->lv[l + (l + 1 < s->L ? 1 : 0)].g;
+        if ((r = launch(s, st, fcl ? K_SWEEP_RR_K : K_SWEEP_JACOBI_K, l,
+                        (z ? 2 : 3) * w(l) + (fcl ? w(l + 1) : 0.0), [&] {
+                          return pm2::launch_jacobi_k<T>(L.g, coef(l), K, z ? nullptr : in, f, out, z, st, nullptr,
+                                                         nullptr, nullptr, fcl ? &gcg : nullptr, fcl);
+                        })) != MG_OK)
           return r;
         std::swap(cur, other);
       } else if ((r = smooth(l, cur, other, f, zero_in && k == 0)) != MG_OK) {
@@ -613,8 +620,12 @@ struct Exec {
     T* t0 = (T*)L.t;
     const int hk = head_sweeps();
     if (hk > 1) {  // fused Jacobi passes: the head is the first pass, up to 3 sweeps
-      if ((r = launch(s, st, K_SWEEP_NORM_K, 0, 3 * w(0), [&] {
-             return pm2::launch_jacobi_k<T>(L.g, coef(0), hk, u0, f0, t0, false, st, s->d_partial, &np);
+      const bool rr = head_rr();  // ... and, running every pre-sweep, the level-0 restriction
+      T* fc = rr ? (T*)s->lv[1].f : nullptr;
+      const Geom gcg = s->lv[s->L > 1 ? 1 : 0].g;
+      if ((r = launch(s, st, K_SWEEP_NORM_K, 0, 3 * w(0) + (rr ? w(1) : 0.0), [&] {
+             return pm2::launch_jacobi_k<T>(L.g, coef(0), hk, u0, f0, t0, false, st, s->d_partial, &np, nullptr,
+                                            rr ? &gcg : nullptr, fc);
            })) != MG_OK)
         return r;
       return norm_finish(0, np, out_dev);
@@ -631,6 +642,14 @@ struct Exec {
     const int p = passes(l, n);
     return p > 0 ? n / p + (n % p ? 1 : 0) : 0;
   }
+  // the last of the passes of n pre-sweeps on level l carries the residual + restriction
+  bool rr_last(int l, int n) const {
+    if (!kfusable(l) || n < 2 || l + 1 >= s->L || s->lv[l + 1].dist || (s->pt.slab && l + 1 == s->pt.la)) return false;
+    const int p = passes(l, n);
+    return pm2::rr_fusable<T>(n / p);  // the last pass has n / p sweeps
+  }
+  // the solve's head carries the level-0 residual + restriction (it runs every pre-sweep)
+  bool head_rr() const { return kfusable(0) && head_sweeps() == s->cfg.nu1 && rr_last(0, s->cfg.nu1); }
   // level-0 pre-sweeps the head runs: the first fused pass, else one sweep
   int head_sweeps() const { return kfusable(0) ? first_k(0, s->cfg.nu1) : 1; }
 
@@ -676,17 +695,27 @@ struct Exec {
         const T* f = l == 0 ? f0 : (const T*)L.f;
         // V_H(0, ...): the zero guess is folded into the first sweep (bitwise identical)
         if (l > 0 && s->cfg.nu1 == 0 && (r = memset0(l, cur[l])) != MG_OK) return r;
+        T* fc = (T*)s->lv[l + 1].f;
+        bool rr_done = false;  // the residual + restriction rode on the last pre-smoothing pass
         {
           const int k0 = (after_head && l == 0) ? head_sweeps() : 0;
-          if ((r = smooth_n(l, cur[l], oth[l], f, s->cfg.nu1 - k0, l > 0 && k0 == 0)) != MG_OK) return r;
+          const int n = s->cfg.nu1 - k0;
+          if (k0 > 0 && n == 0) {
+            rr_done = head_rr();  // the head pass carried it
+          } else {
+            rr_done = rr_last(l, n);
+          }
+          if ((r = smooth_n(l, cur[l], oth[l], f, n, l > 0 && k0 == 0, (rr_done && n > 0) ? fc : nullptr)) != MG_OK)
+            return r;
         }
         T* res = (T*)L.r;
-        T* fc = (T*)s->lv[l + 1].f;
         const Level& C = s->lv[l + 1];
         // coarse planes this rank produces: all of a distributed or single-GPU level, its own
         // chunk of the first agglomerated level
         const Geom gcw = (s->pt.slab && l + 1 == s->pt.la) ? C.gown : C.g;
-        if (pm(l)) {
+        if (rr_done) {
+          // done by the pass
+        } else if (pm(l)) {
           if ((r = exchange(l, cur[l], 2)) != MG_OK) return r;
           const T* uc = cur[l];
           if ((r = launch(s, st, K_RESID_RESTRICT, l, 2 * w(l) + w(l + 1), [&] {
