@@ -16,7 +16,9 @@
  *    [planes][rows][pitch] (x fastest), see mg_layout / mg_level_layout.
  *    3D: planes = z nodes, rows = y nodes; 2D: planes = y nodes, rows = 1.
  *    Node (i,j,k) includes the boundary: i = 0..nx, etc. (cells per axis nx).
- *    Padding elements (x > nx) are never read or written.
+ *    Padding elements (x > nx) of caller arrays are never written; a kernel may
+ *    read them as part of a whole 16-byte vector, and their values never affect
+ *    a result (no NaN/Inf check, no arithmetic that reaches a stored node).
  *  - Caller-owned buffers must stay alive until the stream work completes.
  *    `u` and `f` must not alias.  The library never writes boundary nodes of
  *    the caller's `u` (they hold the Dirichlet data).
