@@ -24,10 +24,10 @@ def _run_ranks(P, case, cycles, u, f):
     group = mgb.LoopbackGroup(P)
     solvers = []
     for p in range(P):
-        S = mgb.Solver(case["dim"], tuple(c + 1 for c in case["cells"]), smoother=case.get("smoother", "rbgs"),
-                       omega=case.get("omega"), nu1=case.get("nu1", 2), nu2=case.get("nu2", 2),
-                       dtype=case.get("dtype", "f64"), rank=p, nranks=P, loopback=group,
-                       flags=mgb.FLAG_NO_GRAPH, pm_min_nx=16)
+        S = mgb.Solver(case["dim"], tuple(c + 1 for c in case["cells"]), levels=case.get("levels", 0),
+                       smoother=case.get("smoother", "rbgs"), omega=case.get("omega"), nu1=case.get("nu1", 2),
+                       nu2=case.get("nu2", 2), coarse=case.get("coarse", "direct"), dtype=case.get("dtype", "f64"),
+                       rank=p, nranks=P, loopback=group, flags=mgb.FLAG_NO_GRAPH, pm_min_nx=16)
         solvers.append(S)
     streams = [torch.cuda.Stream() for _ in range(P)]
     dus = [S.from_numpy(u) for S in solvers]
@@ -129,3 +129,40 @@ def test_slab_loopback_solve_and_p8():
     for S in solvers:
         S.close()
     group.close()
+
+
+def _random_slab_cases(n, seed=31):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        dim = int(rng.choice([2, 3]))
+        P = int(rng.choice([2, 4]))
+        levels = int(rng.integers(3, 5))
+        m = 1 << (levels - 1)
+        hi = 48 if dim == 3 else 320
+        cells = [int(m * rng.integers(2, hi // m + 1)) for _ in range(dim)]
+        cells[-1] = P * m * int(rng.integers(2, 5))  # slab axis: >= 8 (even) planes per rank on level 0
+        unknowns = int(np.prod([c // m - 1 for c in cells]))
+        out.append(dict(P=P, dim=dim, cells=tuple(cells), levels=levels, smoother=str(rng.choice(["rbgs", "jacobi"])),
+                        nu1=int(rng.integers(1, 4)), nu2=int(rng.integers(1, 4)),
+                        dtype=str(rng.choice(["f64", "f32"])), coarse="direct" if unknowns <= 1024 else "sweeps"))
+    return out
+
+
+@pytest.mark.parametrize("case", _random_slab_cases(30),
+                         ids=lambda c: "P{P}-{dim}d-{c}-L{levels}-{smoother}-nu{nu1}{nu2}-{dtype}".format(
+                             c="x".join(map(str, c["cells"])), **c))
+def test_slab_loopback_random_bitwise(case):
+    """Seeded random slab decompositions: ragged in-plane extents, both smoothers, odd and even
+    sweep counts, FP32/FP64 — the gathered iterate equals the single-domain oracle bitwise."""
+    case = dict(case)
+    P = case.pop("P")
+    S0, O = make(case["dim"], case["cells"], case["levels"], case["smoother"], nu1=case["nu1"], nu2=case["nu2"],
+                 dtype=case["dtype"], coarse=case["coarse"])
+    u, f = wl.workload("W4", case["dim"], case["cells"], seed=9, dtype=S0.np_dtype)
+    got, norms, dist = _run_ranks(P, case, 2, u, f)
+    assert dist
+    uo = u.copy()
+    for _ in range(2):
+        O.vcycle_inplace(uo, f)
+    assert np.array_equal(got, uo)
