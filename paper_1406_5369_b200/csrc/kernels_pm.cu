@@ -350,28 +350,27 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
 
     // RB ring threads: warps 0 / 1 the red nodes of rows y0-1 / y0+TY (NR per lane), warp 2
     // lanes [0, RCOL) column x0-1 and [RCOL, 2 RCOL) column x0+TX (one each)
-    const bool ring_row = RB && ry < 2;
-    const bool ring_col = RB && ry == 2 && lane < 2 * RCOL;
+    // (one red ring node per lane and plane: FP32 lanes hold NR = 2 red nodes per ring row, so
+    // 2 NR warps share the two ring rows — warp w: row (w & 1), node m = w >> 1 — keeping every
+    // warp's extra work at one relaxation; the plane barrier waits for the slowest warp)
+    constexpr int RWARPS = 2 * NR;
+    const bool ring_row = RB && ry < RWARPS;
+    const bool ring_col = RB && ry == RWARPS && lane < 2 * RCOL;
+    const int mring = ring_row ? (ry >> 1) : 0;
     auto ring_pos = [&](int pgl, int m, int& x, int& y) {
-      if (ry < 2) {
-        y = ry == 0 ? y0 - 1 : y0 + TY;
+      if (ry < RWARPS) {
+        y = (ry & 1) == 0 ? y0 - 1 : y0 + TY;
         x = x0 + W * lane + 2 * m + ((y + pgl) & 1);  // x0 even
       } else {
         x = lane < RCOL ? x0 - 1 : x0 + TX;
         y = y0 + 2 * (lane % RCOL) + ((x + y0 + pgl) & 1);
       }
     };
-    T rzm[NR];  // ring thread: u(p-1) at its plane-p ring nodes
-#pragma unroll
-    for (int m = 0; m < NR; m++) rzm[m] = (T)0;
+    T rzm = (T)0;  // ring thread: u(p-1) at its plane-p ring node
     if (ring_row || ring_col) {
-#pragma unroll
-      for (int m = 0; m < NR; m++) {
-        if (ring_col && m > 0) break;
-        int x, y;
-        ring_pos(pa - 1 + pg0, m, x, y);
-        rzm[m] = su(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
-      }
+      int x, y;
+      ring_pos(pa - 1 + pg0, mring, x, y);
+      rzm = su(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
     }
     __syncthreads();  // step qlo lives on in registers only: refill its slot
     if (tid == 0 && qlo + G::NS <= qlast) {
@@ -456,21 +455,17 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
           red_stage(std::integral_constant<int, 1>());
         else
           red_stage(std::integral_constant<int, 0>());
-        if (ring_row || ring_col) {  // red ring nodes of plane p
-#pragma unroll
-          for (int m = 0; m < NR; m++) {
-            if (ring_col && m > 0) break;
-            int x, y;
-            ring_pos(pgl, m, x, y);
-            const int rb = (y - y0 + 2) * BX + (x - x0 + HX);
-            const T ctr = su(U0, rb);
-            const T v = relax(c, ctr, su(U0, rb - 1), su(U0, rb + 1), su(U0, rb - BX), su(U0, rb + BX), rzm[m],
-                              su(Up, rb), F0[(y - y0 + 1) * BX + (x - x0 + HX)]);
-            const bool ok = pl_in && x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1;
-            PR[(y - y0 + 1) * PX + (x - x0 + HX)] = ok ? v : ctr;
-            ring_pos(pgl + 1, m, x, y);  // next plane's node: its z-neighbour below is u(p)
-            rzm[m] = su(U0, (y - y0 + 2) * BX + (x - x0 + HX));
-          }
+        if (ring_row || ring_col) {  // the red ring node of plane p
+          int x, y;
+          ring_pos(pgl, mring, x, y);
+          const int rb = (y - y0 + 2) * BX + (x - x0 + HX);
+          const T ctr = su(U0, rb);
+          const T v = relax(c, ctr, su(U0, rb - 1), su(U0, rb + 1), su(U0, rb - BX), su(U0, rb + BX), rzm, su(Up, rb),
+                            F0[(y - y0 + 1) * BX + (x - x0 + HX)]);
+          const bool ok = pl_in && x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1;
+          PR[(y - y0 + 1) * PX + (x - x0 + HX)] = ok ? v : ctr;
+          ring_pos(pgl + 1, mring, x, y);  // next plane's node: its z-neighbour below is u(p)
+          rzm = su(U0, (y - y0 + 2) * BX + (x - x0 + HX));
         }
         __syncthreads();
         // ONESYNC: every thread has finished plane p-2's black update: step p-2 is free.
