@@ -411,7 +411,8 @@ def run_mg(args):
     array_bytes = S.shape[0] * S.shape[1] * S.shape[2] * esz * (2 if cd else 1)
     if array_bytes * 3 < 126e6:  # L2-resident sizes
         roofline["note"] = ("L2-resident grid (three arrays < 126 MB L2): the HBM fraction is not meaningful; "
-                            "the step is bound by launch and barrier latency")
+                            "the step is bound by launch and barrier latency. L2 traffic per kernel "
+                            "(lts__t_bytes, ncu): profiles/r1e_C2_l2_traffic.txt")
     B = cd_model_bytes_per_step(S, esz) if cd else model_bytes_per_step(S, esz)
     breakdown = sorted(({"kernel": r["name"], "ms_per_step": r["ms"] / nprof, "launches_per_step": r["count"] / nprof,
                          "GBps": (r["bytes"] * r["count"] / (r["ms"] * 1e-3) / 1e9) if r["ms"] else None}
