@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
         const T r = j == W - 1 ? er : u0.v[j < W - 1 ? j + 1 : 0];
         const double rr = (double)sub(fv.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
-        if (in[j]) nsum = __dadd_rn(nsum, __dmul_rn(rr, rr));
+        if (in[j]) nsum = acc_sq_d<T>(nsum, rr);
       }
     };
 
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
                 const T r = j == W - 1 ? oedge : u0.v[j < W - 1 ? j + 1 : 0];
                 const double rr =
                     (double)sub(fcur.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
-                if (in[j]) nsum = __dadd_rn(nsum, __dmul_rn(rr, rr));
+                if (in[j]) nsum = acc_sq_d<T>(nsum, rr);
               }
             }
           }
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
             // relax() written out: the residual doubles as the red node's norm term
             const T res = sub(fcur.v[j], apply_A(c, ctr, l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
             const T v = add(ctr, mul(c.wd, res));
-            if (NRM && nrm_here && in[j]) nsum = __dadd_rn(nsum, __dmul_rn((double)res, (double)res));
+            if (NRM && nrm_here && in[j]) nsum = acc_sq<T>(nsum, res);
             const T prv = (pl_in && in[j]) ? v : ctr;
             pv.v[j] = prv;
             pr0[m] = prv;
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
             // relax() written out: with NRM the residual is also the norm term of the input
             const T res = sub(fv.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
             const T v = add(u0.v[j], mul(c.wd, res));
-            if (NRM && in[j]) nsum = __dadd_rn(nsum, __dmul_rn((double)res, (double)res));
+            if (NRM && in[j]) nsum = acc_sq<T>(nsum, res);
             o.v[j] = in[j] ? v : u0.v[j];
           }
           store_vec(orow + (long long)p * g.pstride, ox, in, o);

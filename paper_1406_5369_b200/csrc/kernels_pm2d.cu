@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(NT) k_jacobi2d(const __grid_constant__ CUtenso
           const T l = j == 0 ? l0 : u0.v[j > 0 ? j - 1 : 0];
           const T r = j == W - 1 ? r0 : u0.v[j < W - 1 ? j + 1 : 0];
           const T rr = sub(fv.v[j], A2(c, u0.v[j], l, r, um.v[j], up.v[j]));
-          if ((MODE == 2 || NRM) && in[j]) nsum = __dadd_rn(nsum, __dmul_rn((double)rr, (double)rr));
+          if ((MODE == 2 || NRM) && in[j]) nsum = acc_sq<T>(nsum, rr);
           o.v[j] = in[j] ? add(u0.v[j], mul(c.wd, rr)) : u0.v[j];
         }
         if (MODE != 2 && okv) store_vec(uout + (long long)p * g.pstride, ox, in, o);
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(NT) k_rbgs2d(const __grid_constant__ CUtensorM
             const T l = j == 0 ? Cl : C.v[j > 0 ? j - 1 : 0];
             const T r = j == W - 1 ? Cr : C.v[j < W - 1 ? j + 1 : 0];
             const T rr = sub(fv.v[j], A2(c, C.v[j], l, r, Bo.v[j], Dn.v[j]));
-            if (in[j]) nsum = __dadd_rn(nsum, __dmul_rn((double)rr, (double)rr));
+            if (in[j]) nsum = acc_sq<T>(nsum, rr);
           }
         }
         V prT = C;

@@ -24,6 +24,20 @@ __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, 
 __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+// nsum + r^2 in FP64.  r from FP32 arithmetic: r^2 is exact in double, so one FMA is bitwise
+// the rounded add of the exact product; FP64 r keeps the two roundings (dmul, dadd).
+template <typename T>
+__device__ __forceinline__ double acc_sq(double nsum, T r) {
+  const double d = (double)r;
+  if constexpr (sizeof(T) == 4) return __fma_rn(d, d, nsum);
+  else return __dadd_rn(nsum, __dmul_rn(d, d));
+}
+// ... where r is already the double of a value of the kernel's type T
+template <typename T>
+__device__ __forceinline__ double acc_sq_d(double nsum, double r) {
+  if constexpr (sizeof(T) == 4) return __fma_rn(r, r, nsum);
+  else return __dadd_rn(nsum, __dmul_rn(r, r));
+}
 // c ? a : b as one selp: both operands are computed, no branch around an expensive a
 __device__ __forceinline__ float selv(bool c, float a, float b) {
   float r;
