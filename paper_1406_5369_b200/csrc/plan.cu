@@ -81,18 +81,28 @@ static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
 template <class Fn>
 static mg_status launch(mg_solver* s, cudaStream_t st, Kind kind, int level, double bytes, Fn&& fn) {
   ProfRec rec{};
-  if (s->prof_on) {
+  bool prof = s->prof_on;
+  if (prof) {
     rec.kind = kind;
     rec.level = level;
     rec.bytes = bytes;
-    cudaEventCreate(&rec.a);
-    cudaEventCreate(&rec.b);
-    cudaEventRecord(rec.a, st);
+    if (cudaEventCreate(&rec.a) != cudaSuccess || cudaEventCreate(&rec.b) != cudaSuccess ||
+        cudaEventRecord(rec.a, st) != cudaSuccess) {  // instrumentation only: skip this record
+      if (rec.a) cudaEventDestroy(rec.a);
+      if (rec.b) cudaEventDestroy(rec.b);
+      cudaGetLastError();
+      prof = false;
+    }
   }
   cudaError_t e = fn();
-  if (s->prof_on) {
-    cudaEventRecord(rec.b, st);
-    s->prof.push_back(rec);
+  if (prof) {
+    if (cudaEventRecord(rec.b, st) == cudaSuccess) {
+      s->prof.push_back(rec);
+    } else {
+      cudaEventDestroy(rec.a);
+      cudaEventDestroy(rec.b);
+      cudaGetLastError();
+    }
   }
   if (kind != K_MEMSET && kind != K_HALO && kind != K_ALLGATHER) s->launch_counter++;  // our kernels only
   if (e != cudaSuccess) return cuda_fail(s, e, kKindName[kind]);
