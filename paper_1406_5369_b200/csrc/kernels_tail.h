@@ -14,6 +14,7 @@ struct TailParams {
   int sweeps;      // coarsest: 1 = ncoarse sweeps, 0 = direct
   int ncoarse;
   int zero_first;  // the top tail level starts from a zero guess (always, unless it is level 0)
+  int solo_from;   // levels >= solo_from run on CTA 0 alone (set by launch_tail)
   int m;           // coarsest unknowns (direct)
   double D_coarse;
   const double* chol;
