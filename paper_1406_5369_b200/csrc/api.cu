@@ -321,7 +321,7 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
       if ((st = part(2)) != MG_OK) return st;
       k++;
       double rk = 0.0;
-      if ((st = part(1)) != MG_OK || (st = read(&rk)) != MG_OK) return st;
+      if ((st = part(4)) != MG_OK || (st = read(&rk)) != MG_OK) return st;  // head w/o the boundary refresh
       if (history) history[k] = rk;
       if (!std::isfinite(rk)) {
         if (cycles) *cycles = k;

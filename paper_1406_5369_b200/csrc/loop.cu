@@ -95,7 +95,7 @@ static mg_status build_loop_graph(mg_solver* s, void* u, const void* f, cudaGrap
       cudaSuccess)
     return abort_capture(cuda_fail(s, e, "cudaStreamBeginCaptureToGraph"));
   mg_status rb = split ? plan_run_part(s, 2, u, f, bs) : plan_run_part(s, 0, u, f, bs);
-  if (rb == MG_OK) rb = split ? plan_run_part(s, 1, u, f, bs) : plan_run_part(s, 3, u, f, bs);
+  if (rb == MG_OK) rb = split ? plan_run_part(s, 4, u, f, bs) : plan_run_part(s, 3, u, f, bs);  // 4: no refresh
   if (rb == MG_OK) {
     k_loop_check<<<1, 1, 0, bs>>>(s->d_norm, s->d_loop, h);
     if ((e = cudaGetLastError()) != cudaSuccess) rb = cuda_fail(s, e, "k_loop_check");

@@ -620,8 +620,11 @@ struct Exec {
   }
 
   // head: cycle_start + the first level-0 sweep u0 -> t0 + ||f - A u0|| into out_dev
-  mg_status head(T* u0, const T* f0, double* out_dev) {
-    mg_status r = cycle_start(u0, f0);
+  // refresh = false: a later head of the same solve — the ping-pong partner's boundary and
+  // f's halo planes still hold what the first head wrote (no kernel writes boundary nodes,
+  // f is constant during the solve)
+  mg_status head(T* u0, const T* f0, double* out_dev, bool refresh = true) {
+    mg_status r = refresh ? cycle_start(u0, f0) : MG_OK;
     if (r != MG_OK) return r;
     if ((r = exchange(0, u0, s->cfg.smoother == MG_RBGS ? 2 : 1)) != MG_OK) return r;
     const Level& L = s->lv[0];
@@ -1184,7 +1187,8 @@ template <typename T>
 static mg_status cd_run_part_T(mg_solver* s, int part, T* u, const T* f, cudaStream_t st) {
   CdExec<T> x{s, st};
   switch (part) {
-    case 1: return x.head(u, f, s->d_norm);
+    case 1:
+    case 4: return x.head(u, f, s->d_norm);
     case 2: return x.vcycle(u, f, true, true);
     case 3: return x.norm(0, u, f, s->d_norm);
     default: return x.vcycle(u, f);
@@ -1197,11 +1201,12 @@ static mg_status cd_run_part(mg_solver* s, int part, void* u, const void* f, cud
 
 // ---------------------------------------------------------------- entry points
 // part: 0 whole cycle, 1 head (first sweep + norm of the input into d_norm), 2 tail,
-// 3 norm of (u, f) into d_norm
+// 3 norm of (u, f) into d_norm, 4 head of a later cycle of the same solve (no refresh of the
+// ping-pong partner's boundary or of f's halo planes)
 template <typename T>
 static mg_status run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
   Exec<T> x{s, st};
-  if (part == 1) return x.head((T*)u, (const T*)f, s->d_norm);
+  if (part == 1 || part == 4) return x.head((T*)u, (const T*)f, s->d_norm, part == 1);
   if (part == 2) return x.tail((T*)u, (const T*)f);
   if (part == 3) return x.norm(0, (const T*)u, (const T*)f, s->d_norm);
   return x.vcycle((T*)u, (const T*)f);
@@ -1213,8 +1218,9 @@ mg_status plan_run_part(mg_solver* s, int part, void* u, const void* f, cudaStre
                          : s->esz == 8 ? run_part<double>(s, part, u, f, st) : run_part<float>(s, part, u, f, st);
   // launches of one cycle: the whole cycle, or head + tail of the pipelined split
   if (part == 0) s->launches_per_cycle = s->launch_counter;
-  if (part == 1) s->head_launches = s->launch_counter;
-  if (part == 2) s->launches_per_cycle = s->head_launches + s->launch_counter;
+  if (part == 1 || part == 4) s->head_launches = s->launch_counter;
+  if (part == 2) s->tail_launches = s->launch_counter;
+  if (part == 2 || part == 4) s->launches_per_cycle = s->head_launches + s->tail_launches;
   return r;
 }
 

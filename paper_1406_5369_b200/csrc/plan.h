@@ -105,7 +105,7 @@ struct mg_solver {
   int h_norms_cap = 0;
   // instrumentation
   int64_t launches_per_cycle = 0;
-  int64_t head_launches = 0;
+  int64_t head_launches = 0, tail_launches = 0;
   int64_t launch_counter = 0;
   bool prof_on = false;
   std::vector<mg::ProfRec> prof;
