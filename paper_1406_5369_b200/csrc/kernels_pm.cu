@@ -164,10 +164,7 @@ __device__ __forceinline__ void item_of(int k, int ntiles, int zc, int p_lo, int
 // coarse-grid correction applied to every u box in shared memory as it arrives, so
 // the corrected iterate never makes an HBM round trip (prolongation fused into the
 // first post-smoothing sweep).  Same separable order as k_prolong3d.
-// ESH: the x-neighbours outside the thread's vector (x = ox-1, ox+W) come from the
-// neighbouring lanes' registers by shuffle; only lanes 0 / 31 read them from shared memory
-// (1 wavefront per warp instead of 4 for a strided scalar).  Same values, same arithmetic.
-template <typename T, int MODE, bool ZERO, bool NRM = false, bool CORR = false, bool ESH = false>
+template <typename T, int MODE, bool ZERO, bool NRM = false, bool CORR = false>
 __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     k_sweep3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f, Geom g,
               Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems,
@@ -205,20 +202,6 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
   const int po = (ry + 1) * PX + W * lane + HX;  // PR offset of (ox, oy)
   uint32_t seq = 0;
   double nsum = 0.0;  // MODE 2 / NRM: this thread's sum of r^2
-  // row value at x = ox-1 / ox+W: smem box U (offset bo) or, with ESH, the neighbour lane's
-  // register copy `v` of the same row (v.v[W-1] of lane-1 / v.v[0] of lane+1)
-  auto edge_l = [&](const T* U, T vlast) -> T {
-    if constexpr (!ESH) return su(U, bo - 1);
-    T e = __shfl_up_sync(0xffffffffu, vlast, 1);
-    if (lane == 0) e = su(U, bo - 1);
-    return e;
-  };
-  auto edge_r = [&](const T* U, T vfirst) -> T {
-    if constexpr (!ESH) return su(U, bo + W);
-    T e = __shfl_down_sync(0xffffffffu, vfirst, 1);
-    if (lane == 31) e = su(U, bo + W);
-    return e;
-  };
 
   for (int k = blockIdx.x; k < nitems; k += gridDim.x) {
     int tile, pa, pb;
@@ -234,7 +217,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     // r^2 of the thread's nodes at plane p from registers u(p-1), u(p), u(p+1) and smem u(p), f(p)
     auto acc_norm = [&](const T* U0, const T* F0, const V& um, const V& u0, const V& up) {
       const V fv = ld_vec(F0 + fo), dn = svec(U0, bo - BX), upr = svec(U0, bo + BX);
-      const T el = edge_l(U0, u0.v[W - 1]), er = edge_r(U0, u0.v[0]);
+      const T el = su(U0, bo - 1), er = su(U0, bo + W);
 #pragma unroll
       for (int j = 0; j < W; j++) {
         const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
@@ -433,10 +416,10 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
             dn.v[KR] = su(U0, bo + KR - BX);
             upr.v[KR] = su(U0, bo + KR + BX);
           }
-          const T edge = KR == 0 ? edge_l(U0, u0.v[W - 1]) : edge_r(U0, u0.v[0]);
+          const T edge = KR == 0 ? su(U0, bo - 1) : su(U0, bo + W);
           if constexpr (NRM) {
             if (nrm_here) {  // black nodes of plane p: residual of the old iterate
-              const T oedge = KR == 0 ? edge_r(U0, u0.v[0]) : edge_l(U0, u0.v[W - 1]);
+              const T oedge = KR == 0 ? su(U0, bo + W) : su(U0, bo - 1);
 #pragma unroll
               for (int m = 0; m < NR; m++) {
                 const int j = (1 - KR) + 2 * m;
@@ -507,14 +490,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
               pdn.v[KB] = P[po + KB - PX];
               pup.v[KB] = P[po + KB + PX];
             }
-            // the edge node is a red node of plane bp: the neighbour lane's pr1
-            T edge;
-            if constexpr (ESH) {
-              edge = KB == 0 ? __shfl_up_sync(0xffffffffu, pr1[NR - 1], 1) : __shfl_down_sync(0xffffffffu, pr1[0], 1);
-              if (lane == (KB == 0 ? 0 : 31)) edge = KB == 0 ? P[po - 1] : P[po + W];
-            } else {
-              edge = KB == 0 ? P[po - 1] : P[po + W];
-            }
+            const T edge = KB == 0 ? P[po - 1] : P[po + W];
             const V fb = FKEEP ? fprev : ld_vec(R.F(N(bp)) + fo);
             // plane bp's red nodes (pr1) sit at (1-KB) + 2m
             V o;
@@ -566,7 +542,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         if (MODE == 2) acc_norm(U0, R.F(N(p)), um, u0, up);  // r = f - A u, FP64 squares
         if (MODE != 2) {
           const V fv = ld_vec(R.F(N(p)) + fo), dn = svec(U0, bo - BX), upr = svec(U0, bo + BX);
-          const T el = edge_l(U0, u0.v[W - 1]), er = edge_r(U0, u0.v[0]);
+          const T el = su(U0, bo - 1), er = su(U0, bo + W);
           V o;
 #pragma unroll
           for (int j = 0; j < W; j++) {
@@ -613,11 +589,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
 // low-side ring nodes (row y0-1, column x0-1) into smem; then the coarse nodes
 // of the tile form their x- then y-sums of plane q and keep the last three in
 // registers: when q = 2P+1 the z-sum gives f_H(P) (reading 13 order).
-// XS: the x-sums of the full weighting are formed in registers by the row threads (r of
-// the thread's nodes stays in registers; x = ox-1 from the left lane) and only the x-sums
-// go through shared memory; the y- and z-sums of plane q run one plane later, after the
-// next barrier.  Same sums in the same order.
-template <typename T, bool ESH = false, bool XS = false>
+template <typename T>
 __global__ void __launch_bounds__(NT, Geo<T>::MINB)
     k_resid_restrict3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f,
                        Geom gf, Geom gc, Coef<T> c, T* __restrict__ fc, int tiles_x, int ntiles, int zcc,
@@ -629,9 +601,6 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
   const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
   // r planes alternate between two smem buffers: one barrier per fine plane
   T* const Rr2 = reinterpret_cast<T*>(sm + G::PR_OFF);
-  // XS: x-sums of planes q (buffer q & 1): rows 0 (= fine row y0-1) .. TY, TX/2 columns
-  T* const txb = reinterpret_cast<T*>(sm + G::PR_OFF + 2 * G::PB);
-  static_assert(2 * (TY + 1) * (G::TX / 2) * sizeof(T) <= G::PB, "x-sum buffers fit the third PR plane");
 
   const int tid = threadIdx.x, lane = tid & 31, ry = tid >> 5;
   const int pgf0 = gf.p_glob0;
@@ -685,20 +654,6 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
       R.issue(N(qlo + G::NS), &tm_u, &tm_f, x0, y0, qlo + G::NS + 1, qlo + G::NS, true);
     }
     T ty1 = (T)0, ty2 = (T)0;
-    // coarse stage of fine plane qq from its x-sums (XS)
-    auto coarse_xs = [&](int qq) {
-      if (tid < CN) {
-        const T* tb = txb + (size_t)(qq & 1) * (TY + 1) * CNX + (2 * ccy) * CNX + ccx;
-        const T ty0 = add(add(tb[0], tb[2 * CNX]), mul(two, tb[CNX]));
-        const int pglq = qq + pgf0;
-        if (cnode && (pglq & 1) == 1 && qq >= qf0 + 1) {
-          const int Pc = ((pglq - 1) >> 1) - gc.p_glob0;
-          crow[(long long)Pc * gc.pstride] = mul(add(add(ty2, ty0), mul(two, ty1)), scale);
-        }
-        ty2 = ty1;
-        ty1 = ty0;
-      }
-    };
     for (int q = rlo; q <= rhi; q++) {
       R.wait(N(q));
       const T* U0 = R.U(N(q - 1));
@@ -708,19 +663,10 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
       up = ld_vec(Up + bo);
       const int pgl = q + pgf0;
       const bool pl_in = pgl >= 1 && pgl <= gf.nz - 1;
-      V rv;  // r of the thread's nodes at plane q
       {
         const V fv = ld_vec(F0 + fo), dn = ld_vec(U0 + bo - BX), upr = ld_vec(U0 + bo + BX);
-        T el, er;
-        if constexpr (ESH) {  // x-neighbours from the neighbour lanes (see k_sweep3d ESH)
-          el = __shfl_up_sync(0xffffffffu, u0.v[W - 1], 1);
-          er = __shfl_down_sync(0xffffffffu, u0.v[0], 1);
-          if (lane == 0) el = U0[bo - 1];
-          if (lane == 31) er = U0[bo + W];
-        } else {
-          el = U0[bo - 1];
-          er = U0[bo + W];
-        }
+        const T el = U0[bo - 1], er = U0[bo + W];
+        V rv;
 #pragma unroll
         for (int j = 0; j < W; j++) {
           const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
@@ -728,12 +674,10 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
           const T rr = sub(fv.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
           rv.v[j] = pl_in && in[j] ? rr : (T)0;
         }
-        if constexpr (!XS) {
-          if constexpr (sizeof(T) == 8)
-            *reinterpret_cast<double2*>(Rr + po) = make_double2(rv.v[0], rv.v[1]);
-          else
-            *reinterpret_cast<float4*>(Rr + po) = make_float4(rv.v[0], rv.v[1], rv.v[2], rv.v[3]);
-        }
+        if constexpr (sizeof(T) == 8)
+          *reinterpret_cast<double2*>(Rr + po) = make_double2(rv.v[0], rv.v[1]);
+        else
+          *reinterpret_cast<float4*>(Rr + po) = make_float4(rv.v[0], rv.v[1], rv.v[2], rv.v[3]);
       }
       if (has_ring) {
         const T uc = U0[rb];
@@ -748,25 +692,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
         fence_proxy_async();
         R.issue(N(q - 1 + G::NS), &tm_u, &tm_f, x0, y0, q + G::NS, q - 1 + G::NS, true);
       }
-      if constexpr (XS) {
-        if (q > rlo) coarse_xs(q - 1);
-        // x-sums of plane q: r(2I-1) + r(2I+1) + 2 r(2I) for the thread's coarse columns
-        T left = __shfl_up_sync(0xffffffffu, rv.v[W - 1], 1);
-        if (lane == 0) left = Rr[po - 1];  // the ring column's r (x0-1)
-        T* trow = txb + (size_t)(q & 1) * (TY + 1) * CNX + (ry + 1) * CNX + G::NRED * lane;
-#pragma unroll
-        for (int m = 0; m < G::NRED; m++)
-          trow[m] = add(add(m == 0 ? left : rv.v[m > 0 ? 2 * m - 1 : 0], rv.v[2 * m + 1]), mul(two, rv.v[2 * m]));
-        if (tid >= NT - CNX) {  // last CNX threads (whole warps): the ring row y0-1 from its stored r
-          using P2 = std::conditional_t<sizeof(T) == 8, double2, float2>;
-          const int cc = tid - (NT - CNX);
-          const T* row = Rr + HX + 2 * cc;
-          const P2 pr = *reinterpret_cast<const P2*>(row);
-          T l2 = __shfl_up_sync(0xffffffffu, pr.y, 1);
-          if (lane == 0) l2 = row[-1];
-          txb[(size_t)(q & 1) * (TY + 1) * CNX + cc] = add(add(l2, pr.y), mul(two, pr.x));
-        }
-      } else if (tid < CN) {  // whole warps: CN = 256 (FP64) / 512 (FP32)
+      if (tid < CN) {  // whole warps: CN = 256 (FP64) / 512 (FP32)
         // x-sums r(2I-1) + r(2I+1) + 2 r(2I): (r(2I), r(2I+1)) is one aligned pair load and
         // r(2I-1) the left lane's second element (lane 0 loads it) — 5 smem wavefronts per
         // warp and row instead of 12 for three strided scalars; same values, same order
@@ -790,10 +716,6 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
       }
       um = u0;
       u0 = up;
-    }
-    if constexpr (XS) {
-      __syncthreads();
-      coarse_xs(rhi);
     }
     seq = N(qlast) + 1;
     __syncthreads();
@@ -867,14 +789,6 @@ static CUresult encode_coarse(CUtensorMap* tm, const void* base, const Geom& g, 
 bool supported(const Geom& g, int min_nx) {
   if (!g.three_d) return pm2::supported(g, min_nx);
   return g.three_d && g.nx >= (min_nx < 16 ? 16 : min_nx) && g.ny >= 16 && (g.p_hi - g.p_lo) >= 4;
-}
-
-// Edge shuffles (ESH) on or off per precision: MG_ESH bit 0 = FP64, bit 1 = FP32
-// (A/B switch, tools/eshab.sh); unset = the measured default.
-template <typename T>
-static bool edge_shfl() {
-  static const int mask = getenv("MG_ESH") ? atoi(getenv("MG_ESH")) : 0;  // thread-safe one-time read
-  return (mask >> (sizeof(T) == 8 ? 0 : 1)) & 1;
 }
 
 // First use of a kernel: opt in to its dynamic shared memory and return the
@@ -951,14 +865,7 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   };
   if (ecoarse)
     rbgs ? go(k_sweep3d<T, 1, false, false, true>) : go(k_sweep3d<T, 0, false, false, true>);
-  else if (edge_shfl<T>()) {
-    if (partial && !zero_in)
-      rbgs ? go(k_sweep3d<T, 1, false, true, false, true>) : go(k_sweep3d<T, 0, false, true, false, true>);
-    else if (rbgs)
-      zero_in ? go(k_sweep3d<T, 1, true, false, false, true>) : go(k_sweep3d<T, 1, false, false, false, true>);
-    else
-      zero_in ? go(k_sweep3d<T, 0, true, false, false, true>) : go(k_sweep3d<T, 0, false, false, false, true>);
-  } else if (partial && !zero_in)
+  else if (partial && !zero_in)
     rbgs ? go(k_sweep3d<T, 1, false, true>) : go(k_sweep3d<T, 0, false, true>);
   else if (rbgs)
     zero_in ? go(k_sweep3d<T, 1, true>) : go(k_sweep3d<T, 1, false>);
@@ -1007,7 +914,7 @@ cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f,
   const int tiles_x = (g.nx + G::TX - 1) / G::TX, tiles_y = (g.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = g.p_hi - g.p_lo;
-  auto kernel = edge_shfl<T>() ? k_sweep3d<T, 2, false, false, false, true> : k_sweep3d<T, 2, false>;
+  auto kernel = k_sweep3d<T, 2, false>;
   const int resident = prepare_kernel(kernel, G::SMEM);
   const int zc = choose_zc(ntiles, np, resident, 2, min_zc_for(g, sizeof(T)));
   const int nitems = ntiles * ((np + zc - 1) / zc);
@@ -1270,10 +1177,7 @@ cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>&
   const int tiles_x = (gc.nx + G::TX / 2 - 1) / (G::TX / 2), tiles_y = (gc.ny + TY / 2 - 1) / (TY / 2);
   const int ntiles = tiles_x * tiles_y;
   const int npc = gc.p_hi - gc.p_lo;
-  static const int xs = getenv("MG_RRXS") ? atoi(getenv("MG_RRXS")) : 0;  // A/B: bit 0 FP64, bit 1 FP32
-  const bool x = (xs >> (sizeof(T) == 8 ? 0 : 1)) & 1;
-  auto kernel = edge_shfl<T>() ? (x ? k_resid_restrict3d<T, true, true> : k_resid_restrict3d<T, true, false>)
-                               : (x ? k_resid_restrict3d<T, false, true> : k_resid_restrict3d<T, false, false>);
+  auto kernel = k_resid_restrict3d<T>;
   const int resident = prepare_kernel(kernel, G::SMEM);
   const int zcc = zc_override > 0 ? zc_override : choose_zc(ntiles, npc, resident, 2, min_zc_for(gf, sizeof(T)));
   const int nitems = ntiles * ((npc + zcc - 1) / zcc);
