@@ -1,11 +1,12 @@
 """Regenerate BASELINE.md §4's table (and the oracle paragraph) from profiles/r1e_bench/*.json
-(the bench_all.sh lines): python tools/baseline_table.py"""
+(the bench_all.sh lines): python tools/baseline_table.py [profiles subdir, default r1f_bench]"""
 import json
 import os
 import re
+import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-B = os.path.join(ROOT, "profiles", "r1e_bench")
+B = os.path.join(ROOT, "profiles", sys.argv[1] if len(sys.argv) > 1 else "r1f_bench")
 
 
 def L(c):
