@@ -1157,7 +1157,8 @@ cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cud
   };
   // measured on C3 L0 (tools/prolab.sh): flat<6> 0.411 ms FP64 / 0.225 ms FP32,
   // marching <4,2> 0.425 / 0.238, <2,2,pipelined> 0.419 / 0.228, flat<8> (spills) 0.437 / 0.228,
-  // flat<4> 0.541 / 0.252 (5 CTAs of 256 per SM)
+  // flat<4> 0.541 / 0.252 (5 CTAs of 256 per SM), one plane per item with 8 / 6 CTAs 0.458 / 0.473
+  // (FP64; 2 u vectors in flight per thread beat occupancy alone)
   switch (var) {
     case 1: return go(k_prolong3d<T, 4, 2, false>);
     case 2: return go(k_prolong3d<T, 2, 2, true>);

@@ -3,7 +3,9 @@
 # bench lines with the prolongation's per-step time.
 set -u
 mkdir -p gpurun_out/prolab
-for v in 0 1 3; do
+# variants (launch_prolong): 0 flat 2 planes/item 6 CTAs (default), 1 marching, 2 marching pipelined,
+# 3 flat 8 CTAs (4 / 5, one plane per item with 8 / 6 CTAs, were measured and removed)
+for v in 1 2 3; do
   MG_PROLONG_V=$v timeout 900 python -m pytest -q -x -m gpu tests/test_gpu_parity.py tests/test_gpu_shapes.py \
       tests/test_gpu_random.py tests/test_gpu_slab_loopback.py \
       > gpurun_out/prolab/t_$v.log 2>&1
