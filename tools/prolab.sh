@@ -4,8 +4,9 @@
 set -u
 mkdir -p gpurun_out/prolab
 # variants (launch_prolong): 0 flat 2 planes/item 6 CTAs (default), 1 marching, 2 marching pipelined,
-# 3 flat 8 CTAs (4 / 5, one plane per item with 8 / 6 CTAs, were measured and removed)
-for v in 1 2 3; do
+# 3 flat 8 CTAs (one fine plane per item with 8 / 6 CTAs and two coarse planes per item with
+# 4 / 5 CTAs were measured and removed: profiles/r1f/prolab2.txt, prolab3.txt)
+for v in 0 1 2 3; do
   MG_PROLONG_V=$v timeout 900 python -m pytest -q -x -m gpu tests/test_gpu_parity.py tests/test_gpu_shapes.py \
       tests/test_gpu_random.py tests/test_gpu_slab_loopback.py \
       > gpurun_out/prolab/t_$v.log 2>&1
