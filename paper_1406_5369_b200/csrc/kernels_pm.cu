@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
             upr.v[KR] = su(U0, bo + KR + BX);
           }
           const T edge = KR == 0 ? su(U0, bo - 1) : su(U0, bo + W);
+#ifndef MG_PROBE_RED_ONLY_NORM  // timing probe only (tools/normprobe.sh): drop the black terms
           if constexpr (NRM) {
             if (nrm_here) {  // black nodes of plane p: residual of the old iterate
               const T oedge = KR == 0 ? su(U0, bo + W) : su(U0, bo - 1);
@@ -431,6 +432,7 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
               }
             }
           }
+#endif
           V pv = u0;  // PR row vector: red values at red nodes (black entries are never read)
 #pragma unroll
           for (int m = 0; m < NR; m++) {
