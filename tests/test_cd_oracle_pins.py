@@ -235,3 +235,133 @@ def test_fp32_build_tracks_fp64():
     a = CDOracle(cfg).cycle(u, f)
     b = CDOracle(cfg, np.complex64).cycle(u.astype(np.complex64), f.astype(np.complex64))
     assert np.abs(a - b).max() <= 1e-5 * np.abs(a).max()
+
+
+# ------------------------------------------------------------------ the nonlinear residual norm
+@pytest.mark.parametrize("dim,cells", [(2, (6, 4)), (2, (9, 9)), (3, (4, 3, 2))])
+def test_norm_equals_dense_nonlinear_residual(dim, cells):
+    """S:540-548 (l2_residual): sqrt of the sum over the cells of |f - A u|^2 with the complex
+    modulus, where for complex diffusion A = A(g(u)) is assembled from the diffusivity of the
+    iterate whose residual is taken (reading 21: the driver loop's norm is the nonlinear
+    residual).  Dense A from the definition (dense_A, g_of); negative controls: the squared sum
+    (no sqrt), the real parts only, and A built from a different (lagged) field all differ."""
+    cfg = CDConfig(dim=dim, cells=cells)
+    O = CDOracle(cfg)
+    shape = cfg.shape()
+    u, f = rand_c(shape, 21, 0.8), rand_c(shape, 22)
+    h = [1.0 / c for c in reversed(cells)]
+    r = f.ravel() - dense_A(g_of(u.imag), h) @ u.ravel()
+    ref = math.sqrt(float(np.sum(r.real ** 2 + r.imag ** 2)))
+    got = O.norm(0, u, f)
+    assert abs(got - ref) <= 1e-14 * ref, (got, ref)
+    assert abs(got ** 2 - ref) > 1e-3 * ref                                  # sqrt taken
+    assert abs(got - np.linalg.norm(r.real)) > 1e-3 * ref                     # complex modulus
+    lag = rand_c(shape, 23, 0.8)                                              # g from another field
+    r_lag = f.ravel() - dense_A(g_of(lag.imag), h) @ u.ravel()
+    assert abs(got - np.linalg.norm(r_lag)) > 1e-6 * ref
+
+
+def test_norm_spec_examples():
+    """u = 0, f = 1 on m cells -> sqrt(m); the exact solution of a 1-cell system -> 0."""
+    cfg = CDConfig(dim=2, cells=(5, 7), levels=1)
+    O = CDOracle(cfg)
+    assert O.norm(0, np.zeros(cfg.shape(), complex), np.ones(cfg.shape(), complex)) == math.sqrt(35)
+    O1 = CDOracle(CDConfig(dim=2, cells=(1, 1), levels=1))
+    u1 = np.array([[0.4 - 0.9j]])
+    assert O1.norm(0, u1, u1) == 0.0  # A = I on one cell (no interior faces)
+
+
+# ------------------------------------------------------------------ FAS with the nonlinear operator
+def dense_fas(u, f, cells, levels, smoother, omega, nu1, nu2, ncoarse, coarse_g="restricted_u"):
+    """S:431-439 / S:355 written out in dense algebra, nonlinear operator, recursion over `levels`.
+    At every level visit the lagged diffusivity g = g(Im u_l) is formed ONCE from the level's
+    current iterate ('rebuilt from the current solution once per cycle before smoothing,
+    frozen within the cycle'); the coarse operator of the FAS right-hand side is re-discretised
+    from the restricted iterate u^_H = R u_h (S:355 'ComplexDiffusion: rebuilt from the restricted
+    lagged solution'; S:434 'f_H = A_H(u^_H) + R(f_h - A_h u_h)').  coarse_g selects a WRONG rule
+    for the negative controls ('restricted_g': g_H = R g_h; 'fine_lagged': g_H = g(R u_h at the
+    START of the cycle, before pre-smoothing))."""
+    dim = len(cells)
+    shapes = [tuple(c >> l for c in reversed(cells)) for l in range(levels)]
+
+    def hs(l):
+        return [2.0 ** l / c for c in reversed(cells)]
+
+    def rec(l, u, f, g_hint=None):
+        sh = shapes[l]
+        g = g_of(u.reshape(sh).imag) if g_hint is None else g_hint
+        A = dense_A(g, hs(l))
+        if l == levels - 1:
+            for _ in range(ncoarse):
+                u = dense_smooth(A, f, u, omega, smoother, sh)
+            return u
+        u_start = u.copy()
+        for _ in range(nu1):
+            u = dense_smooth(A, f, u, omega, smoother, sh)
+        R, P = dense_R(sh), dense_P(sh)
+        uh = R @ u
+        if coarse_g == "restricted_u":
+            gH = g_of(uh.reshape(shapes[l + 1]).imag)
+        elif coarse_g == "restricted_g":
+            gH = (R @ g.ravel()).reshape(shapes[l + 1])
+        else:
+            gH = g_of((R @ u_start).reshape(shapes[l + 1]).imag)
+        AH = dense_A(gH, hs(l + 1))
+        fH = AH @ uh + R @ (f - A @ u)
+        uH = rec(l + 1, uh.copy(), fH, None if coarse_g == "restricted_u" else gH)
+        u = u + P @ (uH - uh)
+        for _ in range(nu2):
+            u = dense_smooth(A, f, u, omega, smoother, sh)
+        return u
+
+    return rec(0, u.ravel(), f.ravel()).reshape(shapes[0])
+
+
+@pytest.mark.parametrize("smoother,omega,levels,cells", [(RBGS, 1.0, 2, (8, 8)), (JACOBI, 0.8, 2, (8, 4)),
+                                                         (RBGS, 1.0, 3, (16, 8)), (JACOBI, 0.8, 2, (4, 4, 4))])
+def test_fas_nonlinear_cycle_equals_dense(smoother, omega, levels, cells):
+    """one nonlinear FAS V(2,2) cycle of the oracle equals the cycle
+    evaluated in dense algebra with the coarse operator rebuilt from g(R u_h), for a strongly
+    nonlinear state (|Im u| ~ 1 >> k*theta = 0.21, so g varies by ~10x over the grid).  Negative
+    controls: the same dense cycle with the coarse diffusivity taken from R g_h, or from R of the
+    pre-smoothing iterate, differs from the oracle by far more than the tolerance."""
+    dim = len(cells)
+    cfg = CDConfig(dim=dim, cells=cells, levels=levels, smoother=smoother, omega=omega, ncoarse=3)
+    O = CDOracle(cfg)
+    u0, f = rand_c(cfg.shape(), 31, 1.0), rand_c(cfg.shape(), 32, 1.0)
+    got = O.cycle(u0, f)
+    ref = dense_fas(u0, f, cells, levels, smoother, omega, 2, 2, 3)
+    scale = np.abs(ref).max()
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12 * scale)
+    for wrong in ("restricted_g", "fine_lagged"):
+        bad = dense_fas(u0, f, cells, levels, smoother, omega, 2, 2, 3, coarse_g=wrong)
+        assert np.abs(bad - ref).max() > 1e-6 * scale, wrong
+
+
+def test_fp32_build_ops_within_rounding_bound_of_dense():
+    """The complex64 oracle build, op by op, against the dense FP64 definitions applied to the
+    same complex64 inputs: g (Eq. 3), A(g)u, the omega-Jacobi sweep and the cell-average
+    restriction, each within a bound of a few float32 roundings per term."""
+    eps = float(np.finfo(np.float32).eps)
+    cells = (8, 6)
+    cfg = CDConfig(dim=2, cells=cells, smoother=JACOBI, omega=0.8)
+    O = CDOracle(cfg, np.complex64)
+    shape = cfg.shape()
+    ul = rand_c(shape, 51, 0.5).astype(np.complex64)
+    u, f = rand_c(shape, 52).astype(np.complex64), rand_c(shape, 53).astype(np.complex64)
+    g = O.gfield(0, ul)
+    g_ref = g_of(ul.imag.astype(np.float64))
+    assert np.all(np.abs(g - g_ref) <= 8 * eps * np.abs(g_ref))
+    g64 = g.astype(np.complex128)
+    h = [1.0 / c for c in reversed(cells)]
+    A = dense_A(g64, h)
+    u64, f64 = u.astype(np.complex128).ravel(), f.astype(np.complex128).ravel()
+    Au, _ = O.apply(0, g, u)
+    absAu = np.abs(A) @ np.abs(u64)
+    assert np.all(np.abs(Au.ravel() - A @ u64) <= 24 * eps * absAu)
+    out = O.smooth(0, g, u, f).ravel()
+    ref = dense_smooth(A, f64, u64, 0.8, JACOBI, shape)
+    D = np.abs(np.diag(A))
+    assert np.all(np.abs(out - ref) <= 48 * eps * (np.abs(u64) + (np.abs(f64) + absAu) / D))
+    rc = O.restrict(0, f).ravel()
+    assert np.all(np.abs(rc - dense_R(shape) @ f64) <= 8 * eps * (dense_R(shape) @ np.abs(f64)))

@@ -438,3 +438,48 @@ def test_oracle_thread_count_independent(tmp_path):
         subprocess.run([sys.executable, "-c", code, p], check=True, env=env)
         outs.append(np.load(p))
     assert np.array_equal(outs[0], outs[1])
+
+
+# ---------------------------------------------------------------- the FP32 build, op by op
+EPS32 = float(np.finfo(np.float32).eps)
+
+
+@pytest.mark.parametrize("dim,cells", [(2, (16, 8)), (3, (8, 8, 8)), (3, (8, 4, 16))])
+def test_fp32_ops_within_rounding_bound_of_dense(dim, cells):
+    """Each FP32 oracle operation equals its dense FP64 definition (tests/dense.py) applied to the
+    same float32 inputs, within a forward rounding-error bound of a few float32 roundings per term
+    (standard model |fl(a op b) - (a op b)| <= eps |a op b|, summed over the ~10 operations of a
+    node): residual, omega-Jacobi, RBGS, full weighting, prolongation + correction.  A dropped
+    term, a wrong sign or a transposed operand moves a value by O(|A||u|) >> the bound."""
+    O = orc.Oracle(cfg(dim, cells, levels=2, smoother="jacobi", omega=0.8), np.float32)
+    u = rnd(O.shape(0), 41).astype(np.float32)
+    f = rnd(O.shape(0), 42).astype(np.float32)
+    c, D, _ = dense.coeffs(list(cells), 0)
+    A = dense.assemble_A(list(cells), c)
+    ui, fi = dense.interior(u).astype(np.float64), dense.interior(f).astype(np.float64)
+    absAu = np.abs(A) @ np.abs(ui)
+    # residual: ~8 roundings on terms of size |f| + |A||u|
+    r = dense.interior(O.residual(0, u, f)).astype(np.float64)
+    assert np.all(np.abs(r - (fi - A @ ui)) <= 8 * EPS32 * (np.abs(fi) + absAu))
+    # omega-Jacobi
+    wd = 0.8 / D
+    scale = np.abs(ui) + wd * (np.abs(fi) + absAu)
+    out = dense.interior(O.jacobi(0, u, f)).astype(np.float64)
+    assert np.all(np.abs(out - dense.jacobi(A, D, 0.8, ui, fi)) <= 10 * EPS32 * scale)
+    # RBGS (omega = 1): black nodes read the rounded red values, one more level of propagation
+    O1 = orc.Oracle(cfg(dim, cells, levels=2, smoother="rbgs"), np.float32)
+    out = dense.interior(O1.rbgs(0, u, f)).astype(np.float64)
+    ref = dense.rbgs(A, D, 1.0, ui, fi, list(cells))
+    sc = np.abs(ui) + (np.abs(fi) + np.abs(A) @ (np.abs(ui) + np.abs(ref))) / D
+    assert np.all(np.abs(out - ref) <= 24 * EPS32 * sc)
+    # full weighting and prolongation + correction: sums of nonnegative weights
+    R = dense.assemble_R([n // 2 for n in cells])
+    P = dense.assemble_P([n // 2 for n in cells])
+    fc = dense.interior(O.restrict(0, f)).astype(np.float64)
+    assert np.all(np.abs(fc - R @ fi) <= 8 * EPS32 * (np.abs(R) @ np.abs(fi)))
+    e = rnd(O.shape(1), 43).astype(np.float32)
+    ei = dense.interior(e).astype(np.float64)
+    pc = dense.interior(O.prolong_correct(0, e, u)).astype(np.float64)
+    assert np.all(np.abs(pc - (ui + P @ ei)) <= 8 * EPS32 * (np.abs(ui) + P @ np.abs(ei)))
+    # the bound is tight enough to see float32 at all: the FP32 results are not the FP64 ones
+    assert np.abs(out - ref).max() > 0
