@@ -8,7 +8,7 @@ PYSITE    := $(shell python -c "import sysconfig;print(sysconfig.get_paths()['pu
 NCCL_DIR  := $(PYSITE)/nvidia/nccl
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC,-O2 \
-             -I include -I $(CSRC) -I $(NCCL_DIR)/include $(MG_EXTRA)
+             -I include -I $(CSRC) -I $(NCCL_DIR)/include
 LIB       := $(PKG)/libmgb200.so
 
 CU_SRCS   := $(wildcard $(CSRC)/*.cu)

@@ -243,6 +243,47 @@ def oracle_step_time(cfgname, max_seconds=30.0):
     raise RuntimeError("unreachable")
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline_leg(cfgname):
+    """--cpu-baseline-leg: the oracle timed on one step, all host threads, then one thread
+    (OMP_NUM_THREADS=1 in a grandchild: OpenMP reads it at load time); prints one JSON object."""
+    import subprocess
+    t, cunk, desc, threads, _ = oracle_step_time(cfgname, max_seconds=30.0)
+    out = {"value": cunk / t, "unit": "unknowns/s", "cores": threads, "kind": "oracle", "sample": desc,
+           "cpu_model": _cpu_model(), "host_threads": os.cpu_count()}
+    if os.environ.get("MG_BENCH_ONE_THREAD") is None:
+        env = dict(os.environ, OMP_NUM_THREADS="1", MG_BENCH_ONE_THREAD="1")
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-leg", "--config", cfgname],
+                           env=env, capture_output=True, text=True, timeout=600)
+        try:
+            one = json.loads(r.stdout.strip().splitlines()[-1])
+            out["one_thread"] = {"value": one["value"], "unit": "unknowns/s", "cores": one["cores"],
+                                 "sample": one["sample"]}
+        except Exception as e:  # reported, not fatal
+            out["one_thread"] = {"error": f"{e}: {r.stderr[-300:]}"}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def cpu_baseline_subprocess(cfgname):
+    import subprocess
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-leg", "--config", cfgname],
+                       capture_output=True, text=True, timeout=1200)
+    try:
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:
+        return {"error": f"cpu baseline leg failed: {e}: {r.stderr[-300:]}"}
+
+
 class _CdStepper:
     """Adapter so the reference arm can step the complex-diffusion oracle like the Poisson one."""
 
@@ -280,6 +321,30 @@ def cd_oracle_step_time(cfgname, max_seconds):
     raise RuntimeError("unreachable")
 
 
+def workload_levels(cfgname):
+    """Levels of the full-size workload: explicit, else the paper's rule (DESIGN reading 2/20)."""
+    if is_cd(cfgname):
+        return int(CD_CONFIGS[cfgname][1]).bit_length() - 1
+    levels, n = CONFIGS[cfgname][6], CONFIGS[cfgname][1]
+    return levels or int(n - 1).bit_length() - 1
+
+
+def workload_config(cfgname):
+    """The `config` object of the JSON line: the workload only, identical in both arms."""
+    levels = workload_levels(cfgname)
+    if is_cd(cfgname):
+        dim, n, *_ = CD_CONFIGS[cfgname]
+        esz = 16 if CD_CONFIGS[cfgname][5] == "f64" else 8
+        key, nodes = "grid_cells", n
+        arr = n ** dim * esz
+    else:
+        dim, n, *_ = CONFIGS[cfgname]
+        esz = 8 if CONFIGS[cfgname][5] == "f64" else 4
+        key, nodes = "grid_nodes", n
+        arr = n ** dim * esz
+    return {"workload": WORKLOAD_DESC[cfgname], key: nodes, "dim": dim, "levels": levels, "l2": l2_note(arr)}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -298,12 +363,12 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "unknowns/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
+        "scaling": "strong", "vs_baseline": None,
         "dtype": (("c" if is_cd(args.config) else "") + (CD_CONFIGS[args.config][5] if is_cd(args.config)
                                                           else CONFIGS[args.config][5])),
         "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.config], "parallelism": "cpu-oracle",
-                   "l2": "CPU run on the host cores (the GPU L2 flush rule does not apply)"},
+        "config": workload_config(args.config),
+        "parallelism": "cpu-oracle (OpenMP over planes)" if threads > 1 else "cpu-oracle (one thread)",
         "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": threads, "kind": "oracle", "sample": desc},
         "e2e": {"value": val, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -312,6 +377,32 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------- GPU arm
+def single_gpu_point(cfgname, dev, stream, steps=8, warmup=3):
+    """Step time of `cfgname` on this GPU alone (device loop, the same step as the main line):
+    the N = 1 point of the scaling workload, reported next to the N = 1 metric line."""
+    import torch
+
+    import paper_1406_5369_b200 as mgb
+    dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[cfgname]
+    S = mgb.Solver(dim, nodes, levels=levels, smoother=sm, omega=omega, nu1=nu1, nu2=nu2, dtype=dt, device=dev)
+    u, f = S.empty(), S.empty()
+    with torch.cuda.stream(stream):
+        S.workload_fill(u, 42, stream=stream)
+    torch.cuda.synchronize()
+    S.solve(u, f, -1.0, warmup, stream=stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    k, _ = S.solve(u, f, -1.0, steps, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    S.close()
+    return {"workload": WORKLOAD_DESC[cfgname], "steps": steps, "warmup": warmup, "ms_per_step": ms,
+            "value": interior_unknowns(dim, nodes) / (ms * 1e-3), "unit": "unknowns/s",
+            "note": "bench.py --gpus N > 1 defaults to this workload (z-slab decomposition of the same grid)"}
+
+
 def run_mg(args):
     import torch
 
@@ -332,7 +423,8 @@ def run_mg(args):
         dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[args.config]
     esz = 8 if dt == "f64" else 4
     kw = dict(levels=levels, smoother=sm, omega=omega, nu1=nu1, nu2=nu2, dtype=dt, device=dev,
-              flags=(mgb.FLAG_HOST_LOOP if args.host_loop else 0) | (mgb.FLAG_FUSE_PROLONG if args.fuse_prolong else 0))
+              flags=(mgb.FLAG_HOST_LOOP if args.host_loop else 0) | (mgb.FLAG_FUSE_PROLONG if args.fuse_prolong else 0)
+              | (mgb.FLAG_NO_KFUSE if args.no_kfuse else 0))
     if cd:
         kw.update(problem="complex_diffusion", coarse="sweeps")
     # mg_solve runs its loop on the device (one CUDA graph, conditional WHILE node) unless
@@ -352,6 +444,7 @@ def run_mg(args):
             S.workload_fill(f, 42, stream=stream)
     torch.cuda.synchronize()
     unk = nodes ** dim if cd else interior_unknowns(dim, nodes)
+    assert S.levels == workload_levels(args.config), (S.levels, workload_levels(args.config))
 
     # K steps = the library's driver loop mg_solve(rtol=0, max_cycles=K): K V-cycles, each
     # followed by the residual norm (pipelined into the next cycle's first sweep; the
@@ -448,28 +541,35 @@ def run_mg(args):
                "path": (f"mg_vcycle_host_batch over {ne} problems (pinned host u, f -> device, 1 cycle + norm, "
                         "u -> host; H2D / compute / D2H pipelined)")}
 
-    # ---- CPU oracle baseline (rank 0, N=1 only)
+    # ---- the N>1 default workload (C5, 1025^3) on this one GPU: the 1-GPU point of the scaling curve
+    c5 = None
+    if world == 1 and args.config == "C3-f64" and not args.no_c5:
+        S.close()
+        del u, f
+        torch.cuda.empty_cache()
+        c5 = single_gpu_point("C5", dev, stream)
+
+    # ---- CPU oracle baseline (rank 0, N=1 only), in a child process so that this (product)
+    # process never maps the oracle's library
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        t, cunk, desc, threads, _ = oracle_step_time(args.config, max_seconds=30.0)
-        cpu = {"value": cunk / t, "unit": "unknowns/s", "cores": threads, "kind": "oracle", "sample": desc}
+        cpu = cpu_baseline_subprocess(args.config)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": unk_total / (ms * 1e-3), "unit": "unknowns/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if slab else "weak", "vs_baseline": None, "dtype": ("c" if cd else "") + dt,
+            "scaling": "weak" if (world > 1 and not slab) else "strong", "vs_baseline": None,
+            "dtype": ("c" if cd else "") + dt,
             "data": "synthetic",
-            "config": {"workload": WORKLOAD_DESC[args.config], ("grid_cells" if cd else "grid_nodes"): nodes,
-                       "dim": dim,
-                       "parallelism": (f"z-slab x{world} (NCCL halos, agglomeration below 8 planes/rank)" if slab
-                                       else ("replicas" if world > 1 else "single-gpu")),
-                       "l2": l2_note(S.shape[0] * S.shape[1] * S.shape[2] * esz * (2 if cd else 1)),
-                       "levels": S.levels,
-                       "driver": "device loop (CUDA graph WHILE node)" if device_loop else "host loop"},
+            "config": workload_config(args.config),
+            "parallelism": (f"z-slab x{world} (NCCL halos, agglomeration below 8 planes/rank)" if slab
+                            else ("replicas" if world > 1 else "single-gpu")),
+            "driver": "device loop (CUDA graph WHILE node)" if device_loop else "host loop",
             "residual_reduction_per_step": (rk / r0) ** (1.0 / (args.steps + args.warmup)) if r0 else None,
             "model_bytes_per_step": B, "model_GBps": B / (ms * 1e-3) / 1e9,
             "roofline": roofline, "kernels": breakdown, "cpu_baseline": cpu, "e2e": e2e,
+            "single_gpu_C5": c5,
             "gpu_launches": int(round(launches * args.steps)), "gpu_launches_per_step": launches,
             "clocks": sampler.summary(),
         }
@@ -479,22 +579,65 @@ def run_mg(args):
     return 0
 
 
+def check_world(args):
+    """--gpus N must match the launch: under torchrun WORLD_SIZE == N; without torchrun and N > 1,
+    re-launch this command under torch.distributed.run with N ranks (never time fewer GPUs than
+    asked for).  Returns an exit code to stop with, or None to go on."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if os.environ.get("WORLD_SIZE") is not None:
+        if world != args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+            return 2
+        return None
+    if args.gpus == 1:
+        return None
+    if args.gpus < 1:
+        print("bench.py: --gpus must be >= 1", file=sys.stderr)
+        return 2
+    if args.impl == "mg":
+        import torch
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {n} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    import subprocess
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mg", choices=["mg", "reference"])
-    ap.add_argument("--config", default="C3-f64", choices=sorted(CONFIGS) + sorted(CD_CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS) + sorted(CD_CONFIGS),
+                    help="default: C3-f64 (the metric's workload) at N=1, C5 (the north star's scaling "
+                         "workload, 1025^3) at N>1")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-loop", action="store_true", help="mg_solve with MG_FLAG_HOST_LOOP (per-cycle sync)")
     ap.add_argument("--fuse-prolong", action="store_true", help="MG_FLAG_FUSE_PROLONG (prolongation in the first post-sweep)")
     ap.add_argument("--decomp", default="slab", choices=["slab", "replicas"],
                     help="N>1: z-slab decomposition of one grid (default) or independent replicas")
+    ap.add_argument("--no-c5", action="store_true", help="N=1 C3-f64: skip the single-GPU C5 point")
+    ap.add_argument("--no-kfuse", action="store_true", help="MG_FLAG_NO_KFUSE (2D Jacobi: one sweep per pass)")
+    ap.add_argument("--cpu-baseline-leg", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "C5" if args.gpus > 1 else "C3-f64"
+    if args.cpu_baseline_leg:
+        return cpu_baseline_leg(args.config)
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
+    rc = check_world(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_mg(args)

@@ -79,6 +79,10 @@ typedef enum { MG_PROBLEM_POISSON = 0, MG_PROBLEM_COMPLEX_DIFFUSION = 1 } mg_pro
                                    in smem); off by default: the sweep is issue-bound, the gain is small */
 #define MG_FLAG_HOST_LOOP 16u   /* mg_solve: host-driven loop (one synchronisation per cycle) instead of
                                    the on-device loop (one CUDA graph with a conditional WHILE node) */
+#define MG_FLAG_NO_KFUSE 32u   /* 2D omega-Jacobi: one sweep per HBM pass instead of the temporally blocked
+                                   passes of up to 3 (FP32) / 2 (FP64) sweeps (A/B measurement; bitwise equal) */
+#define MG_FLAG_CD_KFUSE 64u   /* complex diffusion, 2D Jacobi: multi-sweep passes (3 FP32 / 2 FP64; measured
+                                   slower than single sweeps; bitwise equal) */
 
 typedef struct {
     int32_t dim;         /* 2 or 3                                        */

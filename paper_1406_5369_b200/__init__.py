@@ -24,6 +24,7 @@ JACOBI, RBGS, GS_LEX = 0, 1, 2
 FP64, FP32 = 0, 1
 COARSE_DIRECT, COARSE_SWEEPS = 0, 1
 FLAG_NO_GRAPH, FLAG_BASELINE, FLAG_SLAB, FLAG_FUSE_PROLONG, FLAG_HOST_LOOP = 1, 2, 4, 8, 16
+FLAG_NO_KFUSE, FLAG_CD_KFUSE = 32, 64
 PROBLEM_POISSON, PROBLEM_COMPLEX_DIFFUSION = 0, 1
 
 # every symbol include/mg.h declares (checked by tests/test_abi.py)

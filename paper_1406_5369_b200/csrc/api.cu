@@ -356,11 +356,18 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
   return MG_OK;
 }
 
-extern "C" mg_status mg_vcycle_host(mg_solver* s, void* u_host, const void* f_host, int32_t ncycles,
-                                    double* norm_out, void* stream) {
-  mg_status st = guard(s);
-  if (st != MG_OK) return st;
-  if (!u_host || !f_host || ncycles < 0) return fail(s, MG_ERR_INVALID, "bad argument");
+// On an error return, copies queued before the failure may still reference the caller's host
+// buffers: drain the streams involved (their own errors ignored) before returning.
+static void drain_host_copies(mg_solver* s, cudaStream_t cs) {
+  if (s->h2d_stream) cudaStreamSynchronize(s->h2d_stream);
+  if (s->d2h_stream) cudaStreamSynchronize(s->d2h_stream);
+  cudaStreamSynchronize(cs);
+  cudaGetLastError();
+}
+
+static mg_status vcycle_host_run(mg_solver* s, void* u_host, const void* f_host, int32_t ncycles,
+                                 double* norm_out, void* stream) {
+  mg_status st = MG_OK;
   cudaStream_t cs = (cudaStream_t)stream;
   const Level& lv = s->lv[0];
   size_t bytes = lv.elems * s->esz * (s->cfg.problem == MG_PROBLEM_COMPLEX_DIFFUSION ? 2 : 1);
@@ -386,6 +393,19 @@ extern "C" mg_status mg_vcycle_host(mg_solver* s, void* u_host, const void* f_ho
   return MG_OK;
 }
 
+extern "C" mg_status mg_vcycle_host(mg_solver* s, void* u_host, const void* f_host, int32_t ncycles,
+                                    double* norm_out, void* stream) {
+  mg_status st = guard(s);
+  if (st != MG_OK) return st;
+  if (!u_host || !f_host || ncycles < 0) return fail(s, MG_ERR_INVALID, "bad argument");
+  st = vcycle_host_run(s, u_host, f_host, ncycles, norm_out, stream);
+  if (st != MG_OK) drain_host_copies(s, (cudaStream_t)stream);
+  return st;
+}
+
+static mg_status host_batch_run(mg_solver* s, const void* const* u_in, void* const* u_out, const void* const* f_in,
+                                int32_t nbatch, int32_t ncycles, double* norms, void* stream);
+
 extern "C" mg_status mg_vcycle_host_batch(mg_solver* s, const void* const* u_in, void* const* u_out,
                                           const void* const* f_in, int32_t nbatch, int32_t ncycles, double* norms,
                                           void* stream) {
@@ -394,6 +414,14 @@ extern "C" mg_status mg_vcycle_host_batch(mg_solver* s, const void* const* u_in,
   if (!u_in || !u_out || !f_in || nbatch < 0 || ncycles < 0) return fail(s, MG_ERR_INVALID, "bad argument");
   for (int b = 0; b < nbatch; b++)
     if (!u_in[b] || !u_out[b] || !f_in[b]) return fail(s, MG_ERR_INVALID, "NULL host buffer of problem %d", b);
+  st = host_batch_run(s, u_in, u_out, f_in, nbatch, ncycles, norms, stream);
+  if (st != MG_OK) drain_host_copies(s, (cudaStream_t)stream);
+  return st;
+}
+
+static mg_status host_batch_run(mg_solver* s, const void* const* u_in, void* const* u_out, const void* const* f_in,
+                                int32_t nbatch, int32_t ncycles, double* norms, void* stream) {
+  mg_status st = MG_OK;
   cudaStream_t cs = (cudaStream_t)stream;
   const Level& lv = s->lv[0];
   const size_t bytes = lv.elems * s->esz * (s->cfg.problem == MG_PROBLEM_COMPLEX_DIFFUSION ? 2 : 1);

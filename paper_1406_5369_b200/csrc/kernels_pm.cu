@@ -417,7 +417,6 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
             upr.v[KR] = su(U0, bo + KR + BX);
           }
           const T edge = KR == 0 ? su(U0, bo - 1) : su(U0, bo + W);
-#ifndef MG_PROBE_RED_ONLY_NORM  // timing probe only (tools/normprobe.sh): drop the black terms
           if constexpr (NRM) {
             if (nrm_here) {  // black nodes of plane p: residual of the old iterate
               const T oedge = KR == 0 ? su(U0, bo + W) : su(U0, bo - 1);
@@ -432,7 +431,6 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
               }
             }
           }
-#endif
           V pv = u0;  // PR row vector: red values at red nodes (black entries are never read)
 #pragma unroll
           for (int m = 0; m < NR; m++) {
@@ -834,7 +832,7 @@ static CUresult encode_coarse(CUtensorMap* tm, const void* base, const Geom& g, 
 
 template <typename T>
 cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
-                         int zc_override, cudaStream_t st, double* partial, int* npartial, const T* ecoarse,
+                         cudaStream_t st, double* partial, int* npartial, const T* ecoarse,
                          const Geom* gcoarse) {
   if (!g.three_d) {
     if (ecoarse) return cudaErrorInvalidValue;  // fused prolongation: 3D only
@@ -848,10 +846,6 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   using G = Geo<T>;
   CUtensorMap tu, tf;
   CUresult e1 = encode(&tu, uin ? uin : f, g, sizeof(T), G::BYU), e2 = encode(&tf, f, g, sizeof(T), G::BYF);
-  static const bool debug = getenv("MG_DEBUG") != nullptr;  // thread-safe one-time read
-  if (debug)
-    fprintf(stderr, "launch_sweep: encode %d %d nx=%d ny=%d rows=%d np=%d\n", (int)e1, (int)e2, g.nx, g.ny, g.rows,
-            g.p_hi - g.p_lo);
   if (e1 != CUDA_SUCCESS || e2 != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const int tiles_x = (g.nx + G::TX - 1) / G::TX, tiles_y = (g.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
@@ -859,9 +853,8 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   auto go = [&](auto kernel) {
     const int smem = ecoarse ? G::SMEM_CORR : G::SMEM;
     const int resident = prepare_kernel(kernel, smem);
-    const int zc = zc_override > 0 ? zc_override : choose_zc(ntiles, np, resident, rbgs ? 4 : 2, min_zc_for(g, sizeof(T)));
+    const int zc = choose_zc(ntiles, np, resident, rbgs ? 4 : 2, min_zc_for(g, sizeof(T)));
     const int nitems = ntiles * ((np + zc - 1) / zc);
-    if (debug) fprintf(stderr, "launch_sweep: resident=%d zc=%d nitems=%d smem=%d\n", resident, zc, nitems, smem);
     if (npartial) *npartial = nitems;
     kernel<<<nitems, NT, smem, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial, te, gce);
   };
@@ -1131,8 +1124,6 @@ cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cud
   const int tiles_x = (gf.nx + G::TX - 1) / G::TX, tiles_y = (gf.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = gf.p_hi - gf.p_lo;
-  // MG_PROLONG_V selects a variant for A/B measurement (tools/prolab.sh)
-  static const int var = getenv("MG_PROLONG_V") ? atoi(getenv("MG_PROLONG_V")) : 0;  // thread-safe one-time read
   auto go = [&](auto kernel) {
     const int resident = resident_ctas((const void*)kernel, NT, 0);
     const int zc = choose_zc(ntiles, np, resident, 0, min_zc_for(gf, sizeof(T)));
@@ -1157,21 +1148,15 @@ cudaError_t launch_prolong(const Geom& gf, const Geom& gc, const T* e, T* u, cud
     kernel<<<grid, 256, 0, st>>>(gf, gc, e, u, nvec, nrow, (unsigned)n, zg_lo, zg_hi);
     return cudaGetLastError();
   };
-  // measured on C3 L0 (tools/prolab.sh): flat<6> 0.411 ms FP64 / 0.225 ms FP32,
-  // marching <4,2> 0.425 / 0.238, <2,2,pipelined> 0.419 / 0.228, flat<8> (spills) 0.437 / 0.228,
-  // flat<4> 0.541 / 0.252 (5 CTAs of 256 per SM), one plane per item with 8 / 6 CTAs 0.458 / 0.473
-  // (FP64; 2 u vectors in flight per thread beat occupancy alone)
-  switch (var) {
-    case 1: return go(k_prolong3d<T, 4, 2, false>);
-    case 2: return go(k_prolong3d<T, 2, 2, true>);
-    case 3: return go_flat(k_prolong3d_flat<T, 8>);
-    default: return go_flat(k_prolong3d_flat<T, 6>);
-  }
+  // measured on C3 L0: flat<6> 0.411 ms FP64 / 0.225 ms FP32 beat the z-marching
+  // variants (0.419-0.425 / 0.228-0.238) and other occupancies; the marching kernel is kept for
+  // levels with >= 2^31 thread items
+  return go_flat(k_prolong3d_flat<T, 6>);
 }
 
 template <typename T>
 cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>& c, const T* u, const T* f, T* fc,
-                                  int zc_override, cudaStream_t st) {
+                                  cudaStream_t st) {
   if (!gf.three_d) return pm2::launch_resid_restrict<T>(gf, gc, c, u, f, fc, st);
   using G = Geo<T>;
   CUtensorMap tu, tf;
@@ -1182,17 +1167,17 @@ cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>&
   const int npc = gc.p_hi - gc.p_lo;
   auto kernel = k_resid_restrict3d<T>;
   const int resident = prepare_kernel(kernel, G::SMEM);
-  const int zcc = zc_override > 0 ? zc_override : choose_zc(ntiles, npc, resident, 2, min_zc_for(gf, sizeof(T)));
+  const int zcc = choose_zc(ntiles, npc, resident, 2, min_zc_for(gf, sizeof(T)));
   const int nitems = ntiles * ((npc + zcc - 1) / zcc);
   kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, gf, gc, c, fc, tiles_x, ntiles, zcc, nitems);
   return cudaGetLastError();
 }
 
 template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool, const double*, const double*,
-                                          double*, bool, int, cudaStream_t, double*, int*, const double*,
+                                          double*, bool, cudaStream_t, double*, int*, const double*,
                                           const Geom*);
 template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
-                                         bool, int, cudaStream_t, double*, int*, const float*, const Geom*);
+                                         bool, cudaStream_t, double*, int*, const float*, const Geom*);
 template int sweep_partials<double>(const Geom&, bool);
 template int sweep_partials<float>(const Geom&, bool);
 template int norm_partials<double>(const Geom&);
@@ -1204,9 +1189,9 @@ template cudaError_t launch_norm<float>(const Geom&, const Coef<float>&, const f
 template cudaError_t launch_prolong<double>(const Geom&, const Geom&, const double*, double*, cudaStream_t);
 template cudaError_t launch_prolong<float>(const Geom&, const Geom&, const float*, float*, cudaStream_t);
 template cudaError_t launch_resid_restrict<double>(const Geom&, const Geom&, const Coef<double>&, const double*,
-                                                   const double*, double*, int, cudaStream_t);
+                                                   const double*, double*, cudaStream_t);
 template cudaError_t launch_resid_restrict<float>(const Geom&, const Geom&, const Coef<float>&, const float*,
-                                                  const float*, float*, int, cudaStream_t);
+                                                  const float*, float*, cudaStream_t);
 
 }  // namespace pm
 }  // namespace mg

@@ -18,14 +18,14 @@ bool supported(const Geom& g, int min_nx);
 // ecoarse != nullptr: the input is u_in + P ecoarse (prolongation + correction fused, 3D)
 template <typename T>
 cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
-                         int zc, cudaStream_t st, double* partial = nullptr, int* npartial = nullptr,
+                         cudaStream_t st, double* partial = nullptr, int* npartial = nullptr,
                          const T* ecoarse = nullptr, const Geom* gcoarse = nullptr);
 template <typename T>
 int sweep_partials(const Geom& g, bool rbgs);
 // fc (coarse interior) = FW(f - A u) ; coarse boundary untouched
 template <typename T>
 cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>& c, const T* u, const T* f, T* fc,
-                                  int zcc, cudaStream_t st);
+                                  cudaStream_t st);
 // residual-norm partials (one double per CTA); *npartial = count written
 template <typename T>
 cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f, double* partial, int* npartial,

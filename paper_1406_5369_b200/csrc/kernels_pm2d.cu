@@ -822,11 +822,7 @@ static int resident_warps(K kernel, int smem) {
 }
 
 static void split(int nstrips, int rows, int rw, int& nch, int& nblocks) {
-  static const int min_rows = [] {  // tuning knob MG_PM2_MINROWS (thread-safe one-time read)
-    const char* e = getenv("MG_PM2_MINROWS");
-    const int v = e ? atoi(e) : kMinRows;
-    return v < 2 ? 2 : v;
-  }();
+  constexpr int min_rows = kMinRows;
   nch = rw / nstrips;
   const int cap = rows / min_rows;
   if (nch > cap) nch = cap;

@@ -14,6 +14,7 @@
 
 #include "kernels.h"
 #include "kernels_tail.h"
+#include "launch_util.h"
 
 namespace mg {
 
@@ -328,8 +329,9 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
 
 template <typename T>
 cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
-  // 16 CTAs (non-portable) where allowed, else the portable 8 (thread-safe one-time probe)
-  static const int cluster = [] {
+  // 16 CTAs (non-portable) where allowed, else the portable 8; probed once per device (the
+  // non-portable opt-in is a per-device function attribute)
+  const int cluster = per_device_once((const void*)k_tail<T>, [] {
     int c = 8;
     if (cudaFuncSetAttribute(k_tail<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
       cudaLaunchConfig_t q = {};
@@ -347,16 +349,13 @@ cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
     }
     cudaGetLastError();
     return c;
-  }();
+  });
   // tiny tails (a few thousand nodes, e.g. the whole 65^2 C1 hierarchy) run faster on one CTA
   const Geom& g0 = p.g[0];
   const long long top = (long long)(g0.nx - 1) * (g0.three_d ? g0.ny - 1 : 1) * (g0.p_hi - g0.p_lo);
   const int csize = top <= 8192 ? 1 : cluster;
   // levels from solo_from on run on CTA 0 alone with block barriers (all of them on one CTA)
-  static const long long solo_max = [] {  // tuning knob MG_TAIL_SOLO (thread-safe one-time read)
-    const char* e = getenv("MG_TAIL_SOLO");
-    return e ? atoll(e) : 2048ll;
-  }();
+  constexpr long long solo_max = 2048;  // measured: threshold scan 512-8192
   TailParams<T> q = p;
   q.solo_from = p.nl;
   for (int k = 0; k < p.nl; k++) {

@@ -39,4 +39,17 @@ int resident_ctas(const void* kernel, int threads, int smem) {
   return r;
 }
 
+int per_device_once(const void* key, int (*probe)()) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  static std::map<std::pair<int, const void*>, int> cache;
+  const auto k = std::make_pair(dev, key);
+  auto it = cache.find(k);
+  if (it != cache.end()) return it->second;
+  const int r = probe();
+  cache[k] = r;
+  return r;
+}
+
 }  // namespace mg

@@ -391,10 +391,7 @@ struct Exec {
   int tail_level() const {
     if (s->cfg.flags & MG_FLAG_BASELINE) return s->L;
     const int first = s->pt.slab ? s->pt.la : 0;
-    static const long long tail_max = [] {  // tuning knob MG_TAIL_MAX (thread-safe one-time read)
-      const char* e = getenv("MG_TAIL_MAX");
-      return e ? atoll(e) : 48ll * 1024;
-    }();
+    constexpr long long tail_max = 48ll * 1024;  // measured on C2/C3/C4
     for (int l = first; l < s->L; l++) {
       const Geom& g = s->lv[l].g;
       const long long n = (long long)(g.nx - 1) * (g.three_d ? g.ny - 1 : 1) * (g.nz - 1);
@@ -428,12 +425,6 @@ struct Exec {
     double bytes = 0;
     for (int k = 0; k < P.nl; k++) bytes += w(lt + k) * (3.0 * (P.nu1 + P.nu2) + 6.0);
     return launch(s, st, K_TAIL, lt, bytes, [&] { return launch_tail<T>(P, st); });
-  }
-
-  // z-chunk override for tuning (MG_ZC); 0 = the launcher's own choice
-  int zc(int) const {
-    static const int v = getenv("MG_ZC") ? atoi(getenv("MG_ZC")) : 0;  // thread-safe one-time read
-    return v;
   }
 
 
@@ -475,7 +466,7 @@ struct Exec {
         gr.p_lo = lo;
         gr.p_hi = hi;
         return launch(s, st, kind, l, (zero_in ? 2 : 3) * w(l) * (hi - lo) / (L.g.p_hi - L.g.p_lo), [&] {
-          return pm::launch_sweep<T>(gr, coef(l), rb, zero_in ? nullptr : in, f, out, zero_in, zc(l), st);
+          return pm::launch_sweep<T>(gr, coef(l), rb, zero_in ? nullptr : in, f, out, zero_in, st);
         });
       };
       mg_status r;
@@ -542,7 +533,7 @@ struct Exec {
   // 2D omega-Jacobi on a marching level: n sweeps run as passes of up to 3 (FP32) / 2 (FP64)
   // fused sweeps (pm2::launch_jacobi_k, temporal blocking; bitwise equal to single sweeps)
   bool kfusable(int l) const {
-    static const bool off = getenv("MG_NO_KFUSE") != nullptr;
+    const bool off = s->cfg.flags & MG_FLAG_NO_KFUSE;
     const Level& L = s->lv[l];
     return !off && pm(l) && !L.g.three_d && s->cfg.smoother == MG_JACOBI && !L.dist;
   }
@@ -604,7 +595,7 @@ struct Exec {
   // level 0 with the residual norm of its input accumulated on the fly) and a TAIL
   // (the rest).  mg_solve pipelines tail(k) + head(k+1): the norm after cycle k is
   // computed by the next cycle's first sweep, which reads u and f anyway.
-  bool can_split() const { return s->L > 1 && s->cfg.nu1 >= 1 && pm(0); }
+  bool can_split() const { return s->L > 1 && s->cfg.nu1 >= 1 && pm(0) && tail_level() > 0; }
 
   mg_status cycle_start(T* u0, const T* f0) {
     const bool jac = s->cfg.smoother == MG_JACOBI;
@@ -644,7 +635,7 @@ struct Exec {
       return norm_finish(0, np, out_dev);
     }
     if ((r = launch(s, st, K_SWEEP_NORM, 0, 3 * w(0), [&] {
-           return pm::launch_sweep<T>(L.g, coef(0), rb, u0, f0, t0, false, zc(0), st, s->d_partial, &np);
+           return pm::launch_sweep<T>(L.g, coef(0), rb, u0, f0, t0, false, st, s->d_partial, &np);
          })) != MG_OK)
       return r;
     return norm_finish(0, np, out_dev);
@@ -732,7 +723,7 @@ struct Exec {
           if ((r = exchange(l, cur[l], 2)) != MG_OK) return r;
           const T* uc = cur[l];
           if ((r = launch(s, st, K_RESID_RESTRICT, l, 2 * w(l) + w(l + 1), [&] {
-                 return pm::launch_resid_restrict<T>(L.g, gcw, coef(l), uc, f, fc, zc(l + 1), st);
+                 return pm::launch_resid_restrict<T>(L.g, gcw, coef(l), uc, f, fc, st);
                })) != MG_OK)
             return r;
         } else {
@@ -777,7 +768,7 @@ struct Exec {
           T* out = oth[l];
           const Geom gcg = s->lv[l + 1].g;
           if ((r = launch(s, st, K_SWEEP_CORR, l, (3 + 1.0 / (1 << s->cfg.dim)) * w(l), [&] {
-                 return pm::launch_sweep<T>(L.g, coef(l), rb, in, f, out, false, zc(l), st, nullptr, nullptr, e, &gcg);
+                 return pm::launch_sweep<T>(L.g, coef(l), rb, in, f, out, false, st, nullptr, nullptr, e, &gcg);
                })) != MG_OK)
             return r;
           std::swap(cur[l], oth[l]);
@@ -989,15 +980,13 @@ struct CdExec {
   // CD2: the complex sweep is already issue-bound alone, so K = 2 passes
   // are SLOWER than two single sweeps (0.37 vs 0.25 ms at 4096^2 FP32); kmax defaults to 1
   // and the fused kernel serves the solve's head (first sweep + the input's norm in one
-  // pass).  MG_CD_KMAX = 2 / 3 re-enables multi-sweep passes.
+  // pass).  MG_FLAG_CD_KFUSE re-enables multi-sweep passes (3 FP32 / 2 FP64).
   bool kfusable(int l) const {
-    static const bool off = getenv("MG_NO_KFUSE") != nullptr;
+    const bool off = s->cfg.flags & MG_FLAG_NO_KFUSE;
     return !off && s->cfg.smoother == MG_JACOBI && !(s->cfg.flags & MG_FLAG_BASELINE) && cd2d_supported(G(l));
   }
   int kmax() const {
-    static const int env = getenv("MG_CD_KMAX") ? atoi(getenv("MG_CD_KMAX")) : 1;
-    const int cap = sizeof(T) == 4 ? 3 : 2;
-    return env < 1 ? 1 : (env > cap ? cap : env);
+    return (s->cfg.flags & MG_FLAG_CD_KFUSE) ? (sizeof(T) == 4 ? 3 : 2) : 1;
   }
   int passes(int l, int n) const { return kfusable(l) ? (n + kmax() - 1) / kmax() : n; }
   int first_k(int l, int n) const {

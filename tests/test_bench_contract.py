@@ -31,6 +31,47 @@ def test_reference_arm_contract():
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert "workload" in d["config"]
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.workload_config("C1")  # the same config object as the product arm
+
+
+def test_cpu_baseline_leg_reports_all_threads_one_thread_and_model():
+    """The product arm's cpu_baseline comes from this child leg (the product process never maps
+    the oracle): the oracle on all host threads, on one thread, and the host CPU model."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--cpu-baseline-leg", "--config", "C1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["kind"] == "oracle" and d["value"] > 0 and d["cores"] >= 1 and d["sample"]
+    assert d["one_thread"]["cores"] == 1 and d["one_thread"]["value"] > 0
+    assert "cpu_model" in d
+
+
+def test_gpus_must_match_the_launch():
+    """--gpus N is never silently timed on fewer GPUs: WORLD_SIZE != N is rejected, and without
+    torchrun N > 1 needs N visible devices (none here) before bench.py re-launches itself."""
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--impl", "reference",
+                        "--config", "C1"], cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 2 and "WORLD_SIZE=2" in r.stderr and not r.stdout.strip()
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "C1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 2 and "device" in r.stderr and not r.stdout.strip()
+
+
+def test_reference_arm_self_launches_torchrun():
+    """--gpus 2 without torchrun: bench.py re-launches itself under torch.distributed.run with two
+    ranks; rank 0 alone prints the one line."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
+                        "--gpus", "2", "--steps", "2", "--warmup", "3"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
 
 
 @pytest.mark.gpu
@@ -48,6 +89,9 @@ def test_product_arm_contract():
     c = d["clocks"]
     assert c["sm_mhz"] > 0 and c["sm_max_mhz"] > 0 and isinstance(c["reasons"], list)
     assert "workload" in d["config"] and "l2" in d["config"]
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.workload_config("C2")
 
 
 def test_reference_arm_under_torchrun():

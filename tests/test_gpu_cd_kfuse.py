@@ -1,15 +1,11 @@
 """Temporal blocking of the 2D complex-diffusion Jacobi smoother (kernels_cd2d.cu
 k_cd_jacobi2d_k): up to 3 (FP32) / 2 (FP64) sweeps with the frozen lagged diffusivity
-per pass over overlapping strips (opt-in, MG_CD_KMAX; measured slower than single sweeps,
+per pass over overlapping strips (opt-in, MG_FLAG_CD_KFUSE; measured slower than single sweeps,
 DESIGN.md §10), one more level-0 post pass when the pass count would change the
 ping-pong parity, and the solve's head = g(u) + the first pre-smoothing pass with
 ||f - A(g(u)) u|| accumulated by its first stage (default).  Every cell value is a single
 sweep's canonical complex arithmetic (reading 19), so iterates stay
 bitwise the oracle's (oracle/cd_oracle.c) for every (nu1, nu2)."""
-import os
-import subprocess
-import sys
-
 import numpy as np
 import pytest
 
@@ -64,29 +60,22 @@ def test_cd_kfused_strip_edges():
         assert np.array_equal(S.to_numpy(du), O.cycle(u, f)), cells
 
 
-def test_cd_multisweep_passes_bitwise():
-    """MG_CD_KMAX = 3 (FP32) / 2 (FP64): every (nu1, nu2) of NU through K-sweep passes, in a
-    fresh process (the knob is read once per process)."""
-    here = os.path.dirname(os.path.abspath(__file__))
-    code = (
-        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
-        "import numpy as np\n"
-        "from paper_1406_5369_b200 import workloads as wl\n"
-        "from test_gpu_cd import make\n"
-        "from test_gpu_cd_kfuse import NU\n"
-        "bad = []\n"
-        "for dt in ('f32', 'f64'):\n"
-        "    for nu in NU:\n"
-        "        S, O = make(2, (248, 72), 3, 'jacobi', nu1=nu[0], nu2=nu[1], dtype=dt)\n"
-        "        u, f = wl.cd_workload(2, (248, 72), seed=7, dtype=S.np_dtype)\n"
-        "        du, df = S.from_numpy(u), S.from_numpy(f)\n"
-        "        k, hist = S.solve(du, df, 0.0, 2)\n"
-        "        uo, k_or, hist_or = O.solve(u, f, 0.0, 2)\n"
-        "        if not np.array_equal(S.to_numpy(du), uo): bad.append((dt, nu))\n"
-        "        S.vcycle(du, df); uo = O.cycle(uo, f)\n"
-        "        if not np.array_equal(S.to_numpy(du), uo): bad.append((dt, nu, 'vcycle'))\n"
-        "print('BAD', bad)\n"
-        "sys.exit(1 if bad else 0)\n") % (here, os.path.dirname(here))
-    env = dict(os.environ, MG_CD_KMAX="3")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_cd_multisweep_passes_bitwise(dt):
+    """MG_FLAG_CD_KFUSE: passes of 3 (FP32) / 2 (FP64) sweeps, every (nu1, nu2) of NU; solve and
+    vcycle bitwise equal to the oracle."""
+    import paper_1406_5369_b200 as mgb
+    bad = []
+    for nu in NU:
+        S, O = make(2, (248, 72), 3, "jacobi", nu1=nu[0], nu2=nu[1], dtype=dt, flags=mgb.FLAG_CD_KFUSE)
+        u, f = wl.cd_workload(2, (248, 72), seed=7, dtype=S.np_dtype)
+        du, df = S.from_numpy(u), S.from_numpy(f)
+        k, hist = S.solve(du, df, 0.0, 2)
+        uo, k_or, hist_or = O.solve(u, f, 0.0, 2)
+        if not np.array_equal(S.to_numpy(du), uo):
+            bad.append(nu)
+        S.vcycle(du, df)
+        uo = O.cycle(uo, f)
+        if not np.array_equal(S.to_numpy(du), uo):
+            bad.append((nu, "vcycle"))
+    assert not bad, bad

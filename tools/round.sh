@@ -48,9 +48,9 @@ for st in "$@"; do
       timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench/reference_C3-f64.json 2>&1
       tail -1 $OUT/bench/reference_C3-f64.json | cut -c1-300 ;;
     launches)
-      python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --host-loop > $OUT/launches_plain.json 2>&1 && \
+      python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-c5 --host-loop > $OUT/launches_plain.json 2>&1 && \
       ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/C3-f64_launches.csv \
-          python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --host-loop > $OUT/launches_ncu.log 2>&1
+          python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-c5 --host-loop > $OUT/launches_ncu.log 2>&1
       echo "launches rc=$?"
       python tools/launch_shares.py $OUT/C3-f64_launches.csv > $OUT/C3-f64_launch_shares.txt 2>&1
       head -20 $OUT/C3-f64_launch_shares.txt ;;
@@ -74,7 +74,7 @@ for st in "$@"; do
     ab:*)
       cfg=${st#ab:}
       for i in 1 2 3; do
-        timeout 600 python bench.py --config $cfg --no-cpu --no-e2e > $OUT/ab_${cfg}_$i.json 2> /dev/null
+        timeout 600 python bench.py --config $cfg --no-cpu --no-e2e --no-c5 > $OUT/ab_${cfg}_$i.json 2> /dev/null
         summ "$cfg#$i" $OUT/ab_${cfg}_$i.json
       done | tee $OUT/ab_${cfg}.txt ;;
     *) echo "unknown stage $st" ;;
