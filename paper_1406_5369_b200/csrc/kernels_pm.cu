@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <utility>
 
 #include "kernels_pm.h"
 #include "kernels_pm2d.h"
@@ -583,6 +584,329 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Row-blocked sweep (the default for every variant but CORR): the same tile, boxes, ring,
+// arithmetic and red/black schedule as k_sweep3d, but a thread owns RPT consecutive tile
+// rows of its x-vector (NTH = 32 TY / RPT threads per CTA).  The y-neighbours of a row that
+// lie inside the thread's own rows come from registers: its rows' u(p) for the red stage,
+// its rows' post-red values of plane p-1 for the black stage (the black node at (j, row k)
+// has its y-neighbours at the red positions of rows k-1 / k+1 with the same index m).  Only
+// the outer rows read the row above / below from shared memory.  Per-plane fixed costs
+// (ring waits, slot addresses, barrier, loop control) are shared by RPT rows, and the
+// register budget per thread (NTH threads, 2 CTAs per SM) doubles.  Bitwise identical
+// results (the per-node operations and their order are those of k_sweep3d).
+template <int N, class F, int... I>
+__device__ __forceinline__ void sfor_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>()), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  sfor_impl<N>(f, std::make_integer_sequence<int, N>());
+}
+
+template <typename T, int MODE, bool ZERO, bool NRM, int RPT>
+__global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
+    k_sweep3d_rows(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f, Geom g,
+                   Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems,
+                   double* __restrict__ partial) {
+  using G = Geo<T>;
+  using V = Vec<T, G::W>;
+  constexpr int W = G::W, TX = G::TX, BX = G::BX, HX = G::HX, PX = G::PX, NR = G::NRED, RCOL = G::RCOL;
+  constexpr int NTH = 32 * TY / RPT;
+  constexpr bool RB = MODE == 1;
+  static_assert(TY % RPT == 0, "rows per thread");
+  extern __shared__ __align__(128) unsigned char sm[];
+  const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
+  T* spr = reinterpret_cast<T*>(sm + G::PR_OFF);
+  auto PRb = [&](int q) { return spr + (size_t)(((q % 3) + 3) % 3) * (G::PB / sizeof(T)); };
+  auto su = [&](const T* base, int off) -> T { return ZERO ? (T)0 : base[off]; };
+  auto svec = [&](const T* base, int off) -> V {
+    if (ZERO) {
+      V z;
+#pragma unroll
+      for (int k = 0; k < W; k++) z.v[k] = (T)0;
+      return z;
+    }
+    return ld_vec(base + off);
+  };
+
+  const int tid = threadIdx.x, lane = tid & 31, wr = tid >> 5;
+  const int ty0 = wr * RPT;                        // first tile row of the thread
+  const int bo = (ty0 + 2) * BX + W * lane + HX;  // u-box offset of (ox, row 0); row k: + k BX
+  const int fo = (ty0 + 1) * BX + W * lane + HX;  // f-box offset
+  const int po = (ty0 + 1) * PX + W * lane + HX;  // PR offset
+  uint32_t seq = 0;
+  double nsum = 0.0;
+
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    int tile, pa, pb;
+    item_of(it, ntiles, zc, g.p_lo, g.p_hi, tile, pa, pb);
+    const int x0 = (tile % tiles_x) * TX, y0 = (tile / tiles_x) * TY;
+    const int ox = x0 + W * lane, oy0 = y0 + ty0;
+    bool in[RPT][W];
+#pragma unroll
+    for (int k = 0; k < RPT; k++) {
+      const bool rin = oy0 + k >= 1 && oy0 + k <= g.ny - 1;
+#pragma unroll
+      for (int j = 0; j < W; j++) in[k][j] = rin && ox + j >= 1 && ox + j <= g.nx - 1;
+    }
+    T* orow = unew + (long long)oy0 * g.pitch;
+
+    const int qlo = RB ? pa - 3 : pa - 2, qlast = RB ? pb : pb - 1;
+    const uint32_t nlo = seq;
+    auto N = [&](int q) { return nlo + (uint32_t)(q - qlo); };
+    auto issue_step = [&](int q) { R.issue(N(q), &tm_u, &tm_f, x0, y0, q + 1, q, !ZERO); };
+    if (tid == 0)
+      for (int q = qlo; q < qlo + G::NS && q <= qlast; q++) issue_step(q);
+
+    R.wait(N(qlo));
+    R.wait(N(qlo + 1));
+    V um[RPT], u0[RPT], up[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; k++) {
+      um[k] = svec(R.U(N(qlo)), bo + k * BX);
+      u0[k] = svec(R.U(N(qlo + 1)), bo + k * BX);
+    }
+
+    // RB ring threads, as in k_sweep3d (warps 0 .. 2 NR - 1: ring rows; warp 2 NR: ring columns)
+    constexpr int RWARPS = 2 * NR;
+    static_assert(RWARPS < NTH / 32, "ring warps");
+    const bool ring_row = RB && wr < RWARPS;
+    const bool ring_col = RB && wr == RWARPS && lane < 2 * RCOL;
+    const int mring = ring_row ? (wr >> 1) : 0;
+    auto ring_pos = [&](int pgl, int m, int& x, int& y) {
+      if (wr < RWARPS) {
+        y = (wr & 1) == 0 ? y0 - 1 : y0 + TY;
+        x = x0 + W * lane + 2 * m + ((y + pgl) & 1);
+      } else {
+        x = lane < RCOL ? x0 - 1 : x0 + TX;
+        y = y0 + 2 * (lane % RCOL) + ((x + y0 + pgl) & 1);
+      }
+    };
+    T rzm = (T)0;
+    if (ring_row || ring_col) {
+      int x, y;
+      ring_pos(pa - 1 + g.p_glob0, mring, x, y);
+      rzm = su(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
+    }
+    __syncthreads();  // step qlo lives on in registers only: refill its slot
+    if (tid == 0 && qlo + G::NS <= qlast) {
+      fence_proxy_async();
+      issue_step(qlo + G::NS);
+    }
+
+    if constexpr (RB) {
+      T pr1[RPT][NR], pr2[RPT][NR];  // own red values of planes p-1, p-2, per row
+      V fprev[RPT];                   // f(p-1)
+#pragma unroll
+      for (int k = 0; k < RPT; k++) {
+#pragma unroll
+        for (int m = 0; m < NR; m++) pr1[k][m] = pr2[k][m] = (T)0;
+#pragma unroll
+        for (int j = 0; j < W; j++) fprev[k].v[j] = (T)0;
+      }
+      for (int p = pa - 1; p <= pb; p++) {
+        R.wait(N(p));
+        const T* U0 = R.U(N(p - 1));  // u(p)
+        const T* Up = R.U(N(p));      // u(p+1)
+        const T* F0 = R.F(N(p));      // f(p)
+        T* PR = PRb(p);
+#pragma unroll
+        for (int k = 0; k < RPT; k++) up[k] = svec(Up, bo + k * BX);
+        const int pgl = p + g.p_glob0;
+        const bool pl_in = pgl >= 1 && pgl <= g.nz - 1;
+        const int kr0 = (oy0 + pgl) & 1;  // red offset of row 0 (row k: kr0 ^ (k & 1)), warp uniform
+        const bool nrm_here = NRM && p >= pa && p < pb;
+        T pr0[RPT][NR];
+        V fcur[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; k++) fcur[k] = ld_vec(F0 + fo + k * BX);
+        auto red_stage = [&](auto KR0c) {
+          static_for<RPT>([&](auto Kc) {
+            constexpr int K = decltype(Kc)::value;
+            constexpr int KR = decltype(KR0c)::value ^ (K & 1);
+            const V dn = K == 0 ? svec(U0, bo - BX) : u0[K > 0 ? K - 1 : 0];
+            const V upr = K == RPT - 1 ? svec(U0, bo + (K + 1) * BX) : u0[K < RPT - 1 ? K + 1 : 0];
+            const T edge = KR == 0 ? su(U0, bo + K * BX - 1) : su(U0, bo + K * BX + W);
+            if constexpr (NRM) {
+              if (nrm_here) {  // black nodes of plane p: residual of the old iterate
+                const T oedge = KR == 0 ? su(U0, bo + K * BX + W) : su(U0, bo + K * BX - 1);
+#pragma unroll
+                for (int m = 0; m < NR; m++) {
+                  const int j = (1 - KR) + 2 * m;
+                  const T l = j == 0 ? oedge : u0[K].v[j > 0 ? j - 1 : 0];
+                  const T r = j == W - 1 ? oedge : u0[K].v[j < W - 1 ? j + 1 : 0];
+                  const double rr = (double)sub(
+                      fcur[K].v[j], apply_A(c, u0[K].v[j], l, r, dn.v[j], upr.v[j], um[K].v[j], up[K].v[j]));
+                  if (in[K][j]) nsum = acc_sq_d<T>(nsum, rr);
+                }
+              }
+            }
+            V pv = u0[K];
+#pragma unroll
+            for (int m = 0; m < NR; m++) {
+              const int j = KR + 2 * m;
+              const T ctr = u0[K].v[j];
+              const T l = j == 0 ? edge : u0[K].v[j > 0 ? j - 1 : 0];
+              const T r = j == W - 1 ? edge : u0[K].v[j < W - 1 ? j + 1 : 0];
+              const T res = sub(fcur[K].v[j], apply_A(c, ctr, l, r, dn.v[j], upr.v[j], um[K].v[j], up[K].v[j]));
+              const T v = add(ctr, mul(c.wd, res));
+              if (NRM && nrm_here && in[K][j]) nsum = acc_sq<T>(nsum, res);
+              const T prv = (pl_in && in[K][j]) ? v : ctr;
+              pv.v[j] = prv;
+              pr0[K][m] = prv;
+            }
+            if constexpr (sizeof(T) == 8)
+              *reinterpret_cast<double2*>(PR + po + K * PX) = make_double2(pv.v[0], pv.v[1]);
+            else
+              *reinterpret_cast<float4*>(PR + po + K * PX) = make_float4(pv.v[0], pv.v[1], pv.v[2], pv.v[3]);
+          });
+        };
+        if (kr0)
+          red_stage(std::integral_constant<int, 1>());
+        else
+          red_stage(std::integral_constant<int, 0>());
+        if (ring_row || ring_col) {  // the red ring node of plane p
+          int x, y;
+          ring_pos(pgl, mring, x, y);
+          const int rb = (y - y0 + 2) * BX + (x - x0 + HX);
+          const T ctr = su(U0, rb);
+          const T v = relax(c, ctr, su(U0, rb - 1), su(U0, rb + 1), su(U0, rb - BX), su(U0, rb + BX), rzm, su(Up, rb),
+                            F0[(y - y0 + 1) * BX + (x - x0 + HX)]);
+          const bool ok = pl_in && x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1;
+          PR[(y - y0 + 1) * PX + (x - x0 + HX)] = ok ? v : ctr;
+          ring_pos(pgl + 1, mring, x, y);
+          rzm = su(U0, (y - y0 + 2) * BX + (x - x0 + HX));
+        }
+        __syncthreads();
+        // every thread is past plane p-2's black update and plane p's red stage: step p-1
+        // (u(p), f(p-1); f(p-1) is in registers) is consumed
+        if (tid == 0 && p >= pa - 1 && p - 1 + G::NS <= qlast) {
+          fence_proxy_async();
+          issue_step(p - 1 + G::NS);
+        }
+        const int bp = p - 1;
+        if (bp >= pa) {
+          const T* P = PRb(bp);
+          auto black_stage = [&](auto KB0c) {
+            static_for<RPT>([&](auto Kc) {
+              constexpr int K = decltype(Kc)::value;
+              constexpr int KB = decltype(KB0c)::value ^ (K & 1);
+              T pdn[NR], pup[NR];
+              if constexpr (K == 0) {
+                if constexpr (W == 4) {
+                  const V a = ld_vec(P + po - PX);
+#pragma unroll
+                  for (int m = 0; m < NR; m++) pdn[m] = a.v[KB + 2 * m];
+                } else {
+                  pdn[0] = P[po + KB - PX];
+                }
+              } else {
+#pragma unroll
+                for (int m = 0; m < NR; m++) pdn[m] = pr1[K > 0 ? K - 1 : 0][m];
+              }
+              if constexpr (K == RPT - 1) {
+                if constexpr (W == 4) {
+                  const V a = ld_vec(P + po + (K + 1) * PX);
+#pragma unroll
+                  for (int m = 0; m < NR; m++) pup[m] = a.v[KB + 2 * m];
+                } else {
+                  pup[0] = P[po + (K + 1) * PX + KB];
+                }
+              } else {
+#pragma unroll
+                for (int m = 0; m < NR; m++) pup[m] = pr1[K < RPT - 1 ? K + 1 : 0][m];
+              }
+              const T edge = KB == 0 ? P[po + K * PX - 1] : P[po + K * PX + W];
+              V o;
+#pragma unroll
+              for (int m = 0; m < NR; m++) o.v[(1 - KB) + 2 * m] = pr1[K][m];
+#pragma unroll
+              for (int m = 0; m < NR; m++) {
+                const int j = KB + 2 * m;
+                const T ctr = um[K].v[j];
+                const T l = (KB == 0 && m == 0) ? edge : pr1[K][KB == 1 ? m : (m > 0 ? m - 1 : 0)];
+                const T r = (KB == 1 && m == NR - 1) ? edge : pr1[K][KB == 0 ? m : (m + 1 < NR ? m + 1 : 0)];
+                const T v = relax(c, ctr, l, r, pdn[m], pup[m], pr2[K][m], pr0[K][m], fprev[K].v[j]);
+                o.v[j] = in[K][j] ? v : ctr;
+              }
+              store_vec(orow + (long long)K * g.pitch + (long long)bp * g.pstride, ox, in[K], o);
+            });
+          };
+          if (kr0)
+            black_stage(std::integral_constant<int, 1>());
+          else
+            black_stage(std::integral_constant<int, 0>());
+        }
+#pragma unroll
+        for (int k = 0; k < RPT; k++) {
+          um[k] = u0[k];
+          u0[k] = up[k];
+          fprev[k] = fcur[k];
+#pragma unroll
+          for (int m = 0; m < NR; m++) {
+            pr2[k][m] = pr1[k][m];
+            pr1[k][m] = pr0[k][m];
+          }
+        }
+      }
+    } else {
+      for (int p = pa; p < pb; p++) {
+        R.wait(N(p));
+        const T* U0 = R.U(N(p - 1));
+        const T* F0 = R.F(N(p));
+#pragma unroll
+        for (int k = 0; k < RPT; k++) up[k] = svec(R.U(N(p)), bo + k * BX);
+        static_for<RPT>([&](auto Kc) {
+          constexpr int K = decltype(Kc)::value;
+          const V fv = ld_vec(F0 + fo + K * BX);
+          const V dn = K == 0 ? svec(U0, bo - BX) : u0[K > 0 ? K - 1 : 0];
+          const V upr = K == RPT - 1 ? svec(U0, bo + (K + 1) * BX) : u0[K < RPT - 1 ? K + 1 : 0];
+          const T el = su(U0, bo + K * BX - 1), er = su(U0, bo + K * BX + W);
+          V o;
+#pragma unroll
+          for (int j = 0; j < W; j++) {
+            const T l = j == 0 ? el : u0[K].v[j > 0 ? j - 1 : 0];
+            const T r = j == W - 1 ? er : u0[K].v[j < W - 1 ? j + 1 : 0];
+            const T res = sub(fv.v[j], apply_A(c, u0[K].v[j], l, r, dn.v[j], upr.v[j], um[K].v[j], up[K].v[j]));
+            if (MODE == 2) {
+              if (in[K][j]) nsum = acc_sq_d<T>(nsum, (double)res);
+            } else {
+              if (NRM && in[K][j]) nsum = acc_sq<T>(nsum, res);
+              o.v[j] = in[K][j] ? add(u0[K].v[j], mul(c.wd, res)) : u0[K].v[j];
+            }
+          }
+          if (MODE != 2) store_vec(orow + (long long)K * g.pitch + (long long)p * g.pstride, ox, in[K], o);
+        });
+        __syncthreads();
+        if (tid == 0 && p - 1 + G::NS <= qlast) {
+          fence_proxy_async();
+          issue_step(p - 1 + G::NS);
+        }
+#pragma unroll
+        for (int k = 0; k < RPT; k++) {
+          um[k] = u0[k];
+          u0[k] = up[k];
+        }
+      }
+    }
+    seq = N(qlast) + 1;
+    __syncthreads();
+  }
+  if (MODE == 2 || NRM) {  // fixed-order block reduction -> one partial per CTA
+    double* red = reinterpret_cast<double*>(sm);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nsum = __dadd_rn(nsum, __shfl_down_sync(0xffffffffu, nsum, o));
+    if (lane == 0) red[wr] = nsum;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w2 = 0; w2 < NTH / 32; w2++) t = __dadd_rn(t, red[w2]);
+      partial[blockIdx.x] = t;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Fused residual + full-weighting restriction.  Work items are (coarse tile,
 // coarse z-chunk); the fine tile is 2x the coarse tile (x0 = 2 X0).  Per fine
 // plane q: r for every node of the tile (u column in registers) and the
@@ -794,9 +1118,13 @@ bool supported(const Geom& g, int min_nx) {
 // First use of a kernel: opt in to its dynamic shared memory and return the
 // number of CTAs the device keeps resident (cached per kernel).
 template <class K>
-static int prepare_kernel(K kernel, int smem) {
-  return resident_ctas((const void*)kernel, NT, smem);
+static int prepare_kernel(K kernel, int smem, int threads = NT) {
+  return resident_ctas((const void*)kernel, threads, smem);
 }
+
+// rows per thread of the row-blocked sweep (k_sweep3d_rows) and its CTA size
+constexpr int RPT = 2;
+constexpr int NTR = 32 * TY / RPT;
 
 // z-chunk size.  Measured on the 513^3 RBGS sweep (tools/scan_zc.py): what
 // matters is a nearly full last wave of resident CTAs and enough waves (>= ~8)
@@ -850,22 +1178,29 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   const int tiles_x = (g.nx + G::TX - 1) / G::TX, tiles_y = (g.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = g.p_hi - g.p_lo;
-  auto go = [&](auto kernel) {
-    const int smem = ecoarse ? G::SMEM_CORR : G::SMEM;
+  auto go = [&](auto kernel) {  // CORR: the one-row-per-thread kernel
+    const int smem = G::SMEM_CORR;
     const int resident = prepare_kernel(kernel, smem);
     const int zc = choose_zc(ntiles, np, resident, rbgs ? 4 : 2, min_zc_for(g, sizeof(T)));
     const int nitems = ntiles * ((np + zc - 1) / zc);
     if (npartial) *npartial = nitems;
     kernel<<<nitems, NT, smem, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial, te, gce);
   };
+  auto gor = [&](auto kernel) {  // row-blocked
+    const int resident = prepare_kernel(kernel, G::SMEM, NTR);
+    const int zc = choose_zc(ntiles, np, resident, rbgs ? 4 : 2, min_zc_for(g, sizeof(T)));
+    const int nitems = ntiles * ((np + zc - 1) / zc);
+    if (npartial) *npartial = nitems;
+    kernel<<<nitems, NTR, G::SMEM, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial);
+  };
   if (ecoarse)
     rbgs ? go(k_sweep3d<T, 1, false, false, true>) : go(k_sweep3d<T, 0, false, false, true>);
   else if (partial && !zero_in)
-    rbgs ? go(k_sweep3d<T, 1, false, true>) : go(k_sweep3d<T, 0, false, true>);
+    rbgs ? gor(k_sweep3d_rows<T, 1, false, true, RPT>) : gor(k_sweep3d_rows<T, 0, false, true, RPT>);
   else if (rbgs)
-    zero_in ? go(k_sweep3d<T, 1, true>) : go(k_sweep3d<T, 1, false>);
+    zero_in ? gor(k_sweep3d_rows<T, 1, true, false, RPT>) : gor(k_sweep3d_rows<T, 1, false, false, RPT>);
   else
-    zero_in ? go(k_sweep3d<T, 0, true>) : go(k_sweep3d<T, 0, false>);
+    zero_in ? gor(k_sweep3d_rows<T, 0, true, false, RPT>) : gor(k_sweep3d_rows<T, 0, false, false, RPT>);
   return cudaGetLastError();
 }
 
@@ -876,8 +1211,8 @@ int sweep_partials(const Geom& g, bool rbgs) {
   using G = Geo<T>;
   const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
   const int np = g.p_hi - g.p_lo;
-  const int resident = rbgs ? prepare_kernel(k_sweep3d<T, 1, false, true>, G::SMEM)
-                            : prepare_kernel(k_sweep3d<T, 0, false, true>, G::SMEM);
+  const int resident = rbgs ? prepare_kernel(k_sweep3d_rows<T, 1, false, true, RPT>, G::SMEM, NTR)
+                            : prepare_kernel(k_sweep3d_rows<T, 0, false, true, RPT>, G::SMEM, NTR);
   int best = 0;
   for (int halo : {2, 4}) {
     const int zc = choose_zc(ntiles, np, resident, halo, min_zc_for(g, sizeof(T)));
@@ -893,7 +1228,7 @@ int norm_partials(const Geom& g) {
   using G = Geo<T>;
   const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
   const int np = g.p_hi - g.p_lo;
-  const int resident = prepare_kernel(k_sweep3d<T, 2, false>, G::SMEM);
+  const int resident = prepare_kernel(k_sweep3d_rows<T, 2, false, false, RPT>, G::SMEM, NTR);
   const int zc = choose_zc(ntiles, np, resident, 2, min_zc_for(g, sizeof(T)));
   return ntiles * ((np + zc - 1) / zc);
 }
@@ -909,14 +1244,12 @@ cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f,
   const int tiles_x = (g.nx + G::TX - 1) / G::TX, tiles_y = (g.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = g.p_hi - g.p_lo;
-  auto kernel = k_sweep3d<T, 2, false>;
-  const int resident = prepare_kernel(kernel, G::SMEM);
+  auto kernel = k_sweep3d_rows<T, 2, false, false, RPT>;
+  const int resident = prepare_kernel(kernel, G::SMEM, NTR);
   const int zc = choose_zc(ntiles, np, resident, 2, min_zc_for(g, sizeof(T)));
   const int nitems = ntiles * ((np + zc - 1) / zc);
   *npartial = nitems;
-  CUtensorMap te;
-  memset(&te, 0, sizeof te);
-  kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, g, c, nullptr, tiles_x, ntiles, zc, nitems, partial, te, Geom{});
+  kernel<<<nitems, NTR, G::SMEM, st>>>(tu, tf, g, c, nullptr, tiles_x, ntiles, zc, nitems, partial);
   return cudaGetLastError();
 }
 
