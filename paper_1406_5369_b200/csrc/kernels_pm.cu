@@ -603,7 +603,13 @@ __device__ __forceinline__ void static_for(F&& f) {
   sfor_impl<N>(f, std::make_integer_sequence<int, N>());
 }
 
-template <typename T, int MODE, bool ZERO, bool NRM, int RPT>
+// NM (RB / Jacobi): 0 no norm; 1 ||f - A u_in||^2 partials of the sweep's INPUT (the solve's
+// first head); 2 the same, red nodes only (RB: a later head of the solve, whose black nodes'
+// input residuals were accumulated by the previous cycle's last level-0 sweep); 3 (RB) the
+// residuals of the black nodes of the sweep's OUTPUT: a black node's neighbours are all red
+// and final when it is relaxed, so the stencil sum s of its relaxation is the sum the norm
+// forms at the output, and r = f - (D v - s) is that residual bitwise (3 more operations)
+template <typename T, int MODE, bool ZERO, int NM, int RPT>
 __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     k_sweep3d_rows(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f, Geom g,
                    Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems,
@@ -613,7 +619,9 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
   constexpr int W = G::W, TX = G::TX, BX = G::BX, HX = G::HX, PX = G::PX, NR = G::NRED, RCOL = G::RCOL;
   constexpr int NTH = 32 * TY / RPT;
   constexpr bool RB = MODE == 1;
+  constexpr bool NRM = NM == 1 || NM == 2;  // input residuals (NM 2: red nodes only)
   static_assert(TY % RPT == 0, "rows per thread");
+  static_assert(NM != 3 || RB, "output black residuals: RBGS only");
   extern __shared__ __align__(128) unsigned char sm[];
   const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
   T* spr = reinterpret_cast<T*>(sm + G::PR_OFF);
@@ -727,7 +735,7 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
             const V dn = K == 0 ? svec(U0, bo - BX) : u0[K > 0 ? K - 1 : 0];
             const V upr = K == RPT - 1 ? svec(U0, bo + (K + 1) * BX) : u0[K < RPT - 1 ? K + 1 : 0];
             const T edge = KR == 0 ? su(U0, bo + K * BX - 1) : su(U0, bo + K * BX + W);
-            if constexpr (NRM) {
+            if constexpr (NM == 1) {
               if (nrm_here) {  // black nodes of plane p: residual of the old iterate
                 const T oedge = KR == 0 ? su(U0, bo + K * BX + W) : su(U0, bo + K * BX - 1);
 #pragma unroll
@@ -826,7 +834,15 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
                 const T ctr = um[K].v[j];
                 const T l = (KB == 0 && m == 0) ? edge : pr1[K][KB == 1 ? m : (m > 0 ? m - 1 : 0)];
                 const T r = (KB == 1 && m == NR - 1) ? edge : pr1[K][KB == 0 ? m : (m + 1 < NR ? m + 1 : 0)];
-                const T v = relax(c, ctr, l, r, pdn[m], pup[m], pr2[K][m], pr0[K][m], fprev[K].v[j]);
+                // relax() written out: s is also the stencil sum of the output's residual (NM 3)
+                T sm_ = mul(c.cx, add(l, r));
+                sm_ = add(sm_, mul(c.cy, add(pdn[m], pup[m])));
+                sm_ = add(sm_, mul(c.cz, add(pr2[K][m], pr0[K][m])));
+                const T fb = fprev[K].v[j];
+                const T v = add(ctr, mul(c.wd, sub(fb, sub(mul(c.D, ctr), sm_))));
+                if constexpr (NM == 3) {
+                  if (in[K][j]) nsum = acc_sq<T>(nsum, sub(fb, sub(mul(c.D, v), sm_)));
+                }
                 o.v[j] = in[K][j] ? v : ctr;
               }
               store_vec(orow + (long long)K * g.pitch + (long long)bp * g.pstride, ox, in[K], o);
@@ -892,7 +908,7 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     seq = N(qlast) + 1;
     __syncthreads();
   }
-  if (MODE == 2 || NRM) {  // fixed-order block reduction -> one partial per CTA
+  if (MODE == 2 || NM != 0) {  // fixed-order block reduction -> one partial per CTA
     double* red = reinterpret_cast<double*>(sm);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nsum = __dadd_rn(nsum, __shfl_down_sync(0xffffffffu, nsum, o));
@@ -1046,6 +1062,176 @@ __global__ void __launch_bounds__(NT, Geo<T>::MINB)
   }
 }
 
+// Row-blocked residual + restriction (the default): as k_resid_restrict3d, but a thread owns
+// RPT consecutive fine rows of its x-vector (the rows' u(q) y-neighbours inside the thread
+// come from registers) and CN / NTH coarse nodes.  Bitwise identical results.
+template <typename T, int RPT>
+__global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
+    k_resid_restrict3d_rows(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f,
+                            Geom gf, Geom gc, Coef<T> c, T* __restrict__ fc, int tiles_x, int ntiles, int zcc,
+                            int nitems) {
+  using G = Geo<T>;
+  using V = Vec<T, G::W>;
+  constexpr int W = G::W, TX = G::TX, BX = G::BX, HX = G::HX, PX = G::PX;
+  constexpr int NTH = 32 * TY / RPT;
+  extern __shared__ __align__(128) unsigned char sm[];
+  const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
+  T* const Rr2 = reinterpret_cast<T*>(sm + G::PR_OFF);
+
+  const int tid = threadIdx.x, lane = tid & 31, wr = tid >> 5;
+  const int ty0 = wr * RPT;
+  const int pgf0 = gf.p_glob0;
+  const int bo = (ty0 + 2) * BX + W * lane + HX;
+  const int fo = (ty0 + 1) * BX + W * lane + HX;
+  const int po = (ty0 + 1) * PX + W * lane + HX;
+  const T two = (T)2;
+  const T scale = (T)(1.0 / 64.0);
+  constexpr int CNX = TX / 2, CN = (TX / 2) * (TY / 2), NC = CN / NTH;  // coarse nodes per thread
+  static_assert(CN % NTH == 0 && CNX % 32 == 0, "coarse mapping: whole warps per coarse row");
+  uint32_t seq = 0;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    int tile, Pa, Pb;
+    item_of(it, ntiles, zcc, gc.p_lo, gc.p_hi, tile, Pa, Pb);
+    const int X0 = (tile % tiles_x) * (TX / 2), Y0 = (tile / tiles_x) * (TY / 2);
+    const int x0 = 2 * X0, y0 = 2 * Y0;
+    const int ox = x0 + W * lane, oy0 = y0 + ty0;
+    bool in[RPT][W];
+#pragma unroll
+    for (int k = 0; k < RPT; k++) {
+      const bool rin = oy0 + k >= 1 && oy0 + k <= gf.ny - 1;
+#pragma unroll
+      for (int j = 0; j < W; j++) in[k][j] = rin && ox + j >= 1 && ox + j <= gf.nx - 1;
+    }
+    // low-side ring: row y0-1 for x in [x0-1, x0+TX-1] (TX+1 nodes), column x0-1 for y in [y0, y0+TY-1]
+    constexpr int NRING = TX + 1 + TY;
+    constexpr int RING_PER = (NRING + NTH - 1) / NTH;  // ring nodes per thread (1 or 2)
+    int rb[RING_PER], rf[RING_PER], rpo[RING_PER];
+    bool has_ring[RING_PER], ring_in[RING_PER];
+#pragma unroll
+    for (int s = 0; s < RING_PER; s++) {
+      const int e = tid + s * NTH;
+      has_ring[s] = e < NRING;
+      const int rx = e < TX + 1 ? x0 - 1 + e : x0 - 1;
+      const int ryy = e < TX + 1 ? y0 - 1 : y0 + e - (TX + 1);
+      ring_in[s] = rx >= 1 && rx <= gf.nx - 1 && ryy >= 1 && ryy <= gf.ny - 1;
+      rb[s] = (ryy - y0 + 2) * BX + (rx - x0 + HX);
+      rf[s] = (ryy - y0 + 1) * BX + (rx - x0 + HX);
+      rpo[s] = (ryy - y0 + 1) * PX + (rx - x0 + HX);
+    }
+    int co[NC];
+    bool cnode[NC];
+    T* crow[NC];
+#pragma unroll
+    for (int s = 0; s < NC; s++) {
+      const int ci = tid + s * NTH, ccx = ci % CNX, ccy = ci / CNX;
+      co[s] = (2 * ccy + 1) * PX + 2 * ccx + HX;  // r offset of fine (2I, 2J)
+      const int I = X0 + ccx, J = Y0 + ccy;
+      cnode[s] = I >= 1 && I <= gc.nx - 1 && J >= 1 && J <= gc.ny - 1;
+      crow[s] = fc + (long long)J * gc.pitch + I;
+    }
+
+    const int qf0 = 2 * (Pa + gc.p_glob0) - pgf0;
+    const int qf1 = 2 * (Pb - 1 + gc.p_glob0) - pgf0;
+    const int rlo = qf0 - 1, rhi = qf1 + 1;
+    const int qlo = rlo - 2, qlast = rhi;
+    const uint32_t nlo = seq;
+    auto N = [&](int q) { return nlo + (uint32_t)(q - qlo); };
+    if (tid == 0)
+      for (int q = qlo; q < qlo + G::NS && q <= qlast; q++) R.issue(N(q), &tm_u, &tm_f, x0, y0, q + 1, q, true);
+    R.wait(N(qlo));
+    R.wait(N(qlo + 1));
+    V um[RPT], u0[RPT], up[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; k++) {
+      um[k] = ld_vec(R.U(N(qlo)) + bo + k * BX);
+      u0[k] = ld_vec(R.U(N(qlo + 1)) + bo + k * BX);
+    }
+    T rzm[RING_PER];
+#pragma unroll
+    for (int s = 0; s < RING_PER; s++) rzm[s] = has_ring[s] ? R.U(N(qlo))[rb[s]] : (T)0;
+    __syncthreads();
+    if (tid == 0 && qlo + G::NS <= qlast) {
+      fence_proxy_async();
+      R.issue(N(qlo + G::NS), &tm_u, &tm_f, x0, y0, qlo + G::NS + 1, qlo + G::NS, true);
+    }
+    T ty1[NC], ty2[NC];
+#pragma unroll
+    for (int s = 0; s < NC; s++) ty1[s] = ty2[s] = (T)0;
+    for (int q = rlo; q <= rhi; q++) {
+      R.wait(N(q));
+      const T* U0 = R.U(N(q - 1));
+      const T* Up = R.U(N(q));
+      const T* F0 = R.F(N(q));
+      T* Rr = Rr2 + (size_t)(q & 1) * (G::PB / sizeof(T));
+#pragma unroll
+      for (int k = 0; k < RPT; k++) up[k] = ld_vec(Up + bo + k * BX);
+      const int pgl = q + pgf0;
+      const bool pl_in = pgl >= 1 && pgl <= gf.nz - 1;
+      static_for<RPT>([&](auto Kc) {
+        constexpr int K = decltype(Kc)::value;
+        const V fv = ld_vec(F0 + fo + K * BX);
+        const V dn = K == 0 ? ld_vec(U0 + bo - BX) : u0[K > 0 ? K - 1 : 0];
+        const V upr = K == RPT - 1 ? ld_vec(U0 + bo + (K + 1) * BX) : u0[K < RPT - 1 ? K + 1 : 0];
+        const T el = U0[bo + K * BX - 1], er = U0[bo + K * BX + W];
+        V rv;
+#pragma unroll
+        for (int j = 0; j < W; j++) {
+          const T l = j == 0 ? el : u0[K].v[j > 0 ? j - 1 : 0];
+          const T r = j == W - 1 ? er : u0[K].v[j < W - 1 ? j + 1 : 0];
+          const T rr = sub(fv.v[j], apply_A(c, u0[K].v[j], l, r, dn.v[j], upr.v[j], um[K].v[j], up[K].v[j]));
+          rv.v[j] = pl_in && in[K][j] ? rr : (T)0;
+        }
+        if constexpr (sizeof(T) == 8)
+          *reinterpret_cast<double2*>(Rr + po + K * PX) = make_double2(rv.v[0], rv.v[1]);
+        else
+          *reinterpret_cast<float4*>(Rr + po + K * PX) = make_float4(rv.v[0], rv.v[1], rv.v[2], rv.v[3]);
+      });
+#pragma unroll
+      for (int s = 0; s < RING_PER; s++) {
+        if (has_ring[s]) {
+          const int b = rb[s];
+          const T uc = U0[b];
+          const T r = sub(F0[rf[s]], apply_A(c, uc, U0[b - 1], U0[b + 1], U0[b - BX], U0[b + BX], rzm[s], Up[b]));
+          Rr[rpo[s]] = pl_in && ring_in[s] ? r : (T)0;
+          rzm[s] = uc;
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && q - 1 + G::NS <= qlast) {
+        fence_proxy_async();
+        R.issue(N(q - 1 + G::NS), &tm_u, &tm_f, x0, y0, q + G::NS, q - 1 + G::NS, true);
+      }
+      using P2 = std::conditional_t<sizeof(T) == 8, double2, float2>;
+#pragma unroll
+      for (int s = 0; s < NC; s++) {
+        T tx[3];
+#pragma unroll
+        for (int dy = -1; dy <= 1; dy++) {
+          const T* row = Rr + co[s] + dy * PX;
+          const P2 pr = *reinterpret_cast<const P2*>(row);
+          T left = __shfl_up_sync(0xffffffffu, pr.y, 1);
+          if (lane == 0) left = row[-1];
+          tx[dy + 1] = add(add(left, pr.y), mul(two, pr.x));
+        }
+        const T ty0v = add(add(tx[0], tx[2]), mul(two, tx[1]));
+        if (cnode[s] && (pgl & 1) == 1 && q >= qf0 + 1) {
+          const int Pc = ((pgl - 1) >> 1) - gc.p_glob0;
+          crow[s][(long long)Pc * gc.pstride] = mul(add(add(ty2[s], ty0v), mul(two, ty1[s])), scale);
+        }
+        ty2[s] = ty1[s];
+        ty1[s] = ty0v;
+      }
+#pragma unroll
+      for (int k = 0; k < RPT; k++) {
+        um[k] = u0[k];
+        u0[k] = up[k];
+      }
+    }
+    seq = N(qlast) + 1;
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // cuTensorMapEncodeTiled through the runtime's driver entry point, so that the
 // library does not link libcuda (it must load on GPU-less hosts for the ABI tests).
@@ -1161,9 +1347,9 @@ static CUresult encode_coarse(CUtensorMap* tm, const void* base, const Geom& g, 
 template <typename T>
 cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
                          cudaStream_t st, double* partial, int* npartial, const T* ecoarse,
-                         const Geom* gcoarse) {
+                         const Geom* gcoarse, SweepNorm nm) {
   if (!g.three_d) {
-    if (ecoarse) return cudaErrorInvalidValue;  // fused prolongation: 3D only
+    if (ecoarse || (partial && nm != SN_INPUT)) return cudaErrorInvalidValue;  // 3D only
     return pm2::launch_sweep<T>(g, c, rbgs, uin, f, uout, zero_in, st, partial, npartial);
   }
   const Geom gce = gcoarse ? *gcoarse : Geom{};
@@ -1195,12 +1381,21 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   };
   if (ecoarse)
     rbgs ? go(k_sweep3d<T, 1, false, false, true>) : go(k_sweep3d<T, 0, false, false, true>);
-  else if (partial && !zero_in)
-    rbgs ? gor(k_sweep3d_rows<T, 1, false, true, RPT>) : gor(k_sweep3d_rows<T, 0, false, true, RPT>);
-  else if (rbgs)
-    zero_in ? gor(k_sweep3d_rows<T, 1, true, false, RPT>) : gor(k_sweep3d_rows<T, 1, false, false, RPT>);
+  else if (partial && !zero_in) {
+    if (!rbgs) {
+      if (nm != SN_INPUT) return cudaErrorInvalidValue;
+      gor(k_sweep3d_rows<T, 0, false, 1, RPT>);
+    } else if (nm == SN_INPUT) {
+      gor(k_sweep3d_rows<T, 1, false, 1, RPT>);
+    } else if (nm == SN_INPUT_RED) {
+      gor(k_sweep3d_rows<T, 1, false, 2, RPT>);
+    } else {
+      gor(k_sweep3d_rows<T, 1, false, 3, RPT>);
+    }
+  } else if (rbgs)
+    zero_in ? gor(k_sweep3d_rows<T, 1, true, 0, RPT>) : gor(k_sweep3d_rows<T, 1, false, 0, RPT>);
   else
-    zero_in ? gor(k_sweep3d_rows<T, 0, true, false, RPT>) : gor(k_sweep3d_rows<T, 0, false, false, RPT>);
+    zero_in ? gor(k_sweep3d_rows<T, 0, true, 0, RPT>) : gor(k_sweep3d_rows<T, 0, false, 0, RPT>);
   return cudaGetLastError();
 }
 
@@ -1211,8 +1406,8 @@ int sweep_partials(const Geom& g, bool rbgs) {
   using G = Geo<T>;
   const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
   const int np = g.p_hi - g.p_lo;
-  const int resident = rbgs ? prepare_kernel(k_sweep3d_rows<T, 1, false, true, RPT>, G::SMEM, NTR)
-                            : prepare_kernel(k_sweep3d_rows<T, 0, false, true, RPT>, G::SMEM, NTR);
+  const int resident = rbgs ? prepare_kernel(k_sweep3d_rows<T, 1, false, 1, RPT>, G::SMEM, NTR)
+                            : prepare_kernel(k_sweep3d_rows<T, 0, false, 1, RPT>, G::SMEM, NTR);
   int best = 0;
   for (int halo : {2, 4}) {
     const int zc = choose_zc(ntiles, np, resident, halo, min_zc_for(g, sizeof(T)));
@@ -1223,12 +1418,23 @@ int sweep_partials(const Geom& g, bool rbgs) {
 }
 
 template <typename T>
+int sweep_items(const Geom& g, bool rbgs) {
+  using G = Geo<T>;
+  const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
+  const int np = g.p_hi - g.p_lo;
+  const int resident = rbgs ? prepare_kernel(k_sweep3d_rows<T, 1, false, 1, RPT>, G::SMEM, NTR)
+                            : prepare_kernel(k_sweep3d_rows<T, 0, false, 1, RPT>, G::SMEM, NTR);
+  const int zc = choose_zc(ntiles, np, resident, rbgs ? 4 : 2, min_zc_for(g, sizeof(T)));
+  return ntiles * ((np + zc - 1) / zc);
+}
+
+template <typename T>
 int norm_partials(const Geom& g) {
   if (!g.three_d) return pm2::norm_partials<T>(g);
   using G = Geo<T>;
   const int ntiles = ((g.nx + G::TX - 1) / G::TX) * ((g.ny + TY - 1) / TY);
   const int np = g.p_hi - g.p_lo;
-  const int resident = prepare_kernel(k_sweep3d_rows<T, 2, false, false, RPT>, G::SMEM, NTR);
+  const int resident = prepare_kernel(k_sweep3d_rows<T, 2, false, 0, RPT>, G::SMEM, NTR);
   const int zc = choose_zc(ntiles, np, resident, 2, min_zc_for(g, sizeof(T)));
   return ntiles * ((np + zc - 1) / zc);
 }
@@ -1244,7 +1450,7 @@ cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f,
   const int tiles_x = (g.nx + G::TX - 1) / G::TX, tiles_y = (g.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = g.p_hi - g.p_lo;
-  auto kernel = k_sweep3d_rows<T, 2, false, false, RPT>;
+  auto kernel = k_sweep3d_rows<T, 2, false, 0, RPT>;
   const int resident = prepare_kernel(kernel, G::SMEM, NTR);
   const int zc = choose_zc(ntiles, np, resident, 2, min_zc_for(g, sizeof(T)));
   const int nitems = ntiles * ((np + zc - 1) / zc);
@@ -1498,21 +1704,23 @@ cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>&
   const int tiles_x = (gc.nx + G::TX / 2 - 1) / (G::TX / 2), tiles_y = (gc.ny + TY / 2 - 1) / (TY / 2);
   const int ntiles = tiles_x * tiles_y;
   const int npc = gc.p_hi - gc.p_lo;
-  auto kernel = k_resid_restrict3d<T>;
-  const int resident = prepare_kernel(kernel, G::SMEM);
+  auto kernel = k_resid_restrict3d_rows<T, RPT>;
+  const int resident = prepare_kernel(kernel, G::SMEM, NTR);
   const int zcc = choose_zc(ntiles, npc, resident, 2, min_zc_for(gf, sizeof(T)));
   const int nitems = ntiles * ((npc + zcc - 1) / zcc);
-  kernel<<<nitems, NT, G::SMEM, st>>>(tu, tf, gf, gc, c, fc, tiles_x, ntiles, zcc, nitems);
+  kernel<<<nitems, NTR, G::SMEM, st>>>(tu, tf, gf, gc, c, fc, tiles_x, ntiles, zcc, nitems);
   return cudaGetLastError();
 }
 
 template cudaError_t launch_sweep<double>(const Geom&, const Coef<double>&, bool, const double*, const double*,
                                           double*, bool, cudaStream_t, double*, int*, const double*,
-                                          const Geom*);
+                                          const Geom*, SweepNorm);
 template cudaError_t launch_sweep<float>(const Geom&, const Coef<float>&, bool, const float*, const float*, float*,
-                                         bool, cudaStream_t, double*, int*, const float*, const Geom*);
+                                         bool, cudaStream_t, double*, int*, const float*, const Geom*, SweepNorm);
 template int sweep_partials<double>(const Geom&, bool);
 template int sweep_partials<float>(const Geom&, bool);
+template int sweep_items<double>(const Geom&, bool);
+template int sweep_items<float>(const Geom&, bool);
 template int norm_partials<double>(const Geom&);
 template int norm_partials<float>(const Geom&);
 template cudaError_t launch_norm<double>(const Geom&, const Coef<double>&, const double*, const double*, double*,

@@ -13,15 +13,25 @@ CUresult encode_tiled(CUtensorMap* tm, bool fp64, int rank, const void* base, co
                       const unsigned long long* strides, const unsigned* box);
 // true when a level is large enough for the plane-marching kernels
 bool supported(const Geom& g, int min_nx);
+// residual partials a sweep writes when `partial` is given (3D levels):
+//  SN_INPUT      ||f - A u_in||^2 of every interior node
+//  SN_INPUT_RED  the same, red nodes only (RBGS)
+//  SN_OUT_BLACK  ||f - A u_out||^2 of the black nodes (RBGS; with SN_INPUT_RED of the next sweep
+//                of the same u and f, this is the norm of u_out, node by node bitwise)
+enum SweepNorm { SN_INPUT = 1, SN_INPUT_RED = 2, SN_OUT_BLACK = 3 };
 // one RBGS (rbgs=true) or Jacobi sweep u_out = S(u_in); zero_in: u_in is taken as 0 (not read)
-// partial != nullptr: also write ||f - A u_in||^2 partials (one per CTA, *npartial of them)
+// partial != nullptr: also write residual partials (`nm`; one per CTA, *npartial of them)
 // ecoarse != nullptr: the input is u_in + P ecoarse (prolongation + correction fused, 3D)
 template <typename T>
 cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* uin, const T* f, T* uout, bool zero_in,
                          cudaStream_t st, double* partial = nullptr, int* npartial = nullptr,
-                         const T* ecoarse = nullptr, const Geom* gcoarse = nullptr);
+                         const T* ecoarse = nullptr, const Geom* gcoarse = nullptr, SweepNorm nm = SN_INPUT);
+// upper bound of the partials a sweep of level g writes
 template <typename T>
 int sweep_partials(const Geom& g, bool rbgs);
+// exactly the partials a non-fused 3D sweep of level g writes (its CTA count)
+template <typename T>
+int sweep_items(const Geom& g, bool rbgs);
 // fc (coarse interior) = FW(f - A u) ; coarse boundary untouched
 template <typename T>
 cudaError_t launch_resid_restrict(const Geom& gf, const Geom& gc, const Coef<T>& c, const T* u, const T* f, T* fc,

@@ -298,7 +298,7 @@ mg_status plan_build(mg_solver* s) {
   if (pm::supported(s->lv[0].g, 16)) {
     const bool rb = c.smoother == MG_RBGS;
     int a = s->esz == 8 ? pm::sweep_partials<double>(s->lv[0].g, rb) : pm::sweep_partials<float>(s->lv[0].g, rb);
-    if (a > np) np = a;
+    if (2 * a > np) np = 2 * a;  // the split norm: the tail's black partials + the head's red ones
   }
   // coarsest-level direct solve: factor once (reading 3)
   Level& C = s->lv[s->L - 1];
@@ -453,8 +453,22 @@ struct Exec {
   }
 
   // one sweep; zero_in: the iterate is known to be 0 (first sweep after V_H(0,...))
-  mg_status smooth(int l, T*& cur, T*& other, const T* f, bool zero_in = false) {
+  // bpart != nullptr (3D RBGS marching level, not distributed): also write the black nodes'
+  // residual partials of the sweep's output there (pm::SN_OUT_BLACK; the split norm)
+  mg_status smooth(int l, T*& cur, T*& other, const T* f, bool zero_in = false, double* bpart = nullptr) {
     const Level& L = s->lv[l];
+    if (bpart) {
+      T* in = cur;
+      T* out = other;
+      mg_status r = launch(s, st, K_SWEEP_RBGS, l, 3 * w(l), [&] {
+        int nb = 0;
+        cudaError_t e = pm::launch_sweep<T>(L.g, coef(l), true, in, f, out, false, st, bpart, &nb, nullptr, nullptr,
+                                            pm::SN_OUT_BLACK);
+        return (e == cudaSuccess && nb != black_items()) ? cudaErrorInvalidValue : e;
+      });
+      std::swap(cur, other);
+      return r;
+    }
     if (pm(l)) {
       const bool rb = s->cfg.smoother == MG_RBGS;
       T* in = cur;
@@ -544,10 +558,16 @@ struct Exec {
 
   // rr_fc != nullptr: the LAST pass also writes the restriction of its result's residual
   // into rr_fc (level l+1) when it can (rr_last(l, n)); the caller skips its own then
-  mg_status smooth_n(int l, T*& cur, T*& other, const T* f, int n, bool zero_in, T* rr_fc = nullptr) {
+  mg_status smooth_n(int l, T*& cur, T*& other, const T* f, int n, bool zero_in, T* rr_fc = nullptr,
+                     double* bpart = nullptr) {
     const Level& L = s->lv[l];
     const int p = passes(l, n);
     mg_status r = MG_OK;
+    if (bpart) {  // the split norm's black partials from the last sweep (single sweeps: not kfusable)
+      for (int k = 0; k < n; k++)
+        if ((r = smooth(l, cur, other, f, zero_in && k == 0, k == n - 1 ? bpart : nullptr)) != MG_OK) return r;
+      return r;
+    }
     for (int k = 0, i = 0; k < n; i++) {
       const int K = n / p + (i < n % p ? 1 : 0);
       if (K >= 2) {
@@ -596,6 +616,16 @@ struct Exec {
   // (the rest).  mg_solve pipelines tail(k) + head(k+1): the norm after cycle k is
   // computed by the next cycle's first sweep, which reads u and f anyway.
   bool can_split() const { return s->L > 1 && s->cfg.nu1 >= 1 && pm(0) && tail_level() > 0; }
+  // The split norm: with RBGS on a 3D marching level 0 held whole by this rank,
+  // the tail's last level-0 post-sweep writes the black nodes' residual partials of the new
+  // iterate (pm::SN_OUT_BLACK) into d_partial[0, black_items()), and the next head adds only
+  // the red nodes' residuals of its input (pm::SN_INPUT_RED) behind them.
+  bool split_norm() const {
+    const Level& L = s->lv[0];
+    return can_split() && s->cfg.smoother == MG_RBGS && L.g.three_d && !L.dist && s->cfg.nu2 >= 1 &&
+           !((s->cfg.flags & MG_FLAG_FUSE_PROLONG) && s->cfg.nu2 == 1);
+  }
+  int black_items() const { return pm::sweep_items<T>(s->lv[0].g, true); }
 
   mg_status cycle_start(T* u0, const T* f0) {
     const bool jac = s->cfg.smoother == MG_JACOBI;
@@ -634,6 +664,15 @@ struct Exec {
         return r;
       return norm_finish(0, np, out_dev);
     }
+    if (!refresh && split_norm()) {  // a later head: the previous tail wrote the black partials
+      const int nb = black_items();
+      if ((r = launch(s, st, K_SWEEP_NORM, 0, 3 * w(0), [&] {
+             return pm::launch_sweep<T>(L.g, coef(0), rb, u0, f0, t0, false, st, s->d_partial + nb, &np, nullptr,
+                                        nullptr, pm::SN_INPUT_RED);
+           })) != MG_OK)
+        return r;
+      return norm_finish(0, nb + np, out_dev);
+    }
     if ((r = launch(s, st, K_SWEEP_NORM, 0, 3 * w(0), [&] {
            return pm::launch_sweep<T>(L.g, coef(0), rb, u0, f0, t0, false, st, s->d_partial, &np);
          })) != MG_OK)
@@ -671,6 +710,7 @@ struct Exec {
       oth[l] = (T*)s->lv[l].t;
     }
     if (after_head) std::swap(cur[0], oth[0]);
+    const bool bnorm = after_head && split_norm();  // this tail writes the split norm's black partials
     const int lt = tail_level();
     if (lt == 0) return run_tail(0, u0, f0);  // small grid: the whole cycle in one launch
     if (Lv == 1) {
@@ -773,7 +813,9 @@ struct Exec {
             return r;
           std::swap(cur[l], oth[l]);
           for (int k = 1; k < s->cfg.nu2; k++)
-            if ((r = smooth(l, cur[l], oth[l], f)) != MG_OK) return r;
+            if ((r = smooth(l, cur[l], oth[l], f, false,
+                            (bnorm && l == 0 && k == s->cfg.nu2 - 1) ? s->d_partial : nullptr)) != MG_OK)
+              return r;
           continue;
         }
         // level 0: the ping-pong buffers swap once per pass; when fused passes change the
@@ -804,7 +846,9 @@ struct Exec {
              })) != MG_OK)
           return r;
         if (flip) std::swap(cur[l], oth[l]);
-        if ((r = smooth_n(l, cur[l], oth[l], f, s->cfg.nu2, false)) != MG_OK) return r;
+        if ((r = smooth_n(l, cur[l], oth[l], f, s->cfg.nu2, false, nullptr, (bnorm && l == 0) ? s->d_partial : nullptr)) !=
+            MG_OK)
+          return r;
       }
     }
     if (cur[0] != u0) {
