@@ -118,6 +118,11 @@ typedef struct {
                             each driven by its own host thread (the collectives rendezvous
                             on the host and copy device-to-device); requires
                             MG_FLAG_NO_GRAPH.  For testing the multi-rank path on one GPU. */
+    double comm_timeout_s; /* nranks > 1: a blocking entry point that waits on the device polls
+                            the communicator (ncclCommGetAsyncError) and gives up after this many
+                            seconds without completion: the communicator is aborted
+                            (ncclCommAbort), the call returns MG_ERR_NCCL and the solver is
+                            poisoned.  The loopback rendezvous uses the same limit.  0 => 300.  */
 } mg_config;
 
 /* Fill `cfg` with the defaults above for a `dim`-D grid of `nodes` per axis
@@ -231,6 +236,16 @@ mg_status mg_profile_enable(mg_solver* s, int32_t on);
  * (may exceed cap; only min(n,cap) written).  Synchronises the device. */
 int32_t mg_profile_read(mg_solver* s, int32_t cap, const char** names, double* ms,
                         int64_t* count, double* bytes);
+
+/* Fault injection for tests of the failure path: the `countdown`-th halo exchange
+ * from now of this rank (1 = the next one) fails.  MG_FAULT_COMM_ERROR: the exchange reports a
+ * communication error, as a failed ncclSend/ncclRecv would (the call returns MG_ERR_NCCL, the
+ * solver is poisoned).  MG_FAULT_HALO_CORRUPT: the exchange completes but the received halo
+ * planes are overwritten with a wrong finite value (silent data corruption, for showing that
+ * the parity tests catch it).  MG_FAULT_NONE disarms.  Host-only; MG_ERR_INVALID on a
+ * solver without a multi-rank exchange. */
+typedef enum { MG_FAULT_NONE = 0, MG_FAULT_COMM_ERROR = 1, MG_FAULT_HALO_CORRUPT = 2 } mg_fault;
+mg_status mg_fault_inject(mg_solver* s, int32_t kind, int32_t countdown);
 
 /* Loopback group of `nranks` ranks for mg_config.loopback (see there); destroy it after
  * every solver of the group has been destroyed. */

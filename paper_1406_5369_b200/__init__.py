@@ -34,8 +34,9 @@ ABI_SYMBOLS = [
     "mg_loopback_group_destroy", "mg_op_smooth", "mg_op_residual", "mg_op_restrict",
     "mg_op_prolong_correct", "mg_op_coarse_solve", "mg_op_norm", "mg_workload_fill",
     "mg_launches_per_cycle", "mg_profile_enable", "mg_profile_read", "mg_error_string", "mg_destroy",
-    "mg_partition", "mg_nccl_unique_id",
+    "mg_partition", "mg_nccl_unique_id", "mg_fault_inject",
 ]
+FAULT_NONE, FAULT_COMM_ERROR, FAULT_HALO_CORRUPT = 0, 1, 2
 
 
 class MGConfig(ctypes.Structure):
@@ -63,6 +64,7 @@ class MGConfig(ctypes.Structure):
         ("theta", ctypes.c_double),
         ("kappa", ctypes.c_double),
         ("loopback", ctypes.c_void_p),
+        ("comm_timeout_s", ctypes.c_double),
     ]
 
 
@@ -119,6 +121,7 @@ def load_library():
                                  ctypes.POINTER(I32)]
     lib.mg_nccl_unique_id.argtypes = [P]
     lib.mg_destroy.argtypes = [P]
+    lib.mg_fault_inject.argtypes = [P, I32, I32]
     lib.mg_destroy.restype = None
     for name in ABI_SYMBOLS:
         if name not in ("mg_config_default", "mg_num_levels", "mg_launches_per_cycle", "mg_profile_read",
@@ -233,7 +236,8 @@ class Solver:
 
     def __init__(self, dim, nodes, levels=0, smoother="rbgs", omega=None, nu1=2, nu2=2, coarse="direct",
                  ncoarse=10, dtype="f64", device=0, coeff=(1.0, 1.0, 1.0), h=None, flags=0, rank=0, nranks=1,
-                 nccl_id=None, pm_min_nx=0, problem="poisson", tau=None, theta=None, kappa=None, loopback=None):
+                 nccl_id=None, pm_min_nx=0, problem="poisson", tau=None, theta=None, kappa=None, loopback=None,
+                 comm_timeout_s=0.0):
         """problem="complex_diffusion": `nodes` are CELLS per axis, arrays are complex
         (torch complex64 / complex128), coarse defaults to "sweeps" (FAS)."""
         lib = load_library()
@@ -261,6 +265,7 @@ class Solver:
         c.pm_min_nx = pm_min_nx
         c.problem = _problem_code(problem)
         c.loopback = loopback.handle if isinstance(loopback, LoopbackGroup) else loopback
+        c.comm_timeout_s = float(comm_timeout_s)
         self._loopback = loopback  # keep the group alive while this rank exists
         self.complex = c.problem == PROBLEM_COMPLEX_DIFFUSION
         if self.complex and coarse == "direct":
@@ -462,6 +467,10 @@ class Solver:
     def workload_fill(self, dst, seed, lo=0.0, hi=1.0, stream=None):
         self._chk(self.lib.mg_workload_fill(self.h, self._dev(dst, 0, "dst"), ctypes.c_uint64(seed), float(lo), float(hi),
                                             self._stream(stream)))
+
+    def fault_inject(self, kind, countdown=1):
+        """mg_fault_inject (tests of the multi-rank failure path)."""
+        self._chk(self.lib.mg_fault_inject(self.h, int(kind), int(countdown)))
 
     # ---- instrumentation
     @property

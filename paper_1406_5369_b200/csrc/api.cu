@@ -18,6 +18,7 @@
 #include "mg.h"
 #include "partition.h"
 #include "plan.h"
+#include "comm.h"
 
 using namespace mg;
 
@@ -203,9 +204,12 @@ extern "C" mg_status mg_create(const mg_config* cfg, mg_solver** out) {
     return fail(nullptr, MG_ERR_CUDA, "no CUDA device (%s); there is no CPU fallback", cudaGetErrorString(ce));
   if (cfg->device < 0 || cfg->device >= ndev) return fail(nullptr, MG_ERR_INVALID, "bad device %d", cfg->device);
 
+  if (!(cfg->comm_timeout_s >= 0.0) || !std::isfinite(cfg->comm_timeout_s))
+    return fail(nullptr, MG_ERR_INVALID, "comm_timeout_s must be finite and >= 0");
   mg_solver* s = new mg_solver();
   s->cfg = *cfg;
   s->L = L;
+  s->comm_timeout_s = cfg->comm_timeout_s > 0.0 ? cfg->comm_timeout_s : 300.0;
   s->esz = cfg->dtype == MG_FP64 ? 8 : 4;
   st = plan_build(s);
   if (st != MG_OK) {
@@ -214,6 +218,17 @@ extern "C" mg_status mg_create(const mg_config* cfg, mg_solver** out) {
     return st;
   }
   *out = s;
+  return MG_OK;
+}
+
+extern "C" mg_status mg_fault_inject(mg_solver* s, int32_t kind, int32_t countdown) {
+  if (!s) return fail(s, MG_ERR_INVALID, "solver is NULL");
+  if (kind < MG_FAULT_NONE || kind > MG_FAULT_HALO_CORRUPT || (kind != MG_FAULT_NONE && countdown < 1))
+    return fail(s, MG_ERR_INVALID, "bad fault kind %d / countdown %d", kind, countdown);
+  if (kind != MG_FAULT_NONE && !mg::comm_active(s))
+    return fail(s, MG_ERR_INVALID, "fault injection needs a multi-rank exchange (nranks > 1)");
+  s->fault_kind = kind;
+  s->fault_count = kind == MG_FAULT_NONE ? 0 : countdown;
   return MG_OK;
 }
 
@@ -308,7 +323,8 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
     auto part = [&](int p) { return eager ? plan_run_part(s, p, u, f, cs) : plan_graph_part(s, p, u, f, cs); };
     auto read = [&](double* out) -> mg_status {
       CK(cudaMemcpyAsync(s->h_norm, s->d_norm, sizeof(double), cudaMemcpyDeviceToHost, cs));
-      CK(cudaStreamSynchronize(cs));
+      const mg_status w = plan_wait(s, cs, "mg_solve: norm readback");
+      if (w != MG_OK) return w;
       *out = *s->h_norm;
       return MG_OK;
     };
@@ -388,7 +404,7 @@ static mg_status vcycle_host_run(mg_solver* s, void* u_host, const void* f_host,
     if (st != MG_OK) return st;
   }
   CK(cudaMemcpyAsync(u_host, s->stage_u, bytes, cudaMemcpyDeviceToHost, cs));
-  CK(cudaStreamSynchronize(cs));
+  if ((st = plan_wait(s, cs, "mg_vcycle_host")) != MG_OK) return st;
   if (norm_out) *norm_out = *s->h_norm;
   return MG_OK;
 }
@@ -471,8 +487,8 @@ static mg_status host_batch_run(mg_solver* s, const void* const* u_in, void* con
     CK(cudaMemcpyAsync(u_out[b], su, bytes, cudaMemcpyDeviceToHost, s->d2h_stream));
     CK(cudaEventRecord(s->ev_d2h[k], s->d2h_stream));
   }
-  CK(cudaStreamSynchronize(s->d2h_stream));
-  CK(cudaStreamSynchronize(cs));
+  if ((st = plan_wait(s, s->d2h_stream, "mg_vcycle_host_batch")) != MG_OK) return st;
+  if ((st = plan_wait(s, cs, "mg_vcycle_host_batch")) != MG_OK) return st;
   if (norms)
     for (int b = 0; b < nbatch; b++) norms[b] = s->h_norms[b];
   return MG_OK;

@@ -3,8 +3,12 @@
 
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
+#include <cstring>
 #include <mutex>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "plan.h"
@@ -25,17 +29,26 @@ struct LoopGroup {
   std::vector<Post> post;
   std::vector<cudaEvent_t> done;
   explicit LoopGroup(int n) : P(n), post(n), done(n, nullptr) {}
-  // all P ranks' host threads meet here
-  void barrier() {
+  bool broken = false;  // a rank timed out or failed mid-rendezvous: the group is unusable
+  // all P ranks' host threads meet here; false after `timeout_s` without the others (the
+  // group is then broken for every rank, as a communicator with a dead peer would be)
+  bool barrier(double timeout_s) {
     std::unique_lock<std::mutex> lk(m);
+    if (broken) return false;
     const long g = gen;
     if (++arrived == P) {
       arrived = 0;
       gen++;
       cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return gen != g; });
+      return true;
     }
+    const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return gen != g || broken; });
+    if (!ok || gen == g) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
   }
 };
 
@@ -45,7 +58,20 @@ int loop_group_size(const LoopGroup* g) { return g ? g->P : 0; }
 
 bool comm_active(const mg_solver* s) { return s->pt.P > 1 && (s->comm || s->loop); }
 
-static cudaError_t nccl_err(ncclResult_t r) { return r == ncclSuccess ? cudaSuccess : cudaErrorUnknown; }
+// A communication failure: recorded on the solver (the plan maps it to MG_ERR_NCCL and poisons
+// the solver), reported to the caller as a failed call
+static cudaError_t comm_fail(mg_solver* s, const std::string& msg) {
+  s->comm_failed = true;
+  s->comm_msg = msg;
+  return cudaErrorUnknown;
+}
+static cudaError_t nccl_err(mg_solver* s, ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return cudaSuccess;
+  std::string m = std::string(what) + ": " + ncclGetErrorString(r);
+  const char* last = s->comm ? ncclGetLastError(s->comm) : nullptr;
+  if (last && *last) m += std::string(" (") + last + ")";
+  return comm_fail(s, m);
+}
 
 // loopback: publish (base, owned, ready event), rendezvous, copy what the peers expose,
 // publish "copied", rendezvous, and make this stream wait until the peers have copied
@@ -58,21 +84,41 @@ static cudaError_t loop_exchange(mg_solver* s, void* buf, int owned, cudaStream_
   cudaError_t e = cudaEventRecord(s->lb_ready, st);
   if (e != cudaSuccess) return e;
   G->post[rk] = LoopGroup::Post{static_cast<char*>(buf), owned, s->lb_ready};
-  G->barrier();
+  const double to = s->comm_timeout_s;
+  if (!G->barrier(to)) return comm_fail(s, "loopback exchange: a peer did not arrive (timeout or failed peer)");
   for (int q : peers) {
     if ((e = cudaStreamWaitEvent(st, G->post[q].ev, 0)) != cudaSuccess) return e;
     if ((e = copies(q, G->post[q])) != cudaSuccess) return e;
   }
   if ((e = cudaEventRecord(s->lb_done, st)) != cudaSuccess) return e;
   G->done[rk] = s->lb_done;
-  G->barrier();
+  if (!G->barrier(to)) return comm_fail(s, "loopback exchange: a peer did not arrive (timeout or failed peer)");
   for (int q : peers)
     if ((e = cudaStreamWaitEvent(st, G->done[q], 0)) != cudaSuccess) return e;
-  G->barrier();  // nobody re-records its events before every rank has waited on them
+  // nobody re-records its events before every rank has waited on them
+  if (!G->barrier(to)) return comm_fail(s, "loopback exchange: a peer did not arrive (timeout or failed peer)");
   return cudaSuccess;
 }
 
+static cudaError_t comm_halo_impl(mg_solver* s, void* buf, size_t pbytes, int H, int owned, int h, cudaStream_t st);
+
 cudaError_t comm_halo(mg_solver* s, void* buf, size_t pbytes, int H, int owned, int h, cudaStream_t st) {
+  const bool fire = s->fault_kind != 0 && --s->fault_count == 0;
+  const int kind = fire ? s->fault_kind : 0;
+  if (fire) s->fault_kind = 0;
+  if (kind == 1) return comm_fail(s, "halo exchange: injected communication failure (mg_fault_inject)");
+  cudaError_t e = comm_halo_impl(s, buf, pbytes, H, owned, h, st);
+  if (e != cudaSuccess || kind != 2) return e;
+  // injected silent corruption: the received halo planes get a wrong finite value
+  char* b = static_cast<char*>(buf);
+  if (s->pt.rank > 0 && (e = cudaMemsetAsync(b + (size_t)(H - h) * pbytes, 0x40, h * pbytes, st)) != cudaSuccess)
+    return e;
+  if (s->pt.rank < s->pt.P - 1)
+    e = cudaMemsetAsync(b + (size_t)(H + owned) * pbytes, 0x40, h * pbytes, st);
+  return e;
+}
+
+static cudaError_t comm_halo_impl(mg_solver* s, void* buf, size_t pbytes, int H, int owned, int h, cudaStream_t st) {
   const int P = s->pt.P, rk = s->pt.rank;
   char* b = static_cast<char*>(buf);
   if (s->comm) {
@@ -86,7 +132,7 @@ cudaError_t comm_halo(mg_solver* s, void* buf, size_t pbytes, int H, int owned, 
       if (nr == ncclSuccess) nr = ncclRecv(b + (size_t)(H - h) * pbytes, h * pbytes, ncclChar, rk - 1, s->comm, st);
     }
     const ncclResult_t ne = ncclGroupEnd();
-    return nr != ncclSuccess ? nccl_err(nr) : nccl_err(ne);
+    return nr != ncclSuccess ? nccl_err(s, nr, "halo exchange") : nccl_err(s, ne, "halo exchange (group end)");
   }
   std::vector<int> peers;
   if (rk < P - 1) peers.push_back(rk + 1);
@@ -104,13 +150,68 @@ cudaError_t comm_halo(mg_solver* s, void* buf, size_t pbytes, int H, int owned, 
 cudaError_t comm_allgather(mg_solver* s, void* buf, size_t chunk, cudaStream_t st) {
   const int P = s->pt.P, rk = s->pt.rank;
   char* b = static_cast<char*>(buf);
-  if (s->comm) return nccl_err(ncclAllGather(b + (size_t)rk * chunk, b, chunk, ncclChar, s->comm, st));
+  if (s->comm) return nccl_err(s, ncclAllGather(b + (size_t)rk * chunk, b, chunk, ncclChar, s->comm, st), "all-gather");
   std::vector<int> peers;
   for (int q = 0; q < P; q++)
     if (q != rk) peers.push_back(q);
   return loop_exchange(s, buf, 0, st, peers, [&](int q, const LoopGroup::Post& p) {
     return cudaMemcpyAsync(b + (size_t)q * chunk, p.base + (size_t)q * chunk, chunk, cudaMemcpyDeviceToDevice, st);
   });
+}
+
+mg_status plan_wait(mg_solver* s, cudaStream_t st, const char* what) {
+  if (!s->comm) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) return MG_OK;
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    return plan_fail(s, MG_ERR_CUDA, m.c_str());
+  }
+  cudaEvent_t ev = nullptr;
+  cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev, st);
+  if (e != cudaSuccess) {
+    if (ev) cudaEventDestroy(ev);
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    return plan_fail(s, MG_ERR_CUDA, m.c_str());
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  std::string fail_msg;
+  for (int it = 0;; it++) {
+    e = cudaEventQuery(ev);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) {
+      cudaEventDestroy(ev);
+      std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+      return plan_fail(s, MG_ERR_CUDA, m.c_str());
+    }
+    ncclResult_t ae = ncclSuccess;
+    const ncclResult_t qr = ncclCommGetAsyncError(s->comm, &ae);
+    if (qr != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress)) {
+      fail_msg = std::string(what) + ": NCCL asynchronous error: " + ncclGetErrorString(qr != ncclSuccess ? qr : ae);
+      break;
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > s->comm_timeout_s) {
+      fail_msg = std::string(what) + ": timed out after " + std::to_string((int)s->comm_timeout_s) +
+                 " s waiting on the device (a peer rank is stuck or dead)";
+      break;
+    }
+    if (it > 1000) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  if (fail_msg.empty()) {
+    cudaEventDestroy(ev);
+    return MG_OK;
+  }
+  plan_comm_abort(s);  // unblocks the NCCL kernels still queued on the streams
+  cudaEventDestroy(ev);
+  return plan_fail(s, MG_ERR_NCCL, fail_msg.c_str());
+}
+
+void plan_comm_abort(mg_solver* s) {
+  if (s->comm) {
+    ncclCommAbort(s->comm);
+    s->comm = nullptr;
+  }
 }
 
 }  // namespace mg

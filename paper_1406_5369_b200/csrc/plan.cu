@@ -105,7 +105,13 @@ static mg_status launch(mg_solver* s, cudaStream_t st, Kind kind, int level, dou
     }
   }
   if (kind != K_MEMSET && kind != K_HALO && kind != K_ALLGATHER) s->launch_counter++;  // our kernels only
-  if (e != cudaSuccess) return cuda_fail(s, e, kKindName[kind]);
+  if (e != cudaSuccess) {
+    if (s->comm_failed) {  // an exchange failed (comm.cu): the communication error, not a CUDA one
+      s->comm_failed = false;
+      return plan_fail(s, MG_ERR_NCCL, s->comm_msg.c_str());
+    }
+    return cuda_fail(s, e, kKindName[kind]);
+  }
   return MG_OK;
 }
 
@@ -202,6 +208,7 @@ mg_status plan_build(mg_solver* s) {
       return plan_fail(s, MG_ERR_CUDA, "loopback events");
     }
   } else if (c.nranks > 1) {  // NCCL communicator over NVLink (unique id broadcast by the caller)
+    // (ncclCommInitRank blocks until every rank has joined: mg_create is collective)
     ncclUniqueId id;
     memcpy(&id, c.nccl_id, sizeof id);
     ncclResult_t nr = ncclCommInitRank(&s->comm, c.nranks, id, c.rank);
@@ -329,6 +336,8 @@ mg_status plan_build(mg_solver* s) {
 
 void plan_free(mg_solver* s) {
   cudaSetDevice(s->cfg.device);
+  // a poisoned solver's NCCL kernels may wait on a dead peer: abort before anything synchronises
+  if (s->comm && s->poisoned) plan_comm_abort(s);
   for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
   s->graphs.clear();
   for (auto& L : s->lv) {
@@ -345,7 +354,11 @@ void plan_free(mg_solver* s) {
   cudaFree(s->d_partial);
   cudaFree(s->d_norm);
   cudaFree(s->d_rank_sums);
-  if (s->comm) ncclCommDestroy(s->comm);
+  if (s->comm) {  // a poisoned solver's peers may be gone: abort instead of a collective teardown
+    if (s->poisoned) ncclCommAbort(s->comm);
+    else ncclCommDestroy(s->comm);
+    s->comm = nullptr;
+  }
   if (s->lb_ready) cudaEventDestroy(s->lb_ready);
   if (s->lb_done) cudaEventDestroy(s->lb_done);
   if (s->h_norm) cudaFreeHost(s->h_norm);
@@ -1305,8 +1318,7 @@ mg_status plan_norm(mg_solver* s, int level, const void* u, const void* f, doubl
   cudaError_t e = cudaMemcpyAsync(s->h_norm, s->d_norm, sizeof(double), cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return cuda_fail(s, e, "norm readback");
   if (sync) {
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(s, e, "norm synchronise");
+    if ((r = plan_wait(s, st, "norm synchronise")) != MG_OK) return r;
     *out = *s->h_norm;
   }
   return MG_OK;

@@ -113,6 +113,12 @@ struct mg_solver {
   // errors
   std::string err;
   bool poisoned = false;
+  // multi-rank failure path: the last exchange's communication failure (set by comm.cu, mapped
+  // to MG_ERR_NCCL by the plan), fault injection (mg_fault_inject), the blocking-wait limit
+  bool comm_failed = false;
+  std::string comm_msg;
+  int fault_kind = 0, fault_count = 0;
+  double comm_timeout_s = 300.0;
 };
 
 namespace mg {
@@ -130,6 +136,11 @@ bool plan_loop_supported(mg_solver* s);
 mg_status plan_solve_device(mg_solver* s, void* u, const void* f, double rtol, int32_t max_cycles, int32_t* cycles,
                             double* history, cudaStream_t st);
 mg_status plan_norm(mg_solver* s, int level, const void* u, const void* f, double* out, cudaStream_t st, bool sync);
+// wait for `st`: cudaStreamSynchronize, or with an NCCL communicator a poll of the stream and of
+// ncclCommGetAsyncError with the solver's timeout (abort + MG_ERR_NCCL on error or timeout)
+mg_status plan_wait(mg_solver* s, cudaStream_t st, const char* what);
+// abort the NCCL communicator (a poisoned solver's; nothing without one)
+void plan_comm_abort(mg_solver* s);
 mg_status plan_op_smooth(mg_solver* s, int level, const void* uin, const void* f, void* uout, cudaStream_t st);
 mg_status plan_op_residual(mg_solver* s, int level, const void* u, const void* f, void* r, cudaStream_t st);
 mg_status plan_op_restrict(mg_solver* s, int level, const void* r, void* fc, cudaStream_t st);

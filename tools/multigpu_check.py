@@ -43,6 +43,28 @@ def run(dim, nodes, sm, flags):
     return ok
 
 
+def run_solve(dim, nodes, sm):
+    """mg_solve over NCCL (host loop: NCCL cannot run in a conditional graph body) to 1e-10:
+    the cycle count and the norm history against the oracle."""
+    rank = dist.get_rank()
+    cells = (nodes - 1,) * dim
+    S = mgb.distributed_solver(dim, nodes, smoother=sm)
+    u, f = wl.workload("W1", dim, cells, seed=42)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    k, hist = S.solve(du, df, 1e-10, 30)
+    ok = True
+    if rank == 0:
+        O = orc.Oracle(orc.Config(dim=dim, cells=cells, levels=S.levels,
+                                  smoother=orc.RBGS if sm == "rbgs" else orc.JACOBI,
+                                  omega=1.0 if sm == "rbgs" else 0.8))
+        _, k_or, hist_or = O.solve(u, f, 1e-10, 30)
+        rel = max(abs(a / b - 1) for a, b in zip(hist, hist_or))
+        ok = k == k_or and rel < 1e-12
+        print(f"{dim}D {nodes} {sm} solve: cycles {k} (oracle {k_or}) hist_rel={rel:.1e}", flush=True)
+    S.close()
+    return ok
+
+
 def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -51,6 +73,7 @@ def main():
     for dim, nodes, sm in [(3, 129, "rbgs"), (3, 257, "rbgs"), (2, 1025, "jacobi")]:
         for flags in (0, mgb.FLAG_NO_GRAPH):
             ok = run(dim, nodes, sm, flags) and ok
+    ok = run_solve(3, 257, "rbgs") and ok
     if dist.get_rank() == 0:
         print("MULTIGPU_CHECK", "PASS" if ok else "FAIL", flush=True)
     dist.destroy_process_group()
