@@ -195,8 +195,6 @@ extern "C" mg_status mg_create(const mg_config* cfg, mg_solver** out) {
   if (cfg->nranks > 1 && cfg->loopback) {
     if (mg::loop_group_size(static_cast<mg::LoopGroup*>(cfg->loopback)) != cfg->nranks)
       return fail(nullptr, MG_ERR_INVALID, "loopback group size != nranks");
-    if (!(cfg->flags & MG_FLAG_NO_GRAPH))
-      return fail(nullptr, MG_ERR_INVALID, "the loopback transport needs MG_FLAG_NO_GRAPH (eager launches)");
   }
   int ndev = 0;
   cudaError_t ce = cudaGetDeviceCount(&ndev);

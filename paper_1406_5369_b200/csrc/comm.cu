@@ -6,6 +6,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -28,8 +29,30 @@ struct LoopGroup {
   long gen = 0;
   std::vector<Post> post;
   std::vector<cudaEvent_t> done;
-  explicit LoopGroup(int n) : P(n), post(n), done(n, nullptr) {}
+  explicit LoopGroup(int n) : P(n), post(n), done(n, nullptr), uf_post(n), need(n, 0), ev_end(n, nullptr), ev_in(n, nullptr) {}
+  ~LoopGroup() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (cudaEvent_t e : ev_end)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_in)
+      if (e) cudaEventDestroy(e);
+    if (ev_origin) cudaEventDestroy(ev_origin);
+    if (ev_out) cudaEventDestroy(ev_out);
+  }
   bool broken = false;  // a rank timed out or failed mid-rendezvous: the group is unusable
+  // group graphs (loop_graph_part): key = every rank's (u, f) and the part
+  struct Key {
+    std::vector<std::pair<const void*, const void*>> uf;
+    int part;
+    bool operator<(const Key& o) const { return part != o.part ? part < o.part : uf < o.uf; }
+  };
+  std::vector<std::pair<const void*, const void*>> uf_post;
+  std::vector<char> need;
+  std::map<Key, cudaGraphExec_t> graphs;
+  cudaEvent_t ev_origin = nullptr, ev_out = nullptr;
+  std::vector<cudaEvent_t> ev_end, ev_in;
+  cudaError_t capture_err = cudaSuccess;
+  mg_status capture_st = MG_OK;
   // all P ranks' host threads meet here; false after `timeout_s` without the others (the
   // group is then broken for every rank, as a communicator with a dead peer would be)
   bool barrier(double timeout_s) {
@@ -157,6 +180,87 @@ cudaError_t comm_allgather(mg_solver* s, void* buf, size_t chunk, cudaStream_t s
   return loop_exchange(s, buf, 0, st, peers, [&](int q, const LoopGroup::Post& p) {
     return cudaMemcpyAsync(b + (size_t)q * chunk, p.base + (size_t)q * chunk, chunk, cudaMemcpyDeviceToDevice, st);
   });
+}
+
+mg_status loop_graph_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
+  LoopGroup* G = s->loop;
+  const int rk = s->pt.rank, P = G->P;
+  const double to = s->comm_timeout_s;
+  auto bar = [&]() { return G->barrier(to); };
+  auto broken = [&]() { return plan_fail(s, MG_ERR_NCCL, "loopback group graph: a peer did not arrive"); };
+  auto cfail = [&](cudaError_t e, const char* what) {
+    std::string m = std::string("loopback group graph: ") + what + ": " + cudaGetErrorString(e);
+    return plan_fail(s, MG_ERR_CUDA, m.c_str());
+  };
+  cudaError_t e = cudaSuccess;
+  if (!G->ev_end[rk]) {
+    if ((e = cudaEventCreateWithFlags(&G->ev_end[rk], cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&G->ev_in[rk], cudaEventDisableTiming)) != cudaSuccess)
+      return cfail(e, "events");
+  }
+  if (rk == 0 && !G->ev_origin) {
+    if ((e = cudaEventCreateWithFlags(&G->ev_origin, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&G->ev_out, cudaEventDisableTiming)) != cudaSuccess)
+      return cfail(e, "events");
+  }
+  G->uf_post[rk] = {u, f};
+  if (!bar()) return broken();
+  LoopGroup::Key key{G->uf_post, part};
+  const bool have = G->graphs.count(key) > 0;  // read by every rank after the same barrier
+  if (!bar()) return broken();
+  if (!have) {
+    // ---- capture every rank's part into one graph
+    if (rk == 0) {
+      G->capture_err = cudaSuccess;
+      G->capture_st = MG_OK;
+      e = cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeRelaxed);
+      if (e == cudaSuccess) e = cudaEventRecord(G->ev_origin, s->cap_stream);
+      G->capture_err = e;
+    }
+    if (!bar()) return broken();
+    if (G->capture_err != cudaSuccess) return cfail(G->capture_err, "begin capture");
+    if (rk != 0 && (e = cudaStreamWaitEvent(s->cap_stream, G->ev_origin, 0)) != cudaSuccess) G->capture_err = e;
+    mg_status r = plan_run_part(s, part, u, f, s->cap_stream);
+    if (r != MG_OK) G->capture_st = r;
+    if (rk != 0 && (e = cudaEventRecord(G->ev_end[rk], s->cap_stream)) != cudaSuccess) G->capture_err = e;
+    if (!bar()) return broken();
+    if (rk == 0) {
+      for (int q = 1; q < P && e == cudaSuccess; q++) e = cudaStreamWaitEvent(s->cap_stream, G->ev_end[q], 0);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ee = cudaStreamEndCapture(s->cap_stream, &graph);
+      if (e == cudaSuccess) e = ee;
+      cudaGraphExec_t exec = nullptr;
+      if (e == cudaSuccess && G->capture_err == cudaSuccess && G->capture_st == MG_OK)
+        e = cudaGraphInstantiate(&exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      if (e != cudaSuccess && G->capture_err == cudaSuccess) G->capture_err = e;
+      if (exec) {
+        if (G->graphs.size() >= 16) {
+          cudaGraphExecDestroy(G->graphs.begin()->second);
+          G->graphs.erase(G->graphs.begin());
+        }
+        G->graphs.emplace(key, exec);
+      }
+    }
+    if (!bar()) return broken();
+    if (r != MG_OK) return r;
+    if (G->capture_st != MG_OK) return plan_fail(s, G->capture_st, "loopback group graph: a peer's capture failed");
+    if (G->capture_err != cudaSuccess) return cfail(G->capture_err, "capture");
+  }
+  // ---- replay after every rank's stream has reached this point; every stream waits for it
+  if ((e = cudaEventRecord(G->ev_in[rk], st)) != cudaSuccess) return cfail(e, "record");
+  if (!bar()) return broken();
+  if (rk == 0) {
+    for (int q = 0; q < P && e == cudaSuccess; q++) e = cudaStreamWaitEvent(st, G->ev_in[q], 0);
+    if (e == cudaSuccess) e = cudaGraphLaunch(G->graphs.at(key), st);
+    if (e == cudaSuccess) e = cudaEventRecord(G->ev_out, st);
+    G->capture_err = e;
+  }
+  if (!bar()) return broken();
+  if (G->capture_err != cudaSuccess) return cfail(G->capture_err, "launch");
+  if ((e = cudaStreamWaitEvent(st, G->ev_out, 0)) != cudaSuccess) return cfail(e, "wait");
+  if (!bar()) return broken();  // ev_out / ev_in are not re-recorded before every rank has waited
+  return MG_OK;
 }
 
 mg_status plan_wait(mg_solver* s, cudaStream_t st, const char* what) {

@@ -8,6 +8,8 @@
 
 #include <cstddef>
 
+#include "mg.h"
+
 struct mg_solver;
 
 namespace mg {
@@ -20,6 +22,13 @@ bool comm_active(const mg_solver* s);
 cudaError_t comm_halo(mg_solver* s, void* buf, size_t pbytes, int H, int owned, int h, cudaStream_t st);
 // in-place all-gather: rank r's chunk of `chunk` bytes sits at buf + r * chunk
 cudaError_t comm_allgather(mg_solver* s, void* buf, size_t chunk, cudaStream_t st);
+
+// Loopback ranks with CUDA graphs: all ranks of the group call this concurrently (one host
+// thread each) for the same part; ONE graph holding every rank's work of that part is captured
+// the first time (rank 0 begins the capture, the others' streams join it through an event, the
+// exchanges' cross-rank event edges are then edges of that graph), and replayed after each
+// rank's stream has reached the call; every rank's stream waits for the replay.
+mg_status loop_graph_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st);
 
 // loopback group (opaque to the ABI: mg_loopback_group_create / _destroy)
 struct LoopGroup;

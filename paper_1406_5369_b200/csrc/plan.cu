@@ -1280,6 +1280,7 @@ bool plan_can_split(mg_solver* s) {
 }
 
 mg_status plan_graph_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
+  if (s->loop && comm_active(s)) return loop_graph_part(s, part, u, f, st);  // one graph for the group
   auto key = std::make_tuple(u, f, part);
   auto it = s->graphs.find(key);
   if (it == s->graphs.end()) {

@@ -2,7 +2,8 @@
 process (ranks 0..P-1), each driven by its own host thread and stream, joined by the
 library's loopback transport (mg_loopback_group_create: the halo exchanges, the
 agglomeration all-gather and the rank-sum norm become device-to-device copies ordered
-by CUDA events and a host rendezvous — no kernel waits on another rank's kernel).
+by CUDA events and a host rendezvous — no kernel waits on another rank's kernel), eagerly
+and replayed from one CUDA graph of the whole group.
 Everything else — partition, halo planes, the overlapped interior/face sweeps, the
 agglomerated coarse levels run redundantly, the deterministic norm — is the code NCCL
 runs drive.  The gathered iterate must equal the single-domain oracle BIT FOR BIT."""
@@ -18,7 +19,7 @@ from test_gpu_parity import make
 pytestmark = pytest.mark.gpu
 
 
-def _run_ranks(P, case, cycles, u, f):
+def _run_ranks(P, case, cycles, u, f, graph=False):
     import torch
     import paper_1406_5369_b200 as mgb
     group = mgb.LoopbackGroup(P)
@@ -27,7 +28,7 @@ def _run_ranks(P, case, cycles, u, f):
         S = mgb.Solver(case["dim"], tuple(c + 1 for c in case["cells"]), levels=case.get("levels", 0),
                        smoother=case.get("smoother", "rbgs"), omega=case.get("omega"), nu1=case.get("nu1", 2),
                        nu2=case.get("nu2", 2), coarse=case.get("coarse", "direct"), dtype=case.get("dtype", "f64"),
-                       rank=p, nranks=P, loopback=group, flags=mgb.FLAG_NO_GRAPH, pm_min_nx=16)
+                       rank=p, nranks=P, loopback=group, flags=0 if graph else mgb.FLAG_NO_GRAPH, pm_min_nx=16)
         solvers.append(S)
     streams = [torch.cuda.Stream() for _ in range(P)]
     dus = [S.from_numpy(u) for S in solvers]
@@ -68,11 +69,15 @@ def _run_ranks(P, case, cycles, u, f):
     dict(dim=2, cells=(256, 256), smoother="rbgs"),
     dict(dim=3, cells=(128, 128, 128), smoother="rbgs", dtype="f32"),
 ], ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
-def test_slab_loopback_bitwise_vs_oracle(P, case):
+@pytest.mark.parametrize("graph", [False, True], ids=["eager", "graph"])
+def test_slab_loopback_bitwise_vs_oracle(P, case, graph):
+    """graph: every rank's cycle replayed from ONE CUDA graph of the loopback group (comm.cu
+    loop_graph_part: the exchanges' cross-rank event edges captured), as NCCL runs capture
+    their per-rank graphs with the send/recv inside."""
     cycles = 2
     S0, O = make(**case)
     u, f = wl.workload("W1", case["dim"], case["cells"], seed=42, dtype=S0.np_dtype)
-    got, norms, dist = _run_ranks(P, case, cycles, u, f)
+    got, norms, dist = _run_ranks(P, case, cycles, u, f, graph)
     assert dist, "the level-0 grid should be distributed"
     uo = u.copy()
     for _ in range(cycles):
@@ -88,7 +93,8 @@ def test_slab_loopback_bitwise_vs_oracle(P, case):
         assert abs(norms[p][-1] / ref - 1) <= 1e-12
 
 
-def test_slab_loopback_solve_and_p8():
+@pytest.mark.parametrize("graph", [False, True], ids=["eager", "graph"])
+def test_slab_loopback_solve_and_p8(graph):
     """mg_solve on 8 ranks (the pipelined host loop of the multi-rank path: the norm after
     each cycle comes from the next cycle's first sweep): the cycle count and history equal
     the single-domain oracle's, the iterate bitwise."""
@@ -99,7 +105,7 @@ def test_slab_loopback_solve_and_p8():
     u, f = wl.workload("W1", 3, cells, seed=42)
     group = mgb.LoopbackGroup(P)
     solvers = [mgb.Solver(3, tuple(c + 1 for c in cells), rank=p, nranks=P, loopback=group,
-                          flags=mgb.FLAG_NO_GRAPH, pm_min_nx=16) for p in range(P)]
+                          flags=0 if graph else mgb.FLAG_NO_GRAPH, pm_min_nx=16) for p in range(P)]
     streams = [torch.cuda.Stream() for _ in range(P)]
     dus = [S.from_numpy(u) for S in solvers]
     dfs = [S.from_numpy(f) for S in solvers]
@@ -152,7 +158,8 @@ def _random_slab_cases(n, seed=31):
 @pytest.mark.parametrize("case", _random_slab_cases(30),
                          ids=lambda c: "P{P}-{dim}d-{c}-L{levels}-{smoother}-nu{nu1}{nu2}-{dtype}".format(
                              c="x".join(map(str, c["cells"])), **c))
-def test_slab_loopback_random_bitwise(case):
+@pytest.mark.parametrize("graph", [False, True], ids=["eager", "graph"])
+def test_slab_loopback_random_bitwise(case, graph):
     """Seeded random slab decompositions: ragged in-plane extents, both smoothers, odd and even
     sweep counts, FP32/FP64 — the gathered iterate equals the single-domain oracle bitwise."""
     case = dict(case)
@@ -160,7 +167,7 @@ def test_slab_loopback_random_bitwise(case):
     S0, O = make(case["dim"], case["cells"], case["levels"], case["smoother"], nu1=case["nu1"], nu2=case["nu2"],
                  dtype=case["dtype"], coarse=case["coarse"])
     u, f = wl.workload("W4", case["dim"], case["cells"], seed=9, dtype=S0.np_dtype)
-    got, norms, dist = _run_ranks(P, case, 2, u, f)
+    got, norms, dist = _run_ranks(P, case, 2, u, f, graph)
     assert dist
     uo = u.copy()
     for _ in range(2):
