@@ -18,7 +18,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmgb200.so")
+# MG_LIBRARY selects another build of the same library (the tests' CHECKED build,
+# libmgb200_checked.so: guard-banded allocations and bounded mbarrier waits); default: the product
+LIB_PATH = os.environ.get("MG_LIBRARY") or os.path.join(_HERE, "libmgb200.so")
 
 JACOBI, RBGS, GS_LEX = 0, 1, 2
 FP64, FP32 = 0, 1

@@ -182,8 +182,6 @@ extern "C" mg_status mg_partition(const mg_config* cfg, int32_t level, int64_t* 
   return MG_OK;
 }
 
-static int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
-
 extern "C" mg_status mg_create(const mg_config* cfg, mg_solver** out) {
   if (!out) return fail(nullptr, MG_ERR_INVALID, "out is NULL");
   *out = nullptr;

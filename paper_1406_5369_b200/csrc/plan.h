@@ -13,6 +13,7 @@
 #include "partition.h"
 #include "kernels_cd.h"
 #include "comm.h"
+#include "checked.h"
 
 typedef struct ncclComm* ncclComm_t;
 

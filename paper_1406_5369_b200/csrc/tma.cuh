@@ -27,6 +27,22 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef MG_CHECKED  // bounded: a phase that never completes traps (CUDA error) instead of hanging
+  uint32_t done = 0;
+  for (long long it = 0; !done; it++) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (it > (1ll << 24)) __trap();
+  }
+  return;
+#endif
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"

@@ -63,9 +63,11 @@ for st in "$@"; do
       echo "full $cfg rc=$?"
       python tools/ncu_summary.py $OUT/${cfg}_full.ncu-rep > $OUT/${cfg}_full_summary.txt 2>&1
       head -40 $OUT/${cfg}_full_summary.txt ;;
-    sanitize)
+    sanitize)  # compute-sanitizer (closed on this pool) then the checked build
       mkdir -p $OUT/sanitizer
       python tools/sanitize.py > $OUT/sanitizer/plain.log 2>&1; echo "sanitize plain rc=$?"
+      MG_LIBRARY=paper_1406_5369_b200/libmgb200_checked.so CUDA_LAUNCH_BLOCKING=1 python tools/sanitize.py \
+        > $OUT/sanitizer/checked_build.log 2>&1; echo "checked build rc=$?"; tail -3 $OUT/sanitizer/checked_build.log
       for tool in memcheck initcheck synccheck racecheck; do
         timeout 600 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 50 \
           python tools/sanitize.py > $OUT/sanitizer/$tool.log 2>&1
