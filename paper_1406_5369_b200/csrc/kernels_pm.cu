@@ -9,21 +9,25 @@
 // staged in shared memory by TMA (cp.async.bulk.tensor.3d) into an NS-deep
 // slot ring signalled by mbarriers, so every HBM byte is read once per sweep.
 //
-// Thread t owns the x-pair (ox, ox+1) = (x0 + 2*(t%32), y0 + t/32); a warp is
-// one tile row, so every colour decision is warp-uniform.  The pair's values
-// of planes p-1, p, p+1 live in registers (z-neighbours never touch smem).
+// Thread t owns one 16-byte x-vector (W = 2 FP64 / 4 FP32 nodes) of RPT = 2
+// consecutive tile rows; a warp is a pair of tile rows, so every colour decision
+// is warp-uniform.  Its values of planes p-1, p, p+1 live in registers
+// (z-neighbours never touch smem; y-neighbours inside the thread's rows neither).
 // Arithmetic is the canonical per-point order of mg_common.cuh (no FMA):
 // results are bitwise identical to the op-by-op kernels and to the oracle.
 //
-//  k_sweep3d<RB>     RB: one red-black Gauss-Seidel sweep in ONE pass
+//  k_sweep3d_rows    RB: one red-black Gauss-Seidel sweep in ONE pass
 //                    (listing P:299-305), ping-pong u_old -> u_new: red
 //                    ("post-red", PR) values of plane p on the tile + 1-node
 //                    ring, then the black nodes of plane p-1 from PR.  No CTA
 //                    reads what another CTA writes: race free.  Jacobi: one
 //                    omega-Jacobi sweep.  Both 3 words/node of HBM.
-//  k_resid_restrict3d  r = f - A u (Alg. 1 line 4) per fine plane into smem,
-//                    full weighting as x/y sums per plane and the z
-//                    sum in registers: read u, f; write f_H = 2 + 1/8 words.
+//                    A thread owns RPT rows of its x-vector.  Variants: the
+//                    residual norm of the input / of the output's black nodes,
+//                    a zero input, the prolongation fused in (CORR).
+//  k_resid_restrict3d_rows  r = f - A u (Alg. 1 line 4) per fine plane into
+//                    smem, full weighting as x/y sums per plane and
+//                    the z sum in registers: read u, f; write f_H = 2 + 1/8 words.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -81,8 +85,6 @@ struct Geo {
   static constexpr int CBX = rup(TX / 2 + 2 + CHX, CHX);  // 36 (FP64) / 72 (FP32)
   static constexpr int CBY = TY / 2 + 3;
   static constexpr int CB = rup(CBX * CBY * (int)sizeof(T), 128);
-  static constexpr int COFF = PR_OFF + 2 * PB;  // CORR keeps 2 PR planes (two barriers per plane)
-  static constexpr int SMEM_CORR = COFF + 3 * CB;
   static constexpr int NRED = W / 2;  // red (and black) nodes per thread and plane
   static constexpr int RCOL = TY / 2;  // red ring nodes per ring column and plane
   static constexpr int NRING_CORR = 4 * (TX + 4) + 4 * TY;  // box nodes outside the tile that are read
@@ -108,19 +110,21 @@ __device__ __forceinline__ T relax(const Coef<T>& c, T ctr, T l, T r, T d, T u, 
 // carries u of plane q+1 and f of plane q, where q = first plane + n.  While
 // plane q is processed only steps q-1 (u(q), f(q-1)) and q (u(q+1), f(q)) are
 // read, so NS-2 steps stream in behind them.
-template <typename T>
+template <typename T, int NSR = Geo<T>::NS>
 struct Ring {
+  static constexpr int NS = NSR;
+  static constexpr int BAR_OFF = NSR * (Geo<T>::UB + Geo<T>::FB);  // then NSR mbarriers (128 B)
   unsigned char* sm;
   uint64_t* full;
-  __device__ T* U(uint32_t n) const { return reinterpret_cast<T*>(sm + (n % Geo<T>::NS) * Geo<T>::UB); }
+  __device__ T* U(uint32_t n) const { return reinterpret_cast<T*>(sm + (n % NSR) * Geo<T>::UB); }
   __device__ T* F(uint32_t n) const {
-    return reinterpret_cast<T*>(sm + Geo<T>::NS * Geo<T>::UB + (n % Geo<T>::NS) * Geo<T>::FB);
+    return reinterpret_cast<T*>(sm + NSR * Geo<T>::UB + (n % NSR) * Geo<T>::FB);
   }
-  __device__ void wait(uint32_t n) const { mbar_wait(&full[n % Geo<T>::NS], (n / Geo<T>::NS) & 1u); }
+  __device__ void wait(uint32_t n) const { mbar_wait(&full[n % NSR], (n / NSR) & 1u); }
   // step n: u plane qu (unless !load_u), f plane qf
   __device__ void issue(uint32_t n, const CUtensorMap* tu, const CUtensorMap* tf, int x, int y, int qu, int qf,
                         bool load_u) const {
-    uint64_t* bar = &full[n % Geo<T>::NS];
+    uint64_t* bar = &full[n % NSR];
     const uint32_t ub = (uint32_t)(Geo<T>::BX * Geo<T>::BYU * sizeof(T));
     const uint32_t fb = (uint32_t)(Geo<T>::BX * Geo<T>::BYF * sizeof(T));
     mbar_expect_tx(bar, (load_u ? ub : 0u) + fb);
@@ -129,15 +133,15 @@ struct Ring {
   }
 };
 
-template <typename T>
-__device__ __forceinline__ Ring<T> ring_setup(unsigned char* sm, const CUtensorMap* tu, const CUtensorMap* tf) {
-  Ring<T> R;
+template <typename T, int NSR = Geo<T>::NS>
+__device__ __forceinline__ Ring<T, NSR> ring_setup(unsigned char* sm, const CUtensorMap* tu, const CUtensorMap* tf) {
+  Ring<T, NSR> R;
   R.sm = sm;
-  R.full = reinterpret_cast<uint64_t*>(sm + Geo<T>::BAR_OFF);
+  R.full = reinterpret_cast<uint64_t*>(sm + Ring<T, NSR>::BAR_OFF);
   if (threadIdx.x == 0) {
     prefetch_tmap(tu);
     prefetch_tmap(tf);
-    for (int s = 0; s < Geo<T>::NS; s++) mbar_init(&R.full[s], 1);
+    for (int s = 0; s < NSR; s++) mbar_init(&R.full[s], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -152,435 +156,6 @@ __device__ __forceinline__ void item_of(int k, int ntiles, int zc, int p_lo, int
   tile = k % ntiles;
   pa = p_lo + (k / ntiles) * zc;
   pb = min(pa + zc, p_hi);
-}
-
-// ---------------------------------------------------------------------------
-// MODE 0: Jacobi sweep; 1: red-black GS sweep; 2: residual-norm partials (one
-// double per CTA in `partial`, fixed reduction tree: deterministic).
-// ZERO: the input iterate is 0 (first coarse sweep after V_H(0, ...)); u not read.
-// NRM (modes 0, 1): also accumulate ||f - A u_in||^2 partials of the sweep's INPUT
-// (the norm after the previous cycle comes for free with the next cycle's first
-// sweep: u and f are read anyway).
-// CORR (modes 0, 1): the sweep's input is u + P e (Alg. 1 line 6), the
-// coarse-grid correction applied to every u box in shared memory as it arrives, so
-// the corrected iterate never makes an HBM round trip (prolongation fused into the
-// first post-smoothing sweep).  Same separable order as k_prolong3d.
-template <typename T, int MODE, bool ZERO, bool NRM = false, bool CORR = false>
-__global__ void __launch_bounds__(NT, Geo<T>::MINB)
-    k_sweep3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f, Geom g,
-              Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems,
-              double* __restrict__ partial, const __grid_constant__ CUtensorMap tm_e, Geom gc) {
-  using G = Geo<T>;
-  using V = Vec<T, G::W>;
-  constexpr int W = G::W, TX = G::TX, BX = G::BX, HX = G::HX, PX = G::PX, NR = G::NRED, RCOL = G::RCOL;
-  constexpr bool RB = MODE == 1;
-  // one barrier per plane (3 PR planes, refill one plane later) except with CORR, whose
-  // in-smem correction pass needs the shared-memory budget of the third PR plane
-  constexpr bool ONESYNC = !CORR;
-  // keep f(p-1) in registers for the black stage, except in the register-tight FP64 CORR variant
-  constexpr bool FKEEP = !(CORR && sizeof(T) == 8);
-  extern __shared__ __align__(128) unsigned char sm[];
-  const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
-  T* spr = reinterpret_cast<T*>(sm + G::PR_OFF);
-  auto PRb = [&](int q) {
-    return spr + (size_t)(ONESYNC ? ((q % 3) + 3) % 3 : (q & 1)) * (G::PB / sizeof(T));
-  };
-  auto su = [&](const T* base, int off) -> T { return ZERO ? (T)0 : base[off]; };
-  auto svec = [&](const T* base, int off) -> V {
-    if (ZERO) {
-      V z;
-#pragma unroll
-      for (int k = 0; k < W; k++) z.v[k] = (T)0;
-      return z;
-    }
-    return ld_vec(base + off);
-  };
-
-  const int tid = threadIdx.x, lane = tid & 31, ry = tid >> 5;
-  const int pg0 = g.p_glob0;
-  const int bo = (ry + 2) * BX + W * lane + HX;  // u-box offset of (ox, oy)
-  const int fo = (ry + 1) * BX + W * lane + HX;  // f-box offset of (ox, oy)
-  const int po = (ry + 1) * PX + W * lane + HX;  // PR offset of (ox, oy)
-  uint32_t seq = 0;
-  double nsum = 0.0;  // MODE 2 / NRM: this thread's sum of r^2
-
-  for (int k = blockIdx.x; k < nitems; k += gridDim.x) {
-    int tile, pa, pb;
-    item_of(k, ntiles, zc, g.p_lo, g.p_hi, tile, pa, pb);
-    const int x0 = (tile % tiles_x) * TX, y0 = (tile / tiles_x) * TY;
-    const int ox = x0 + W * lane, oy = y0 + ry;
-    const bool rin = oy >= 1 && oy <= g.ny - 1;
-    bool in[W];
-#pragma unroll
-    for (int j = 0; j < W; j++) in[j] = rin && ox + j >= 1 && ox + j <= g.nx - 1;
-    T* orow = unew + (long long)oy * g.pitch;
-
-    // r^2 of the thread's nodes at plane p from registers u(p-1), u(p), u(p+1) and smem u(p), f(p)
-    auto acc_norm = [&](const T* U0, const T* F0, const V& um, const V& u0, const V& up) {
-      const V fv = ld_vec(F0 + fo), dn = svec(U0, bo - BX), upr = svec(U0, bo + BX);
-      const T el = su(U0, bo - 1), er = su(U0, bo + W);
-#pragma unroll
-      for (int j = 0; j < W; j++) {
-        const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
-        const T r = j == W - 1 ? er : u0.v[j < W - 1 ? j + 1 : 0];
-        const double rr = (double)sub(fv.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
-        if (in[j]) nsum = acc_sq_d<T>(nsum, rr);
-      }
-    };
-
-    // step for plane q carries u(q+1), f(q); steps q = qlo .. qlast
-    const int qlo = RB ? pa - 3 : pa - 2, qlast = RB ? pb : pb - 1;
-    const uint32_t nlo = seq;
-    auto N = [&](int q) { return nlo + (uint32_t)(q - qlo); };
-    // CORR: coarse plane K lives in coarse slot K % 3; step q (fine u plane z = q+1) also
-    // loads coarse plane (z+1)/2 when z is odd (first needed there), the first step also
-    // z/2 (TMA, zero-filled outside the coarse array)
-    const int X0c = x0 / 2, Y0c = y0 / 2;
-    auto Cs = [&](int K) -> T* {
-      return reinterpret_cast<T*>(sm + G::COFF + (size_t)(((K % 3) + 3) % 3) * G::CB);
-    };
-    auto issue_step = [&](int q) {  // thread 0
-      if (CORR) {
-        uint64_t* bar = &R.full[N(q) % G::NS];
-        const int zg = q + 1 + pg0;
-        auto ld = [&](int K) {
-          mbar_add_tx(bar, (uint32_t)(G::CBX * G::CBY * sizeof(T)));
-          tma_load_3d(Cs(K), &tm_e, X0c - G::CHX, Y0c - 1, K - gc.p_glob0, bar);
-        };
-        if (q == qlo) ld(zg >> 1);
-        if (zg & 1) ld((zg + 1) >> 1);
-      }
-      R.issue(N(q), &tm_u, &tm_f, x0, y0, q + 1, q, !ZERO);
-    };
-    if (tid == 0)
-      for (int q = qlo; q < qlo + G::NS && q <= qlast; q++) issue_step(q);
-
-    // ---- CORR: u += P e on the u box of fine local plane zl (in smem, right after its arrival)
-    const T half = (T)0.5;
-    int cZ = -1000000;
-    V cA, cB;
-    bool cHaveB = false;
-    auto e_at = [&](int X, int Y, int Zg) -> T {
-      return Cs(Zg)[(Y - Y0c + 1) * G::CBX + (X - X0c + G::CHX)];
-    };
-    auto Vvec = [&](int Zg) -> V {  // the thread's W nodes of row oy after the x- and y-interpolation
-      const int X = ox >> 1, Y = oy >> 1;
-      T a[NR + 1], b[NR + 1];
-#pragma unroll
-      for (int i = 0; i <= NR; i++) a[i] = e_at(X + i, Y, Zg);
-      V v;
-#pragma unroll
-      for (int i = 0; i < NR; i++) {
-        v.v[2 * i] = a[i];
-        v.v[2 * i + 1] = mul(half, add(a[i], a[i + 1]));
-      }
-      if (oy & 1) {
-#pragma unroll
-        for (int i = 0; i <= NR; i++) b[i] = e_at(X + i, Y + 1, Zg);
-#pragma unroll
-        for (int i = 0; i < NR; i++) {
-          v.v[2 * i] = mul(half, add(v.v[2 * i], b[i]));
-          v.v[2 * i + 1] = mul(half, add(v.v[2 * i + 1], mul(half, add(b[i], b[i + 1]))));
-        }
-      }
-      return v;
-    };
-    auto interp = [&](int x, int y, int zg) -> T {  // single node, reading 13 order
-      const int X = x >> 1, dx = x & 1, Y = y >> 1, dy = y & 1, Z = zg >> 1, dz = zg & 1;
-      T vy[2];
-      for (int zz = 0; zz <= dz; zz++) {
-        T vx[2];
-        for (int yy = 0; yy <= dy; yy++)
-          vx[yy] = dx ? mul(half, add(e_at(X, Y + yy, Z + zz), e_at(X + 1, Y + yy, Z + zz))) : e_at(X, Y + yy, Z + zz);
-        vy[zz] = dy ? mul(half, add(vx[0], vx[1])) : vx[0];
-      }
-      return dz ? mul(half, add(vy[0], vy[1])) : vy[0];
-    };
-    auto correct = [&](T* Ub, int zl) {
-      const int zg = zl + pg0;
-      if (zg < 1 || zg > g.nz - 1) return;  // boundary / outside planes: no correction
-      bool any = false;
-#pragma unroll
-      for (int j = 0; j < W; j++) any = any || in[j];
-      if (any) {
-        if ((zg >> 1) != cZ) {
-          cA = (cHaveB && (zg >> 1) == cZ + 1) ? cB : Vvec(zg >> 1);
-          cZ = zg >> 1;
-          cHaveB = false;
-        }
-        V v = cA;
-        if (zg & 1) {
-          if (!cHaveB) {
-            cB = Vvec(cZ + 1);
-            cHaveB = true;
-          }
-#pragma unroll
-          for (int j = 0; j < W; j++) v.v[j] = mul(half, add(cA.v[j], cB.v[j]));
-        }
-        T* up_ = Ub + bo;
-#pragma unroll
-        for (int j = 0; j < W; j++)
-          if (in[j]) up_[j] = add(up_[j], v.v[j]);
-      }
-      for (int e = tid; e < G::NRING_CORR; e += NT) {  // box nodes around the tile that the stencils read
-        int x, y;
-        if (e < 4 * (TX + 4)) {
-          const int rr = e / (TX + 4);
-          y = rr < 2 ? y0 - 2 + rr : y0 + TY + rr - 2;
-          x = x0 - 2 + e % (TX + 4);
-        } else {
-          const int t2 = e - 4 * (TX + 4), cc = t2 / TY;
-          x = cc < 2 ? x0 - 2 + cc : x0 + TX + cc - 2;
-          y = y0 + t2 % TY;
-        }
-        if (x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1) {
-          T* q = Ub + (y - y0 + 2) * BX + (x - x0 + HX);
-          *q = add(*q, interp(x, y, zg));
-        }
-      }
-    };
-
-    R.wait(N(qlo));
-    R.wait(N(qlo + 1));
-    if (CORR) {
-      correct(R.U(N(qlo)), qlo + 1);
-      correct(R.U(N(qlo + 1)), qlo + 2);
-      __syncthreads();
-    }
-    V um = svec(R.U(N(qlo)), bo), u0 = svec(R.U(N(qlo + 1)), bo), up;
-
-    // RB ring threads: warps 0 / 1 the red nodes of rows y0-1 / y0+TY (NR per lane), warp 2
-    // lanes [0, RCOL) column x0-1 and [RCOL, 2 RCOL) column x0+TX (one each)
-    // (one red ring node per lane and plane: FP32 lanes hold NR = 2 red nodes per ring row, so
-    // 2 NR warps share the two ring rows — warp w: row (w & 1), node m = w >> 1 — keeping every
-    // warp's extra work at one relaxation; the plane barrier waits for the slowest warp)
-    constexpr int RWARPS = 2 * NR;
-    const bool ring_row = RB && ry < RWARPS;
-    const bool ring_col = RB && ry == RWARPS && lane < 2 * RCOL;
-    const int mring = ring_row ? (ry >> 1) : 0;
-    auto ring_pos = [&](int pgl, int m, int& x, int& y) {
-      if (ry < RWARPS) {
-        y = (ry & 1) == 0 ? y0 - 1 : y0 + TY;
-        x = x0 + W * lane + 2 * m + ((y + pgl) & 1);  // x0 even
-      } else {
-        x = lane < RCOL ? x0 - 1 : x0 + TX;
-        y = y0 + 2 * (lane % RCOL) + ((x + y0 + pgl) & 1);
-      }
-    };
-    T rzm = (T)0;  // ring thread: u(p-1) at its plane-p ring node
-    if (ring_row || ring_col) {
-      int x, y;
-      ring_pos(pa - 1 + pg0, mring, x, y);
-      rzm = su(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
-    }
-    __syncthreads();  // step qlo lives on in registers only: refill its slot
-    if (tid == 0 && qlo + G::NS <= qlast) {
-      fence_proxy_async();
-      issue_step(qlo + G::NS);
-    }
-
-    if (RB) {
-      T pr1[NR], pr2[NR];  // own red values of planes p-1, p-2 (index m: node kr + 2m of that plane)
-#pragma unroll
-      for (int m = 0; m < NR; m++) pr1[m] = pr2[m] = (T)0;
-      V fprev;  // f(p-1) of the thread's nodes (loaded by the previous plane's red stage)
-#pragma unroll
-      for (int j = 0; j < W; j++) fprev.v[j] = (T)0;
-      for (int p = pa - 1; p <= pb; p++) {
-        R.wait(N(p));
-        if (CORR) {
-          correct(R.U(N(p)), p + 1);
-          __syncthreads();
-        }
-        const T* U0 = R.U(N(p - 1));  // u(p)
-        const T* Up = R.U(N(p));      // u(p+1)
-        const T* F0 = R.F(N(p));      // f(p)
-        T* PR = PRb(p);
-        up = svec(Up, bo);
-        const int pgl = p + pg0;
-        const bool pl_in = pgl >= 1 && pgl <= g.nz - 1;
-        const int kr = (oy + pgl) & 1;  // warp uniform: red nodes at ox + kr + 2m
-        // NRM: ||f - A u_in||^2 of plane p; the red nodes' residuals come from the red stage below
-        // (the same operands), only the black nodes' are computed separately
-        const bool nrm_here = NRM && p >= pa && p < pb;
-        T pr0[NR];
-        const V fcur = ld_vec(F0 + fo);  // f(p) of the thread's nodes (kept for plane p's black stage)
-        auto red_stage = [&](auto KRc) {
-          constexpr int KR = decltype(KRc)::value;
-          // FP32: 16-B vector loads of the rows above / below (one LDS.128 instead of two
-          // 4-way-conflicted scalars); FP64 (one red node per thread): the scalar is as cheap
-          V dn, upr;
-          if constexpr (W == 4 || NRM) {
-            dn = svec(U0, bo - BX);
-            upr = svec(U0, bo + BX);
-          } else {
-            dn.v[KR] = su(U0, bo + KR - BX);
-            upr.v[KR] = su(U0, bo + KR + BX);
-          }
-          const T edge = KR == 0 ? su(U0, bo - 1) : su(U0, bo + W);
-          if constexpr (NRM) {
-            if (nrm_here) {  // black nodes of plane p: residual of the old iterate
-              const T oedge = KR == 0 ? su(U0, bo + W) : su(U0, bo - 1);
-#pragma unroll
-              for (int m = 0; m < NR; m++) {
-                const int j = (1 - KR) + 2 * m;
-                const T l = j == 0 ? oedge : u0.v[j > 0 ? j - 1 : 0];
-                const T r = j == W - 1 ? oedge : u0.v[j < W - 1 ? j + 1 : 0];
-                const double rr =
-                    (double)sub(fcur.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
-                if (in[j]) nsum = acc_sq_d<T>(nsum, rr);
-              }
-            }
-          }
-          V pv = u0;  // PR row vector: red values at red nodes (black entries are never read)
-#pragma unroll
-          for (int m = 0; m < NR; m++) {
-            const int j = KR + 2 * m;
-            const T ctr = u0.v[j];
-            const T l = j == 0 ? edge : u0.v[j > 0 ? j - 1 : 0];
-            const T r = j == W - 1 ? edge : u0.v[j < W - 1 ? j + 1 : 0];
-            // relax() written out: the residual doubles as the red node's norm term
-            const T res = sub(fcur.v[j], apply_A(c, ctr, l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
-            const T v = add(ctr, mul(c.wd, res));
-            if (NRM && nrm_here && in[j]) nsum = acc_sq<T>(nsum, res);
-            const T prv = (pl_in && in[j]) ? v : ctr;
-            pv.v[j] = prv;
-            pr0[m] = prv;
-          }
-          if constexpr (sizeof(T) == 8)
-            *reinterpret_cast<double2*>(PR + po) = make_double2(pv.v[0], pv.v[1]);
-          else
-            *reinterpret_cast<float4*>(PR + po) = make_float4(pv.v[0], pv.v[1], pv.v[2], pv.v[3]);
-        };
-        if (kr)
-          red_stage(std::integral_constant<int, 1>());
-        else
-          red_stage(std::integral_constant<int, 0>());
-        if (ring_row || ring_col) {  // the red ring node of plane p
-          int x, y;
-          ring_pos(pgl, mring, x, y);
-          const int rb = (y - y0 + 2) * BX + (x - x0 + HX);
-          const T ctr = su(U0, rb);
-          const T v = relax(c, ctr, su(U0, rb - 1), su(U0, rb + 1), su(U0, rb - BX), su(U0, rb + BX), rzm, su(Up, rb),
-                            F0[(y - y0 + 1) * BX + (x - x0 + HX)]);
-          const bool ok = pl_in && x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1;
-          PR[(y - y0 + 1) * PX + (x - x0 + HX)] = ok ? v : ctr;
-          ring_pos(pgl + 1, mring, x, y);  // next plane's node: its z-neighbour below is u(p)
-          rzm = su(U0, (y - y0 + 2) * BX + (x - x0 + HX));
-        }
-        __syncthreads();
-        // ONESYNC: every thread has finished plane p-2's black update: step p-2 is free.
-        // FKEEP (f(p-1) kept in registers for the black stage): step p-1 (u(p), f(p-1)) is
-        // read only by plane p's red stage, so it is free here already — one plane deeper
-        // prefetch with the same NS slots
-        constexpr int LAG = FKEEP ? 1 : 2;
-        if (ONESYNC && tid == 0 && p >= pa - 2 + LAG && p - LAG + G::NS <= qlast) {
-          fence_proxy_async();
-          issue_step(p - LAG + G::NS);
-        }
-        const int bp = p - 1;  // black nodes of plane p-1: they sit where plane p's red nodes are
-        if (bp >= pa) {
-          const T* P = PRb(bp);
-          auto black_stage = [&](auto KBc) {
-            constexpr int KB = decltype(KBc)::value;
-            V pdn, pup;
-            if constexpr (W == 4) {
-              pdn = ld_vec(P + po - PX);
-              pup = ld_vec(P + po + PX);
-            } else {
-              pdn.v[KB] = P[po + KB - PX];
-              pup.v[KB] = P[po + KB + PX];
-            }
-            const T edge = KB == 0 ? P[po - 1] : P[po + W];
-            const V fb = FKEEP ? fprev : ld_vec(R.F(N(bp)) + fo);
-            // plane bp's red nodes (pr1) sit at (1-KB) + 2m
-            V o;
-#pragma unroll
-            for (int m = 0; m < NR; m++) o.v[(1 - KB) + 2 * m] = pr1[m];
-#pragma unroll
-            for (int m = 0; m < NR; m++) {
-              const int j = KB + 2 * m;
-              const T ctr = um.v[j];
-              // x-1: red of plane bp at j-1 = (1-KB) + 2m' -> m' = m - (1-KB)
-              const T l = (KB == 0 && m == 0) ? edge : pr1[KB == 1 ? m : (m > 0 ? m - 1 : 0)];
-              // x+1: m' = m + KB
-              const T r = (KB == 1 && m == NR - 1) ? edge : pr1[KB == 0 ? m : (m + 1 < NR ? m + 1 : 0)];
-              const T v = relax(c, ctr, l, r, pdn.v[j], pup.v[j], pr2[m], pr0[m], fb.v[j]);
-              o.v[j] = in[j] ? v : ctr;
-            }
-            store_vec(orow + (long long)bp * g.pstride, ox, in, o);
-          };
-          if (kr)
-            black_stage(std::integral_constant<int, 1>());
-          else
-            black_stage(std::integral_constant<int, 0>());
-        }
-        if (!ONESYNC) {
-          __syncthreads();
-          if (tid == 0 && p - 1 + G::NS <= qlast) {  // step p-1 (u(p), f(p-1)) is consumed
-            fence_proxy_async();
-            issue_step(p - 1 + G::NS);
-          }
-        }
-        um = u0;
-        u0 = up;
-        if (FKEEP) fprev = fcur;
-#pragma unroll
-        for (int m = 0; m < NR; m++) {
-          pr2[m] = pr1[m];
-          pr1[m] = pr0[m];
-        }
-      }
-    } else {
-      for (int p = pa; p < pb; p++) {
-        R.wait(N(p));
-        if (CORR) {
-          correct(R.U(N(p)), p + 1);
-          __syncthreads();
-        }
-        const T* U0 = R.U(N(p - 1));
-        up = svec(R.U(N(p)), bo);
-        if (MODE == 2) acc_norm(U0, R.F(N(p)), um, u0, up);  // r = f - A u, FP64 squares
-        if (MODE != 2) {
-          const V fv = ld_vec(R.F(N(p)) + fo), dn = svec(U0, bo - BX), upr = svec(U0, bo + BX);
-          const T el = su(U0, bo - 1), er = su(U0, bo + W);
-          V o;
-#pragma unroll
-          for (int j = 0; j < W; j++) {
-            const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
-            const T r = j == W - 1 ? er : u0.v[j < W - 1 ? j + 1 : 0];
-            // relax() written out: with NRM the residual is also the norm term of the input
-            const T res = sub(fv.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
-            const T v = add(u0.v[j], mul(c.wd, res));
-            if (NRM && in[j]) nsum = acc_sq<T>(nsum, res);
-            o.v[j] = in[j] ? v : u0.v[j];
-          }
-          store_vec(orow + (long long)p * g.pstride, ox, in, o);
-        }
-        __syncthreads();
-        if (tid == 0 && p - 1 + G::NS <= qlast) {
-          fence_proxy_async();
-          issue_step(p - 1 + G::NS);
-        }
-        um = u0;
-        u0 = up;
-      }
-    }
-    seq = N(qlast) + 1;
-    __syncthreads();
-  }
-  if (MODE == 2 || NRM) {  // fixed-order block reduction -> one partial per CTA
-    double* red = reinterpret_cast<double*>(sm);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nsum = __dadd_rn(nsum, __shfl_down_sync(0xffffffffu, nsum, o));
-    if (lane == 0) red[ry] = nsum;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w2 = 0; w2 < NT / 32; w2++) t = __dadd_rn(t, red[w2]);
-      partial[blockIdx.x] = t;
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -609,11 +184,20 @@ __device__ __forceinline__ void static_for(F&& f) {
 // residuals of the black nodes of the sweep's OUTPUT: a black node's neighbours are all red
 // and final when it is relaxed, so the stencil sum s of its relaxation is the sum the norm
 // forms at the output, and r = f - (D v - s) is that residual bitwise (3 more operations)
-template <typename T, int MODE, bool ZERO, int NM, int RPT>
+//
+// CORR (the first post-smoothing sweep, MG_FLAG_FUSE_PROLONG): the sweep's input is u + P e (Alg. 1
+// line 6).  The coarse planes of e arrive by TMA with the u box (3 slots; the u/f
+// ring has 3 slots then, for shared memory).  While plane p is processed, the box of plane p+1
+// (just arrived) is corrected in place: every thread its own rows (in registers, then written
+// back), the box ring nodes by all threads, the red ring threads the one node of that box they
+// read during plane p themselves; nothing else reads that box before the plane barrier, so
+// one barrier per plane remains.  The corrected iterate never reaches HBM.  Same separable
+// interpolation order as k_prolong3d_flat (bitwise equal to the separate prolongation).
+template <typename T, int MODE, bool ZERO, int NM, int RPT, bool CORR = false>
 __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     k_sweep3d_rows(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f, Geom g,
                    Coef<T> c, T* __restrict__ unew, int tiles_x, int ntiles, int zc, int nitems,
-                   double* __restrict__ partial) {
+                   double* __restrict__ partial, const __grid_constant__ CUtensorMap tm_e, Geom gc) {
   using G = Geo<T>;
   using V = Vec<T, G::W>;
   constexpr int W = G::W, TX = G::TX, BX = G::BX, HX = G::HX, PX = G::PX, NR = G::NRED, RCOL = G::RCOL;
@@ -622,9 +206,13 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
   constexpr bool NRM = NM == 1 || NM == 2;  // input residuals (NM 2: red nodes only)
   static_assert(TY % RPT == 0, "rows per thread");
   static_assert(NM != 3 || RB, "output black residuals: RBGS only");
+  static_assert(!CORR || (NM == 0 && !ZERO && MODE != 2), "CORR: a plain sweep");
+  constexpr int NSR = CORR ? 3 : G::NS;                     // u/f ring slots
+  constexpr int PR_OFF = Ring<T, NSR>::BAR_OFF + 128;       // 3 PR planes, then (CORR) 3 coarse boxes
+  constexpr int COFF = PR_OFF + 3 * G::PB;
   extern __shared__ __align__(128) unsigned char sm[];
-  const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
-  T* spr = reinterpret_cast<T*>(sm + G::PR_OFF);
+  const Ring<T, NSR> R = ring_setup<T, NSR>(sm, &tm_u, &tm_f);
+  T* spr = reinterpret_cast<T*>(sm + PR_OFF);
   auto PRb = [&](int q) { return spr + (size_t)(((q % 3) + 3) % 3) * (G::PB / sizeof(T)); };
   auto su = [&](const T* base, int off) -> T { return ZERO ? (T)0 : base[off]; };
   auto svec = [&](const T* base, int off) -> V {
@@ -662,13 +250,135 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     const int qlo = RB ? pa - 3 : pa - 2, qlast = RB ? pb : pb - 1;
     const uint32_t nlo = seq;
     auto N = [&](int q) { return nlo + (uint32_t)(q - qlo); };
-    auto issue_step = [&](int q) { R.issue(N(q), &tm_u, &tm_f, x0, y0, q + 1, q, !ZERO); };
+    // CORR: coarse plane K lives in coarse slot K % 3; step q (fine u plane z = q+1) also loads
+    // coarse plane (z+1)/2 when z is odd (first needed there), the first step also z/2
+    const int X0c = x0 / 2, Y0c = y0 / 2;
+    auto Cs = [&](int K) -> T* { return reinterpret_cast<T*>(sm + COFF + (size_t)(((K % 3) + 3) % 3) * G::CB); };
+    auto issue_step = [&](int q) {
+      if (CORR) {
+        uint64_t* bar = &R.full[N(q) % NSR];
+        const int zg = q + 1 + g.p_glob0;
+        auto ld = [&](int K) {
+          mbar_add_tx(bar, (uint32_t)(G::CBX * G::CBY * sizeof(T)));
+          tma_load_3d(Cs(K), &tm_e, X0c - G::CHX, Y0c - 1, K - gc.p_glob0, bar);
+        };
+        if (q == qlo) ld(zg >> 1);
+        if (zg & 1) ld((zg + 1) >> 1);
+      }
+      R.issue(N(q), &tm_u, &tm_f, x0, y0, q + 1, q, !ZERO);
+    };
     if (tid == 0)
-      for (int q = qlo; q < qlo + G::NS && q <= qlast; q++) issue_step(q);
+      for (int q = qlo; q < qlo + NSR && q <= qlast; q++) issue_step(q);
+
+    // ---- CORR: u += P e (reading 13 order: x, then y, then z interpolation)
+    const T half = (T)0.5;
+    auto e_at = [&](int X, int Y, int Zg) -> T { return Cs(Zg)[(Y - Y0c + 1) * G::CBX + (X - X0c + G::CHX)]; };
+    auto interp = [&](int x, int y, int zg) -> T {  // one node
+      const int X = x >> 1, dx = x & 1, Y = y >> 1, dy = y & 1, Z = zg >> 1, dz = zg & 1;
+      T vy[2];
+      for (int zz = 0; zz <= dz; zz++) {
+        T vx[2];
+        for (int yy = 0; yy <= dy; yy++)
+          vx[yy] = dx ? mul(half, add(e_at(X, Y + yy, Z + zz), e_at(X + 1, Y + yy, Z + zz))) : e_at(X, Y + yy, Z + zz);
+        vy[zz] = dy ? mul(half, add(vx[0], vx[1])) : vx[0];
+      }
+      return dz ? mul(half, add(vy[0], vy[1])) : vy[0];
+    };
+    auto Vrow = [&](int k, int Zg) -> V {  // row k's W nodes after the x- and y-interpolation of coarse plane Zg
+      const int X = ox >> 1, Y = (oy0 + k) >> 1;
+      T a[NR + 1], b[NR + 1];
+#pragma unroll
+      for (int i = 0; i <= NR; i++) a[i] = e_at(X + i, Y, Zg);
+      V v;
+#pragma unroll
+      for (int i = 0; i < NR; i++) {
+        v.v[2 * i] = a[i];
+        v.v[2 * i + 1] = mul(half, add(a[i], a[i + 1]));
+      }
+      if ((oy0 + k) & 1) {
+#pragma unroll
+        for (int i = 0; i <= NR; i++) b[i] = e_at(X + i, Y + 1, Zg);
+#pragma unroll
+        for (int i = 0; i < NR; i++) {
+          v.v[2 * i] = mul(half, add(v.v[2 * i], b[i]));
+          v.v[2 * i + 1] = mul(half, add(v.v[2 * i + 1], mul(half, add(b[i], b[i + 1]))));
+        }
+      }
+      return v;
+    };
+    int cZ = -1000000;  // coarse plane of cA (cB: cZ + 1 when cHaveB)
+    V cA[RPT], cB[RPT];
+    bool cHaveB = false;
+    // own rows of fine plane zl (local) in registers: uv[k] += P e
+    auto correct_own = [&](V* uv, int zl) {
+      const int zg = zl + g.p_glob0;
+      if (zg < 1 || zg > g.nz - 1) return;  // boundary / outside planes: no correction
+      if ((zg >> 1) != cZ) {
+        const bool shift = cHaveB && (zg >> 1) == cZ + 1;
+#pragma unroll
+        for (int k = 0; k < RPT; k++) cA[k] = shift ? cB[k] : Vrow(k, zg >> 1);
+        cZ = zg >> 1;
+        cHaveB = false;
+      }
+      if ((zg & 1) && !cHaveB) {
+#pragma unroll
+        for (int k = 0; k < RPT; k++) cB[k] = Vrow(k, cZ + 1);
+        cHaveB = true;
+      }
+#pragma unroll
+      for (int k = 0; k < RPT; k++)
+#pragma unroll
+        for (int j = 0; j < W; j++) {
+          const T v = (zg & 1) ? mul(half, add(cA[k].v[j], cB[k].v[j])) : cA[k].v[j];
+          if (in[k][j]) uv[k].v[j] = add(uv[k].v[j], v);
+        }
+    };
+    auto box_ring_node = [&](int e, int& x, int& y) {  // box nodes around the tile that the stencils read
+      if (e < 4 * (TX + 4)) {
+        const int rr = e / (TX + 4);
+        y = rr < 2 ? y0 - 2 + rr : y0 + TY + rr - 2;
+        x = x0 - 2 + e % (TX + 4);
+      } else {
+        const int t2 = e - 4 * (TX + 4), cc = t2 / TY;
+        x = cc < 2 ? x0 - 2 + cc : x0 + TX + cc - 2;
+        y = y0 + t2 % TY;
+      }
+    };
+    // the box ring nodes of fine plane zl in shared memory; skip_red_pgl >= 0: leave out the red
+    // ring-1 nodes of plane skip_red_pgl that the ring threads correct themselves
+    auto correct_ring = [&](T* Ub, int zl, int skip_red_pgl) {
+      const int zg = zl + g.p_glob0;
+      if (zg < 1 || zg > g.nz - 1) return;
+      for (int e = tid; e < G::NRING_CORR; e += NTH) {
+        int x, y;
+        box_ring_node(e, x, y);
+        if (x < 1 || x > g.nx - 1 || y < 1 || y > g.ny - 1) continue;
+        if (skip_red_pgl >= 0 && ((x + y + skip_red_pgl) & 1) == 0 &&
+            (((y == y0 - 1 || y == y0 + TY) && x >= x0 && x < x0 + TX) ||
+             ((x == x0 - 1 || x == x0 + TX) && y >= y0 && y < y0 + TY)))
+          continue;
+        T* q = Ub + (y - y0 + 2) * BX + (x - x0 + HX);
+        *q = add(*q, interp(x, y, zg));
+      }
+    };
 
     R.wait(N(qlo));
     R.wait(N(qlo + 1));
     V um[RPT], u0[RPT], up[RPT];
+    if constexpr (CORR) {  // the first two boxes, in shared memory, before anyone reads them
+#pragma unroll
+      for (int b = 0; b < 2; b++) {
+        T* Ub = R.U(N(qlo + b));
+        V own[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; k++) own[k] = ld_vec(Ub + bo + k * BX);
+        correct_own(own, qlo + 1 + b);
+#pragma unroll
+        for (int k = 0; k < RPT; k++) st_vec(Ub + bo + k * BX, own[k]);
+        correct_ring(Ub, qlo + 1 + b, -1);
+      }
+      __syncthreads();
+    }
 #pragma unroll
     for (int k = 0; k < RPT; k++) {
       um[k] = svec(R.U(N(qlo)), bo + k * BX);
@@ -697,9 +407,9 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
       rzm = su(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
     }
     __syncthreads();  // step qlo lives on in registers only: refill its slot
-    if (tid == 0 && qlo + G::NS <= qlast) {
+    if (tid == 0 && qlo + NSR <= qlast) {
       fence_proxy_async();
-      issue_step(qlo + G::NS);
+      issue_step(qlo + NSR);
     }
 
     if constexpr (RB) {
@@ -721,6 +431,12 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
 #pragma unroll
         for (int k = 0; k < RPT; k++) up[k] = svec(Up, bo + k * BX);
         const int pgl = p + g.p_glob0;
+        if constexpr (CORR) {  // plane p+1's box: own rows (registers + write-back) and its ring
+          correct_own(up, p + 1);
+#pragma unroll
+          for (int k = 0; k < RPT; k++) st_vec(const_cast<T*>(Up) + bo + k * BX, up[k]);
+          correct_ring(const_cast<T*>(Up), p + 1, pgl);
+        }
         const bool pl_in = pgl >= 1 && pgl <= g.nz - 1;
         const int kr0 = (oy0 + pgl) & 1;  // red offset of row 0 (row k: kr0 ^ (k & 1)), warp uniform
         const bool nrm_here = NRM && p >= pa && p < pb;
@@ -778,7 +494,15 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
           ring_pos(pgl, mring, x, y);
           const int rb = (y - y0 + 2) * BX + (x - x0 + HX);
           const T ctr = su(U0, rb);
-          const T v = relax(c, ctr, su(U0, rb - 1), su(U0, rb + 1), su(U0, rb - BX), su(U0, rb + BX), rzm, su(Up, rb),
+          T zp = su(Up, rb);  // u(p+1) at the node (CORR: this thread corrects it in the box)
+          if constexpr (CORR) {
+            const int zg1 = pgl + 1;
+            if (x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1 && zg1 >= 1 && zg1 <= g.nz - 1) {
+              zp = add(zp, interp(x, y, zg1));
+              const_cast<T*>(Up)[rb] = zp;
+            }
+          }
+          const T v = relax(c, ctr, su(U0, rb - 1), su(U0, rb + 1), su(U0, rb - BX), su(U0, rb + BX), rzm, zp,
                             F0[(y - y0 + 1) * BX + (x - x0 + HX)]);
           const bool ok = pl_in && x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1;
           PR[(y - y0 + 1) * PX + (x - x0 + HX)] = ok ? v : ctr;
@@ -788,9 +512,9 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
         __syncthreads();
         // every thread is past plane p-2's black update and plane p's red stage: step p-1
         // (u(p), f(p-1); f(p-1) is in registers) is consumed
-        if (tid == 0 && p >= pa - 1 && p - 1 + G::NS <= qlast) {
+        if (tid == 0 && p >= pa - 1 && p - 1 + NSR <= qlast) {
           fence_proxy_async();
-          issue_step(p - 1 + G::NS);
+          issue_step(p - 1 + NSR);
         }
         const int bp = p - 1;
         if (bp >= pa) {
@@ -872,6 +596,13 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
         const T* F0 = R.F(N(p));
 #pragma unroll
         for (int k = 0; k < RPT; k++) up[k] = svec(R.U(N(p)), bo + k * BX);
+        if constexpr (CORR) {
+          T* Upw = R.U(N(p));
+          correct_own(up, p + 1);
+#pragma unroll
+          for (int k = 0; k < RPT; k++) st_vec(Upw + bo + k * BX, up[k]);
+          correct_ring(Upw, p + 1, -1);
+        }
         static_for<RPT>([&](auto Kc) {
           constexpr int K = decltype(Kc)::value;
           const V fv = ld_vec(F0 + fo + K * BX);
@@ -894,9 +625,9 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
           if (MODE != 2) store_vec(orow + (long long)K * g.pitch + (long long)p * g.pstride, ox, in[K], o);
         });
         __syncthreads();
-        if (tid == 0 && p - 1 + G::NS <= qlast) {
+        if (tid == 0 && p - 1 + NSR <= qlast) {
           fence_proxy_async();
-          issue_step(p - 1 + G::NS);
+          issue_step(p - 1 + NSR);
         }
 #pragma unroll
         for (int k = 0; k < RPT; k++) {
@@ -929,139 +660,6 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
 // low-side ring nodes (row y0-1, column x0-1) into smem; then the coarse nodes
 // of the tile form their x- then y-sums of plane q and keep the last three in
 // registers: when q = 2P+1 the z-sum gives f_H(P) (reading 13 order).
-template <typename T>
-__global__ void __launch_bounds__(NT, Geo<T>::MINB)
-    k_resid_restrict3d(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_f,
-                       Geom gf, Geom gc, Coef<T> c, T* __restrict__ fc, int tiles_x, int ntiles, int zcc,
-                       int nitems) {
-  using G = Geo<T>;
-  using V = Vec<T, G::W>;
-  constexpr int W = G::W, TX = G::TX, BX = G::BX, HX = G::HX, PX = G::PX;
-  extern __shared__ __align__(128) unsigned char sm[];
-  const Ring<T> R = ring_setup<T>(sm, &tm_u, &tm_f);
-  // r planes alternate between two smem buffers: one barrier per fine plane
-  T* const Rr2 = reinterpret_cast<T*>(sm + G::PR_OFF);
-
-  const int tid = threadIdx.x, lane = tid & 31, ry = tid >> 5;
-  const int pgf0 = gf.p_glob0;
-  const int bo = (ry + 2) * BX + W * lane + HX;
-  const int fo = (ry + 1) * BX + W * lane + HX;
-  const int po = (ry + 1) * PX + W * lane + HX;
-  const T two = (T)2;
-  const T scale = (T)(1.0 / 64.0);
-  // coarse node of this thread (tile of TX/2 x TY/2 coarse nodes)
-  constexpr int CNX = TX / 2, CN = (TX / 2) * (TY / 2);
-  const int ccx = tid % CNX, ccy = tid / CNX;
-  const int co = (2 * ccy + 1) * PX + 2 * ccx + HX;  // r offset of fine (2I, 2J)
-  uint32_t seq = 0;
-  for (int k = blockIdx.x; k < nitems; k += gridDim.x) {
-    int tile, Pa, Pb;
-    item_of(k, ntiles, zcc, gc.p_lo, gc.p_hi, tile, Pa, Pb);
-    const int X0 = (tile % tiles_x) * (TX / 2), Y0 = (tile / tiles_x) * (TY / 2);
-    const int x0 = 2 * X0, y0 = 2 * Y0;
-    const int ox = x0 + W * lane, oy = y0 + ry;
-    const bool rin = oy >= 1 && oy <= gf.ny - 1;
-    bool in[W];
-#pragma unroll
-    for (int j = 0; j < W; j++) in[j] = rin && ox + j >= 1 && ox + j <= gf.nx - 1;
-    // low-side ring: row y0-1 for x in [x0-1, x0+TX-1] (TX+1 nodes), column x0-1 for y in [y0, y0+TY-1]
-    const bool has_ring = tid < TX + 1 + TY;
-    const int rx = tid < TX + 1 ? x0 - 1 + tid : x0 - 1;
-    const int ryy = tid < TX + 1 ? y0 - 1 : y0 + tid - (TX + 1);
-    const bool ring_in = rx >= 1 && rx <= gf.nx - 1 && ryy >= 1 && ryy <= gf.ny - 1;
-    const int rb = (ryy - y0 + 2) * BX + (rx - x0 + HX);
-    const int rf = (ryy - y0 + 1) * BX + (rx - x0 + HX);
-    const int rpo = (ryy - y0 + 1) * PX + (rx - x0 + HX);
-    const int I = X0 + ccx, J = Y0 + ccy;
-    const bool cnode = tid < CN && I >= 1 && I <= gc.nx - 1 && J >= 1 && J <= gc.ny - 1;
-    T* crow = fc + (long long)J * gc.pitch + I;
-
-    const int qf0 = 2 * (Pa + gc.p_glob0) - pgf0;      // fine centre of the first coarse plane
-    const int qf1 = 2 * (Pb - 1 + gc.p_glob0) - pgf0;  // ... of the last
-    const int rlo = qf0 - 1, rhi = qf1 + 1;              // r planes needed
-    const int qlo = rlo - 2, qlast = rhi;                // steps: u(q+1), f(q)
-    const uint32_t nlo = seq;
-    auto N = [&](int q) { return nlo + (uint32_t)(q - qlo); };
-    if (tid == 0)
-      for (int q = qlo; q < qlo + G::NS && q <= qlast; q++) R.issue(N(q), &tm_u, &tm_f, x0, y0, q + 1, q, true);
-    R.wait(N(qlo));
-    R.wait(N(qlo + 1));
-    V um = ld_vec(R.U(N(qlo)) + bo), u0 = ld_vec(R.U(N(qlo + 1)) + bo), up;
-    T rzm = has_ring ? R.U(N(qlo))[rb] : (T)0;
-    __syncthreads();  // step qlo lives on in registers only: refill its slot
-    if (tid == 0 && qlo + G::NS <= qlast) {
-      fence_proxy_async();
-      R.issue(N(qlo + G::NS), &tm_u, &tm_f, x0, y0, qlo + G::NS + 1, qlo + G::NS, true);
-    }
-    T ty1 = (T)0, ty2 = (T)0;
-    for (int q = rlo; q <= rhi; q++) {
-      R.wait(N(q));
-      const T* U0 = R.U(N(q - 1));
-      const T* Up = R.U(N(q));
-      const T* F0 = R.F(N(q));
-      T* Rr = Rr2 + (size_t)(q & 1) * (G::PB / sizeof(T));
-      up = ld_vec(Up + bo);
-      const int pgl = q + pgf0;
-      const bool pl_in = pgl >= 1 && pgl <= gf.nz - 1;
-      {
-        const V fv = ld_vec(F0 + fo), dn = ld_vec(U0 + bo - BX), upr = ld_vec(U0 + bo + BX);
-        const T el = U0[bo - 1], er = U0[bo + W];
-        V rv;
-#pragma unroll
-        for (int j = 0; j < W; j++) {
-          const T l = j == 0 ? el : u0.v[j > 0 ? j - 1 : 0];
-          const T r = j == W - 1 ? er : u0.v[j < W - 1 ? j + 1 : 0];
-          const T rr = sub(fv.v[j], apply_A(c, u0.v[j], l, r, dn.v[j], upr.v[j], um.v[j], up.v[j]));
-          rv.v[j] = pl_in && in[j] ? rr : (T)0;
-        }
-        if constexpr (sizeof(T) == 8)
-          *reinterpret_cast<double2*>(Rr + po) = make_double2(rv.v[0], rv.v[1]);
-        else
-          *reinterpret_cast<float4*>(Rr + po) = make_float4(rv.v[0], rv.v[1], rv.v[2], rv.v[3]);
-      }
-      if (has_ring) {
-        const T uc = U0[rb];
-        const T r = sub(F0[rf], apply_A(c, uc, U0[rb - 1], U0[rb + 1], U0[rb - BX], U0[rb + BX], rzm, Up[rb]));
-        Rr[rpo] = pl_in && ring_in ? r : (T)0;
-        rzm = uc;
-      }
-      __syncthreads();
-      // every thread is past plane q-1's coarse sums and plane q's residuals: step q-1
-      // (u(q), f(q-1)) is consumed, and Rr of plane q-1 may be overwritten next plane
-      if (tid == 0 && q - 1 + G::NS <= qlast) {
-        fence_proxy_async();
-        R.issue(N(q - 1 + G::NS), &tm_u, &tm_f, x0, y0, q + G::NS, q - 1 + G::NS, true);
-      }
-      if (tid < CN) {  // whole warps: CN = 256 (FP64) / 512 (FP32)
-        // x-sums r(2I-1) + r(2I+1) + 2 r(2I): (r(2I), r(2I+1)) is one aligned pair load and
-        // r(2I-1) the left lane's second element (lane 0 loads it) — 5 smem wavefronts per
-        // warp and row instead of 12 for three strided scalars; same values, same order
-        using P2 = std::conditional_t<sizeof(T) == 8, double2, float2>;
-        T tx[3];
-#pragma unroll
-        for (int dy = -1; dy <= 1; dy++) {
-          const T* row = Rr + co + dy * PX;
-          const P2 pr = *reinterpret_cast<const P2*>(row);
-          T left = __shfl_up_sync(0xffffffffu, pr.y, 1);
-          if (lane == 0) left = row[-1];
-          tx[dy + 1] = add(add(left, pr.y), mul(two, pr.x));
-        }
-        const T ty0 = add(add(tx[0], tx[2]), mul(two, tx[1]));
-        if (cnode && (pgl & 1) == 1 && q >= qf0 + 1) {  // fine plane 2P+1 completes coarse plane P
-          const int Pc = ((pgl - 1) >> 1) - gc.p_glob0;
-          crow[(long long)Pc * gc.pstride] = mul(add(add(ty2, ty0), mul(two, ty1)), scale);
-        }
-        ty2 = ty1;
-        ty1 = ty0;
-      }
-      um = u0;
-      u0 = up;
-    }
-    seq = N(qlast) + 1;
-    __syncthreads();
-  }
-}
-
 // Row-blocked residual + restriction (the default): as k_resid_restrict3d, but a thread owns
 // RPT consecutive fine rows of its x-vector (the rows' u(q) y-neighbours inside the thread
 // come from registers) and CN / NTH coarse nodes.  Bitwise identical results.
@@ -1364,38 +962,33 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
   const int tiles_x = (g.nx + G::TX - 1) / G::TX, tiles_y = (g.ny + TY - 1) / TY;
   const int ntiles = tiles_x * tiles_y;
   const int np = g.p_hi - g.p_lo;
-  auto go = [&](auto kernel) {  // CORR: the one-row-per-thread kernel
-    const int smem = G::SMEM_CORR;
-    const int resident = prepare_kernel(kernel, smem);
+  auto gor = [&](auto kernel, int smem) {
+    const int resident = prepare_kernel(kernel, smem, NTR);
     const int zc = choose_zc(ntiles, np, resident, rbgs ? 4 : 2, min_zc_for(g, sizeof(T)));
     const int nitems = ntiles * ((np + zc - 1) / zc);
     if (npartial) *npartial = nitems;
-    kernel<<<nitems, NT, smem, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial, te, gce);
+    kernel<<<nitems, NTR, smem, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial, te, gce);
   };
-  auto gor = [&](auto kernel) {  // row-blocked
-    const int resident = prepare_kernel(kernel, G::SMEM, NTR);
-    const int zc = choose_zc(ntiles, np, resident, rbgs ? 4 : 2, min_zc_for(g, sizeof(T)));
-    const int nitems = ntiles * ((np + zc - 1) / zc);
-    if (npartial) *npartial = nitems;
-    kernel<<<nitems, NTR, G::SMEM, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial);
-  };
-  if (ecoarse)
-    rbgs ? go(k_sweep3d<T, 1, false, false, true>) : go(k_sweep3d<T, 0, false, false, true>);
-  else if (partial && !zero_in) {
+  if (ecoarse) {  // CORR: 3-slot u/f ring + 3 coarse boxes
+    constexpr int smem_corr = Ring<T, 3>::BAR_OFF + 128 + 3 * G::PB + 3 * G::CB;
+    static_assert(smem_corr <= G::SMEM, "CORR fits the plain sweep's shared memory");
+    rbgs ? gor(k_sweep3d_rows<T, 1, false, 0, RPT, true>, smem_corr)
+         : gor(k_sweep3d_rows<T, 0, false, 0, RPT, true>, smem_corr);
+  } else if (partial && !zero_in) {
     if (!rbgs) {
       if (nm != SN_INPUT) return cudaErrorInvalidValue;
-      gor(k_sweep3d_rows<T, 0, false, 1, RPT>);
+      gor(k_sweep3d_rows<T, 0, false, 1, RPT>, G::SMEM);
     } else if (nm == SN_INPUT) {
-      gor(k_sweep3d_rows<T, 1, false, 1, RPT>);
+      gor(k_sweep3d_rows<T, 1, false, 1, RPT>, G::SMEM);
     } else if (nm == SN_INPUT_RED) {
-      gor(k_sweep3d_rows<T, 1, false, 2, RPT>);
+      gor(k_sweep3d_rows<T, 1, false, 2, RPT>, G::SMEM);
     } else {
-      gor(k_sweep3d_rows<T, 1, false, 3, RPT>);
+      gor(k_sweep3d_rows<T, 1, false, 3, RPT>, G::SMEM);
     }
   } else if (rbgs)
-    zero_in ? gor(k_sweep3d_rows<T, 1, true, 0, RPT>) : gor(k_sweep3d_rows<T, 1, false, 0, RPT>);
+    zero_in ? gor(k_sweep3d_rows<T, 1, true, 0, RPT>, G::SMEM) : gor(k_sweep3d_rows<T, 1, false, 0, RPT>, G::SMEM);
   else
-    zero_in ? gor(k_sweep3d_rows<T, 0, true, 0, RPT>) : gor(k_sweep3d_rows<T, 0, false, 0, RPT>);
+    zero_in ? gor(k_sweep3d_rows<T, 0, true, 0, RPT>, G::SMEM) : gor(k_sweep3d_rows<T, 0, false, 0, RPT>, G::SMEM);
   return cudaGetLastError();
 }
 
@@ -1455,7 +1048,9 @@ cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f,
   const int zc = choose_zc(ntiles, np, resident, 2, min_zc_for(g, sizeof(T)));
   const int nitems = ntiles * ((np + zc - 1) / zc);
   *npartial = nitems;
-  kernel<<<nitems, NTR, G::SMEM, st>>>(tu, tf, g, c, nullptr, tiles_x, ntiles, zc, nitems, partial);
+  CUtensorMap te;
+  memset(&te, 0, sizeof te);
+  kernel<<<nitems, NTR, G::SMEM, st>>>(tu, tf, g, c, nullptr, tiles_x, ntiles, zc, nitems, partial, te, Geom{});
   return cudaGetLastError();
 }
 

@@ -5,11 +5,17 @@
 // V_lt(0, f_lt) — every operation of Alg. 1 on levels lt..L-1:
 // pre-smoothing, residual + full weighting, the coarsest solve, prolongation +
 // correction, post-smoothing — inside ONE thread-block cluster (16 CTAs x 1024
-// threads, one per SM), a cluster barrier (barrier.cluster release/acquire,
-// ~0.2 us) between passes, data in global memory (L2 resident).  The
-// per-node arithmetic is the same canonical device code as every other kernel
-// (mg_common.cuh), so results are bitwise identical to the op-by-op schedule.
-// With lt = 0 (small 2D grids such as C1) the whole cycle is one launch.
+// threads, one per SM), a cluster barrier (barrier.cluster release/acquire)
+// between passes, data in global memory (L2 resident).  Levels of at most a few
+// thousand nodes run on CTA 0 alone with block barriers ("solo"), their arrays
+// held in CTA 0's shared memory when they fit (a pass is then a few hundred
+// cycles: no L2 round trip).  With lt = 0 (small 2D grids such as C1) the whole
+// cycle is one launch on one CTA, the level-0 arrays copied in and u copied out.
+// Work of a pass is distributed by rows: a warp takes a row of the level (one
+// integer division per row, none per node) and its lanes the row's nodes (every
+// other node for a red-black colour).  The per-node arithmetic is the same
+// canonical device code as every other kernel (mg_common.cuh), so results are
+// bitwise identical to the op-by-op schedule.
 #include <cstdlib>
 
 #include "kernels.h"
@@ -21,19 +27,24 @@ namespace mg {
 namespace {
 
 constexpr int NTT = 1024;
+constexpr int WPC = NTT / 32;  // warps per CTA
 
 // all CTAs of the cluster (= the grid): release/acquire at cluster scope makes the
 // pass's global writes visible to the next pass (and invalidates L1)
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// Work distribution of a pass.  A SOLO level (a few thousand nodes) runs on CTA 0 alone with
-// block barriers — a block barrier costs a fraction of a cluster barrier and the level's work
-// is too small to pay for 16 SMs; the other CTAs skip solo passes entirely and meet CTA 0 at
-// the next cluster barrier (the transitions in k_tail).
+// Work distribution of a pass.  A SOLO level runs on CTA 0 alone with block barriers — a block
+// barrier costs a fraction of a cluster barrier and the level's work is too small to pay for 16
+// SMs; the other CTAs skip solo passes entirely and meet CTA 0 at the next cluster barrier (the
+// transitions in k_tail).
 struct Mode {
   bool solo;
   __device__ bool active() const { return !solo || blockIdx.x == 0; }
+  __device__ int wstart() const {
+    return solo ? (int)(threadIdx.x >> 5) : (int)(blockIdx.x * WPC + (threadIdx.x >> 5));
+  }
+  __device__ int wstride() const { return solo ? WPC : (int)(gridDim.x * WPC); }
   __device__ int start() const { return solo ? (int)threadIdx.x : (int)(blockIdx.x * NTT + threadIdx.x); }
   __device__ int stride() const { return solo ? NTT : (int)(gridDim.x * NTT); }
   __device__ void sync() const {
@@ -44,53 +55,86 @@ struct Mode {
   }
 };
 
-struct Idx {
-  int i, j, pl;
+// A level's geometry in registers (32-bit strides: tail levels are small).  Every pass copies
+// it out of the kernel parameters once, so the node loops index with plain integer adds.
+struct LG {
+  int nx, ny, p_lo, p_hi, pg0, sy, sz, planes, rows;
+  int shA, shC;  // log2 of the lane group of for_rows: all nodes / one colour of a row
+  float inv_nr;  // 1 / rows per plane
 };
+__device__ __forceinline__ int ceil_log2_32(int v) { return v >= 32 ? 5 : (v <= 1 ? 0 : 32 - __clz(v - 1)); }
+__device__ __forceinline__ LG lg_of(const Geom& g) {
+  const int ni = g.nx - 1, nr = g.three_d ? g.ny - 1 : 1;
+  return LG{g.nx, g.ny, g.p_lo, g.p_hi, g.p_glob0, (int)g.pitch, (int)g.pstride, g.planes, g.rows,
+            ceil_log2_32(ni), ceil_log2_32((ni + 1) >> 1), __frcp_rn((float)nr)};
+}
+__device__ __forceinline__ int lin(const LG& g, int i, int j, int pl) { return pl * g.sz + j * g.sy + i; }
 
-// interior node number q -> (i, j, plane)
-__device__ __forceinline__ Idx interior_node(const Geom& g, int q) {
+// f - A u at p, canonical order (mg_common.cuh point_residual), DIM known at compile time
+template <typename T, int DIM>
+__device__ __forceinline__ T pres(const T* u, int p, const LG& g, const Coef<T>& c, T fp) {
+  T s = mul(c.cx, add(u[p - 1], u[p + 1]));
+  if (DIM == 3) s = add(s, mul(c.cy, add(u[p - g.sy], u[p + g.sy])));
+  s = add(s, mul(c.cz, add(u[p - g.sz], u[p + g.sz])));
+  return sub(fp, sub(mul(c.D, u[p]), s));
+}
+
+// f(i, j, plane, linear index) for the interior nodes of g; par >= 0: only the nodes with
+// (i + j + global plane) & 1 == par (a red-black colour).  A warp takes 32/G rows at a time, a
+// group of G lanes (G = the power of two >= the nodes to visit per row, at most 32) one row,
+// so short rows of small levels do not idle most of the lanes.  Row -> (plane, y) by one
+// float multiply: exact for the tail's levels (rows < 2^13, quotient error << 1/(2 nr)).
+template <int DIM, class F>
+__device__ __forceinline__ void for_rows(const Mode& M, const LG& g, int par, F&& f) {
+  if (!M.active()) return;
+  const int lane = threadIdx.x & 31;
   const int ni = g.nx - 1;
-  const int nr = g.three_d ? g.ny - 1 : 1;
-  Idx d;
-  d.i = 1 + q % ni;
-  const int t = q / ni;
-  d.j = g.three_d ? 1 + t % nr : 0;
-  d.pl = g.p_lo + t / nr;
-  return d;
-}
-__device__ __forceinline__ int interior_count(const Geom& g) {
-  return (g.nx - 1) * (g.three_d ? g.ny - 1 : 1) * (g.p_hi - g.p_lo);
-}
-__device__ __forceinline__ long long lin(const Geom& g, int i, int j, int pl) {
-  return (long long)pl * g.pstride + (long long)j * g.pitch + i;
+  const int nr = DIM == 3 ? g.ny - 1 : 1;
+  const int nrows = nr * (g.p_hi - g.p_lo);
+  const int sh = par < 0 ? g.shA : g.shC;
+  const int G = 1 << sh, rpw = 32 >> sh;
+  const int sub_ = lane & (G - 1);
+  const float inv_nr = g.inv_nr;
+  for (int rb = M.wstart() * rpw; rb < nrows; rb += M.wstride() * rpw) {
+    const int row = rb + (lane >> sh);
+    if (row >= nrows) continue;
+    const int dp = DIM == 3 ? __float2int_rz(((float)row + 0.5f) * inv_nr) : row;
+    const int pl = g.p_lo + dp;
+    const int j = DIM == 3 ? 1 + row - dp * nr : 0;
+    const int base = pl * g.sz + j * g.sy;
+    if (par < 0) {
+      for (int i = 1 + sub_; i <= ni; i += G) f(i, j, pl, base + i);
+    } else {
+      const int i0 = 1 + ((1 + j + pl + g.pg0 + par) & 1);  // first i of the colour
+      for (int i = i0 + 2 * sub_; i <= ni; i += 2 * G) f(i, j, pl, base + i);
+    }
+  }
 }
 
 template <typename T>
-__device__ void zero_level(const Mode& M, const Geom& g, T* u) {
+__device__ void zero_level(const Mode& M, const LG& g, T* u) {
   if (!M.active()) return;
-  const long long n = (long long)g.planes * g.pstride;
-  for (long long q = M.start(); q < n; q += M.stride()) u[q] = (T)0;
+  const int n = g.planes * g.sz;
+  for (int q = M.start(); q < n; q += M.stride()) u[q] = (T)0;
 }
 
 // one sweep of the smoother; Jacobi ping-pongs (returns the new current buffer)
-template <typename T>
-__device__ T* sweep(const Mode& M, const Geom& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f) {
+template <typename T, int DIM>
+__device__ T* sweep(const Mode& M, const LG& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f) {
   const bool act = M.active();
-  const int n = interior_count(g);
   if (rbgs == 2) {  // lexicographic omega-GS: hyperplanes i + j + global plane = s in order
-    const int nj = g.three_d ? g.ny - 1 : 1;
+    const int nj = DIM == 3 ? g.ny - 1 : 1;
     const int m = nj * (g.p_hi - g.p_lo);
-    const int smin = 1 + (g.three_d ? 1 : 0) + g.p_lo + g.p_glob0;
-    const int smax = (g.nx - 1) + (g.three_d ? g.ny - 1 : 0) + g.p_hi - 1 + g.p_glob0;
+    const int smin = 1 + (DIM == 3 ? 1 : 0) + g.p_lo + g.pg0;
+    const int smax = (g.nx - 1) + (DIM == 3 ? g.ny - 1 : 0) + g.p_hi - 1 + g.pg0;
     for (int s = smin; s <= smax; s++) {
       for (int q = act ? M.start() : m; q < m; q += M.stride()) {
-        const int j = g.three_d ? 1 + q % nj : 0;
+        const int j = DIM == 3 ? 1 + q % nj : 0;
         const int pl = g.p_lo + q / nj;
-        const int i = s - j - (pl + g.p_glob0);
+        const int i = s - j - (pl + g.pg0);
         if (i < 1 || i > g.nx - 1) continue;
-        const long long p = lin(g, i, j, pl);
-        u[p] = add(u[p], mul(c.wd, point_residual(u, p, g, c, f[p])));
+        const int p = lin(g, i, j, pl);
+        u[p] = add(u[p], mul(c.wd, pres<T, DIM>(u, p, g, c, f[p])));
       }
       M.sync();
     }
@@ -98,65 +142,50 @@ __device__ T* sweep(const Mode& M, const Geom& g, const Coef<T>& c, int rbgs, T*
   }
   if (rbgs) {
     for (int colour = 0; colour < 2; colour++) {
-      for (int q = act ? M.start() : n; q < n; q += M.stride()) {
-        const Idx d = interior_node(g, q);
-        if (((d.i + d.j + d.pl + g.p_glob0) & 1) != colour) continue;
-        const long long p = lin(g, d.i, d.j, d.pl);
-        u[p] = add(u[p], mul(c.wd, point_residual(u, p, g, c, f[p])));
-      }
+      for_rows<DIM>(M, g, colour,
+                    [&](int, int, int, int p) { u[p] = add(u[p], mul(c.wd, pres<T, DIM>(u, p, g, c, f[p]))); });
       M.sync();
     }
     return u;
   }
-  for (int q = act ? M.start() : n; q < n; q += M.stride()) {
-    const Idx d = interior_node(g, q);
-    const long long p = lin(g, d.i, d.j, d.pl);
-    t[p] = add(u[p], mul(c.wd, point_residual(u, p, g, c, f[p])));
-  }
+  for_rows<DIM>(M, g, -1, [&](int, int, int, int p) { t[p] = add(u[p], mul(c.wd, pres<T, DIM>(u, p, g, c, f[p]))); });
   M.sync();
   return t;
 }
 
-template <typename T>
-__device__ void residual(const Mode& M, const Geom& g, const Coef<T>& c, const T* u, const T* f, T* r) {
-  const bool act = M.active();
-  const int n = interior_count(g);
-  for (int q = act ? M.start() : n; q < n; q += M.stride()) {
-    const Idx d = interior_node(g, q);
-    const long long p = lin(g, d.i, d.j, d.pl);
-    r[p] = point_residual(u, p, g, c, f[p]);
-  }
+template <typename T, int DIM>
+__device__ void residual(const Mode& M, const LG& g, const Coef<T>& c, const T* u, const T* f, T* r) {
+  for_rows<DIM>(M, g, -1, [&](int, int, int, int p) { r[p] = pres<T, DIM>(u, p, g, c, f[p]); });
   M.sync();
 }
 
 // full weighting, separable x -> y -> plane axis (reading 13)
-template <typename T>
-__device__ void restrict_fw(const Mode& M, const Geom& gf, const Geom& gc, const T* r, T* fc) {
-  const bool act = M.active();
-  const int n = interior_count(gc);
+template <typename T, int DIM>
+__device__ void restrict_fw(const Mode& M, const LG& gf, const LG& gc, const T* r, T* fc) {
   const T two = (T)2;
-  const T scale = gc.three_d ? (T)(1.0 / 64.0) : (T)(1.0 / 16.0);
-  for (int q = act ? M.start() : n; q < n; q += M.stride()) {
-    const Idx d = interior_node(gc, q);
-    const int pf = 2 * (d.pl + gc.p_glob0) - gf.p_glob0;
+  const T scale = DIM == 3 ? (T)(1.0 / 64.0) : (T)(1.0 / 16.0);
+  for_rows<DIM>(M, gc, -1, [&](int I, int J, int PL, int pc) {
+    const int pf = 2 * (PL + gc.pg0) - gf.pg0;
     T tz[3];
+#pragma unroll
     for (int dz = -1; dz <= 1; dz++) {
       T ty;
-      if (gc.three_d) {
+      if (DIM == 3) {
         T tx[3];
+#pragma unroll
         for (int dy = -1; dy <= 1; dy++) {
-          const long long p = lin(gf, 2 * d.i, 2 * d.j + dy, pf + dz);
+          const int p = lin(gf, 2 * I, 2 * J + dy, pf + dz);
           tx[dy + 1] = add(add(r[p - 1], r[p + 1]), mul(two, r[p]));
         }
         ty = add(add(tx[0], tx[2]), mul(two, tx[1]));
       } else {
-        const long long p = lin(gf, 2 * d.i, 0, pf + dz);
+        const int p = lin(gf, 2 * I, 0, pf + dz);
         ty = add(add(r[p - 1], r[p + 1]), mul(two, r[p]));
       }
       tz[dz + 1] = ty;
     }
-    fc[lin(gc, d.i, d.j, d.pl)] = mul(add(add(tz[0], tz[2]), mul(two, tz[1])), scale);
-  }
+    fc[pc] = mul(add(add(tz[0], tz[2]), mul(two, tz[1])), scale);
+  });
   M.sync();
 }
 
@@ -164,72 +193,110 @@ __device__ void restrict_fw(const Mode& M, const Geom& gf, const Geom& gc, const
 // t = 0 + wd (f - A 0) = 0 + wd f; RBGS's red pass writes 0 + wd f at red nodes and 0 at black
 // nodes (the black pass then runs as usual).  With A 0 = D*0 - 0 = +0 and f - (+0) = f the
 // values are bitwise those of a sweep over a zeroed array.
-template <typename T>
-__device__ T* sweep_from_zero(const Mode& M, const Geom& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f) {
-  const bool act = M.active();
-  const int n = interior_count(g);
+template <typename T, int DIM>
+__device__ T* sweep_from_zero(const Mode& M, const LG& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f) {
   const T zero = (T)0;
   if (!rbgs) {
-    for (int q = act ? M.start() : n; q < n; q += M.stride()) {
-      const Idx d = interior_node(g, q);
-      const long long p = lin(g, d.i, d.j, d.pl);
-      t[p] = add(zero, mul(c.wd, sub(f[p], zero)));
-    }
+    for_rows<DIM>(M, g, -1, [&](int, int, int, int p) { t[p] = add(zero, mul(c.wd, sub(f[p], zero))); });
     M.sync();
     return t;
   }
-  for (int q = act ? M.start() : n; q < n; q += M.stride()) {  // red pass (colour 0) + zero black nodes
-    const Idx d = interior_node(g, q);
-    const long long p = lin(g, d.i, d.j, d.pl);
-    u[p] = ((d.i + d.j + d.pl + g.p_glob0) & 1) == 0 ? add(zero, mul(c.wd, sub(f[p], zero))) : zero;
-  }
+  for_rows<DIM>(M, g, 0, [&](int, int, int, int p) { u[p] = add(zero, mul(c.wd, sub(f[p], zero))); });  // red
+  for_rows<DIM>(M, g, 1, [&](int, int, int, int p) { u[p] = zero; });                                 // black: 0
   M.sync();
-  for (int q = act ? M.start() : n; q < n; q += M.stride()) {  // black pass
-    const Idx d = interior_node(g, q);
-    if (((d.i + d.j + d.pl + g.p_glob0) & 1) != 1) continue;
-    const long long p = lin(g, d.i, d.j, d.pl);
-    u[p] = add(u[p], mul(c.wd, point_residual(u, p, g, c, f[p])));
-  }
+  for_rows<DIM>(M, g, 1, [&](int, int, int, int p) {  // black pass
+    u[p] = add(u[p], mul(c.wd, pres<T, DIM>(u, p, g, c, f[p])));
+  });
   M.sync();
   return u;
 }
 
 // u += P e, separable x -> y -> plane axis
-template <typename T>
-__device__ void prolong(const Mode& M, const Geom& gf, const Geom& gc, const T* e, T* u) {
-  const bool act = M.active();
-  const int n = interior_count(gf);
+template <typename T, int DIM>
+__device__ void prolong(const Mode& M, const LG& gf, const LG& gc, const T* e, T* u) {
   const T half = (T)0.5;
-  for (int q = act ? M.start() : n; q < n; q += M.stride()) {
-    const Idx d = interior_node(gf, q);
-    const int pg = d.pl + gf.p_glob0;
-    const int I = d.i >> 1, dx = d.i & 1;
-    const int J = d.j >> 1, dy = gf.three_d ? (d.j & 1) : 0;
-    const int P = (pg >> 1) - gc.p_glob0, dz = pg & 1;
+  for_rows<DIM>(M, gf, -1, [&](int i, int j, int pl, int pu) {
+    const int pg = pl + gf.pg0;
+    const int I = i >> 1, dx = i & 1;
+    const int J = j >> 1, dy = DIM == 3 ? (j & 1) : 0;
+    const int P = (pg >> 1) - gc.pg0, dz = pg & 1;
     T vy[2];
     for (int zz = 0; zz <= dz; zz++) {
       T vx[2];
       for (int yy = 0; yy <= dy; yy++) {
-        const long long p = lin(gc, I, J + yy, P + zz);
+        const int p = lin(gc, I, J + yy, P + zz);
         vx[yy] = dx ? mul(half, add(e[p], e[p + 1])) : e[p];
       }
       vy[zz] = dy ? mul(half, add(vx[0], vx[1])) : vx[0];
     }
     const T v = dz ? mul(half, add(vy[0], vy[1])) : vy[0];
-    const long long p = lin(gf, d.i, d.j, d.pl);
-    u[p] = add(u[p], v);
-  }
+    u[pu] = add(u[pu], v);
+  });
   M.sync();
 }
 
+// copy every node (x <= nx, all rows and planes) of a level's array between two layouts
 template <typename T>
+__device__ void copy_all(const Mode& M, const LG& gs, const T* src, const LG& gd, T* dst) {
+  if (!M.active()) return;
+  const int nx1 = gs.nx + 1;
+  const int nrows = gs.rows * gs.planes;
+  for (int row = M.wstart(); row < nrows; row += M.wstride()) {
+    const int pl = row / gs.rows, j = row - pl * gs.rows;
+    const T* a = src + pl * gs.sz + j * gs.sy;
+    T* b = dst + pl * gd.sz + j * gd.sy;
+    for (int i = threadIdx.x & 31; i < nx1; i += 32) b[i] = a[i];
+  }
+}
+// interior nodes only
+template <typename T, int DIM>
+__device__ void copy_interior(const Mode& M, const LG& gs, const T* src, const LG& gd, T* dst) {
+  for_rows<DIM>(M, gs, -1, [&](int i, int j, int pl, int p) { dst[lin(gd, i, j, pl)] = src[p]; });
+}
+
+template <typename T, int DIM>
 __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
+  extern __shared__ __align__(16) unsigned char tsm[];
   auto mode = [&](int k) { return Mode{k >= P.solo_from}; };
+  const bool sm_lv0 = P.smem_from == 0;  // the top tail level lives in shared memory (one CTA)
+  // ---- level arrays: levels >= smem_from in CTA 0's shared memory (compact layout P.gs[k]),
+  // four arrays u, t, f, r each; the others in global memory
+  auto G = [&](int k) { return lg_of(k >= P.smem_from ? P.gs[k] : P.g[k]); };
+  auto sarr = [&](int k, int a) -> T* {
+    const int n = P.gs[k].planes * (int)P.gs[k].pstride;
+    const int n16 = (n * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);
+    return reinterpret_cast<T*>(tsm + P.soff[k]) + a * n16;
+  };
+  auto U = [&](int k) { return k >= P.smem_from ? sarr(k, 0) : P.u[k]; };
+  auto Tt = [&](int k) { return k >= P.smem_from ? sarr(k, 1) : P.t[k]; };
+  auto F = [&](int k) { return k >= P.smem_from ? sarr(k, 2) : P.f[k]; };
+  auto R = [&](int k) { return k >= P.smem_from ? sarr(k, 3) : P.r[k]; };
+  if (P.smem_from < P.nl && blockIdx.x == 0) {
+    // zero the shared-memory levels (boundaries, residual borders, coarse guesses), then the
+    // top level's inputs when it lives there: u (also into t: the Jacobi partner's Dirichlet
+    // boundary) and f
+    const unsigned char* end = tsm + P.smem_bytes;
+    for (uint4* q = reinterpret_cast<uint4*>(tsm + P.soff[P.smem_from]) + threadIdx.x;
+         reinterpret_cast<const unsigned char*>(q) < end; q += NTT)
+      *q = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    if (sm_lv0) {
+      const Mode M0{true};
+      const LG g0 = lg_of(P.g[0]), s0 = G(0);
+      if (!P.zero_first) {
+        copy_all(M0, g0, (const T*)P.u[0], s0, U(0));
+        copy_all(M0, g0, (const T*)P.u[0], s0, Tt(0));
+      }
+      copy_all(M0, g0, (const T*)P.f[0], s0, F(0));
+      __syncthreads();
+    }
+  }
   // ---- descend
   T* cur[kTailMax];
-  for (int k = 0; k < P.nl; k++) cur[k] = P.u[k];
+  for (int k = 0; k < P.nl; k++) cur[k] = U(k);
   for (int k = 0; k < P.nl - 1; k++) {
-    const Geom& g = P.g[k];
+    const LG g = G(k);
+    const Coef<T> c = P.c[k];
     const Mode M = mode(k);
     const bool zero = k > 0 || P.zero_first;  // V_H(0, ...)
     const bool fold = zero && P.nu1 > 0 && P.rbgs != 2;  // the zero guess folded into the first sweep
@@ -238,21 +305,22 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
       M.sync();
     }
     for (int s = 0; s < P.nu1; s++) {
-      T* oth = cur[k] == P.u[k] ? P.t[k] : P.u[k];
-      cur[k] = (s == 0 && fold) ? sweep_from_zero(M, g, P.c[k], P.rbgs, cur[k], oth, P.f[k])
-                                : sweep(M, g, P.c[k], P.rbgs, cur[k], oth, P.f[k]);
+      T* oth = cur[k] == U(k) ? Tt(k) : U(k);
+      cur[k] = (s == 0 && fold) ? sweep_from_zero<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k))
+                                : sweep<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k));
     }
     // separate residual and restriction passes: measured faster than one fused pass whose
     // coarse threads each evaluate 3^d fine residuals (latency-bound serial chains)
-    residual(M, g, P.c[k], cur[k], P.f[k], P.r[k]);
+    residual<T, DIM>(M, g, c, cur[k], F(k), R(k));
     // the restriction writes level k+1: its mode (a solo coarse level is restricted by CTA 0,
     // reading the residual the cluster barrier above made visible)
-    restrict_fw(mode(k + 1), g, P.g[k + 1], P.r[k], P.f[k + 1]);
+    restrict_fw<T, DIM>(mode(k + 1), g, G(k + 1), R(k), F(k + 1));
   }
   // ---- coarsest level (Alg. 1 line 2)
   {
     const int k = P.nl - 1;
-    const Geom& g = P.g[k];
+    const LG g = G(k);
+    const Coef<T> c = P.c[k];
     const Mode M = mode(k);
     const bool zero = P.nl > 1 || P.zero_first;
     // DIRECT writes every interior node, so its zero guess needs no pass; SWEEPS folds it
@@ -264,25 +332,26 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
     }
     if (P.sweeps) {
       for (int s = 0; s < P.ncoarse; s++) {
-        T* oth = cur[k] == P.u[k] ? P.t[k] : P.u[k];
-        cur[k] = (s == 0 && fold) ? sweep_from_zero(M, g, P.c[k], P.rbgs, cur[k], oth, P.f[k])
-                                  : sweep(M, g, P.c[k], P.rbgs, cur[k], oth, P.f[k]);
+        T* oth = cur[k] == U(k) ? Tt(k) : U(k);
+        cur[k] = (s == 0 && fold) ? sweep_from_zero<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k))
+                                  : sweep<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k));
       }
     } else {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         // same loop order as k_coarse_direct / the oracle
-        const int jlo = g.three_d ? 1 : 0, jhi = g.three_d ? g.ny - 1 : 0;
+        const int jlo = DIM == 3 ? 1 : 0, jhi = DIM == 3 ? g.ny - 1 : 0;
         const int m = P.m;
         const double* L = P.chol;
+        const T* fk = F(k);
         if (m == 1) {
-          const long long p = lin(g, 1, jlo, g.p_lo);
-          cur[k][p] = (T)__ddiv_rn((double)P.f[k][p], P.D_coarse);
+          const int p = lin(g, 1, jlo, g.p_lo);
+          cur[k][p] = (T)__ddiv_rn((double)fk[p], P.D_coarse);
         } else {
           double* y = P.work;
           int q = 0;
           for (int pl = g.p_lo; pl < g.p_hi; pl++)
             for (int j = jlo; j <= jhi; j++)
-              for (int i = 1; i < g.nx; i++) y[q++] = (double)P.f[k][lin(g, i, j, pl)];
+              for (int i = 1; i < g.nx; i++) y[q++] = (double)fk[lin(g, i, j, pl)];
           for (int i = 0; i < m; i++) {
             double sacc = y[i];
             for (int kk = 0; kk < i; kk++) sacc = __dsub_rn(sacc, __dmul_rn(L[(long long)i * m + kk], y[kk]));
@@ -304,25 +373,29 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   }
   // ---- ascend
   for (int k = P.nl - 2; k >= 0; k--) {
-    const Geom& g = P.g[k];
     const Mode M = mode(k);
-    if (mode(k + 1).solo && !M.solo) cluster_sync();  // CTA 0's solo levels visible to every CTA
-    prolong(M, g, P.g[k + 1], cur[k + 1], cur[k]);
+    const LG g = G(k);
+    const Coef<T> c = P.c[k];
+    const T* e = cur[k + 1];
+    LG ge = G(k + 1);
+    if (mode(k + 1).solo && !M.solo) {  // CTA 0's solo levels visible to every CTA
+      if (k + 1 >= P.smem_from) {  // the correction lives in CTA 0's shared memory: publish it
+        const LG gg = lg_of(P.g[k + 1]);
+        if (blockIdx.x == 0) {
+          copy_interior<T, DIM>(Mode{true}, ge, e, gg, P.u[k + 1]);
+          __syncthreads();
+        }
+        e = P.u[k + 1];
+        ge = gg;
+      }
+      cluster_sync();
+    }
+    prolong<T, DIM>(M, g, ge, e, cur[k]);
     for (int s = 0; s < P.nu2; s++)
-      cur[k] = sweep(M, g, P.c[k], P.rbgs, cur[k], cur[k] == P.u[k] ? P.t[k] : P.u[k], P.f[k]);
+      cur[k] = sweep<T, DIM>(M, g, c, P.rbgs, cur[k], cur[k] == U(k) ? Tt(k) : U(k), F(k));
   }
   // result of the top tail level in u[0]
-  if (cur[0] != P.u[0]) {
-    const Mode M = mode(0);
-    const bool act = M.active();
-    const Geom& g = P.g[0];
-    const int n = interior_count(g);
-    for (int q = act ? M.start() : n; q < n; q += M.stride()) {
-      const Idx d = interior_node(g, q);
-      const long long p = lin(g, d.i, d.j, d.pl);
-      P.u[0][p] = cur[0][p];
-    }
-  }
+  if (sm_lv0 || cur[0] != P.u[0]) copy_interior<T, DIM>(mode(0), G(0), (const T*)cur[0], lg_of(P.g[0]), P.u[0]);
 }
 
 }  // namespace
@@ -330,13 +403,17 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
 template <typename T>
 cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
   // 16 CTAs (non-portable) where allowed, else the portable 8; probed once per device (the
-  // non-portable opt-in is a per-device function attribute)
-  const int cluster = per_device_once((const void*)k_tail<T>, [] {
+  // non-portable opt-in and the shared-memory opt-in are per-device function attributes)
+  const int cluster = per_device_once((const void*)k_tail<T, 3>, [] {
+    cudaFuncSetAttribute(k_tail<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax);
+    cudaFuncSetAttribute(k_tail<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax);
     int c = 8;
-    if (cudaFuncSetAttribute(k_tail<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    if (cudaFuncSetAttribute(k_tail<T, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+        cudaFuncSetAttribute(k_tail<T, 3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3(16);
       q.blockDim = dim3(NTT);
+      q.dynamicSmemBytes = kTailSmemMax;
       cudaLaunchAttribute a;
       a.id = cudaLaunchAttributeClusterDimension;
       a.val.clusterDim.x = 16;
@@ -345,31 +422,52 @@ cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
       q.attrs = &a;
       q.numAttrs = 1;
       int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, k_tail<T>, &q) == cudaSuccess && n >= 1) c = 16;
+      if (cudaOccupancyMaxActiveClusters(&n, k_tail<T, 3>, &q) == cudaSuccess && n >= 1) c = 16;
     }
     cudaGetLastError();
     return c;
   });
-  // tiny tails (a few thousand nodes, e.g. the whole 65^2 C1 hierarchy) run faster on one CTA
-  const Geom& g0 = p.g[0];
-  const long long top = (long long)(g0.nx - 1) * (g0.three_d ? g0.ny - 1 : 1) * (g0.p_hi - g0.p_lo);
-  const int csize = top <= 8192 ? 1 : cluster;
+  auto interior = [](const Geom& g) {
+    return (long long)(g.nx - 1) * (g.three_d ? g.ny - 1 : 1) * (g.p_hi - g.p_lo);
+  };
+  // tiny tails (a few thousand nodes, e.g. the whole 65^2 C1 hierarchy) run on one CTA
+  const int csize = interior(p.g[0]) <= 8192 ? 1 : cluster;
   // levels from solo_from on run on CTA 0 alone with block barriers (all of them on one CTA)
-  constexpr long long solo_max = 2048;  // measured: threshold scan 512-8192
+  // measured (C2, C3, C4): 2048 interior nodes in 3D (a 17^3 level is faster on the cluster),
+  // 8192 in 2D (a 65^2 level is faster on CTA 0 with its arrays in shared memory)
+  const long long solo_max = p.g[0].three_d ? 2048 : 8192;
   TailParams<T> q = p;
   q.solo_from = p.nl;
-  for (int k = 0; k < p.nl; k++) {
-    const Geom& g = p.g[k];
-    const long long n = (long long)(g.nx - 1) * (g.three_d ? g.ny - 1 : 1) * (g.p_hi - g.p_lo);
-    if (csize == 1 || n <= solo_max) {
+  for (int k = 0; k < p.nl; k++)
+    if (csize == 1 || interior(p.g[k]) <= solo_max) {
       q.solo_from = k;
       break;
     }
+  // the solo levels' arrays (u, t, f, r) in CTA 0's shared memory, compact layout: the coarsest
+  // levels that fit (a solo level above them stays in global memory)
+  auto words = [](const Geom& g) { return ((long long)g.planes * g.pstride * (long long)sizeof(T) + 15) / 16 * 16; };
+  q.smem_from = p.nl;
+  long long total = 0;
+  for (int k = p.nl - 1; k >= q.solo_from; k--) {
+    Geom g = p.g[k];
+    g.pitch = g.nx + 1;
+    g.pstride = g.three_d ? (long long)(g.ny + 1) * (g.nx + 1) : g.pitch;
+    if (total + 4 * words(g) > kTailSmemMax) break;
+    total += 4 * words(g);
+    q.gs[k] = g;
+    q.smem_from = k;
   }
+  long long off = 0;
+  for (int k = q.smem_from; k < p.nl; k++) {
+    q.soff[k] = (int)off;
+    off += 4 * words(q.gs[k]);
+  }
+  q.smem_bytes = (int)off;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(csize);
   cfg.blockDim = dim3(NTT);
   cfg.stream = st;
+  cfg.dynamicSmemBytes = q.smem_bytes;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
   attr.val.clusterDim.x = csize;
@@ -377,7 +475,7 @@ cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = csize > 1 ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, k_tail<T>, q);
+  return p.g[0].three_d ? cudaLaunchKernelEx(&cfg, k_tail<T, 3>, q) : cudaLaunchKernelEx(&cfg, k_tail<T, 2>, q);
 }
 
 template cudaError_t launch_tail<double>(const TailParams<double>&, cudaStream_t);

@@ -5,6 +5,7 @@
 namespace mg {
 
 constexpr int kTailMax = 12;  // levels handled by one tail launch
+constexpr int kTailSmemMax = 200 * 1024;  // CTA 0's shared memory for the solo levels' arrays
 
 template <typename T>
 struct TailParams {
@@ -15,6 +16,10 @@ struct TailParams {
   int ncoarse;
   int zero_first;  // the top tail level starts from a zero guess (always, unless it is level 0)
   int solo_from;   // levels >= solo_from run on CTA 0 alone (set by launch_tail)
+  int smem_from;   // levels >= smem_from (all solo) keep u, t, f, r in CTA 0's shared memory (launch_tail)
+  int smem_bytes;  // their dynamic shared memory
+  int soff[kTailMax];   // byte offset of level k's four arrays
+  Geom gs[kTailMax];    // level k's compact shared-memory layout (pitch nx+1, no padding)
   int m;           // coarsest unknowns (direct)
   double D_coarse;
   const double* chol;

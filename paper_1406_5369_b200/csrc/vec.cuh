@@ -45,6 +45,15 @@ __device__ __forceinline__ Vec<T, 16 / sizeof(T)> ld_vec_nc(const T* p) {
   return r;
 }
 
+// store the whole vector at p (16-byte aligned)
+template <typename T>
+__device__ __forceinline__ void st_vec(T* p, const Vec<T, 16 / sizeof(T)>& o) {
+  if constexpr (sizeof(T) == 8)
+    *reinterpret_cast<double2*>(p) = make_double2(o.v[0], o.v[1]);
+  else
+    *reinterpret_cast<float4*>(p) = make_float4(o.v[0], o.v[1], o.v[2], o.v[3]);
+}
+
 // store the vector at dst[x..x+W), element k only if ok[k]
 template <typename T>
 __device__ __forceinline__ void store_vec(T* dst, int x, const bool* ok, const Vec<T, 16 / sizeof(T)>& o) {
