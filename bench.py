@@ -423,7 +423,7 @@ def run_mg(args):
         dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[args.config]
     esz = 8 if dt == "f64" else 4
     kw = dict(levels=levels, smoother=sm, omega=omega, nu1=nu1, nu2=nu2, dtype=dt, device=dev,
-              flags=(mgb.FLAG_HOST_LOOP if args.host_loop else 0) | (mgb.FLAG_FUSE_PROLONG if args.fuse_prolong else 0)
+              flags=(mgb.FLAG_HOST_LOOP if args.host_loop else 0) | (mgb.FLAG_SEPARATE_PROLONG if args.separate_prolong else 0)
               | (mgb.FLAG_NO_KFUSE if args.no_kfuse else 0))
     if cd:
         kw.update(problem="complex_diffusion", coarse="sweeps")
@@ -622,7 +622,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--host-loop", action="store_true", help="mg_solve with MG_FLAG_HOST_LOOP (per-cycle sync)")
-    ap.add_argument("--fuse-prolong", action="store_true", help="MG_FLAG_FUSE_PROLONG (prolongation in the first post-sweep)")
+    ap.add_argument("--separate-prolong", action="store_true",
+                    help="MG_FLAG_SEPARATE_PROLONG (prolongation as its own pass, not in the first post-sweep)")
     ap.add_argument("--decomp", default="slab", choices=["slab", "replicas"],
                     help="N>1: z-slab decomposition of one grid (default) or independent replicas")
     ap.add_argument("--no-c5", action="store_true", help="N=1 C3-f64: skip the single-GPU C5 point")

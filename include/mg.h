@@ -75,8 +75,9 @@ typedef enum { MG_PROBLEM_POISSON = 0, MG_PROBLEM_COMPLEX_DIFFUSION = 1 } mg_pro
 #define MG_FLAG_NO_GRAPH 1u   /* launch eagerly instead of replaying a CUDA graph   */
 #define MG_FLAG_BASELINE 2u   /* op-by-op kernels only (no fusion; two-pass RBGS)   */
 #define MG_FLAG_SLAB 4u       /* slab layout (halos, agglomeration) even with nranks == 1 */
-#define MG_FLAG_FUSE_PROLONG 8u /* fuse prolongation+correction into the first post-sweep (u+Pe formed
-                                   in smem); off by default: the sweep is issue-bound, the gain is small */
+#define MG_FLAG_SEPARATE_PROLONG 8u /* 3D marching levels: prolongation + correction as its own pass; by
+                                       default it is fused into the first post-sweep (u + P e formed in
+                                       shared memory, never stored); A/B switch, bitwise equal */
 #define MG_FLAG_HOST_LOOP 16u   /* mg_solve: host-driven loop (one synchronisation per cycle) instead of
                                    the on-device loop (one CUDA graph with a conditional WHILE node) */
 #define MG_FLAG_NO_KFUSE 32u   /* 2D omega-Jacobi: one sweep per HBM pass instead of the temporally blocked

@@ -25,7 +25,7 @@ LIB_PATH = os.environ.get("MG_LIBRARY") or os.path.join(_HERE, "libmgb200.so")
 JACOBI, RBGS, GS_LEX = 0, 1, 2
 FP64, FP32 = 0, 1
 COARSE_DIRECT, COARSE_SWEEPS = 0, 1
-FLAG_NO_GRAPH, FLAG_BASELINE, FLAG_SLAB, FLAG_FUSE_PROLONG, FLAG_HOST_LOOP = 1, 2, 4, 8, 16
+FLAG_NO_GRAPH, FLAG_BASELINE, FLAG_SLAB, FLAG_SEPARATE_PROLONG, FLAG_HOST_LOOP = 1, 2, 4, 8, 16
 FLAG_NO_KFUSE, FLAG_CD_KFUSE = 32, 64
 PROBLEM_POISSON, PROBLEM_COMPLEX_DIFFUSION = 0, 1
 

@@ -83,8 +83,8 @@ static mg_status validate_cd(const mg_config* c, int* levels_out) {
     return fail(s, MG_ERR_INVALID, "complex diffusion needs coarse = MG_COARSE_SWEEPS, ncoarse >= 1 (FAS, S:437)");
   if (c->dtype != MG_FP64 && c->dtype != MG_FP32) return fail(s, MG_ERR_INVALID, "bad dtype");
   if (c->nranks != 1) return fail(s, MG_ERR_INVALID, "complex diffusion runs on one rank (nranks = 1)");
-  if (c->flags & (MG_FLAG_SLAB | MG_FLAG_FUSE_PROLONG))
-    return fail(s, MG_ERR_INVALID, "MG_FLAG_SLAB / MG_FLAG_FUSE_PROLONG do not apply to complex diffusion");
+  if (c->flags & (MG_FLAG_SLAB | MG_FLAG_SEPARATE_PROLONG))
+    return fail(s, MG_ERR_INVALID, "MG_FLAG_SLAB / MG_FLAG_SEPARATE_PROLONG do not apply to complex diffusion");
   if (!(c->tau > 0.0) || !(c->theta > 0.0 && c->theta < M_PI / 2) || !(c->kappa > 0.0))
     return fail(s, MG_ERR_INVALID, "need tau > 0, theta in (0, pi/2), kappa > 0 (S:303)");
   int64_t mincells = INT64_MAX;

@@ -87,7 +87,6 @@ struct Geo {
   static constexpr int CB = rup(CBX * CBY * (int)sizeof(T), 128);
   static constexpr int NRED = W / 2;  // red (and black) nodes per thread and plane
   static constexpr int RCOL = TY / 2;  // red ring nodes per ring column and plane
-  static constexpr int NRING_CORR = 4 * (TX + 4) + 4 * TY;  // box nodes outside the tile that are read
 };
 
 // A u at a node in the canonical order: D*u - [cx*(l+r) + cy*(d+u) + cz*(m+p)]
@@ -185,7 +184,7 @@ __device__ __forceinline__ void static_for(F&& f) {
 // and final when it is relaxed, so the stencil sum s of its relaxation is the sum the norm
 // forms at the output, and r = f - (D v - s) is that residual bitwise (3 more operations)
 //
-// CORR (the first post-smoothing sweep, MG_FLAG_FUSE_PROLONG): the sweep's input is u + P e (Alg. 1
+// CORR (the first post-smoothing sweep, the default on 3D levels): the sweep's input is u + P e (Alg. 1
 // line 6).  The coarse planes of e arrive by TMA with the u box (3 slots; the u/f
 // ring has 3 slots then, for shared memory).  While plane p is processed, the box of plane p+1
 // (just arrived) is corrected in place: every thread its own rows (in registers, then written
@@ -272,32 +271,22 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
 
     // ---- CORR: u += P e (reading 13 order: x, then y, then z interpolation)
     const T half = (T)0.5;
-    auto e_at = [&](int X, int Y, int Zg) -> T { return Cs(Zg)[(Y - Y0c + 1) * G::CBX + (X - X0c + G::CHX)]; };
-    auto interp = [&](int x, int y, int zg) -> T {  // one node
-      const int X = x >> 1, dx = x & 1, Y = y >> 1, dy = y & 1, Z = zg >> 1, dz = zg & 1;
-      T vy[2];
-      for (int zz = 0; zz <= dz; zz++) {
-        T vx[2];
-        for (int yy = 0; yy <= dy; yy++)
-          vx[yy] = dx ? mul(half, add(e_at(X, Y + yy, Z + zz), e_at(X + 1, Y + yy, Z + zz))) : e_at(X, Y + yy, Z + zz);
-        vy[zz] = dy ? mul(half, add(vx[0], vx[1])) : vx[0];
-      }
-      return dz ? mul(half, add(vy[0], vy[1])) : vy[0];
-    };
-    auto Vrow = [&](int k, int Zg) -> V {  // row k's W nodes after the x- and y-interpolation of coarse plane Zg
-      const int X = ox >> 1, Y = (oy0 + k) >> 1;
+    // V(x, y, Zg): the W nodes (x .. x+W-1, x even) of row y after the x- and y-interpolation of
+    // coarse plane Zg; fine plane z then takes V(z/2), or (V(Z) + V(Z+1)) / 2 when z is odd
+    auto Vxy = [&](int x, int y, int Zg) -> V {
+      const T* cb = Cs(Zg) + ((y >> 1) - Y0c + 1) * G::CBX + ((x >> 1) - X0c + G::CHX);
       T a[NR + 1], b[NR + 1];
 #pragma unroll
-      for (int i = 0; i <= NR; i++) a[i] = e_at(X + i, Y, Zg);
+      for (int i = 0; i <= NR; i++) a[i] = cb[i];
       V v;
 #pragma unroll
       for (int i = 0; i < NR; i++) {
         v.v[2 * i] = a[i];
         v.v[2 * i + 1] = mul(half, add(a[i], a[i + 1]));
       }
-      if ((oy0 + k) & 1) {
+      if (y & 1) {
 #pragma unroll
-        for (int i = 0; i <= NR; i++) b[i] = e_at(X + i, Y + 1, Zg);
+        for (int i = 0; i <= NR; i++) b[i] = cb[G::CBX + i];
 #pragma unroll
         for (int i = 0; i < NR; i++) {
           v.v[2 * i] = mul(half, add(v.v[2 * i], b[i]));
@@ -306,60 +295,88 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
       }
       return v;
     };
+    // The box vectors around the tile that the stencils read, one per thread of warps 0-5:
+    // rows y0-1 / y0+TY (warps 0 / 1: the ring rows whose red nodes those warps relax), the
+    // halo vectors of the tile rows (warp 2, which relaxes the ring columns), rows y0-2 /
+    // y0+TY+1 (warps 3 / 4), the corner vectors (warp 5)
+    constexpr int VH = TX / W + 1;  // index of the right halo vector (left: 0)
+    int rvy = -1000000, rvi = 0;
+    if (CORR) {
+      if (wr == 0 || wr == 1 || wr == 3 || wr == 4) {
+        rvy = wr == 0 ? y0 - 1 : wr == 1 ? y0 + TY : wr == 3 ? y0 - 2 : y0 + TY + 1;
+        rvi = lane + 1;
+      } else if (wr == 2) {
+        rvy = y0 + (lane & 15);
+        rvi = lane < 16 ? 0 : VH;
+      } else if (wr == 5 && lane < 8) {
+        const int rr = lane & 3;
+        rvy = rr < 2 ? y0 - 2 + rr : y0 + TY + rr - 2;
+        rvi = lane < 4 ? 0 : VH;
+      }
+    }
+    const bool has_rv = rvy > -1000000;
+    const int rvx = x0 - HX + W * rvi;
+    const int rbo = (rvy - y0 + 2) * BX + W * rvi;
+    bool rin[W];
+#pragma unroll
+    for (int j = 0; j < W; j++) rin[j] = has_rv && rvy >= 1 && rvy <= g.ny - 1 && rvx + j >= 1 && rvx + j <= g.nx - 1;
+    bool own_all = true;
+#pragma unroll
+    for (int k = 0; k < RPT; k++)
+#pragma unroll
+      for (int j = 0; j < W; j++) own_all = own_all && in[k][j];
     int cZ = -1000000;  // coarse plane of cA (cB: cZ + 1 when cHaveB)
-    V cA[RPT], cB[RPT];
+    V cA[RPT + 1], cB[RPT + 1];  // [RPT]: the ring vector
     bool cHaveB = false;
-    // own rows of fine plane zl (local) in registers: uv[k] += P e
-    auto correct_own = [&](V* uv, int zl) {
+    auto cache_row = [&](int k, int Zg) { return k < RPT ? Vxy(ox, oy0 + k, Zg) : Vxy(rvx, rvy, Zg); };
+    // fine plane zl (local): the own rows uv[k] += P e in registers, the ring vector in the box Ub
+    auto correct = [&](V* uv, int zl, T* Ub) {
       const int zg = zl + g.p_glob0;
       if (zg < 1 || zg > g.nz - 1) return;  // boundary / outside planes: no correction
+      const int nk = has_rv ? RPT + 1 : RPT;
       if ((zg >> 1) != cZ) {
         const bool shift = cHaveB && (zg >> 1) == cZ + 1;
 #pragma unroll
-        for (int k = 0; k < RPT; k++) cA[k] = shift ? cB[k] : Vrow(k, zg >> 1);
+        for (int k = 0; k <= RPT; k++)
+          if (k < nk) cA[k] = shift ? cB[k] : cache_row(k, zg >> 1);
         cZ = zg >> 1;
         cHaveB = false;
       }
       if ((zg & 1) && !cHaveB) {
 #pragma unroll
-        for (int k = 0; k < RPT; k++) cB[k] = Vrow(k, cZ + 1);
+        for (int k = 0; k <= RPT; k++)
+          if (k < nk) cB[k] = cache_row(k, cZ + 1);
         cHaveB = true;
       }
+      // the plane parity is CTA-uniform and most threads' nodes are all interior: branch on both
+      // instead of selecting per element
+      auto apply = [&](auto ODDc) {
+        constexpr bool ODD = decltype(ODDc)::value;
+        auto pe = [&](int k, int j) { return ODD ? mul(half, add(cA[k].v[j], cB[k].v[j])) : cA[k].v[j]; };
+        if (own_all) {
 #pragma unroll
-      for (int k = 0; k < RPT; k++)
+          for (int k = 0; k < RPT; k++)
 #pragma unroll
-        for (int j = 0; j < W; j++) {
-          const T v = (zg & 1) ? mul(half, add(cA[k].v[j], cB[k].v[j])) : cA[k].v[j];
-          if (in[k][j]) uv[k].v[j] = add(uv[k].v[j], v);
+            for (int j = 0; j < W; j++) uv[k].v[j] = add(uv[k].v[j], pe(k, j));
+        } else {
+#pragma unroll
+          for (int k = 0; k < RPT; k++)
+#pragma unroll
+            for (int j = 0; j < W; j++)
+              if (in[k][j]) uv[k].v[j] = add(uv[k].v[j], pe(k, j));
         }
-    };
-    auto box_ring_node = [&](int e, int& x, int& y) {  // box nodes around the tile that the stencils read
-      if (e < 4 * (TX + 4)) {
-        const int rr = e / (TX + 4);
-        y = rr < 2 ? y0 - 2 + rr : y0 + TY + rr - 2;
-        x = x0 - 2 + e % (TX + 4);
-      } else {
-        const int t2 = e - 4 * (TX + 4), cc = t2 / TY;
-        x = cc < 2 ? x0 - 2 + cc : x0 + TX + cc - 2;
-        y = y0 + t2 % TY;
-      }
-    };
-    // the box ring nodes of fine plane zl in shared memory; skip_red_pgl >= 0: leave out the red
-    // ring-1 nodes of plane skip_red_pgl that the ring threads correct themselves
-    auto correct_ring = [&](T* Ub, int zl, int skip_red_pgl) {
-      const int zg = zl + g.p_glob0;
-      if (zg < 1 || zg > g.nz - 1) return;
-      for (int e = tid; e < G::NRING_CORR; e += NTH) {
-        int x, y;
-        box_ring_node(e, x, y);
-        if (x < 1 || x > g.nx - 1 || y < 1 || y > g.ny - 1) continue;
-        if (skip_red_pgl >= 0 && ((x + y + skip_red_pgl) & 1) == 0 &&
-            (((y == y0 - 1 || y == y0 + TY) && x >= x0 && x < x0 + TX) ||
-             ((x == x0 - 1 || x == x0 + TX) && y >= y0 && y < y0 + TY)))
-          continue;
-        T* q = Ub + (y - y0 + 2) * BX + (x - x0 + HX);
-        *q = add(*q, interp(x, y, zg));
-      }
+        if (has_rv) {
+          V rv = ld_vec(Ub + rbo);
+#pragma unroll
+          for (int j = 0; j < W; j++)
+            if (rin[j]) rv.v[j] = add(rv.v[j], pe(RPT, j));
+          st_vec(Ub + rbo, rv);
+        }
+      };
+      if (zg & 1)
+        apply(std::true_type());
+      else
+        apply(std::false_type());
     };
 
     R.wait(N(qlo));
@@ -372,10 +389,9 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
         V own[RPT];
 #pragma unroll
         for (int k = 0; k < RPT; k++) own[k] = ld_vec(Ub + bo + k * BX);
-        correct_own(own, qlo + 1 + b);
+        correct(own, qlo + 1 + b, Ub);
 #pragma unroll
         for (int k = 0; k < RPT; k++) st_vec(Ub + bo + k * BX, own[k]);
-        correct_ring(Ub, qlo + 1 + b, -1);
       }
       __syncthreads();
     }
@@ -385,12 +401,17 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
       u0[k] = svec(R.U(N(qlo + 1)), bo + k * BX);
     }
 
-    // RB ring threads, as in k_sweep3d (warps 0 .. 2 NR - 1: ring rows; warp 2 NR: ring columns)
-    constexpr int RWARPS = 2 * NR;
+    // RB ring threads: the red nodes of the ring rows y0-1 / y0+TY and of the ring columns
+    // x0-1 / x0+TX, one node per lane (FP32, NR = 2 per lane and row: warps 0-3, warp w row
+    // w & 1, node w >> 1), the columns by warp RWARPS.  CORR: warps 0 / 1 take both nodes of
+    // their lane's vector (the vector they corrected), the columns warp 2.
+    constexpr int RWARPS = CORR ? 2 : 2 * NR;
+    constexpr int MPL = CORR ? NR : 1;  // ring-row nodes per lane
     static_assert(RWARPS < NTH / 32, "ring warps");
     const bool ring_row = RB && wr < RWARPS;
     const bool ring_col = RB && wr == RWARPS && lane < 2 * RCOL;
-    const int mring = ring_row ? (wr >> 1) : 0;
+    const int mring = (ring_row && !CORR) ? (wr >> 1) : 0;
+    const int nring = ring_row ? MPL : (ring_col ? 1 : 0);
     auto ring_pos = [&](int pgl, int m, int& x, int& y) {
       if (wr < RWARPS) {
         y = (wr & 1) == 0 ? y0 - 1 : y0 + TY;
@@ -400,11 +421,15 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
         y = y0 + 2 * (lane % RCOL) + ((x + y0 + pgl) & 1);
       }
     };
-    T rzm = (T)0;
-    if (ring_row || ring_col) {
-      int x, y;
-      ring_pos(pa - 1 + g.p_glob0, mring, x, y);
-      rzm = su(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
+    T rzm[MPL];  // ring thread: u(p-1) at its plane-p ring node(s)
+#pragma unroll
+    for (int mm = 0; mm < MPL; mm++) {
+      rzm[mm] = (T)0;
+      if (mm < nring) {
+        int x, y;
+        ring_pos(pa - 1 + g.p_glob0, mring + mm, x, y);
+        rzm[mm] = su(R.U(N(qlo)), (y - y0 + 2) * BX + (x - x0 + HX));
+      }
     }
     __syncthreads();  // step qlo lives on in registers only: refill its slot
     if (tid == 0 && qlo + NSR <= qlast) {
@@ -431,11 +456,11 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
 #pragma unroll
         for (int k = 0; k < RPT; k++) up[k] = svec(Up, bo + k * BX);
         const int pgl = p + g.p_glob0;
-        if constexpr (CORR) {  // plane p+1's box: own rows (registers + write-back) and its ring
-          correct_own(up, p + 1);
+        if constexpr (CORR) {  // plane p+1's box: own rows (registers + write-back) and the ring vectors
+          correct(up, p + 1, const_cast<T*>(Up));
 #pragma unroll
           for (int k = 0; k < RPT; k++) st_vec(const_cast<T*>(Up) + bo + k * BX, up[k]);
-          correct_ring(const_cast<T*>(Up), p + 1, pgl);
+          if (wr == RWARPS) __syncwarp();  // the ring columns' z+1 nodes, corrected by other lanes
         }
         const bool pl_in = pgl >= 1 && pgl <= g.nz - 1;
         const int kr0 = (oy0 + pgl) & 1;  // red offset of row 0 (row k: kr0 ^ (k & 1)), warp uniform
@@ -489,25 +514,20 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
           red_stage(std::integral_constant<int, 1>());
         else
           red_stage(std::integral_constant<int, 0>());
-        if (ring_row || ring_col) {  // the red ring node of plane p
-          int x, y;
-          ring_pos(pgl, mring, x, y);
-          const int rb = (y - y0 + 2) * BX + (x - x0 + HX);
-          const T ctr = su(U0, rb);
-          T zp = su(Up, rb);  // u(p+1) at the node (CORR: this thread corrects it in the box)
-          if constexpr (CORR) {
-            const int zg1 = pgl + 1;
-            if (x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1 && zg1 >= 1 && zg1 <= g.nz - 1) {
-              zp = add(zp, interp(x, y, zg1));
-              const_cast<T*>(Up)[rb] = zp;
-            }
+#pragma unroll
+        for (int mm = 0; mm < MPL; mm++) {  // the red ring node(s) of plane p
+          if (mm < nring) {
+            int x, y;
+            ring_pos(pgl, mring + mm, x, y);
+            const int rb = (y - y0 + 2) * BX + (x - x0 + HX);
+            const T ctr = su(U0, rb);
+            const T v = relax(c, ctr, su(U0, rb - 1), su(U0, rb + 1), su(U0, rb - BX), su(U0, rb + BX), rzm[mm],
+                              su(Up, rb), F0[(y - y0 + 1) * BX + (x - x0 + HX)]);
+            const bool ok = pl_in && x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1;
+            PR[(y - y0 + 1) * PX + (x - x0 + HX)] = ok ? v : ctr;
+            ring_pos(pgl + 1, mring + mm, x, y);
+            rzm[mm] = su(U0, (y - y0 + 2) * BX + (x - x0 + HX));
           }
-          const T v = relax(c, ctr, su(U0, rb - 1), su(U0, rb + 1), su(U0, rb - BX), su(U0, rb + BX), rzm, zp,
-                            F0[(y - y0 + 1) * BX + (x - x0 + HX)]);
-          const bool ok = pl_in && x >= 1 && x <= g.nx - 1 && y >= 1 && y <= g.ny - 1;
-          PR[(y - y0 + 1) * PX + (x - x0 + HX)] = ok ? v : ctr;
-          ring_pos(pgl + 1, mring, x, y);
-          rzm = su(U0, (y - y0 + 2) * BX + (x - x0 + HX));
         }
         __syncthreads();
         // every thread is past plane p-2's black update and plane p's red stage: step p-1
@@ -598,10 +618,9 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
         for (int k = 0; k < RPT; k++) up[k] = svec(R.U(N(p)), bo + k * BX);
         if constexpr (CORR) {
           T* Upw = R.U(N(p));
-          correct_own(up, p + 1);
+          correct(up, p + 1, Upw);
 #pragma unroll
           for (int k = 0; k < RPT; k++) st_vec(Upw + bo + k * BX, up[k]);
-          correct_ring(Upw, p + 1, -1);
         }
         static_for<RPT>([&](auto Kc) {
           constexpr int K = decltype(Kc)::value;
@@ -1060,7 +1079,7 @@ cudaError_t launch_norm(const Geom& g, const Coef<T>& c, const T* u, const T* f,
 // marching z.  The thread's coarse values after the x- and y-interpolation of a
 // coarse plane K, V(K), stay in registers for the 3 fine planes that use it;
 // fine plane z = 2Z+dz gets dz ? (V(Z)+V(Z+1))/2 : V(Z) (reading 13 order).
-// (The default; MG_FLAG_FUSE_PROLONG folds it into the first post-sweep instead.)
+// (Used with MG_FLAG_SEPARATE_PROLONG; by default the first post-sweep does it, CORR.)
 // KZ planes per batch; MINB resident CTAs per SM (register cap); PIPE: the next batch's
 // u vectors are loaded before the current batch is stored (software pipelining).
 template <typename T, int KZ, int MINB, bool PIPE>

@@ -636,9 +636,14 @@ struct Exec {
   bool split_norm() const {
     const Level& L = s->lv[0];
     return can_split() && s->cfg.smoother == MG_RBGS && L.g.three_d && !L.dist && s->cfg.nu2 >= 1 &&
-           !((s->cfg.flags & MG_FLAG_FUSE_PROLONG) && s->cfg.nu2 == 1);
+           !(fuse_prolong(0) && s->cfg.nu2 == 1);
   }
   int black_items() const { return pm::sweep_items<T>(s->lv[0].g, true); }
+  // the prolongation + correction of level l rides on its first post-sweep (3D marching levels;
+  // measured C3 FP64 3.52 -> 3.31 ms); MG_FLAG_SEPARATE_PROLONG keeps its own pass
+  bool fuse_prolong(int l) const {
+    return pm(l) && s->lv[l].g.three_d && s->cfg.nu2 >= 1 && l + 1 < s->L && !(s->cfg.flags & MG_FLAG_SEPARATE_PROLONG);
+  }
 
   mg_status cycle_start(T* u0, const T* f0) {
     const bool jac = s->cfg.smoother == MG_JACOBI;
@@ -809,10 +814,12 @@ struct Exec {
       for (int l = (lt < Lv ? lt : Lv - 1) - 1; l >= 0; l--) {
         const Level& L = s->lv[l];
         const T* f = l == 0 ? f0 : (const T*)L.f;
-        if ((r = exchange(l + 1, cur[l + 1], 1)) != MG_OK) return r;  // e_H neighbour planes (slabs)
+        // e_H neighbour planes (slabs); the fused first post-sweep also corrects the u halo planes,
+        // whose top one (odd, above the slab) reads the second coarse plane above
+        if ((r = exchange(l + 1, cur[l + 1], fuse_prolong(l) ? 2 : 1)) != MG_OK) return r;
         const T* e = cur[l + 1];
         const bool pml = pm(l);
-        if (pml && L.g.three_d && s->cfg.nu2 >= 1 && (s->cfg.flags & MG_FLAG_FUSE_PROLONG)) {
+        if (fuse_prolong(l)) {
           // prolongation + correction fused into the first post-sweep: u + P e is formed in
           // shared memory, only S(u + P e) is written
           const bool rb = s->cfg.smoother == MG_RBGS;

@@ -227,13 +227,13 @@ def test_profile_counts_launches():
     assert all(r["ms"] > 0 for r in recs)
 
 
-@pytest.mark.parametrize("variant", ["default-threshold", "baseline", "fuse-prolong"])
+@pytest.mark.parametrize("variant", ["default-threshold", "baseline", "separate-prolong"])
 def test_schedule_variants_identical(variant):
     """The plane-marching, mixed (default threshold) and op-by-op (MG_FLAG_BASELINE)
     schedules give bitwise identical iterates (same canonical arithmetic)."""
     import paper_1406_5369_b200 as mgb
     kw = {"default-threshold": dict(pm_min_nx=0), "baseline": dict(flags=mgb.FLAG_BASELINE),
-          "fuse-prolong": dict(flags=mgb.FLAG_FUSE_PROLONG)}[variant]
+          "separate-prolong": dict(flags=mgb.FLAG_SEPARATE_PROLONG)}[variant]
     outs = []
     for extra in (dict(), kw):
         S, _ = make(3, (128, 128, 128), **extra)
@@ -275,12 +275,12 @@ def test_slab_mode_single_rank(case):
 
 
 @pytest.mark.parametrize("dt", ["f64", "f32"])
-def test_fused_prolongation_sweep_parity(dt):
-    """MG_FLAG_FUSE_PROLONG (u + P e formed in shared memory by the first post-sweep) against
-    the oracle per cycle, both smoothers."""
+def test_separate_prolongation_parity(dt):
+    """MG_FLAG_SEPARATE_PROLONG (the prolongation + correction as its own pass instead of fused
+    into the first post-sweep, the default) against the oracle per cycle, both smoothers."""
     import paper_1406_5369_b200 as mgb
     for sm in ("rbgs", "jacobi"):
-        S, O = make(3, (128, 128, 128), smoother=sm, dtype=dt, flags=mgb.FLAG_FUSE_PROLONG)
+        S, O = make(3, (128, 128, 128), smoother=sm, dtype=dt, flags=mgb.FLAG_SEPARATE_PROLONG)
         u, f = wl.workload("W4", 3, (128, 128, 128), seed=3, dtype=S.np_dtype)
         du, df = S.from_numpy(u), S.from_numpy(f)
         uo = u.copy()

@@ -32,10 +32,10 @@ def test_ragged_3d_bitwise(cells, sm, dt):
 
 
 @pytest.mark.parametrize("dt", ["f64", "f32"])
-def test_ragged_3d_fused_prolongation(dt):
+def test_ragged_3d_separate_prolongation(dt):
     import paper_1406_5369_b200 as mgb
     cells = (160, 104, 40)
-    S, O = make(3, cells, 4, "rbgs", dtype=dt, pm_min_nx=0, flags=mgb.FLAG_FUSE_PROLONG)
+    S, O = make(3, cells, 4, "rbgs", dtype=dt, pm_min_nx=0, flags=mgb.FLAG_SEPARATE_PROLONG)
     u, f = wl.workload("W4", 3, cells, seed=13, dtype=S.np_dtype)
     du, df = S.from_numpy(u), S.from_numpy(f)
     uo = u.copy()

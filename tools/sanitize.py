@@ -110,7 +110,7 @@ CASES = {
     "p3_129_rbgs_f64": lambda: poisson(3, 129, "rbgs", "f64", pm_min_nx=64),
     "p3_129_rbgs_f32": lambda: poisson(3, 129, "rbgs", "f32", pm_min_nx=64),
     "p3_97_rbgs_f64_ragged": lambda: poisson(3, 97, "rbgs", "f64"),
-    "p3_65_fuseprolong_f64": lambda: poisson(3, 65, "rbgs", "f64", flags=mgb.FLAG_FUSE_PROLONG),
+    "p3_65_separate_prolong_f64": lambda: poisson(3, 65, "rbgs", "f64", flags=mgb.FLAG_SEPARATE_PROLONG),
     "p3_65_baseline_f64": lambda: poisson(3, 65, "rbgs", "f64", flags=mgb.FLAG_BASELINE),
     "p3_33_lex_f64": lambda: poisson(3, 33, "gs_lex", "f64"),
     "p2_257_jac33_f32": lambda: poisson(2, 257, "jacobi", "f32", nu=(3, 3)),
