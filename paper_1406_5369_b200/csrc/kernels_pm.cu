@@ -273,8 +273,7 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     const T half = (T)0.5;
     // V(x, y, Zg): the W nodes (x .. x+W-1, x even) of row y after the x- and y-interpolation of
     // coarse plane Zg; fine plane z then takes V(z/2), or (V(Z) + V(Z+1)) / 2 when z is odd
-    auto Vxy = [&](int x, int y, int Zg) -> V {
-      const T* cb = Cs(Zg) + ((y >> 1) - Y0c + 1) * G::CBX + ((x >> 1) - X0c + G::CHX);
+    auto Vxy = [&](const T* cb, bool yodd) -> V {  // cb: the coarse box at (x/2, y/2)
       T a[NR + 1], b[NR + 1];
 #pragma unroll
       for (int i = 0; i <= NR; i++) a[i] = cb[i];
@@ -284,7 +283,7 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
         v.v[2 * i] = a[i];
         v.v[2 * i + 1] = mul(half, add(a[i], a[i + 1]));
       }
-      if (y & 1) {
+      if (yodd) {
 #pragma unroll
         for (int i = 0; i <= NR; i++) b[i] = cb[G::CBX + i];
 #pragma unroll
@@ -328,24 +327,37 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     int cZ = -1000000;  // coarse plane of cA (cB: cZ + 1 when cHaveB)
     V cA[RPT + 1], cB[RPT + 1];  // [RPT]: the ring vector
     bool cHaveB = false;
-    auto cache_row = [&](int k, int Zg) { return k < RPT ? Vxy(ox, oy0 + k, Zg) : Vxy(rvx, rvy, Zg); };
+    // offsets of the thread's vectors in a coarse box (constant over the item's planes)
+    int coff[RPT + 1];
+#pragma unroll
+    for (int k = 0; k < RPT; k++) coff[k] = (((oy0 + k) >> 1) - Y0c + 1) * G::CBX + ((ox >> 1) - X0c + G::CHX);
+    coff[RPT] = has_rv ? ((rvy >> 1) - Y0c + 1) * G::CBX + ((rvx >> 1) - X0c + G::CHX) : 0;
+    auto cache_row = [&](int k, const T* base) {
+      return Vxy(base + coff[k], k < RPT ? (((oy0 + k) & 1) != 0) : ((rvy & 1) != 0));
+    };
     // fine plane zl (local): the own rows uv[k] += P e in registers, the ring vector in the box Ub
     auto correct = [&](V* uv, int zl, T* Ub) {
       const int zg = zl + g.p_glob0;
       if (zg < 1 || zg > g.nz - 1) return;  // boundary / outside planes: no correction
       const int nk = has_rv ? RPT + 1 : RPT;
       if ((zg >> 1) != cZ) {
-        const bool shift = cHaveB && (zg >> 1) == cZ + 1;
+        if (cHaveB && (zg >> 1) == cZ + 1) {
 #pragma unroll
-        for (int k = 0; k <= RPT; k++)
-          if (k < nk) cA[k] = shift ? cB[k] : cache_row(k, zg >> 1);
+          for (int k = 0; k <= RPT; k++) cA[k] = cB[k];
+        } else {
+          const T* base = Cs(zg >> 1);
+#pragma unroll
+          for (int k = 0; k <= RPT; k++)
+            if (k < nk) cA[k] = cache_row(k, base);
+        }
         cZ = zg >> 1;
         cHaveB = false;
       }
       if ((zg & 1) && !cHaveB) {
+        const T* base = Cs(cZ + 1);
 #pragma unroll
         for (int k = 0; k <= RPT; k++)
-          if (k < nk) cB[k] = cache_row(k, cZ + 1);
+          if (k < nk) cB[k] = cache_row(k, base);
         cHaveB = true;
       }
       // the plane parity is CTA-uniform and most threads' nodes are all interior: branch on both
