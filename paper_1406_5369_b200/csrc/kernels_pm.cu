@@ -212,7 +212,6 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
   extern __shared__ __align__(128) unsigned char sm[];
   const Ring<T, NSR> R = ring_setup<T, NSR>(sm, &tm_u, &tm_f);
   T* spr = reinterpret_cast<T*>(sm + PR_OFF);
-  auto PRb = [&](int q) { return spr + (size_t)(((q % 3) + 3) % 3) * (G::PB / sizeof(T)); };
   auto su = [&](const T* base, int off) -> T { return ZERO ? (T)0 : base[off]; };
   auto svec = [&](const T* base, int off) -> V {
     if (ZERO) {
@@ -237,13 +236,18 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     item_of(it, ntiles, zc, g.p_lo, g.p_hi, tile, pa, pb);
     const int x0 = (tile % tiles_x) * TX, y0 = (tile / tiles_x) * TY;
     const int ox = x0 + W * lane, oy0 = y0 + ty0;
-    bool in[RPT][W];
+    // interior flags of the thread's nodes as bits (k W + j): one register instead of RPT W
+    // predicates, which the register-tight variants would otherwise recompute at every use
+    uint32_t inm = 0;
 #pragma unroll
     for (int k = 0; k < RPT; k++) {
       const bool rin = oy0 + k >= 1 && oy0 + k <= g.ny - 1;
 #pragma unroll
-      for (int j = 0; j < W; j++) in[k][j] = rin && ox + j >= 1 && ox + j <= g.nx - 1;
+      for (int j = 0; j < W; j++)
+        if (rin && ox + j >= 1 && ox + j <= g.nx - 1) inm |= 1u << (k * W + j);
     }
+    auto in = [&](int k, int j) -> bool { return (inm >> (k * W + j)) & 1u; };
+    auto inrow = [&](int k) -> uint32_t { return (inm >> (k * W)) & ((1u << W) - 1u); };
     T* orow = unew + (long long)oy0 * g.pitch;
 
     const int qlo = RB ? pa - 3 : pa - 2, qlast = RB ? pb : pb - 1;
@@ -316,14 +320,15 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     const bool has_rv = rvy > -1000000;
     const int rvx = x0 - HX + W * rvi;
     const int rbo = (rvy - y0 + 2) * BX + W * rvi;
-    bool rin[W];
+    uint32_t rinm = 0;  // interior flags of the ring vector's nodes
 #pragma unroll
-    for (int j = 0; j < W; j++) rin[j] = has_rv && rvy >= 1 && rvy <= g.ny - 1 && rvx + j >= 1 && rvx + j <= g.nx - 1;
+    for (int j = 0; j < W; j++)
+      if (has_rv && rvy >= 1 && rvy <= g.ny - 1 && rvx + j >= 1 && rvx + j <= g.nx - 1) rinm |= 1u << j;
     bool own_all = true;
 #pragma unroll
     for (int k = 0; k < RPT; k++)
 #pragma unroll
-      for (int j = 0; j < W; j++) own_all = own_all && in[k][j];
+      for (int j = 0; j < W; j++) own_all = own_all && in(k, j);
     int cZ = -1000000;  // coarse plane of cA (cB: cZ + 1 when cHaveB)
     V cA[RPT + 1], cB[RPT + 1];  // [RPT]: the ring vector
     bool cHaveB = false;
@@ -375,13 +380,13 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
           for (int k = 0; k < RPT; k++)
 #pragma unroll
             for (int j = 0; j < W; j++)
-              if (in[k][j]) uv[k].v[j] = add(uv[k].v[j], pe(k, j));
+              if (in(k, j)) uv[k].v[j] = add(uv[k].v[j], pe(k, j));
         }
         if (has_rv) {
           V rv = ld_vec(Ub + rbo);
 #pragma unroll
           for (int j = 0; j < W; j++)
-            if (rin[j]) rv.v[j] = add(rv.v[j], pe(RPT, j));
+            if ((rinm >> j) & 1u) rv.v[j] = add(rv.v[j], pe(RPT, j));
           st_vec(Ub + rbo, rv);
         }
       };
@@ -459,12 +464,13 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
 #pragma unroll
         for (int j = 0; j < W; j++) fprev[k].v[j] = (T)0;
       }
+      int ps = (((pa - 1) % 3) + 3) % 3;  // PR slot of plane p (rotates 0, 1, 2)
       for (int p = pa - 1; p <= pb; p++) {
         R.wait(N(p));
         const T* U0 = R.U(N(p - 1));  // u(p)
         const T* Up = R.U(N(p));      // u(p+1)
         const T* F0 = R.F(N(p));      // f(p)
-        T* PR = PRb(p);
+        T* PR = spr + (size_t)ps * (G::PB / sizeof(T));
 #pragma unroll
         for (int k = 0; k < RPT; k++) up[k] = svec(Up, bo + k * BX);
         const int pgl = p + g.p_glob0;
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
                   const T r = j == W - 1 ? oedge : u0[K].v[j < W - 1 ? j + 1 : 0];
                   const double rr = (double)sub(
                       fcur[K].v[j], apply_A(c, u0[K].v[j], l, r, dn.v[j], upr.v[j], um[K].v[j], up[K].v[j]));
-                  if (in[K][j]) nsum = acc_sq_d<T>(nsum, rr);
+                  if (in(K, j)) nsum = acc_sq_d<T>(nsum, rr);
                 }
               }
             }
@@ -511,8 +517,8 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
               const T r = j == W - 1 ? edge : u0[K].v[j < W - 1 ? j + 1 : 0];
               const T res = sub(fcur[K].v[j], apply_A(c, ctr, l, r, dn.v[j], upr.v[j], um[K].v[j], up[K].v[j]));
               const T v = add(ctr, mul(c.wd, res));
-              if (NRM && nrm_here && in[K][j]) nsum = acc_sq<T>(nsum, res);
-              const T prv = (pl_in && in[K][j]) ? v : ctr;
+              if (NRM && nrm_here && in(K, j)) nsum = acc_sq<T>(nsum, res);
+              const T prv = (pl_in && in(K, j)) ? v : ctr;
               pv.v[j] = prv;
               pr0[K][m] = prv;
             }
@@ -550,7 +556,7 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
         }
         const int bp = p - 1;
         if (bp >= pa) {
-          const T* P = PRb(bp);
+          const T* P = spr + (size_t)(ps == 0 ? 2 : ps - 1) * (G::PB / sizeof(T));
           auto black_stage = [&](auto KB0c) {
             static_for<RPT>([&](auto Kc) {
               constexpr int K = decltype(Kc)::value;
@@ -597,11 +603,11 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
                 const T fb = fprev[K].v[j];
                 const T v = add(ctr, mul(c.wd, sub(fb, sub(mul(c.D, ctr), sm_))));
                 if constexpr (NM == 3) {
-                  if (in[K][j]) nsum = acc_sq<T>(nsum, sub(fb, sub(mul(c.D, v), sm_)));
+                  if (in(K, j)) nsum = acc_sq<T>(nsum, sub(fb, sub(mul(c.D, v), sm_)));
                 }
-                o.v[j] = in[K][j] ? v : ctr;
+                o.v[j] = in(K, j) ? v : ctr;
               }
-              store_vec(orow + (long long)K * g.pitch + (long long)bp * g.pstride, ox, in[K], o);
+              store_vec_m(orow + (long long)K * g.pitch + (long long)bp * g.pstride, ox, inrow(K), o);
             });
           };
           if (kr0)
@@ -609,6 +615,7 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
           else
             black_stage(std::integral_constant<int, 0>());
         }
+        ps = ps == 2 ? 0 : ps + 1;
 #pragma unroll
         for (int k = 0; k < RPT; k++) {
           um[k] = u0[k];
@@ -647,13 +654,13 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
             const T r = j == W - 1 ? er : u0[K].v[j < W - 1 ? j + 1 : 0];
             const T res = sub(fv.v[j], apply_A(c, u0[K].v[j], l, r, dn.v[j], upr.v[j], um[K].v[j], up[K].v[j]));
             if (MODE == 2) {
-              if (in[K][j]) nsum = acc_sq_d<T>(nsum, (double)res);
+              if (in(K, j)) nsum = acc_sq_d<T>(nsum, (double)res);
             } else {
-              if (NRM && in[K][j]) nsum = acc_sq<T>(nsum, res);
-              o.v[j] = in[K][j] ? add(u0[K].v[j], mul(c.wd, res)) : u0[K].v[j];
+              if (NRM && in(K, j)) nsum = acc_sq<T>(nsum, res);
+              o.v[j] = in(K, j) ? add(u0[K].v[j], mul(c.wd, res)) : u0[K].v[j];
             }
           }
-          if (MODE != 2) store_vec(orow + (long long)K * g.pitch + (long long)p * g.pstride, ox, in[K], o);
+          if (MODE != 2) store_vec_m(orow + (long long)K * g.pitch + (long long)p * g.pstride, ox, inrow(K), o);
         });
         __syncthreads();
         if (tid == 0 && p - 1 + NSR <= qlast) {

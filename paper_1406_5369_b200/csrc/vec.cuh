@@ -74,4 +74,17 @@ __device__ __forceinline__ void store_vec(T* dst, int x, const bool* ok, const V
   }
 }
 
+// the same with the W flags as the low bits of `ok`
+template <typename T>
+__device__ __forceinline__ void store_vec_m(T* dst, int x, uint32_t ok, const Vec<T, 16 / sizeof(T)>& o) {
+  constexpr int W = 16 / sizeof(T);
+  if (ok == (1u << W) - 1u) {
+    st_vec(dst + x, o);
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; k++)
+      if ((ok >> k) & 1u) dst[x + k] = o.v[k];
+  }
+}
+
 }  // namespace mg
