@@ -731,12 +731,13 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     const int X0 = (tile % tiles_x) * (TX / 2), Y0 = (tile / tiles_x) * (TY / 2);
     const int x0 = 2 * X0, y0 = 2 * Y0;
     const int ox = x0 + W * lane, oy0 = y0 + ty0;
-    bool in[RPT][W];
+    uint32_t inm = 0;  // interior flags (bit k W + j), as in k_sweep3d_rows
 #pragma unroll
     for (int k = 0; k < RPT; k++) {
       const bool rin = oy0 + k >= 1 && oy0 + k <= gf.ny - 1;
 #pragma unroll
-      for (int j = 0; j < W; j++) in[k][j] = rin && ox + j >= 1 && ox + j <= gf.nx - 1;
+      for (int j = 0; j < W; j++)
+        if (rin && ox + j >= 1 && ox + j <= gf.nx - 1) inm |= 1u << (k * W + j);
     }
     // low-side ring: row y0-1 for x in [x0-1, x0+TX-1] (TX+1 nodes), column x0-1 for y in [y0, y0+TY-1]
     constexpr int NRING = TX + 1 + TY;
@@ -815,7 +816,7 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
           const T l = j == 0 ? el : u0[K].v[j > 0 ? j - 1 : 0];
           const T r = j == W - 1 ? er : u0[K].v[j < W - 1 ? j + 1 : 0];
           const T rr = sub(fv.v[j], apply_A(c, u0[K].v[j], l, r, dn.v[j], upr.v[j], um[K].v[j], up[K].v[j]));
-          rv.v[j] = pl_in && in[K][j] ? rr : (T)0;
+          rv.v[j] = pl_in && ((inm >> (K * W + j)) & 1u) ? rr : (T)0;
         }
         if constexpr (sizeof(T) == 8)
           *reinterpret_cast<double2*>(Rr + po + K * PX) = make_double2(rv.v[0], rv.v[1]);
