@@ -4,7 +4,7 @@
 // microseconds of launch and barrier for a few thousand nodes).  k_tail runs
 // V_lt(0, f_lt) — every operation of Alg. 1 on levels lt..L-1:
 // pre-smoothing, residual + full weighting, the coarsest solve, prolongation +
-// correction, post-smoothing — inside ONE thread-block cluster (16 CTAs x 1024
+// correction, post-smoothing — inside ONE thread-block cluster (16 CTAs x 512
 // threads, one per SM), a cluster barrier (barrier.cluster release/acquire)
 // between passes, data in global memory (L2 resident).  Levels of at most a few
 // thousand nodes run on CTA 0 alone with block barriers ("solo"), their arrays
@@ -26,7 +26,7 @@ namespace mg {
 
 namespace {
 
-constexpr int NTT = 1024;
+constexpr int NTT = 512;  // measured: 512 beats 1024 (C1 63.6 -> 59.3 us, C2, C4) and 256
 constexpr int WPC = NTT / 32;  // warps per CTA
 
 // all CTAs of the cluster (= the grid): release/acquire at cluster scope makes the
