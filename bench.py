@@ -97,6 +97,25 @@ def model_bytes_per_step(S, esz):
     return total + 2 * n0 * esz
 
 
+def unfused_bytes_per_step(dim, nodes, levels, smoother, nu1, nu2, esz):
+    """B_unfused of SURVEY §8(a): Alg. 1 op by op (the oracle's schedule; two-pass RBGS, w = 6) + the
+    norm pass, for the full-size workload."""
+    w = 6 if smoother == "rbgs" else 3
+    q = 2.0 ** -dim
+    total = 0.0
+    for l in range(levels - 1):
+        total += ((nodes - 1) // 2 ** l + 1) ** dim * (w * (nu1 + nu2) + 3 + (1 + q) + q + (2 + q)) * esz
+    return total + 2 * nodes ** dim * esz
+
+
+def ncu_cycle_bytes(config):
+    """Measured DRAM bytes of one cycle + norm (all kernels, ncu; profiles/ncu_cycle_bytes.json)."""
+    p = os.path.join(ROOT, "profiles", "ncu_cycle_bytes.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get(config)
+
+
 def l2_note(array_bytes):
     if array_bytes > 126e6:
         return f"inputs larger than L2 ({array_bytes / 1e9:.3f} GB per array), no flush needed"
@@ -225,6 +244,12 @@ def oracle_step_time(cfgname, max_seconds=30.0):
     cells = (nodes - 1,) * dim
     # full size when it fits the budget, else the largest power-of-two grid that does
     npdt = np.float64 if dt == "f64" else np.float32
+    # untimed warm-up on a small grid: the OpenMP runtime starts its thread pool on the first
+    # parallel region (≈ 1 s on this host), which must not be charged to the timed cycle
+    wc = orc.Config(dim=dim, cells=(8,) * dim)
+    Ow = orc.Oracle(wc, npdt)
+    uw, fw = wl.workload("W1", dim, (8,) * dim, seed=1, dtype=npdt)
+    Ow.vcycle_inplace(uw, fw)
     for n in [nodes - 1, (nodes - 1) // 2, (nodes - 1) // 4]:
         cells = (n,) * dim
         c = orc.Config(dim=dim, cells=cells, levels=levels if n == nodes - 1 else 0,
@@ -260,6 +285,13 @@ def cpu_baseline_leg(cfgname):
     t, cunk, desc, threads, _ = oracle_step_time(cfgname, max_seconds=30.0)
     out = {"value": cunk / t, "unit": "unknowns/s", "cores": threads, "kind": "oracle", "sample": desc,
            "cpu_model": _cpu_model(), "host_threads": os.cpu_count()}
+    if not is_cd(cfgname):  # the oracle's effective bandwidth over B_unfused (its schedule)
+        dim, nodes, sm, nu1, nu2, dt, levels, omega = CONFIGS[cfgname]
+        ns = int(round(cunk ** (1.0 / dim))) + 2
+        lv = levels if ns == nodes else int(ns - 1).bit_length() - 1
+        b = unfused_bytes_per_step(dim, ns, lv, sm, nu1, nu2, 8 if dt == "f64" else 4)
+        out["unfused_bytes_per_step"] = b
+        out["effective_GBps"] = b / t / 1e9
     if os.environ.get("MG_BENCH_ONE_THREAD") is None:
         env = dict(os.environ, OMP_NUM_THREADS="1", MG_BENCH_ONE_THREAD="1")
         r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-leg", "--config", cfgname],
@@ -496,6 +528,7 @@ def run_mg(args):
     roofline = {
         "bound": "hbm", "kernel": dom["name"], "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "traffic": ncu_traffic(args.config, dom["name"]), "peak_source": peak_src,
+        "frac_of_nominal_8TBps": achieved / 8000.0,
         "alg_bytes_per_launch": dom["bytes"], "avg_launch_ms": dom_avg_ms,
         "share_of_step": dom["ms"] / tot if tot else None,
         "timing": ("per-kernel CUDA events on the solver stream, separate instrumented eager pass of the same "
@@ -541,6 +574,21 @@ def run_mg(args):
                "path": (f"mg_vcycle_host_batch over {ne} problems (pinned host u, f -> device, 1 cycle + norm, "
                         "u -> host; H2D / compute / D2H pipelined)")}
 
+    # ---- for the rtol configs also the whole solve to 1e-10 (time and cycle count)
+    solve = None
+    if world == 1 and not cd and args.config in ("C3-f64", "C3-f32", "C2", "C5"):
+        with torch.cuda.stream(stream):
+            S.workload_fill(u, 42, stream=stream)
+            f.zero_()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        kc, sh = S.solve(u, f, 1e-10, 40, stream=stream)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        solve = {"rtol": 1e-10, "cycles": kc, "ms": s0.elapsed_time(s1), "final_reduction": sh[-1] / sh[0],
+                 "note": "mg_solve from the W1 start (device loop): initial norm + cycles until ||r|| <= 1e-10 ||r0||"}
+
     # ---- the N>1 default workload (C5, 1025^3) on this one GPU: the 1-GPU point of the scaling curve
     c5 = None
     if world == 1 and args.config == "C3-f64" and not args.no_c5:
@@ -569,7 +617,8 @@ def run_mg(args):
             "residual_reduction_per_step": (rk / r0) ** (1.0 / (args.steps + args.warmup)) if r0 else None,
             "model_bytes_per_step": B, "model_GBps": B / (ms * 1e-3) / 1e9,
             "roofline": roofline, "kernels": breakdown, "cpu_baseline": cpu, "e2e": e2e,
-            "single_gpu_C5": c5,
+            "single_gpu_C5": c5, "solve_to_1e-10": solve,
+            "measured_bytes_per_step": ncu_cycle_bytes(args.config),
             "gpu_launches": int(round(launches * args.steps)), "gpu_launches_per_step": launches,
             "clocks": sampler.summary(),
         }

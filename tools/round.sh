@@ -10,6 +10,7 @@
 #   full:CFG   ncu --set full of CFG's level-0 3D kernels (tools/prof_solve.py) -> TAG/CFG_full.ncu-rep
 #   sanitize   compute-sanitizer memcheck/racecheck/synccheck/initcheck over tools/sanitize.py
 #   ab:CFG     bench CFG three times (A/B runs of a kernel change)  -> TAG/ab_CFG.txt
+#   bmeas:CFG  ncu DRAM bytes of one whole cycle (all kernels)      -> profiles/ncu_cycle_bytes.json
 set -u
 TAG=$1; shift
 OUT=gpurun_out/$TAG
@@ -63,6 +64,13 @@ for st in "$@"; do
       echo "full $cfg rc=$?"
       python tools/ncu_summary.py $OUT/${cfg}_full.ncu-rep > $OUT/${cfg}_full_summary.txt 2>&1
       head -40 $OUT/${cfg}_full_summary.txt ;;
+    bmeas:*)  # SURVEY §8(d) B_meas: DRAM bytes of one cycle (all kernels) -> profiles/ncu_cycle_bytes.json
+      cfg=${st#bmeas:}
+      for n in 1 2; do
+        ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
+            --log-file $OUT/${cfg}_bmeas_$n.csv python tools/prof_solve.py $cfg $n > /dev/null 2>&1
+      done
+      python tools/ncu_cycle_bytes.py $cfg $OUT/${cfg}_bmeas_1.csv $OUT/${cfg}_bmeas_2.csv ;;
     sanitize)  # compute-sanitizer (closed on this pool) then the checked build
       mkdir -p $OUT/sanitizer
       python tools/sanitize.py > $OUT/sanitizer/plain.log 2>&1; echo "sanitize plain rc=$?"
