@@ -94,3 +94,40 @@ def test_gs_lex_per_op_and_solve():
     _, k_or, hist_or = O.solve(u1, f1, 1e-10, 40)
     assert k == k_or
     np.testing.assert_allclose(hist, hist_or, rtol=1e-12)
+
+
+@pytest.mark.parametrize("omega", [1.15, 0.8])
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_sor_rb_3d_solve_split_norm(omega, dt):
+    """3D omega-RBGS through mg_solve: the residual norm is split between the last post-sweep
+    (black nodes of its output: r = f - (D v - s) from the relaxation's own stencil sum, valid for
+    any omega) and the next head (red nodes of its input).  Cycle count and history equal the
+    oracle's (norms to 1e-12: same per-node residuals, summation order only), iterate bitwise."""
+    S, O = make(3, (128, 128, 128), smoother="rbgs", omega=omega, dtype=dt)
+    u, f = wl.workload("W4", 3, (128, 128, 128), seed=21, dtype=S.np_dtype)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    rtol = 1e-10 if dt == "f64" else 1e-5
+    k, hist = S.solve(du, df, rtol, 40)
+    uo, k_or, hist_or = O.solve(u, f, rtol, 40)
+    assert k == k_or, (k, k_or)
+    assert all(abs(a / b - 1) <= 1e-12 for a, b in zip(hist, hist_or))
+    assert np.array_equal(S.to_numpy(du), uo)
+
+
+@pytest.mark.parametrize("cells,levels,dt", [((88, 88), 4, "f64"), ((88, 88), 4, "f32"), ((120, 40), 3, "f64"),
+                                             ((24, 16, 40), 3, "f64")])
+def test_coarse_tail_shared_memory_mix(cells, levels, dt):
+    """The coarse tail with its top level too large for CTA 0's shared memory (4 arrays of 89^2
+    FP64 > 200 KB) but small enough for one CTA: the level stays in global memory, the levels
+    below live in shared memory (kernels_tail.cu); also 3D grids entirely inside the tail."""
+    S, O = make(len(cells), cells, levels, "jacobi" if len(cells) == 2 else "rbgs", dtype=dt)
+    u, f = wl.workload("W4", len(cells), cells, seed=5, dtype=S.np_dtype)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    uo = u.copy()
+    for _ in range(2):
+        S.vcycle(du, df)
+        O.vcycle_inplace(uo, f)
+        assert np.array_equal(S.to_numpy(du), uo)
+    k, hist = S.solve(S.from_numpy(u), df, 0.0, 3)
+    _, k_or, hist_or = O.solve(u, f, 0.0, 3)
+    assert k == k_or and all(abs(a / b - 1) <= 1e-12 for a, b in zip(hist, hist_or) if b)
