@@ -56,9 +56,12 @@ def main():
         else:
             domc, bw = dom, f"{r['achieved']:.0f} GB/s ({b(format(r['frac'], '.3f'))})"
         out.append(f"| {name} | {b(msf)} | {b(fmt(v))} | {domc} | {bw} | {fmt(d['e2e']['value'])} | {paper} |")
-        if c == "C4":
-            out.append("| C4 one sweep per pass (`MG_NO_KFUSE=1`, `tools/kf.sh`) | 1.61 | 4.16e10 | Jacobi L0 | "
-                       "5420 GB/s (0.840) | — | — |")
+        nk = os.path.join(B, "C4-nokfuse.json")
+        if c == "C4" and os.path.exists(nk):
+            k = json.loads(open(nk).read().strip().splitlines()[-1])
+            kr = k["roofline"]
+            out.append(f"| C4 one sweep per pass (`bench.py --no-kfuse`, MG_FLAG_NO_KFUSE) | {k['ms_per_step']:.2f} | "
+                       f"{fmt(k['value'])} | Jacobi L0 | {kr['achieved']:.0f} GB/s ({kr['frac']:.3f}) | — | — |")
     p = os.path.join(ROOT, "BASELINE.md")
     s = open(p).read()
     a = s.index("| Config | ms / step | unknowns/s |")

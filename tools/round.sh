@@ -46,6 +46,8 @@ for st in "$@"; do
         timeout 600 python bench.py --config $c > $OUT/bench/$c.json 2> $OUT/bench/$c.err
         summ $c $OUT/bench/$c.json
       done
+      timeout 600 python bench.py --config C4 --no-kfuse --no-cpu --no-e2e > $OUT/bench/C4-nokfuse.json 2> $OUT/bench/C4-nokfuse.err
+      summ C4-nokfuse $OUT/bench/C4-nokfuse.json
       timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench/reference_C3-f64.json 2>&1
       tail -1 $OUT/bench/reference_C3-f64.json | cut -c1-300 ;;
     launches)
