@@ -309,54 +309,36 @@ extern "C" mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol,
   if (u == f) return fail(s, MG_ERR_INVALID, "u and f must not alias");
   cudaStream_t cs = (cudaStream_t)stream;
   const bool eager_mode = (s->cfg.flags & MG_FLAG_NO_GRAPH) || s->prof_on;
-  if (!eager_mode && !(s->cfg.flags & MG_FLAG_HOST_LOOP) && plan_loop_supported(s))
-    return plan_solve_device(s, u, f, rtol, max_cycles, cycles, history, cs);
-  if (plan_can_split(s)) {
-    // pipelined driver loop: head(k) = first sweep of cycle k+1 into the ping-pong buffer
-    // + ||f - A u_k|| of its input; tail(k) = the rest of cycle k+1.  u holds u_k
-    // whenever a norm is read, so stopping after a head is exact.
-    const bool eager = (s->cfg.flags & MG_FLAG_NO_GRAPH) || s->prof_on;
-    auto part = [&](int p) { return eager ? plan_run_part(s, p, u, f, cs) : plan_graph_part(s, p, u, f, cs); };
-    auto read = [&](double* out) -> mg_status {
-      CK(cudaMemcpyAsync(s->h_norm, s->d_norm, sizeof(double), cudaMemcpyDeviceToHost, cs));
-      const mg_status w = plan_wait(s, cs, "mg_solve: norm readback");
-      if (w != MG_OK) return w;
-      *out = *s->h_norm;
-      return MG_OK;
-    };
-    double r0 = 0.0;
-    if ((st = part(1)) != MG_OK || (st = read(&r0)) != MG_OK) return st;
-    if (history) history[0] = r0;
-    if (!std::isfinite(r0)) return fail(s, MG_ERR_NONFINITE, "initial residual norm is not finite");
-    int k = 0;
-    while (k < max_cycles) {
-      if ((st = part(2)) != MG_OK) return st;
-      k++;
-      double rk = 0.0;
-      if ((st = part(4)) != MG_OK || (st = read(&rk)) != MG_OK) return st;  // head w/o the boundary refresh
-      if (history) history[k] = rk;
-      if (!std::isfinite(rk)) {
-        if (cycles) *cycles = k;
-        return fail(s, MG_ERR_NONFINITE, "residual norm not finite after cycle %d (S:535)", k);
-      }
-      if (test_on && rk <= rtol * r0) break;
-    }
-    if (cycles) *cycles = k;
-    return MG_OK;
+  if (!(s->cfg.flags & MG_FLAG_HOST_LOOP)) {
+    if (plan_solve_in_tail(s))  // one launch for the whole solve (eager: without a graph)
+      return plan_solve_device(s, u, f, rtol, max_cycles, cycles, history, cs, eager_mode);
+    if (!eager_mode && plan_loop_supported(s)) return plan_solve_device(s, u, f, rtol, max_cycles, cycles, history, cs);
   }
+  // host-driven loop with the device loop's parts: pipelined split (plan_can_split) — head(k) =
+  // first sweep of cycle k+1 into the ping-pong buffer + ||f - A u_k|| of its input, tail(k) =
+  // the rest of cycle k+1 (u holds u_k whenever a norm is read, so stopping after a head is
+  // exact); unsplit — the norm of u_0, then per cycle the cycle and the norm of its result
+  const bool split = plan_can_split(s);
+  const bool eager = (s->cfg.flags & MG_FLAG_NO_GRAPH) || s->prof_on;
+  auto part = [&](int p) { return eager ? plan_run_part(s, p, u, f, cs) : plan_graph_part(s, p, u, f, cs); };
+  auto read = [&](double* out) -> mg_status {
+    CK(cudaMemcpyAsync(s->h_norm, s->d_norm, sizeof(double), cudaMemcpyDeviceToHost, cs));
+    const mg_status w = plan_wait(s, cs, "mg_solve: norm readback");
+    if (w != MG_OK) return w;
+    *out = *s->h_norm;
+    return MG_OK;
+  };
   double r0 = 0.0;
-  st = mg_residual_norm(s, u, f, &r0, stream);
-  if (st != MG_OK) return st;
+  if ((st = part(split ? 1 : 3)) != MG_OK || (st = read(&r0)) != MG_OK) return st;
   if (history) history[0] = r0;
   if (!std::isfinite(r0)) return fail(s, MG_ERR_NONFINITE, "initial residual norm is not finite");
   int k = 0;
   while (k < max_cycles) {
-    st = mg_vcycle(s, u, f, stream);
-    if (st != MG_OK) return st;
+    if ((st = part(split ? 2 : 5)) != MG_OK) return st;
     k++;
     double rk = 0.0;
-    st = mg_residual_norm(s, u, f, &rk, stream);
-    if (st != MG_OK) return st;
+    if (split && (st = part(4)) != MG_OK) return st;  // head w/o the boundary refresh
+    if ((st = read(&rk)) != MG_OK) return st;
     if (history) history[k] = rk;
     if (!std::isfinite(rk)) {
       if (cycles) *cycles = k;

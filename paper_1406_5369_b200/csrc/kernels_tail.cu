@@ -235,23 +235,104 @@ __device__ void prolong(const Mode& M, const LG& gf, const LG& gc, const T* e, T
   M.sync();
 }
 
-// copy every node (x <= nx, all rows and planes) of a level's array between two layouts
+// the top level's inputs into its shared-memory layout gd: every node (x <= nx, all rows and
+// planes) of f, and of u into both U and Tt (with_u); eight elements per thread in flight (a
+// warp-per-row copy waited an L2 round trip per element: measured 9.7 us of C1's cycle)
 template <typename T>
-__device__ void copy_all(const Mode& M, const LG& gs, const T* src, const LG& gd, T* dst) {
-  if (!M.active()) return;
+__device__ void copy_in(const LG& gs, const T* u, const T* f, const LG& gd, T* U, T* Tt, T* F, bool with_u) {
+  constexpr int B = 8;
   const int nx1 = gs.nx + 1;
-  const int nrows = gs.rows * gs.planes;
-  for (int row = M.wstart(); row < nrows; row += M.wstride()) {
-    const int pl = row / gs.rows, j = row - pl * gs.rows;
-    const T* a = src + pl * gs.sz + j * gs.sy;
-    T* b = dst + pl * gd.sz + j * gd.sy;
-    for (int i = threadIdx.x & 31; i < nx1; i += 32) b[i] = a[i];
+  const int n = nx1 * gs.rows * gs.planes;
+  for (int q0 = threadIdx.x; q0 < n; q0 += B * NTT) {
+    T vu[B], vf[B];
+    int pd[B];
+#pragma unroll
+    for (int k = 0; k < B; k++) {
+      const int q = q0 + k * NTT;
+      const int row = q / nx1, i = q - row * nx1;
+      const int pl = row / gs.rows, j = row - pl * gs.rows;
+      const int ps = pl * gs.sz + j * gs.sy + i;
+      pd[k] = pl * gd.sz + j * gd.sy + i;
+      if (q < n) {
+        vf[k] = f[ps];
+        if (with_u) vu[k] = u[ps];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < B; k++)
+      if (q0 + k * NTT < n) {
+        F[pd[k]] = vf[k];
+        if (with_u) {
+          U[pd[k]] = vu[k];
+          Tt[pd[k]] = vu[k];
+        }
+      }
   }
 }
 // interior nodes only
 template <typename T, int DIM>
 __device__ void copy_interior(const Mode& M, const LG& gs, const T* src, const LG& gd, T* dst) {
   for_rows<DIM>(M, gs, -1, [&](int i, int j, int pl, int p) { dst[lin(gd, i, j, pl)] = src[p]; });
+}
+
+// a / b correctly rounded (bitwise __ddiv_rn) from y = RN(1/b), without div.rn's reciprocal
+// refinement on the critical path (a dependent div.rn measured 440 cycles on this GPU, the
+// coarse substitutions of C1 are 18 of them in a chain): q = RN(a y) with one Markstein
+// correction, accepted only when the exact remainder a - b q (exact for a faithful q) puts
+// a / b strictly inside q's rounding interval — half an ulp each side, a quarter below a power
+// of two — else div.rn.  An accepted q is therefore RN(a / b) whatever y was.
+__device__ __forceinline__ double div_rn_via(double a, double b, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double q = __fma_rn(__fma_rn(-b, q0, a), y, q0);
+  const double r = __fma_rn(-b, q, a);
+  const long long bits = __double_as_longlong(q);
+  const int e = (int)((bits >> 52) & 0x7ff);
+  if (e > 60 && e < 2040) {
+    const double hu = __longlong_as_double((long long)(e - 53) << 52);  // half an ulp of q
+    const bool below = (r < 0.0) != (b < 0.0);                         // a / b < q
+    const bool pow2 = (bits & 0xfffffffffffffll) == 0;
+    const double h = __dmul_rn(below && pow2 ? 0.5 * hu : hu, fabs(b));
+    if (h > 0x1p-960 && fabs(r) < h) return q;
+  }
+  return __ddiv_rn(a, b);
+}
+
+// ||f - A u|| of a level into *P.norm_out: FP64 sum of squares per thread in for_rows order,
+// warp shuffles, the CTA's warps in order, then (cluster mode) the CTAs in rank order — a fixed
+// order for a given launch shape (k_tail's norm-only and fused uses share it)
+template <typename T, int DIM>
+__device__ double tail_norm(const Mode& M, const LG& g, const Coef<T>& c, const T* u, const T* f,
+                            const TailParams<T>& P) {
+  if (!M.active()) return 0.0;
+  double acc = 0.0;
+  for_rows<DIM>(M, g, -1, [&](int, int, int, int p) {
+    const double r = (double)pres<T, DIM>(u, p, g, c, f[p]);
+    acc = __dadd_rn(acc, __dmul_rn(r, r));
+  });
+  __shared__ double wsum[WPC];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < WPC; w++) t = __dadd_rn(t, wsum[w]);
+  if (M.solo) {
+    if (threadIdx.x == 0) {
+      t = __dsqrt_rn(t);
+      if (P.norm_out) *P.norm_out = t;
+    }
+    return t;  // (thread 0 of CTA 0)
+  }
+  if (threadIdx.x == 0) P.nscratch[blockIdx.x] = t;
+  cluster_sync();
+  double sum = 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int b = 0; b < (int)gridDim.x; b++) sum = __dadd_rn(sum, P.nscratch[b]);
+    sum = __dsqrt_rn(sum);
+    if (P.norm_out) *P.norm_out = sum;
+  }
+  return sum;
 }
 
 template <typename T, int DIM>
@@ -271,29 +352,65 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   auto Tt = [&](int k) { return k >= P.smem_from ? sarr(k, 1) : P.t[k]; };
   auto F = [&](int k) { return k >= P.smem_from ? sarr(k, 2) : P.f[k]; };
   auto R = [&](int k) { return k >= P.smem_from ? sarr(k, 3) : P.r[k]; };
-  if (P.smem_from < P.nl && blockIdx.x == 0) {
-    // zero the shared-memory levels (boundaries, residual borders, coarse guesses), then the
-    // top level's inputs when it lives there: u (also into t: the Jacobi partner's Dirichlet
-    // boundary) and f
-    const unsigned char* end = tsm + P.smem_bytes;
-    for (uint4* q = reinterpret_cast<uint4*>(tsm + P.soff[P.smem_from]) + threadIdx.x;
-         reinterpret_cast<const unsigned char*>(q) < end; q += NTT)
-      *q = make_uint4(0u, 0u, 0u, 0u);
-    __syncthreads();
-    if (sm_lv0) {
-      const Mode M0{true};
-      const LG g0 = lg_of(P.g[0]), s0 = G(0);
-      if (!P.zero_first) {
-        copy_all(M0, g0, (const T*)P.u[0], s0, U(0));
-        copy_all(M0, g0, (const T*)P.u[0], s0, Tt(0));
-      }
-      copy_all(M0, g0, (const T*)P.f[0], s0, F(0));
-      __syncthreads();
-    }
+  if (P.norm_only) {
+    tail_norm<T, DIM>(mode(0), lg_of(P.g[0]), P.c[0], P.u[0], P.f[0], P);
+    return;
   }
-  // ---- descend
+  if (blockIdx.x == 0 && (P.smem_from < P.nl || P.chol_off >= 0)) {
+    // CTA 0's shared memory: the top level's inputs when it lives there (u, also into t: the
+    // Jacobi partner's Dirichlet boundary; f), the coarse factor, zeros everywhere else in the
+    // shared-memory levels (boundaries, residual borders, coarse guesses); one barrier
+    auto zero = [&](const unsigned char* a, const unsigned char* b) {
+      for (uint4* q = reinterpret_cast<uint4*>(const_cast<unsigned char*>(a)) + threadIdx.x;
+           reinterpret_cast<const unsigned char*>(q) < b; q += NTT)
+        *q = make_uint4(0u, 0u, 0u, 0u);
+    };
+    if (P.chol_off >= 0) {
+      double* Ls = reinterpret_cast<double*>(tsm + P.chol_off);
+      for (int q = threadIdx.x; q < P.m * P.m; q += NTT) Ls[q] = P.chol[q];
+    }
+    if (P.y_off >= 0) {  // reciprocals of the factor's diagonal behind y (div_rn_via)
+      double* rd = reinterpret_cast<double*>(tsm + P.y_off) + P.m;
+      for (int i = threadIdx.x; i < P.m; i += NTT) rd[i] = __drcp_rn(P.chol[(long long)i * P.m + i]);
+    }
+    if (P.smem_from < P.nl) {
+      const unsigned char* end = tsm + P.smem_bytes;
+      if (sm_lv0) {
+        copy_in<T>(lg_of(P.g[0]), P.u[0], P.f[0], G(0), U(0), Tt(0), F(0), !P.zero_first);
+        const unsigned char* f0 = reinterpret_cast<const unsigned char*>(F(0));
+        if (P.zero_first) zero(tsm + P.soff[0], f0);  // u and t of the zero guess
+        zero(reinterpret_cast<const unsigned char*>(R(0)), end);
+      } else {
+        zero(tsm + P.soff[P.smem_from], end);
+      }
+    }
+    __syncthreads();
+  }
+  // ---- P.solve: the driver loop of mg_solve in this launch — the level arrays stay
+  // where they are between cycles (the top level's iterate in cur[0]); else one cycle
   T* cur[kTailMax];
-  for (int k = 0; k < P.nl; k++) cur[k] = U(k);
+  cur[0] = U(0);
+  __shared__ int s_flag;
+  auto bcast = [&](int v) -> int {  // thread 0 of CTA 0's decision to every thread
+    if (gridDim.x == 1) {
+      if (threadIdx.x == 0) s_flag = v;
+      __syncthreads();
+      return s_flag;
+    }
+    volatile int* g = reinterpret_cast<volatile int*>(P.nscratch + gridDim.x);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *g = v;
+    cluster_sync();
+    return *g;
+  };
+  if (P.solve) {
+    const double r0 = tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
+    int go = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) go = loop_begin(r0, P.solve) ? 1 : 0;
+    if (!bcast(go)) return;  // u unchanged
+  }
+  for (;;) {
+  // ---- descend
+  for (int k = 1; k < P.nl; k++) cur[k] = U(k);
   for (int k = 0; k < P.nl - 1; k++) {
     const LG g = G(k);
     const Coef<T> c = P.c[k];
@@ -341,11 +458,34 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
         // same loop order as k_coarse_direct / the oracle
         const int jlo = DIM == 3 ? 1 : 0, jhi = DIM == 3 ? g.ny - 1 : 0;
         const int m = P.m;
-        const double* L = P.chol;
+        // the factor and the vector in shared memory: the substitutions are serial chains of
+        // dependent loads (a global y costs an L2 round trip per step: measured 8.5 us at m = 9)
+        const double* L = P.chol_off >= 0 ? reinterpret_cast<const double*>(tsm + P.chol_off) : P.chol;
         const T* fk = F(k);
         if (m == 1) {
           const int p = lin(g, 1, jlo, g.p_lo);
-          cur[k][p] = (T)__ddiv_rn((double)fk[p], P.D_coarse);
+          cur[k][p] = (T)div_rn_via((double)fk[p], P.D_coarse, P.rD_coarse);
+        } else if (P.y_off >= 0) {  // y and the diagonal's reciprocals (the prologue's) in shared memory
+          double* y = reinterpret_cast<double*>(tsm + P.y_off);
+          const double* rd = y + m;
+          int q = 0;
+          for (int pl = g.p_lo; pl < g.p_hi; pl++)
+            for (int j = jlo; j <= jhi; j++)
+              for (int i = 1; i < g.nx; i++) y[q++] = (double)fk[lin(g, i, j, pl)];
+          for (int i = 0; i < m; i++) {
+            double sacc = y[i];
+            for (int kk = 0; kk < i; kk++) sacc = __dsub_rn(sacc, __dmul_rn(L[(long long)i * m + kk], y[kk]));
+            y[i] = div_rn_via(sacc, L[(long long)i * m + i], rd[i]);
+          }
+          for (int i = m - 1; i >= 0; i--) {
+            double sacc = y[i];
+            for (int kk = i + 1; kk < m; kk++) sacc = __dsub_rn(sacc, __dmul_rn(L[(long long)kk * m + i], y[kk]));
+            y[i] = div_rn_via(sacc, L[(long long)i * m + i], rd[i]);
+          }
+          q = 0;
+          for (int pl = g.p_lo; pl < g.p_hi; pl++)
+            for (int j = jlo; j <= jhi; j++)
+              for (int i = 1; i < g.nx; i++) cur[k][lin(g, i, j, pl)] = (T)y[q++];
         } else {
           double* y = P.work;
           int q = 0;
@@ -394,35 +534,45 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
     for (int s = 0; s < P.nu2; s++)
       cur[k] = sweep<T, DIM>(M, g, c, P.rbgs, cur[k], cur[k] == U(k) ? Tt(k) : U(k), F(k));
   }
+  if (!P.solve) break;
+  const double rk = tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
+  int go = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) go = loop_step(rk, P.solve) ? 1 : 0;
+  if (!bcast(go)) break;
+  }  // for (;;)
   // result of the top tail level in u[0]
   if (sm_lv0 || cur[0] != P.u[0]) copy_interior<T, DIM>(mode(0), G(0), (const T*)cur[0], lg_of(P.g[0]), P.u[0]);
+  if (P.norm_out && !P.solve) {
+    const double rk = tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
+    if (P.loop && blockIdx.x == 0 && threadIdx.x == 0) loop_check(rk, P.loop, P.loop_h);
+  }
 }
 
 }  // namespace
 
 template <typename T>
-cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
+void tail_prepare(TailParams<T>& q) {
   // 16 CTAs (non-portable) where allowed, else the portable 8; probed once per device (the
   // non-portable opt-in and the shared-memory opt-in are per-device function attributes)
   const int cluster = per_device_once((const void*)k_tail<T, 3>, [] {
-    cudaFuncSetAttribute(k_tail<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax);
-    cudaFuncSetAttribute(k_tail<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemMax);
+    cudaFuncSetAttribute(k_tail<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemCap);
+    cudaFuncSetAttribute(k_tail<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTailSmemCap);
     int c = 8;
     if (cudaFuncSetAttribute(k_tail<T, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
         cudaFuncSetAttribute(k_tail<T, 3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
-      cudaLaunchConfig_t q = {};
-      q.gridDim = dim3(16);
-      q.blockDim = dim3(NTT);
-      q.dynamicSmemBytes = kTailSmemMax;
+      cudaLaunchConfig_t c16 = {};
+      c16.gridDim = dim3(16);
+      c16.blockDim = dim3(NTT);
+      c16.dynamicSmemBytes = kTailSmemCap;
       cudaLaunchAttribute a;
       a.id = cudaLaunchAttributeClusterDimension;
       a.val.clusterDim.x = 16;
       a.val.clusterDim.y = 1;
       a.val.clusterDim.z = 1;
-      q.attrs = &a;
-      q.numAttrs = 1;
+      c16.attrs = &a;
+      c16.numAttrs = 1;
       int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, k_tail<T, 3>, &q) == cudaSuccess && n >= 1) c = 16;
+      if (cudaOccupancyMaxActiveClusters(&n, k_tail<T, 3>, &c16) == cudaSuccess && n >= 1) c = 16;
     }
     cudaGetLastError();
     return c;
@@ -431,25 +581,25 @@ cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
     return (long long)(g.nx - 1) * (g.three_d ? g.ny - 1 : 1) * (g.p_hi - g.p_lo);
   };
   // tiny tails (a few thousand nodes, e.g. the whole 65^2 C1 hierarchy) run on one CTA
-  const int csize = interior(p.g[0]) <= 8192 ? 1 : cluster;
+  q.csize = interior(q.g[0]) <= 8192 ? 1 : cluster;
   // levels from solo_from on run on CTA 0 alone with block barriers (all of them on one CTA)
   // measured (C2, C3, C4): 2048 interior nodes in 3D (a 17^3 level is faster on the cluster),
   // 8192 in 2D (a 65^2 level is faster on CTA 0 with its arrays in shared memory)
-  const long long solo_max = p.g[0].three_d ? 2048 : 8192;
-  TailParams<T> q = p;
-  q.solo_from = p.nl;
-  for (int k = 0; k < p.nl; k++)
-    if (csize == 1 || interior(p.g[k]) <= solo_max) {
+  const long long solo_max = q.g[0].three_d ? 2048 : 8192;
+  q.solo_from = q.nl;
+  for (int k = 0; k < q.nl; k++)
+    if (q.csize == 1 || interior(q.g[k]) <= solo_max) {
       q.solo_from = k;
       break;
     }
   // the solo levels' arrays (u, t, f, r) in CTA 0's shared memory, compact layout: the coarsest
   // levels that fit (a solo level above them stays in global memory)
-  auto words = [](const Geom& g) { return ((long long)g.planes * g.pstride * (long long)sizeof(T) + 15) / 16 * 16; };
-  q.smem_from = p.nl;
+  auto bytes16 = [](long long b) { return (b + 15) / 16 * 16; };
+  auto words = [&](const Geom& g) { return bytes16((long long)g.planes * g.pstride * (long long)sizeof(T)); };
+  q.smem_from = q.nl;
   long long total = 0;
-  for (int k = p.nl - 1; k >= q.solo_from; k--) {
-    Geom g = p.g[k];
+  for (int k = q.nl - 1; k >= q.solo_from; k--) {
+    Geom g = q.g[k];
     g.pitch = g.nx + 1;
     g.pstride = g.three_d ? (long long)(g.ny + 1) * (g.nx + 1) : g.pitch;
     if (total + 4 * words(g) > kTailSmemMax) break;
@@ -458,26 +608,46 @@ cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st) {
     q.smem_from = k;
   }
   long long off = 0;
-  for (int k = q.smem_from; k < p.nl; k++) {
+  for (int k = q.smem_from; k < q.nl; k++) {
     q.soff[k] = (int)off;
     off += 4 * words(q.gs[k]);
   }
   q.smem_bytes = (int)off;
+  // direct coarsest solve: its vector and (when it fits) the factor behind the levels
+  q.chol_off = q.y_off = -1;
+  if (!q.sweeps && q.m > 1) {
+    const long long lb = bytes16((long long)q.m * q.m * 8), yb = bytes16((long long)q.m * 16);  // y, 1 / L_ii
+    if (off + lb + yb <= kTailSmemCap) {
+      q.chol_off = (int)off;
+      off += lb;
+    }
+    if (off + yb <= kTailSmemCap) {
+      q.y_off = (int)off;
+      off += yb;
+    }
+  }
+  q.smem_total = (int)off;
+}
+
+template <typename T>
+cudaError_t launch_tail(const TailParams<T>& q, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(csize);
+  cfg.gridDim = dim3(q.csize);
   cfg.blockDim = dim3(NTT);
   cfg.stream = st;
-  cfg.dynamicSmemBytes = q.smem_bytes;
+  cfg.dynamicSmemBytes = q.norm_only ? 0 : q.smem_total;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = csize;
+  attr.val.clusterDim.x = q.csize;
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
-  cfg.numAttrs = csize > 1 ? 1 : 0;
-  return p.g[0].three_d ? cudaLaunchKernelEx(&cfg, k_tail<T, 3>, q) : cudaLaunchKernelEx(&cfg, k_tail<T, 2>, q);
+  cfg.numAttrs = q.csize > 1 ? 1 : 0;
+  return q.g[0].three_d ? cudaLaunchKernelEx(&cfg, k_tail<T, 3>, q) : cudaLaunchKernelEx(&cfg, k_tail<T, 2>, q);
 }
 
+template void tail_prepare<double>(TailParams<double>&);
+template void tail_prepare<float>(TailParams<float>&);
 template cudaError_t launch_tail<double>(const TailParams<double>&, cudaStream_t);
 template cudaError_t launch_tail<float>(const TailParams<float>&, cudaStream_t);
 

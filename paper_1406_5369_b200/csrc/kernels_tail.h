@@ -1,11 +1,13 @@
 // kernels_tail.h — single-CTA coarse tail of the V-cycle (kernels_tail.cu).
 #pragma once
 #include "mg_common.cuh"
+#include "loop_state.cuh"
 
 namespace mg {
 
 constexpr int kTailMax = 12;  // levels handled by one tail launch
 constexpr int kTailSmemMax = 200 * 1024;  // CTA 0's shared memory for the solo levels' arrays
+constexpr int kTailSmemCap = 226 * 1024;  // all dynamic shared memory (+ the coarse factor, below)
 
 template <typename T>
 struct TailParams {
@@ -18,12 +20,27 @@ struct TailParams {
   int solo_from;   // levels >= solo_from run on CTA 0 alone (set by launch_tail)
   int smem_from;   // levels >= smem_from (all solo) keep u, t, f, r in CTA 0's shared memory (launch_tail)
   int smem_bytes;  // their dynamic shared memory
+  int smem_total;  // all dynamic shared memory (levels, coarse factor and vector)
   int soff[kTailMax];   // byte offset of level k's four arrays
   Geom gs[kTailMax];    // level k's compact shared-memory layout (pitch nx+1, no padding)
+  int csize;       // CTAs (one cluster; set by tail_prepare)
   int m;           // coarsest unknowns (direct)
   double D_coarse;
+  double rD_coarse;  // RN(1 / D_coarse) (m = 1)
   const double* chol;
   double* work;
+  int chol_off;    // direct solve: byte offset of the staged factor in shared memory, -1: read global
+  int y_off;       // ... and of its right-hand side / solution vector (m doubles) + 1 / L_ii (m)
+  // the residual norm ||f - A u|| of the top tail level when it is level 0:
+  // norm_only = 1 evaluates it for (u[0], f[0]) without a cycle; otherwise, with norm_out set,
+  // of the cycle's result.  Both run the same distribution and reduction order, so the
+  // solve's history is bitwise that of mg_residual_norm.
+  int norm_only;
+  double* norm_out;
+  double* nscratch;  // csize doubles (per-CTA sums)
+  LoopState* loop;   // with norm_out inside the device loop's body: also the per-cycle check
+  LoopState* solve;  // lt = 0: the whole driver loop in this launch (r0, cycles, norms, stop test)
+  cudaGraphConditionalHandle loop_h;
   Geom g[kTailMax];
   Coef<T> c[kTailMax];
   T* u[kTailMax];
@@ -32,6 +49,10 @@ struct TailParams {
   T* f[kTailMax];
 };
 
+// work distribution and shared-memory layout (solo_from, smem_from, soff, gs, smem_bytes,
+// csize, chol_off, y_off) from the levels: call once before launch_tail
+template <typename T>
+void tail_prepare(TailParams<T>& p);
 template <typename T>
 cudaError_t launch_tail(const TailParams<T>& p, cudaStream_t st);
 

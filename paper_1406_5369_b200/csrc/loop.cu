@@ -20,24 +20,11 @@
 namespace mg {
 
 __global__ void k_loop_init(const double* __restrict__ d_norm, LoopState* st, cudaGraphConditionalHandle h) {
-  const double r0 = *d_norm;
-  const bool fin = isfinite(r0);
-  st->r0 = r0;
-  st->k = 0;
-  st->status = fin ? 0 : 1;
-  if (st->hist) st->hist[0] = r0;
-  cudaGraphSetConditional(h, (fin && st->max > 0) ? 1u : 0u);
+  cudaGraphSetConditional(h, loop_begin(*d_norm, st) ? 1u : 0u);
 }
 
 __global__ void k_loop_check(const double* __restrict__ d_norm, LoopState* st, cudaGraphConditionalHandle h) {
-  const int k = st->k + 1;
-  const double rk = *d_norm;
-  const bool fin = isfinite(rk);
-  st->k = k;
-  if (st->hist) st->hist[k] = rk;
-  if (!fin) st->status = 2;
-  const bool done = !fin || k >= st->max || (st->rtol >= 0.0 && rk <= st->rtol * st->r0);  // rtol < 0: no test
-  cudaGraphSetConditional(h, done ? 0u : 1u);
+  loop_check(*d_norm, st, h);
 }
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
@@ -48,7 +35,7 @@ static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
 
 bool plan_loop_supported(mg_solver* s) { return !comm_active(s); }
 
-// Capture: [head | norm] -> init -> WHILE { [tail + head | cycle + norm] -> check }.
+// Capture: [head | norm] -> init -> WHILE { [tail + head | cycle + norm (part 5)] -> check }.
 static mg_status build_loop_graph(mg_solver* s, void* u, const void* f, cudaGraphExec_t* out) {
   const bool split = plan_can_split(s);
   cudaStream_t cs = s->cap_stream;
@@ -94,9 +81,14 @@ static mg_status build_loop_graph(mg_solver* s, void* u, const void* f, cudaGrap
   if ((e = cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) !=
       cudaSuccess)
     return abort_capture(cuda_fail(s, e, "cudaStreamBeginCaptureToGraph"));
-  mg_status rb = split ? plan_run_part(s, 2, u, f, bs) : plan_run_part(s, 0, u, f, bs);
-  if (rb == MG_OK) rb = split ? plan_run_part(s, 4, u, f, bs) : plan_run_part(s, 3, u, f, bs);  // 4: no refresh
-  if (rb == MG_OK) {
+  // 4: no refresh; 5: the cycle and its norm (one launch, with the check, for a whole-cycle tail)
+  s->cap_loop = true;
+  s->cap_h = h;
+  s->cap_loop_fused = false;
+  mg_status rb = split ? plan_run_part(s, 2, u, f, bs) : plan_run_part(s, 5, u, f, bs);
+  if (rb == MG_OK && split) rb = plan_run_part(s, 4, u, f, bs);
+  s->cap_loop = false;
+  if (rb == MG_OK && !s->cap_loop_fused) {
     k_loop_check<<<1, 1, 0, bs>>>(s->d_norm, s->d_loop, h);
     if ((e = cudaGetLastError()) != cudaSuccess) rb = cuda_fail(s, e, "k_loop_check");
   }
@@ -116,18 +108,24 @@ static mg_status build_loop_graph(mg_solver* s, void* u, const void* f, cudaGrap
 }
 
 mg_status plan_solve_device(mg_solver* s, void* u, const void* f, double rtol, int32_t max_cycles, int32_t* cycles,
-                            double* history, cudaStream_t st) {
-  auto key = std::make_tuple(u, f, 16);
-  auto it = s->graphs.find(key);
-  if (it == s->graphs.end()) {
-    cudaGraphExec_t exec;
-    mg_status r = build_loop_graph(s, u, f, &exec);
-    if (r != MG_OK) return r;
-    if (s->graphs.size() >= 16) {
-      cudaGraphExecDestroy(s->graphs.begin()->second);
-      s->graphs.erase(s->graphs.begin());
+                            double* history, cudaStream_t st, bool eager) {
+  // a whole-cycle tail grid runs the loop inside one kernel (plan_solve_in_tail, part 6):
+  // launched directly when eager, else as a one-launch graph; other grids: the WHILE graph
+  const bool in_tail = plan_solve_in_tail(s);
+  auto it = s->graphs.end();
+  if (!in_tail) {
+    auto key = std::make_tuple(u, f, 16);
+    it = s->graphs.find(key);
+    if (it == s->graphs.end()) {
+      cudaGraphExec_t exec;
+      mg_status r = build_loop_graph(s, u, f, &exec);
+      if (r != MG_OK) return r;
+      if (s->graphs.size() >= 16) {
+        cudaGraphExecDestroy(s->graphs.begin()->second);
+        s->graphs.erase(s->graphs.begin());
+      }
+      it = s->graphs.emplace(key, exec).first;
     }
-    it = s->graphs.emplace(key, exec).first;
   }
   if (history && (int64_t)max_cycles + 1 > s->hist_cap) {
     cudaFree(s->d_hist);
@@ -147,7 +145,13 @@ mg_status plan_solve_device(mg_solver* s, void* u, const void* f, double rtol, i
   hl->k = 0;
   hl->status = 0;
   cudaError_t e = cudaMemcpyAsync(s->d_loop, hl, sizeof(LoopState), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaGraphLaunch(it->second, st);
+  if (e != cudaSuccess) return cuda_fail(s, e, "solve");
+  if (in_tail) {
+    const mg_status r = eager ? plan_run_part(s, 6, u, f, st) : plan_graph_part(s, 6, u, f, st);
+    if (r != MG_OK) return r;
+  } else {
+    e = cudaGraphLaunch(it->second, st);
+  }
   if (e == cudaSuccess) e = cudaMemcpyAsync(hl, s->d_loop, sizeof(LoopState), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(s, e, "solve");

@@ -57,6 +57,9 @@ enum Kind {
   K_CD_JACOBI_K,
   K_CD_JACOBI_K_NORM,
   K_SWEEP_RR_K,
+  K_TAIL_NORM,
+  K_TAIL_NORM_FUSED,
+  K_TAIL_SOLVE,
   K_NUM
 };
 static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residual",     "restrict",
@@ -69,7 +72,8 @@ static const char* kKindName[K_NUM] = {"jacobi",        "rbgs_colour",   "residu
                                        "cd_fas_rhs",    "cd_prolong",    "cd_norm_partial", "cd_residual",
                                        "cd_copy",       "cd_tail",       "gs_lex_plane",  "jacobi_pm_xK",
                                        "jacobi_pm_xK+norm", "prolong+jacobi_xK",
-                                       "cd_jacobi_xK",  "cd_jacobi_xK+norm", "jacobi_xK+resid_restrict"};
+                                       "cd_jacobi_xK",  "cd_jacobi_xK+norm", "jacobi_xK+resid_restrict",
+                                       "tail_norm",     "coarse_tail+norm", "coarse_tail_solve"};
 
 static mg_status cuda_fail(mg_solver* s, cudaError_t e, const char* what) {
   char buf[384];
@@ -153,6 +157,7 @@ static mg_status alloc_common(mg_solver* s, int np);
 
 // norm partials / scalar, capture streams, driver-loop state (both problems)
 static mg_status alloc_common(mg_solver* s, int np) {
+  if (np < 64) np = 64;  // also the coarse tail's scratch (per-CTA norm sums + its loop flag)
   s->n_partial_cap = np;
   if (cudaMalloc(&s->d_partial, sizeof(double) * np) != cudaSuccess ||
       cudaMalloc(&s->d_norm, sizeof(double)) != cudaSuccess ||
@@ -413,7 +418,45 @@ struct Exec {
     return s->L;
   }
 
-  mg_status run_tail(int lt, T* u_top, const T* f_top) {
+  // the coarse tail (levels lt..L-1) in one launch; norm_out: also ||f - A u|| of the result
+  // (lt = 0); norm_only: only that norm of (u_top, f_top), no cycle
+  mg_status run_tail(int lt, T* u_top, const T* f_top, double* norm_out = nullptr, bool norm_only = false) {
+    TailParams<T> P = tail_params(lt, u_top, f_top);
+    P.norm_out = norm_out;
+    P.norm_only = norm_only ? 1 : 0;
+    P.nscratch = s->d_partial;
+    if (norm_out && !norm_only && s->cap_loop) {  // the device loop's per-cycle check rides along
+      P.loop = s->d_loop;
+      P.loop_h = s->cap_h;
+      s->cap_loop_fused = true;
+    }
+    if (norm_only) return launch(s, st, K_TAIL_NORM, 0, 2 * w(0), [&] { return launch_tail<T>(P, st); });
+    // a whole cycle on one CTA with level 0 in shared memory (the kernel copies u into both
+    // ping-pong arrays there) needs no boundary copy into the global partner t
+    if (lt == 0 && P.smem_from != 0) {
+      const mg_status r = cycle_start(u_top, f_top);
+      if (r != MG_OK) return r;
+    }
+    double bytes = 0;
+    for (int k = 0; k < P.nl; k++) bytes += w(lt + k) * (3.0 * (P.nu1 + P.nu2) + 6.0);
+    return launch(s, st, norm_out ? K_TAIL_NORM_FUSED : K_TAIL, lt, bytes, [&] { return launch_tail<T>(P, st); });
+  }
+  // mg_solve on a whole-cycle tail grid (tail_level() = 0): r0, the cycles, their norms and
+  // the stop test in ONE launch, the hierarchy resident in shared memory across cycles; the
+  // loop state (rtol, max, history, results) in s->d_loop as for the graph loop
+  mg_status solve_tail(T* u, const T* f) {
+    TailParams<T> P = tail_params(0, u, f);
+    P.solve = s->d_loop;
+    P.nscratch = s->d_partial;
+    if (P.smem_from != 0) {
+      const mg_status r = cycle_start(u, f);
+      if (r != MG_OK) return r;
+    }
+    double bytes = 0;
+    for (int k = 0; k < P.nl; k++) bytes += w(k) * (3.0 * (P.nu1 + P.nu2) + 6.0);
+    return launch(s, st, K_TAIL_SOLVE, 0, bytes, [&] { return launch_tail<T>(P, st); });
+  }
+  TailParams<T> tail_params(int lt, T* u_top, const T* f_top) {
     TailParams<T> P{};
     P.nl = s->L - lt;
     P.rbgs = s->cfg.smoother == MG_RBGS ? 1 : (s->cfg.smoother == MG_GS_LEX ? 2 : 0);
@@ -424,6 +467,7 @@ struct Exec {
     P.zero_first = lt > 0;
     P.m = s->m_coarse;
     P.D_coarse = s->lv[s->L - 1].D;
+    P.rD_coarse = 1.0 / P.D_coarse;  // IEEE division: RN(1 / D)
     P.chol = s->d_chol;
     P.work = s->d_work;
     for (int k = 0; k < P.nl; k++) {
@@ -435,9 +479,8 @@ struct Exec {
       P.t[k] = (T*)L.t;
       P.r[k] = (T*)L.r;
     }
-    double bytes = 0;
-    for (int k = 0; k < P.nl; k++) bytes += w(lt + k) * (3.0 * (P.nu1 + P.nu2) + 6.0);
-    return launch(s, st, K_TAIL, lt, bytes, [&] { return launch_tail<T>(P, st); });
+    tail_prepare<T>(P);
+    return P;
   }
 
 
@@ -715,13 +758,23 @@ struct Exec {
   int head_sweeps() const { return kfusable(0) ? first_k(0, s->cfg.nu1) : 1; }
 
   mg_status vcycle(T* u0, const T* f0) { return vcycle_impl(u0, f0, false); }
+  // a cycle and the residual norm of its result into out_dev: one launch when the whole
+  // cycle is the tail (C1-sized grids), else the cycle followed by norm()
+  mg_status cycle_norm(T* u0, const T* f0, double* out_dev) {
+    if (tail_level() == 0) return vcycle_impl(u0, f0, false, out_dev);
+    const mg_status r = vcycle_impl(u0, f0, false);
+    return r != MG_OK ? r : norm(0, u0, f0, out_dev);
+  }
   mg_status tail(T* u0, const T* f0) { return vcycle_impl(u0, f0, true); }
 
   // after_head: the head already ran (first level-0 sweep result is in t0)
-  mg_status vcycle_impl(T* u0, const T* f0, bool after_head) {
+  // norm_out (lt = 0 only): the whole-cycle tail also writes ||f - A u|| of its result there
+  mg_status vcycle_impl(T* u0, const T* f0, bool after_head, double* norm_out = nullptr) {
     const int Lv = s->L;
     std::vector<T*> cur(Lv), oth(Lv);
     mg_status r;
+    const int lt = tail_level();
+    if (lt == 0) return run_tail(0, u0, f0, norm_out);  // small grid: the whole cycle in one launch
     if (!after_head && (r = cycle_start(u0, f0)) != MG_OK) return r;
     for (int l = 0; l < Lv; l++) {
       cur[l] = l == 0 ? u0 : (T*)s->lv[l].u;
@@ -729,8 +782,6 @@ struct Exec {
     }
     if (after_head) std::swap(cur[0], oth[0]);
     const bool bnorm = after_head && split_norm();  // this tail writes the split norm's black partials
-    const int lt = tail_level();
-    if (lt == 0) return run_tail(0, u0, f0);  // small grid: the whole cycle in one launch
     if (Lv == 1) {
       // single-level hierarchy: solve in correction form (honours Dirichlet data)
       if (s->cfg.coarse == MG_COARSE_SWEEPS) {
@@ -885,6 +936,9 @@ struct Exec {
 
   mg_status norm(int l, const T* u, const T* f, double* out_dev) {
     const Level& L = s->lv[l];
+    // whole-cycle tails evaluate the norm with the tail's own distribution and order (the
+    // fused norm of cycle_norm is then bitwise this one)
+    if (l == 0 && tail_level() == 0) return run_tail(0, const_cast<T*>(u), f, out_dev, true);
     int np = norm_num_partials<T>(L.g);
     const bool pml = pm(l);
     // slabs: the residual of the owned face planes reads the neighbours' planes, and the
@@ -1244,6 +1298,10 @@ static mg_status cd_run_part_T(mg_solver* s, int part, T* u, const T* f, cudaStr
     case 4: return x.head(u, f, s->d_norm);
     case 2: return x.vcycle(u, f, true, true);
     case 3: return x.norm(0, u, f, s->d_norm);
+    case 5: {
+      const mg_status r = x.vcycle(u, f);
+      return r != MG_OK ? r : x.norm(0, u, f, s->d_norm);
+    }
     default: return x.vcycle(u, f);
   }
 }
@@ -1255,13 +1313,17 @@ static mg_status cd_run_part(mg_solver* s, int part, void* u, const void* f, cud
 // ---------------------------------------------------------------- entry points
 // part: 0 whole cycle, 1 head (first sweep + norm of the input into d_norm), 2 tail,
 // 3 norm of (u, f) into d_norm, 4 head of a later cycle of the same solve (no refresh of the
-// ping-pong partner's boundary or of f's halo planes)
+// ping-pong partner's boundary or of f's halo planes), 5 whole cycle + norm of its result
+// into d_norm (the unsplit driver loop's body), 6 the whole driver loop in one launch
+// (plan_solve_in_tail; loop state in d_loop)
 template <typename T>
 static mg_status run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st) {
   Exec<T> x{s, st};
   if (part == 1 || part == 4) return x.head((T*)u, (const T*)f, s->d_norm, part == 1);
   if (part == 2) return x.tail((T*)u, (const T*)f);
   if (part == 3) return x.norm(0, (const T*)u, (const T*)f, s->d_norm);
+  if (part == 5) return x.cycle_norm((T*)u, (const T*)f, s->d_norm);
+  if (part == 6) return x.solve_tail((T*)u, (const T*)f);
   return x.vcycle((T*)u, (const T*)f);
 }
 
@@ -1269,8 +1331,8 @@ mg_status plan_run_part(mg_solver* s, int part, void* u, const void* f, cudaStre
   s->launch_counter = 0;
   mg_status r = is_cd(s) ? cd_run_part(s, part, u, f, st)
                          : s->esz == 8 ? run_part<double>(s, part, u, f, st) : run_part<float>(s, part, u, f, st);
-  // launches of one cycle: the whole cycle, or head + tail of the pipelined split
-  if (part == 0) s->launches_per_cycle = s->launch_counter;
+  // launches of one cycle: the whole cycle (5: with its norm), or head + tail of the pipelined split
+  if (part == 0 || part == 5) s->launches_per_cycle = s->launch_counter;
   if (part == 1 || part == 4) s->head_launches = s->launch_counter;
   if (part == 2) s->tail_launches = s->launch_counter;
   if (part == 2 || part == 4) s->launches_per_cycle = s->head_launches + s->tail_launches;
@@ -1279,6 +1341,11 @@ mg_status plan_run_part(mg_solver* s, int part, void* u, const void* f, cudaStre
 
 mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st) {
   return plan_run_part(s, 0, u, f, st);
+}
+
+bool plan_solve_in_tail(mg_solver* s) {
+  if (is_cd(s) || comm_active(s)) return false;
+  return s->esz == 8 ? Exec<double>{s, 0}.tail_level() == 0 : Exec<float>{s, 0}.tail_level() == 0;
 }
 
 bool plan_can_split(mg_solver* s) {

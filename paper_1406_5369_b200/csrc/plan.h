@@ -14,6 +14,7 @@
 #include "kernels_cd.h"
 #include "comm.h"
 #include "checked.h"
+#include "loop_state.cuh"
 
 typedef struct ncclComm* ncclComm_t;
 
@@ -40,15 +41,6 @@ struct Level {
 };
 
 // state of the on-device driver loop (loop.cu); written by the host before each solve
-struct LoopState {
-  double rtol;     // in: stopping tolerance (r_k <= rtol * r0)
-  double r0;       // out: initial norm
-  double* hist;    // in: device history buffer (max+1 doubles) or NULL
-  int32_t max;     // in: max_cycles
-  int32_t k;       // out: cycles run
-  int32_t status;  // out: 0 ok, 1 r0 non-finite, 2 r_k non-finite
-  int32_t pad;
-};
 
 struct ProfRec {
   int kind;               // index into the kernel-name table
@@ -92,6 +84,11 @@ struct mg_solver {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   mg::LoopState* d_loop = nullptr;
   mg::LoopState* h_loop = nullptr;   // pinned
+  // while build_loop_graph captures the loop body: its conditional handle, so a whole-cycle
+  // tail can run the per-cycle check itself (cap_loop_fused: it did, no k_loop_check)
+  bool cap_loop = false;
+  bool cap_loop_fused = false;
+  cudaGraphConditionalHandle cap_h = 0;
   double* d_hist = nullptr;
   int64_t hist_cap = 0;
   std::map<std::tuple<void*, const void*, int>, cudaGraphExec_t> graphs;  // (u, f, part)
@@ -128,14 +125,18 @@ mg_status plan_build(mg_solver* s);
 void plan_free(mg_solver* s);
 mg_status plan_run_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st);
 mg_status plan_graph_vcycle(mg_solver* s, void* u, const void* f, cudaStream_t st);
-// part: 0 whole cycle, 1 head (first sweep + input norm -> d_norm), 2 tail, 3 norm -> d_norm
+// part: 0 whole cycle, 1 head (first sweep + input norm -> d_norm), 2 tail, 3 norm -> d_norm,
+// 4 later head, 5 cycle + its norm, 6 the whole solve in one launch (see plan.cu)
 mg_status plan_run_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st);
 mg_status plan_graph_part(mg_solver* s, int part, void* u, const void* f, cudaStream_t st);
 bool plan_can_split(mg_solver* s);
 // on-device driver loop (loop.cu): one graph launch runs the whole mg_solve loop
 bool plan_loop_supported(mg_solver* s);
+// the whole loop as one tail launch (tail_level() = 0: the grid is a whole-cycle tail)
+bool plan_solve_in_tail(mg_solver* s);
+// eager: launch plan_solve_in_tail's kernel directly (no graph; MG_FLAG_NO_GRAPH / profiling)
 mg_status plan_solve_device(mg_solver* s, void* u, const void* f, double rtol, int32_t max_cycles, int32_t* cycles,
-                            double* history, cudaStream_t st);
+                            double* history, cudaStream_t st, bool eager = false);
 mg_status plan_norm(mg_solver* s, int level, const void* u, const void* f, double* out, cudaStream_t st, bool sync);
 // wait for `st`: cudaStreamSynchronize, or with an NCCL communicator a poll of the stream and of
 // ncclCommGetAsyncError with the solver's timeout (abort + MG_ERR_NCCL on error or timeout)

@@ -1,5 +1,6 @@
 """On-device driver loop (loop.cu): mg_solve as one CUDA graph
-with a conditional WHILE node against the host-driven loop (MG_FLAG_HOST_LOOP) and
+with a conditional WHILE node — or, for grids whose whole cycle is the coarse tail, as
+one kernel launch — against the host-driven loop (MG_FLAG_HOST_LOOP) and
 the oracle's or_solve (the `Application` listing): identical cycle
 counts, bitwise identical iterates and residual histories."""
 import numpy as np
@@ -19,6 +20,12 @@ LOOP_CASES = [
     dict(dim=3, cells=(64, 64, 64), smoother="rbgs", dtype="f32"),
     dict(dim=2, cells=(32, 32), levels=1, smoother="rbgs"),               # single level, direct
     dict(dim=3, cells=(16, 16, 16), levels=2, smoother="rbgs", coarse="sweeps", ncoarse=10),
+    # whole-cycle tails (tail_level 0): mg_solve is ONE launch (plan_solve_in_tail) — on one CTA
+    # with the hierarchy in shared memory, or on the 16-CTA cluster with level 0 in global memory
+    dict(dim=2, cells=(64, 64), levels=5, smoother="jacobi", dtype="f32"),
+    dict(dim=3, cells=(32, 32, 32), smoother="rbgs"),
+    dict(dim=2, cells=(128, 128), smoother="jacobi", nu1=3, nu2=3),
+    dict(dim=2, cells=(64, 64), levels=4, smoother="rbgs"),              # direct coarse 7^2 (m = 49)
 ]
 
 
