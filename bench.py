@@ -518,9 +518,9 @@ def run_mg(args):
     S.profile_enable(False)
     ours = [r for r in recs if not (r["name"].startswith("memset") or r["name"].startswith("nccl"))]
     launches = sum(r["count"] for r in ours) / nprof  # our kernels per step (incl. the norm pipeline)
-    if device_loop and not any(r["name"].startswith(("coarse_tail+norm", "coarse_tail_solve")) for r in ours):
+    if device_loop and not any(r["name"].startswith("coarse_tail_solve") for r in ours):
         # the loop's check kernel (k_loop_check) per cycle (the profile pass is eager); a
-        # whole-cycle tail runs the check itself, or the whole solve (one launch)
+        # whole-cycle tail grid runs the whole solve in one launch
         launches += 1
     tot = sum(r["ms"] for r in recs)
     dom = max(recs, key=lambda r: r["ms"])  # the dominant kernel of the step

@@ -338,24 +338,45 @@ __device__ double tail_norm(const Mode& M, const LG& g, const Coef<T>& c, const 
 template <typename T, int DIM>
 __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   extern __shared__ __align__(16) unsigned char tsm[];
-  auto mode = [&](int k) { return Mode{k >= P.solo_from}; };
-  const bool sm_lv0 = P.smem_from == 0;  // the top tail level lives in shared memory (one CTA)
-  // ---- level arrays: levels >= smem_from in CTA 0's shared memory (compact layout P.gs[k]),
-  // four arrays u, t, f, r each; the others in global memory
-  auto G = [&](int k) { return lg_of(k >= P.smem_from ? P.gs[k] : P.g[k]); };
-  auto sarr = [&](int k, int a) -> T* {
-    const int n = P.gs[k].planes * (int)P.gs[k].pstride;
-    const int n16 = (n * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);
-    return reinterpret_cast<T*>(tsm + P.soff[k]) + a * n16;
-  };
-  auto U = [&](int k) { return k >= P.smem_from ? sarr(k, 0) : P.u[k]; };
-  auto Tt = [&](int k) { return k >= P.smem_from ? sarr(k, 1) : P.t[k]; };
-  auto F = [&](int k) { return k >= P.smem_from ? sarr(k, 2) : P.f[k]; };
-  auto R = [&](int k) { return k >= P.smem_from ? sarr(k, 3) : P.r[k]; };
   if (P.norm_only) {
-    tail_norm<T, DIM>(mode(0), lg_of(P.g[0]), P.c[0], P.u[0], P.f[0], P);
+    tail_norm<T, DIM>(Mode{0 >= P.solo_from}, lg_of(P.g[0]), P.c[0], P.u[0], P.f[0], P);
     return;
   }
+  const bool sm_lv0 = P.smem_from == 0;  // the top tail level lives in shared memory (one CTA)
+  // ---- per-level constants, derived once per launch into shared memory: levels >= smem_from
+  // keep their four arrays u, t, f, r in CTA 0's shared memory (compact layout P.gs[k]), the
+  // others in global memory.  (Re-deriving layouts and pointers from the kernel parameters at
+  // every use was 30% of a C1 cycle's instructions.)
+  struct LvRT {
+    LG g;
+    T* a[4];
+    int solo;
+  };
+  __shared__ LvRT lvt[kTailMax];
+  __shared__ Coef<T> lvc[kTailMax];
+  if (threadIdx.x < P.nl) {
+    const int k = threadIdx.x;
+    const bool sm = k >= P.smem_from;
+    LvRT e;
+    e.g = lg_of(sm ? P.gs[k] : P.g[k]);
+    const int n = P.gs[k].planes * (int)P.gs[k].pstride;
+    const int n16 = (n * (int)sizeof(T) + 15) / 16 * 16 / (int)sizeof(T);
+    T* base = reinterpret_cast<T*>(tsm + P.soff[k]);
+    e.a[0] = sm ? base : P.u[k];
+    e.a[1] = sm ? base + n16 : P.t[k];
+    e.a[2] = sm ? base + 2 * n16 : P.f[k];
+    e.a[3] = sm ? base + 3 * n16 : P.r[k];
+    e.solo = k >= P.solo_from;
+    lvt[k] = e;
+    lvc[k] = P.c[k];
+  }
+  __syncthreads();
+  auto mode = [&](int k) { return Mode{lvt[k].solo != 0}; };
+  auto G = [&](int k) { return lvt[k].g; };
+  auto U = [&](int k) { return lvt[k].a[0]; };
+  auto Tt = [&](int k) { return lvt[k].a[1]; };
+  auto F = [&](int k) { return lvt[k].a[2]; };
+  auto R = [&](int k) { return lvt[k].a[3]; };
   if (blockIdx.x == 0 && (P.smem_from < P.nl || P.chol_off >= 0)) {
     // CTA 0's shared memory: the top level's inputs when it lives there (u, also into t: the
     // Jacobi partner's Dirichlet boundary; f), the coarse factor, zeros everywhere else in the
@@ -413,7 +434,7 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   for (int k = 1; k < P.nl; k++) cur[k] = U(k);
   for (int k = 0; k < P.nl - 1; k++) {
     const LG g = G(k);
-    const Coef<T> c = P.c[k];
+    const Coef<T> c = lvc[k];
     const Mode M = mode(k);
     const bool zero = k > 0 || P.zero_first;  // V_H(0, ...)
     const bool fold = zero && P.nu1 > 0 && P.rbgs != 2;  // the zero guess folded into the first sweep
@@ -437,7 +458,7 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   {
     const int k = P.nl - 1;
     const LG g = G(k);
-    const Coef<T> c = P.c[k];
+    const Coef<T> c = lvc[k];
     const Mode M = mode(k);
     const bool zero = P.nl > 1 || P.zero_first;
     // DIRECT writes every interior node, so its zero guess needs no pass; SWEEPS folds it
@@ -454,10 +475,47 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
                                   : sweep<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k));
       }
     } else {
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const int m = P.m;
+      if (m > 1 && m <= 32 && P.y_off >= 0) {
+        // warp 0, lane i owns row i and node i (the oracle's row order: plane, y, x).  Bitwise
+        // the sequential substitutions: forward, column k finalises y_k and every row below
+        // subtracts L_ik y_k — row i still subtracts in the order k = 0, 1, ..; backward, x_kk
+        // arrives in descending kk, so lane i parks its products L_kk,i x_kk in shared memory
+        // and folds them in ascending kk once x_{i+1} is known.  The chains of dependent loads
+        // and divisions of one thread (measured 5000 cycles per substitution at m = 9) become
+        // one shuffle and one division per step.
+        if (blockIdx.x == 0 && threadIdx.x < 32) {
+          const int lane = threadIdx.x;
+          const bool own = lane < m;
+          const int jlo = DIM == 3 ? 1 : 0, nj = DIM == 3 ? g.ny - 1 : 1, ni = g.nx - 1;
+          const double* L = P.chol_off >= 0 ? reinterpret_cast<const double*>(tsm + P.chol_off) : P.chol;
+          const double* rd = reinterpret_cast<const double*>(tsm + P.y_off) + m;
+          double* Ps = reinterpret_cast<double*>(tsm + P.y_off) + 2 * m;  // [kk][i], 32 x 32
+          int node = 0;
+          if (own) {
+            const int r = lane / ni;
+            node = lin(g, 1 + lane - r * ni, jlo + r % nj, g.p_lo + r / nj);
+          }
+          double acc = own ? (double)F(k)[node] : 0.0;
+          for (int kk = 0; kk < m; kk++) {
+            if (lane == kk) acc = div_rn_via(acc, L[kk * m + kk], rd[kk]);
+            const double ykk = __shfl_sync(0xffffffffu, acc, kk);
+            if (lane > kk && own) acc = __dsub_rn(acc, __dmul_rn(L[lane * m + kk], ykk));
+          }
+          for (int i = m - 1; i >= 0; i--) {
+            if (lane == i) {
+              double sacc = acc;
+              for (int kk = i + 1; kk < m; kk++) sacc = __dsub_rn(sacc, Ps[kk * 32 + i]);
+              acc = div_rn_via(sacc, L[i * m + i], rd[i]);
+            }
+            const double xi = __shfl_sync(0xffffffffu, acc, i);
+            if (lane < i) Ps[i * 32 + lane] = __dmul_rn(L[i * m + lane], xi);
+          }
+          if (own) cur[k][node] = (T)acc;
+        }
+      } else if (blockIdx.x == 0 && threadIdx.x == 0) {
         // same loop order as k_coarse_direct / the oracle
         const int jlo = DIM == 3 ? 1 : 0, jhi = DIM == 3 ? g.ny - 1 : 0;
-        const int m = P.m;
         // the factor and the vector in shared memory: the substitutions are serial chains of
         // dependent loads (a global y costs an L2 round trip per step: measured 8.5 us at m = 9)
         const double* L = P.chol_off >= 0 ? reinterpret_cast<const double*>(tsm + P.chol_off) : P.chol;
@@ -515,7 +573,7 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   for (int k = P.nl - 2; k >= 0; k--) {
     const Mode M = mode(k);
     const LG g = G(k);
-    const Coef<T> c = P.c[k];
+    const Coef<T> c = lvc[k];
     const T* e = cur[k + 1];
     LG ge = G(k + 1);
     if (mode(k + 1).solo && !M.solo) {  // CTA 0's solo levels visible to every CTA
@@ -542,10 +600,7 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   }  // for (;;)
   // result of the top tail level in u[0]
   if (sm_lv0 || cur[0] != P.u[0]) copy_interior<T, DIM>(mode(0), G(0), (const T*)cur[0], lg_of(P.g[0]), P.u[0]);
-  if (P.norm_out && !P.solve) {
-    const double rk = tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
-    if (P.loop && blockIdx.x == 0 && threadIdx.x == 0) loop_check(rk, P.loop, P.loop_h);
-  }
+  if (P.norm_out && !P.solve) tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
 }
 
 }  // namespace
@@ -616,7 +671,8 @@ void tail_prepare(TailParams<T>& q) {
   // direct coarsest solve: its vector and (when it fits) the factor behind the levels
   q.chol_off = q.y_off = -1;
   if (!q.sweeps && q.m > 1) {
-    const long long lb = bytes16((long long)q.m * q.m * 8), yb = bytes16((long long)q.m * 16);  // y, 1 / L_ii
+    // y, 1 / L_ii, and for m <= 32 the backward substitution's 32 x 32 products
+    const long long lb = bytes16((long long)q.m * q.m * 8), yb = bytes16((long long)q.m * 16 + (q.m <= 32 ? 8192 : 0));
     if (off + lb + yb <= kTailSmemCap) {
       q.chol_off = (int)off;
       off += lb;

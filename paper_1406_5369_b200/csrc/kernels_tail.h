@@ -7,7 +7,7 @@ namespace mg {
 
 constexpr int kTailMax = 12;  // levels handled by one tail launch
 constexpr int kTailSmemMax = 200 * 1024;  // CTA 0's shared memory for the solo levels' arrays
-constexpr int kTailSmemCap = 226 * 1024;  // all dynamic shared memory (+ the coarse factor, below)
+constexpr int kTailSmemCap = 224 * 1024;  // all dynamic shared memory (+ the coarse factor; 3 KB static below 227 KB)
 
 template <typename T>
 struct TailParams {
@@ -38,9 +38,7 @@ struct TailParams {
   int norm_only;
   double* norm_out;
   double* nscratch;  // csize doubles (per-CTA sums)
-  LoopState* loop;   // with norm_out inside the device loop's body: also the per-cycle check
   LoopState* solve;  // lt = 0: the whole driver loop in this launch (r0, cycles, norms, stop test)
-  cudaGraphConditionalHandle loop_h;
   Geom g[kTailMax];
   Coef<T> c[kTailMax];
   T* u[kTailMax];

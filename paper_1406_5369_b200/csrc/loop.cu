@@ -81,14 +81,10 @@ static mg_status build_loop_graph(mg_solver* s, void* u, const void* f, cudaGrap
   if ((e = cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) !=
       cudaSuccess)
     return abort_capture(cuda_fail(s, e, "cudaStreamBeginCaptureToGraph"));
-  // 4: no refresh; 5: the cycle and its norm (one launch, with the check, for a whole-cycle tail)
-  s->cap_loop = true;
-  s->cap_h = h;
-  s->cap_loop_fused = false;
+  // 4: no refresh; 5: the cycle and its norm
   mg_status rb = split ? plan_run_part(s, 2, u, f, bs) : plan_run_part(s, 5, u, f, bs);
   if (rb == MG_OK && split) rb = plan_run_part(s, 4, u, f, bs);
-  s->cap_loop = false;
-  if (rb == MG_OK && !s->cap_loop_fused) {
+  if (rb == MG_OK) {
     k_loop_check<<<1, 1, 0, bs>>>(s->d_norm, s->d_loop, h);
     if ((e = cudaGetLastError()) != cudaSuccess) rb = cuda_fail(s, e, "k_loop_check");
   }

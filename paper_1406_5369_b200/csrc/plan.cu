@@ -425,11 +425,6 @@ struct Exec {
     P.norm_out = norm_out;
     P.norm_only = norm_only ? 1 : 0;
     P.nscratch = s->d_partial;
-    if (norm_out && !norm_only && s->cap_loop) {  // the device loop's per-cycle check rides along
-      P.loop = s->d_loop;
-      P.loop_h = s->cap_h;
-      s->cap_loop_fused = true;
-    }
     if (norm_only) return launch(s, st, K_TAIL_NORM, 0, 2 * w(0), [&] { return launch_tail<T>(P, st); });
     // a whole cycle on one CTA with level 0 in shared memory (the kernel copies u into both
     // ping-pong arrays there) needs no boundary copy into the global partner t

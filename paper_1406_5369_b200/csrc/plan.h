@@ -84,11 +84,6 @@ struct mg_solver {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   mg::LoopState* d_loop = nullptr;
   mg::LoopState* h_loop = nullptr;   // pinned
-  // while build_loop_graph captures the loop body: its conditional handle, so a whole-cycle
-  // tail can run the per-cycle check itself (cap_loop_fused: it did, no k_loop_check)
-  bool cap_loop = false;
-  bool cap_loop_fused = false;
-  cudaGraphConditionalHandle cap_h = 0;
   double* d_hist = nullptr;
   int64_t hist_cap = 0;
   std::map<std::tuple<void*, const void*, int>, cudaGraphExec_t> graphs;  // (u, f, part)

@@ -1,4 +1,4 @@
-"""Run mg_solve with the host loop (ncu cannot profile kernels inside conditional graphs):
+"""Run mg_solve with the host loop, eager launches (ncu cannot profile kernels inside conditional graphs):
 python tools/prof_solve.py [config] [cycles] [separate-prolong] — the same kernels as the bench's timed steps."""
 import sys
 sys.path.insert(0, ".")
@@ -10,7 +10,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 dim, nodes, sm, nu1, nu2, dt, levels, omega = bench.CONFIGS[cfg]
 S = mgb.Solver(dim, nodes, levels=levels, smoother=sm, omega=omega, nu1=nu1, nu2=nu2, dtype=dt,
-               flags=mgb.FLAG_HOST_LOOP | (mgb.FLAG_SEPARATE_PROLONG if "separate-prolong" in sys.argv[3:] else 0))
+               flags=mgb.FLAG_HOST_LOOP | mgb.FLAG_NO_GRAPH | (mgb.FLAG_SEPARATE_PROLONG if "separate-prolong" in sys.argv[3:] else 0))
 u, f = S.empty(), S.empty()
 S.workload_fill(u, 42)
 k, hist = S.solve(u, f, 0.0, n)
