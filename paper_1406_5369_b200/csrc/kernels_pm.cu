@@ -954,10 +954,11 @@ constexpr int NTR = 32 * TY / RPT;
 // to balance SMs; the halo re-loads of short chunks mostly hit L2.  So: among
 // chunk lengths >= 16 planes, minimise (ceil(waves)/waves) * (1 + halo/(2 zc))
 // plus a small penalty below 8 waves.
-// L2-resident levels (three arrays < 48 MB) may use chunks down to 4 planes: their halo
-// re-reads are L2 hits, and 16-plane chunks leave most of the GPU idle on 129^3.
+// L2-resident levels (three arrays < 100 MB of the 126 MB L2) may use chunks down to 4 planes: their halo
+// re-reads are L2 hits, and 16-plane chunks leave most of the GPU idle on 129^3 (measured C2
+// 0.190 -> 0.165 ms moving this bound from 48 to 100 MB: the 129^3 FP64 level is 55 MB).
 static int min_zc_for(const Geom& g, size_t esz) {
-  return (double)g.planes * (double)g.pstride * (double)esz * 3.0 < 48e6 ? 4 : 16;
+  return (double)g.planes * (double)g.pstride * (double)esz * 3.0 < 100e6 ? 4 : 16;
 }
 
 static int choose_zc(long long ntiles, int np, int resident, int halo, int min_zc = 16) {
