@@ -16,7 +16,10 @@
 // other node for a red-black colour).  The per-node arithmetic is the same
 // canonical device code as every other kernel (mg_common.cuh), so results are
 // bitwise identical to the op-by-op schedule.
+#include <algorithm>
 #include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "kernels.h"
 #include "kernels_tail.h"
@@ -37,16 +40,21 @@ __device__ __forceinline__ void cluster_sync() {
 // Work distribution of a pass.  A SOLO level runs on CTA 0 alone with block barriers — a block
 // barrier costs a fraction of a cluster barrier and the level's work is too small to pay for 16
 // SMs; the other CTAs skip solo passes entirely and meet CTA 0 at the next cluster barrier (the
-// transitions in k_tail).
+// transitions in k_tail).  A DIST level is split into slabs of planes, one per CTA, each held
+// with a halo plane on either side in that CTA's shared memory (LG::p_lo..p_hi are the CTA's own
+// planes): the CTA's warps take its own rows, writes to its first/last plane are mirrored into
+// the neighbours' halos through distributed shared memory (Mir), a cluster barrier between passes.
 struct Mode {
   bool solo;
+  bool dist = false;
   __device__ bool active() const { return !solo || blockIdx.x == 0; }
+  __device__ bool local() const { return solo || dist; }
   __device__ int wstart() const {
-    return solo ? (int)(threadIdx.x >> 5) : (int)(blockIdx.x * WPC + (threadIdx.x >> 5));
+    return local() ? (int)(threadIdx.x >> 5) : (int)(blockIdx.x * WPC + (threadIdx.x >> 5));
   }
-  __device__ int wstride() const { return solo ? WPC : (int)(gridDim.x * WPC); }
-  __device__ int start() const { return solo ? (int)threadIdx.x : (int)(blockIdx.x * NTT + threadIdx.x); }
-  __device__ int stride() const { return solo ? NTT : (int)(gridDim.x * NTT); }
+  __device__ int wstride() const { return local() ? WPC : (int)(gridDim.x * WPC); }
+  __device__ int start() const { return local() ? (int)threadIdx.x : (int)(blockIdx.x * NTT + threadIdx.x); }
+  __device__ int stride() const { return local() ? NTT : (int)(gridDim.x * NTT); }
   __device__ void sync() const {
     if (!solo)
       cluster_sync();
@@ -61,14 +69,51 @@ struct LG {
   int nx, ny, p_lo, p_hi, pg0, sy, sz, planes, rows;
   int shA, shC;  // log2 of the lane group of for_rows: all nodes / one colour of a row
   float inv_nr;  // 1 / rows per plane
+  int zoff;      // plane of the array's first stored plane (a dist slab's lower halo; else 0)
 };
 __device__ __forceinline__ int ceil_log2_32(int v) { return v >= 32 ? 5 : (v <= 1 ? 0 : 32 - __clz(v - 1)); }
 __device__ __forceinline__ LG lg_of(const Geom& g) {
   const int ni = g.nx - 1, nr = g.three_d ? g.ny - 1 : 1;
   return LG{g.nx, g.ny, g.p_lo, g.p_hi, g.p_glob0, (int)g.pitch, (int)g.pstride, g.planes, g.rows,
-            ceil_log2_32(ni), ceil_log2_32((ni + 1) >> 1), __frcp_rn((float)nr)};
+            ceil_log2_32(ni), ceil_log2_32((ni + 1) >> 1), __frcp_rn((float)nr), 0};
 }
-__device__ __forceinline__ int lin(const LG& g, int i, int j, int pl) { return pl * g.sz + j * g.sy + i; }
+__device__ __forceinline__ int lin(const LG& g, int i, int j, int pl) { return (pl - g.zoff) * g.sz + j * g.sy + i; }
+
+// A dist level's mirrors: after a pass, the CTA's first (last) own plane of the array it wrote
+// is copied whole into the lower (upper) halo of the CTAs whose slab window holds that plane —
+// the neighbour, and past it neighbours with empty slabs — through distributed shared memory
+// (rem: remote bases shifted to this CTA's local indexing), 16-byte stores by every thread after
+// a block barrier; the pass's cluster barrier then publishes them.  (Mirroring each node as it
+// was written cost more than the pass: measured 20% more instructions.)
+template <typename T>
+struct Mir {
+  int plo = -1, phi = -1, nlo = 0, nhi = 0;
+  int sz = 0, zoff = 0;
+  T* a[3] = {nullptr, nullptr, nullptr};  // the local u, t, r arrays (the mirrored ones)
+  T* rem[2][3][3];                        // [side][target][array]
+  __device__ __forceinline__ void push(const T* arr) const {
+    if (nlo + nhi == 0) return;  // uniform over the CTA (shared-memory table)
+    __syncthreads();
+    const int ai = arr == a[0] ? 0 : (arr == a[1] ? 1 : 2);
+    const bool v16 = ((long long)sz * (long long)sizeof(T)) % 16 == 0;
+    for (int side = 0; side < 2; side++) {
+      const int n = side ? nhi : nlo;
+      if (n == 0) continue;
+      const long long o = (long long)((side ? phi : plo) - zoff) * sz;
+      for (int t = 0; t < n; t++) {
+        T* dst = rem[side][t][ai] + o;
+        const T* src = arr + o;
+        if (v16) {
+          const int nv = sz * (int)sizeof(T) / 16;
+          for (int q = threadIdx.x; q < nv; q += NTT)
+            reinterpret_cast<uint4*>(dst)[q] = reinterpret_cast<const uint4*>(src)[q];
+        } else {
+          for (int q = threadIdx.x; q < sz; q += NTT) dst[q] = src[q];
+        }
+      }
+    }
+  }
+};
 
 // f - A u at p, canonical order (mg_common.cuh point_residual), DIM known at compile time
 template <typename T, int DIM>
@@ -101,7 +146,7 @@ __device__ __forceinline__ void for_rows(const Mode& M, const LG& g, int par, F&
     const int dp = DIM == 3 ? __float2int_rz(((float)row + 0.5f) * inv_nr) : row;
     const int pl = g.p_lo + dp;
     const int j = DIM == 3 ? 1 + row - dp * nr : 0;
-    const int base = pl * g.sz + j * g.sy;
+    const int base = (pl - g.zoff) * g.sz + j * g.sy;
     if (par < 0) {
       for (int i = 1 + sub_; i <= ni; i += G) f(i, j, pl, base + i);
     } else {
@@ -120,7 +165,7 @@ __device__ void zero_level(const Mode& M, const LG& g, T* u) {
 
 // one sweep of the smoother; Jacobi ping-pongs (returns the new current buffer)
 template <typename T, int DIM>
-__device__ T* sweep(const Mode& M, const LG& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f) {
+__device__ T* sweep(const Mode& M, const LG& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f, const Mir<T>& mi) {
   const bool act = M.active();
   if (rbgs == 2) {  // lexicographic omega-GS: hyperplanes i + j + global plane = s in order
     const int nj = DIM == 3 ? g.ny - 1 : 1;
@@ -144,18 +189,21 @@ __device__ T* sweep(const Mode& M, const LG& g, const Coef<T>& c, int rbgs, T* u
     for (int colour = 0; colour < 2; colour++) {
       for_rows<DIM>(M, g, colour,
                     [&](int, int, int, int p) { u[p] = add(u[p], mul(c.wd, pres<T, DIM>(u, p, g, c, f[p]))); });
+      mi.push(u);
       M.sync();
     }
     return u;
   }
   for_rows<DIM>(M, g, -1, [&](int, int, int, int p) { t[p] = add(u[p], mul(c.wd, pres<T, DIM>(u, p, g, c, f[p]))); });
+  mi.push(t);
   M.sync();
   return t;
 }
 
 template <typename T, int DIM>
-__device__ void residual(const Mode& M, const LG& g, const Coef<T>& c, const T* u, const T* f, T* r) {
+__device__ void residual(const Mode& M, const LG& g, const Coef<T>& c, const T* u, const T* f, T* r, const Mir<T>& mi) {
   for_rows<DIM>(M, g, -1, [&](int, int, int, int p) { r[p] = pres<T, DIM>(u, p, g, c, f[p]); });
+  mi.push(r);
   M.sync();
 }
 
@@ -194,26 +242,30 @@ __device__ void restrict_fw(const Mode& M, const LG& gf, const LG& gc, const T* 
 // nodes (the black pass then runs as usual).  With A 0 = D*0 - 0 = +0 and f - (+0) = f the
 // values are bitwise those of a sweep over a zeroed array.
 template <typename T, int DIM>
-__device__ T* sweep_from_zero(const Mode& M, const LG& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f) {
+__device__ T* sweep_from_zero(const Mode& M, const LG& g, const Coef<T>& c, int rbgs, T* u, T* t, const T* f,
+                              const Mir<T>& mi) {
   const T zero = (T)0;
   if (!rbgs) {
     for_rows<DIM>(M, g, -1, [&](int, int, int, int p) { t[p] = add(zero, mul(c.wd, sub(f[p], zero))); });
+    mi.push(t);
     M.sync();
     return t;
   }
   for_rows<DIM>(M, g, 0, [&](int, int, int, int p) { u[p] = add(zero, mul(c.wd, sub(f[p], zero))); });  // red
   for_rows<DIM>(M, g, 1, [&](int, int, int, int p) { u[p] = zero; });                                 // black: 0
+  mi.push(u);
   M.sync();
   for_rows<DIM>(M, g, 1, [&](int, int, int, int p) {  // black pass
     u[p] = add(u[p], mul(c.wd, pres<T, DIM>(u, p, g, c, f[p])));
   });
+  mi.push(u);
   M.sync();
   return u;
 }
 
 // u += P e, separable x -> y -> plane axis
 template <typename T, int DIM>
-__device__ void prolong(const Mode& M, const LG& gf, const LG& gc, const T* e, T* u) {
+__device__ void prolong(const Mode& M, const LG& gf, const LG& gc, const T* e, T* u, const Mir<T>& mi) {
   const T half = (T)0.5;
   for_rows<DIM>(M, gf, -1, [&](int i, int j, int pl, int pu) {
     const int pg = pl + gf.pg0;
@@ -232,6 +284,7 @@ __device__ void prolong(const Mode& M, const LG& gf, const LG& gc, const T* e, T
     const T v = dz ? mul(half, add(vy[0], vy[1])) : vy[0];
     u[pu] = add(u[pu], v);
   });
+  mi.push(u);
   M.sync();
 }
 
@@ -266,6 +319,33 @@ __device__ void copy_in(const LG& gs, const T* u, const T* f, const LG& gd, T* U
           U[pd[k]] = vu[k];
           Tt[pd[k]] = vu[k];
         }
+      }
+  }
+}
+// every node (x <= nx, all rows) of planes [pa, pb) from the layout gs into gd (a dist slab:
+// gd.zoff), into d1 and d2 (if set); eight elements per thread in flight
+template <typename T>
+__device__ void copy_planes(const LG& gs, const T* src, const LG& gd, T* d1, T* d2, int pa, int pb) {
+  constexpr int B = 8;
+  const int nx1 = gs.nx + 1;
+  const int n = nx1 * gs.rows * (pb - pa);
+  for (int q0 = threadIdx.x; q0 < n; q0 += B * NTT) {
+    T v[B];
+    int pd[B];
+#pragma unroll
+    for (int k = 0; k < B; k++) {
+      const int q = q0 + k * NTT;
+      const int row = q / nx1, i = q - row * nx1;
+      const int dpl = row / gs.rows, j = row - dpl * gs.rows;
+      const int pl = pa + dpl;
+      pd[k] = (pl - gd.zoff) * gd.sz + j * gd.sy + i;
+      if (q < n) v[k] = src[(pl - gs.zoff) * gs.sz + j * gs.sy + i];
+    }
+#pragma unroll
+    for (int k = 0; k < B; k++)
+      if (q0 + k * NTT < n) {
+        d1[pd[k]] = v[k];
+        if (d2) d2[pd[k]] = v[k];
       }
   }
 }
@@ -338,22 +418,29 @@ __device__ double tail_norm(const Mode& M, const LG& g, const Coef<T>& c, const 
 template <typename T, int DIM>
 __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   extern __shared__ __align__(16) unsigned char tsm[];
-  if (P.norm_only) {
-    tail_norm<T, DIM>(Mode{0 >= P.solo_from}, lg_of(P.g[0]), P.c[0], P.u[0], P.f[0], P);
+  if (P.norm_only) {  // the distribution of the cycle's fused norm (a dist level 0: this CTA's slab)
+    LG g0 = lg_of(P.g[0]);
+    if (P.dist_n > 0) {
+      g0.p_lo = P.zr[0][blockIdx.x];
+      g0.p_hi = P.zr[0][blockIdx.x + 1];
+    }
+    tail_norm<T, DIM>(Mode{0 >= P.solo_from, P.dist_n > 0}, g0, P.c[0], P.u[0], P.f[0], P);
     return;
   }
   const bool sm_lv0 = P.smem_from == 0;  // the top tail level lives in shared memory (one CTA)
   // ---- per-level constants, derived once per launch into shared memory: levels >= smem_from
-  // keep their four arrays u, t, f, r in CTA 0's shared memory (compact layout P.gs[k]), the
-  // others in global memory.  (Re-deriving layouts and pointers from the kernel parameters at
-  // every use was 30% of a C1 cycle's instructions.)
+  // keep their four arrays u, t, f, r in CTA 0's shared memory (compact layout P.gs[k]), dist
+  // levels (k < dist_n) their slabs in every CTA's, the others live in global memory.
+  // (Re-deriving layouts and pointers from the kernel parameters at every use was 30% of a C1
+  // cycle's instructions.)
   struct LvRT {
     LG g;
     T* a[4];
-    int solo;
+    int solo, dist;
   };
   __shared__ LvRT lvt[kTailMax];
   __shared__ Coef<T> lvc[kTailMax];
+  __shared__ Mir<T> lvm[kTailDistMax + 1];  // the dist levels' mirrors; [kTailDistMax]: none
   if (threadIdx.x < P.nl) {
     const int k = threadIdx.x;
     const bool sm = k >= P.smem_from;
@@ -367,25 +454,75 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
     e.a[2] = sm ? base + 2 * n16 : P.f[k];
     e.a[3] = sm ? base + 3 * n16 : P.r[k];
     e.solo = k >= P.solo_from;
+    e.dist = k < P.dist_n;
+    if (e.dist) {
+      namespace cg = cooperative_groups;
+      const int r = blockIdx.x, C = gridDim.x;
+      const int z0 = P.zr[k][r], z1 = P.zr[k][r + 1];
+      e.g = lg_of(P.gd[k]);
+      e.g.p_lo = z0;
+      e.g.p_hi = z1;
+      e.g.zoff = z0 - 1;
+      T* b = reinterpret_cast<T*>(tsm + P.doff[k]);
+      const int m = P.dn16[k];
+      e.a[0] = b;                               // u
+      e.a[2] = b + m;                           // f
+      e.a[3] = b + 2 * m;                       // r
+      e.a[1] = P.rbgs ? nullptr : b + 3 * m;    // t (Jacobi)
+      Mir<T> mi;
+      mi.a[0] = e.a[0];
+      mi.a[1] = e.a[1];
+      mi.a[2] = e.a[3];
+      mi.sz = e.g.sz;
+      mi.zoff = e.g.zoff;
+      if (z1 > z0) {
+        mi.plo = z0;
+        mi.phi = z1 - 1;
+        const int sz = e.g.sz;
+        // ranks whose window [zr[s] - 1, zr[s+1]] holds my first / last plane
+        for (int s2 = r - 1; s2 >= 0 && P.zr[k][s2 + 1] == z0 && mi.nlo < 3; s2--, mi.nlo++)
+          for (int ai = 0; ai < 3; ai++)
+            mi.rem[0][mi.nlo][ai] = mi.a[ai] ? cg::this_cluster().map_shared_rank(mi.a[ai], s2) +
+                                                   (z0 - P.zr[k][s2]) * sz
+                                             : nullptr;
+        for (int s2 = r + 1; s2 < C && P.zr[k][s2] == z1 && mi.nhi < 3; s2++, mi.nhi++)
+          for (int ai = 0; ai < 3; ai++)
+            mi.rem[1][mi.nhi][ai] = mi.a[ai] ? cg::this_cluster().map_shared_rank(mi.a[ai], s2) +
+                                                   (z0 - P.zr[k][s2]) * sz
+                                             : nullptr;
+      }
+      lvm[k] = mi;
+    }
     lvt[k] = e;
     lvc[k] = P.c[k];
   }
+  if (threadIdx.x == 0) lvm[kTailDistMax] = Mir<T>{};
   __syncthreads();
-  auto mode = [&](int k) { return Mode{lvt[k].solo != 0}; };
+  auto mode = [&](int k) { return Mode{lvt[k].solo != 0, lvt[k].dist != 0}; };
+  auto MI = [&](int k) -> const Mir<T>& { return lvm[k < P.dist_n ? k : kTailDistMax]; };
   auto G = [&](int k) { return lvt[k].g; };
   auto U = [&](int k) { return lvt[k].a[0]; };
   auto Tt = [&](int k) { return lvt[k].a[1]; };
   auto F = [&](int k) { return lvt[k].a[2]; };
   auto R = [&](int k) { return lvt[k].a[3]; };
+  auto zero = [&](const unsigned char* a, const unsigned char* b) {
+    for (uint4* q = reinterpret_cast<uint4*>(const_cast<unsigned char*>(a)) + threadIdx.x;
+         reinterpret_cast<const unsigned char*>(q) < b; q += NTT)
+      *q = make_uint4(0u, 0u, 0u, 0u);
+  };
+  if (P.dist_n > 0) {
+    // every CTA: zeroed slabs (halos, boundaries, coarse guesses), then the top level's inputs
+    // when it is dist — f on the own planes, u (also into t) on the window with its halos
+    zero(tsm, tsm + P.doff[P.dist_n - 1] + (P.rbgs ? 3 : 4) * P.dn16[P.dist_n - 1] * (int)sizeof(T));
+    __syncthreads();
+    const LG g0 = lg_of(P.g[0]), d0 = G(0);
+    copy_planes<T>(g0, P.f[0], d0, F(0), nullptr, d0.p_lo, d0.p_hi);
+    if (!P.zero_first) copy_planes<T>(g0, P.u[0], d0, U(0), Tt(0), d0.p_lo - 1, d0.p_hi + 1);
+  }
   if (blockIdx.x == 0 && (P.smem_from < P.nl || P.chol_off >= 0)) {
     // CTA 0's shared memory: the top level's inputs when it lives there (u, also into t: the
     // Jacobi partner's Dirichlet boundary; f), the coarse factor, zeros everywhere else in the
     // shared-memory levels (boundaries, residual borders, coarse guesses); one barrier
-    auto zero = [&](const unsigned char* a, const unsigned char* b) {
-      for (uint4* q = reinterpret_cast<uint4*>(const_cast<unsigned char*>(a)) + threadIdx.x;
-           reinterpret_cast<const unsigned char*>(q) < b; q += NTT)
-        *q = make_uint4(0u, 0u, 0u, 0u);
-    };
     if (P.chol_off >= 0) {
       double* Ls = reinterpret_cast<double*>(tsm + P.chol_off);
       for (int q = threadIdx.x; q < P.m * P.m; q += NTT) Ls[q] = P.chol[q];
@@ -405,8 +542,9 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
         zero(tsm + P.soff[P.smem_from], end);
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
+  if (P.dist_n > 0) cluster_sync();  // no CTA mirrors into a slab its owner is still zeroing
   // ---- P.solve: the driver loop of mg_solve in this launch — the level arrays stay
   // where they are between cycles (the top level's iterate in cur[0]); else one cycle
   T* cur[kTailMax];
@@ -444,15 +582,28 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
     }
     for (int s = 0; s < P.nu1; s++) {
       T* oth = cur[k] == U(k) ? Tt(k) : U(k);
-      cur[k] = (s == 0 && fold) ? sweep_from_zero<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k))
-                                : sweep<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k));
+      cur[k] = (s == 0 && fold) ? sweep_from_zero<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k), MI(k))
+                                : sweep<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k), MI(k));
     }
     // separate residual and restriction passes: measured faster than one fused pass whose
     // coarse threads each evaluate 3^d fine residuals (latency-bound serial chains)
-    residual<T, DIM>(M, g, c, cur[k], F(k), R(k));
+    residual<T, DIM>(M, g, c, cur[k], F(k), R(k), MI(k));
     // the restriction writes level k+1: its mode (a solo coarse level is restricted by CTA 0,
-    // reading the residual the cluster barrier above made visible)
-    restrict_fw<T, DIM>(mode(k + 1), g, G(k + 1), R(k), F(k + 1));
+    // reading the residual the cluster barrier above made visible); from a dist level every CTA
+    // restricts the coarse planes of its slab (zr[k+1]) from its own residual slab, into the
+    // coarse f wherever it lives (its own slab, CTA 0's shared memory, global memory)
+    if (M.dist) {
+      LG gc = G(k + 1);
+      T* fc = F(k + 1);
+      if (!mode(k + 1).dist) {
+        gc.p_lo = P.zr[k + 1][blockIdx.x];
+        gc.p_hi = P.zr[k + 1][blockIdx.x + 1];
+        if (k + 1 >= P.smem_from) fc = cooperative_groups::this_cluster().map_shared_rank(fc, 0);
+      }
+      restrict_fw<T, DIM>(Mode{false, true}, g, gc, R(k), fc);
+    } else {
+      restrict_fw<T, DIM>(mode(k + 1), g, G(k + 1), R(k), F(k + 1));
+    }
   }
   // ---- coarsest level (Alg. 1 line 2)
   {
@@ -471,8 +622,8 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
     if (P.sweeps) {
       for (int s = 0; s < P.ncoarse; s++) {
         T* oth = cur[k] == U(k) ? Tt(k) : U(k);
-        cur[k] = (s == 0 && fold) ? sweep_from_zero<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k))
-                                  : sweep<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k));
+        cur[k] = (s == 0 && fold) ? sweep_from_zero<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k), MI(k))
+                                  : sweep<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k), MI(k));
       }
     } else {
       const int m = P.m;
@@ -576,7 +727,10 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
     const Coef<T> c = lvc[k];
     const T* e = cur[k + 1];
     LG ge = G(k + 1);
-    if (mode(k + 1).solo && !M.solo) {  // CTA 0's solo levels visible to every CTA
+    if (mode(k + 1).solo && M.dist) {  // read CTA 0's coarse correction in place (DSMEM)
+      if (k + 1 >= P.smem_from) e = cooperative_groups::this_cluster().map_shared_rank(cur[k + 1], 0);
+      cluster_sync();
+    } else if (mode(k + 1).solo && !M.solo) {  // CTA 0's solo levels visible to every CTA
       if (k + 1 >= P.smem_from) {  // the correction lives in CTA 0's shared memory: publish it
         const LG gg = lg_of(P.g[k + 1]);
         if (blockIdx.x == 0) {
@@ -588,9 +742,9 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
       }
       cluster_sync();
     }
-    prolong<T, DIM>(M, g, ge, e, cur[k]);
+    prolong<T, DIM>(M, g, ge, e, cur[k], MI(k));
     for (int s = 0; s < P.nu2; s++)
-      cur[k] = sweep<T, DIM>(M, g, c, P.rbgs, cur[k], cur[k] == U(k) ? Tt(k) : U(k), F(k));
+      cur[k] = sweep<T, DIM>(M, g, c, P.rbgs, cur[k], cur[k] == U(k) ? Tt(k) : U(k), F(k), MI(k));
   }
   if (!P.solve) break;
   const double rk = tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
@@ -601,6 +755,7 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
   // result of the top tail level in u[0]
   if (sm_lv0 || cur[0] != P.u[0]) copy_interior<T, DIM>(mode(0), G(0), (const T*)cur[0], lg_of(P.g[0]), P.u[0]);
   if (P.norm_out && !P.solve) tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
+  if (P.dist_n > 0) cluster_sync();  // every slab stays alive until no CTA can touch it
 }
 
 }  // namespace
@@ -647,22 +802,67 @@ void tail_prepare(TailParams<T>& q) {
       q.solo_from = k;
       break;
     }
-  // the solo levels' arrays (u, t, f, r) in CTA 0's shared memory, compact layout: the coarsest
-  // levels that fit (a solo level above them stays in global memory)
   auto bytes16 = [](long long b) { return (b + 15) / 16 * 16; };
   auto words = [&](const Geom& g) { return bytes16((long long)g.planes * g.pstride * (long long)sizeof(T)); };
-  q.smem_from = q.nl;
-  long long total = 0;
-  for (int k = q.nl - 1; k >= q.solo_from; k--) {
-    Geom g = q.g[k];
+  auto compact = [](Geom g) {
     g.pitch = g.nx + 1;
     g.pstride = g.three_d ? (long long)(g.ny + 1) * (g.nx + 1) : g.pitch;
+    return g;
+  };
+  // dist levels: the leading cluster levels, split into plane slabs — level 0 evenly over the
+  // CTAs, each coarser level by ceil(z / 2) of the finer slab boundaries, so that a CTA owns
+  // coarse plane P iff it owns fine plane 2P: the restriction of its coarse planes and the
+  // prolongation into its fine planes read only its slabs and their one-plane halos.  They
+  // take the front of every CTA's shared memory, as long as they fit.
+  q.dist_n = 0;
+  long long dbytes = 0;
+  if (q.csize > 1 && q.rbgs != 2) {
+    const int C = q.csize;
+    const int kmax = std::min(q.solo_from, q.nl - 1);  // the coarsest level is never dist
+    for (int r = 0; r <= C; r++) q.zr[0][r] = q.g[0].p_lo + (int)((long long)(q.g[0].p_hi - q.g[0].p_lo) * r / C);
+    for (int k = 1; k <= kmax; k++)
+      for (int r = 0; r <= C; r++) q.zr[k][r] = (q.zr[k - 1][r] + 1) / 2;
+    for (int k = 0; k < kmax && k < kTailDistMax; k++) {
+      const Geom& g = q.g[k];
+      bool ok = g.p_glob0 == 0 && q.zr[k][0] == g.p_lo && q.zr[k][C] == g.p_hi;
+      if (k + 1 <= kmax) ok = ok && q.zr[k + 1][0] == q.g[k + 1].p_lo && q.zr[k + 1][C] == q.g[k + 1].p_hi;
+      int wmax = 0;
+      for (int r = 0; r < C && ok; r++) {
+        const int w = q.zr[k][r + 1] - q.zr[k][r];
+        wmax = std::max(wmax, w);
+        if (w > 0) {  // mirror targets: the neighbour and the empty slabs past it (at most 3)
+          int lo = 1, hi = 1;
+          for (int s2 = r - 1; s2 > 0 && q.zr[k][s2] == q.zr[k][r]; s2--) lo++;
+          for (int s2 = r + 1; s2 < C - 1 && q.zr[k][s2 + 1] == q.zr[k][r + 1]; s2++) hi++;
+          ok = lo <= 3 && hi <= 3;
+        }
+      }
+      if (!ok) break;
+      Geom gd = compact(g);
+      gd.planes = wmax + 2;
+      gd.p_glob0 = 0;
+      const long long m = words(gd) / (long long)sizeof(T);
+      const long long bytes = m * (long long)sizeof(T) * (q.rbgs ? 3 : 4);
+      if (dbytes + bytes > kTailSmemMax) break;
+      q.gd[k] = gd;
+      q.doff[k] = (int)dbytes;
+      q.dn16[k] = (int)m;
+      dbytes += bytes;
+      q.dist_n = k + 1;
+    }
+  }
+  // the solo levels' arrays (u, t, f, r) in CTA 0's shared memory behind the dist slabs,
+  // compact layout: the coarsest levels that fit (a solo level above them stays in global memory)
+  q.smem_from = q.nl;
+  long long total = dbytes;
+  for (int k = q.nl - 1; k >= q.solo_from; k--) {
+    const Geom g = compact(q.g[k]);
     if (total + 4 * words(g) > kTailSmemMax) break;
     total += 4 * words(g);
     q.gs[k] = g;
     q.smem_from = k;
   }
-  long long off = 0;
+  long long off = dbytes;
   for (int k = q.smem_from; k < q.nl; k++) {
     q.soff[k] = (int)off;
     off += 4 * words(q.gs[k]);

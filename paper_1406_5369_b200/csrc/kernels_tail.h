@@ -6,8 +6,10 @@
 namespace mg {
 
 constexpr int kTailMax = 12;  // levels handled by one tail launch
+constexpr int kTailCluster = 16;  // CTAs of the largest tail cluster
+constexpr int kTailDistMax = 4;   // dist levels at most
 constexpr int kTailSmemMax = 200 * 1024;  // CTA 0's shared memory for the solo levels' arrays
-constexpr int kTailSmemCap = 224 * 1024;  // all dynamic shared memory (+ the coarse factor; 3 KB static below 227 KB)
+constexpr int kTailSmemCap = 222 * 1024;  // all dynamic shared memory (+ the coarse factor; 5 KB static below 227 KB)
 
 template <typename T>
 struct TailParams {
@@ -24,6 +26,15 @@ struct TailParams {
   int soff[kTailMax];   // byte offset of level k's four arrays
   Geom gs[kTailMax];    // level k's compact shared-memory layout (pitch nx+1, no padding)
   int csize;       // CTAs (one cluster; set by tail_prepare)
+  // dist levels: the leading dist_n cluster levels are split into slabs of planes,
+  // CTA r holding planes [zr[k][r], zr[k][r+1]) plus a halo plane each side in its own shared
+  // memory at doff[k] (arrays u, f, r[, t] of dn16[k] elements, compact layout gd[k] whose
+  // `planes` is the largest window); zr is also set for level dist_n (the restriction into it)
+  int dist_n;
+  int zr[kTailMax][kTailCluster + 1];
+  int doff[kTailMax];
+  int dn16[kTailMax];
+  Geom gd[kTailMax];
   int m;           // coarsest unknowns (direct)
   double D_coarse;
   double rD_coarse;  // RN(1 / D_coarse) (m = 1)
