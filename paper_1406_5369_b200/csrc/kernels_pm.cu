@@ -249,6 +249,14 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
     auto in = [&](int k, int j) -> bool { return (inm >> (k * W + j)) & 1u; };
     auto inrow = [&](int k) -> uint32_t { return (inm >> (k * W)) & ((1u << W) - 1u); };
     T* orow = unew + (long long)oy0 * g.pitch;
+    // CORR (128 registers): the interior mask and the output row in shared memory, reloaded per
+    // plane, so that their live ranges end at the plane instead of being rematerialised at every
+    // use (measured FP32 0.449 -> 0.405 ms per level-0 launch; FP64 unchanged)
+    constexpr int TCOFF = PR_OFF + 3 * G::PB + 3 * G::CB;
+    if constexpr (CORR) {
+      reinterpret_cast<uint32_t*>(sm + TCOFF)[tid] = inm;
+      reinterpret_cast<T**>(sm + TCOFF + 1024)[tid] = orow;
+    }
 
     const int qlo = RB ? pa - 3 : pa - 2, qlast = RB ? pb : pb - 1;
     const uint32_t nlo = seq;
@@ -467,6 +475,10 @@ __global__ void __launch_bounds__(32 * TY / RPT, Geo<T>::MINB)
       int ps = (((pa - 1) % 3) + 3) % 3;  // PR slot of plane p (rotates 0, 1, 2)
       for (int p = pa - 1; p <= pb; p++) {
         R.wait(N(p));
+        if constexpr (CORR) {
+          inm = reinterpret_cast<volatile uint32_t*>(sm + TCOFF)[tid];
+          orow = reinterpret_cast<T* volatile*>(sm + TCOFF + 1024)[tid];
+        }
         const T* U0 = R.U(N(p - 1));  // u(p)
         const T* Up = R.U(N(p));      // u(p+1)
         const T* F0 = R.F(N(p));      // f(p)
@@ -1010,7 +1022,7 @@ cudaError_t launch_sweep(const Geom& g, const Coef<T>& c, bool rbgs, const T* ui
     kernel<<<nitems, NTR, smem, st>>>(tu, tf, g, c, uout, tiles_x, ntiles, zc, nitems, partial, te, gce);
   };
   if (ecoarse) {  // CORR: 3-slot u/f ring + 3 coarse boxes
-    constexpr int smem_corr = Ring<T, 3>::BAR_OFF + 128 + 3 * G::PB + 3 * G::CB;
+    constexpr int smem_corr = Ring<T, 3>::BAR_OFF + 128 + 3 * G::PB + 3 * G::CB + 1024 + 2048;
     static_assert(smem_corr <= G::SMEM, "CORR fits the plain sweep's shared memory");
     rbgs ? gor(k_sweep3d_rows<T, 1, false, 0, RPT, true>, smem_corr)
          : gor(k_sweep3d_rows<T, 0, false, 0, RPT, true>, smem_corr);

@@ -25,7 +25,7 @@ ROWS = [
     ("C2", "C2 129³ RBGS FP64", None, "—", False),
     ("C4", "C4 8193² Jacobi V(3,3) FP32 (2D warp-marching, 3 sweeps per pass, level 0 two HBM passes per cycle)",
      "head: norm + 3 Jacobi sweeps + residual/restriction L0 (issue-bound)", "2D 4095² Jacobi FP32: 60 ms", False),
-    ("C1", "C1 65² Jacobi V(2,2) FP64 (one launch per cycle)", None, "—", False),
+    ("C1", "C1 65² Jacobi V(2,2) FP64 (the whole solve in one launch)", None, "—", False),
     ("C2-lex", "C2-lex 129³ lexicographic GS V(2,2) FP64 (one launch per hyperplane)", None, "—", False),
     ("CD2-f32", "CD2 complex diffusion 4096² cells, Jacobi FAS V(2,2), complex FP32", "CD Jacobi L0 (warp-marching)",
      "**275 ms** generated (P:558), 37 ms hand-tuned (P:581)", True),
@@ -69,9 +69,21 @@ def main():
     s = s[:a] + "\n".join(out) + s[s.index("\n\n", a):]
     c3, c5 = L("C3-f64"), L("C5")
     ref = json.loads(open(os.path.join(B, "reference_C3-f64.json")).read().strip().splitlines()[-1])
-    s = re.sub(r"timed regions except C3 FP64 \(\d+ MHz median\) and C5 \(\d+ MHz\), both under `sw_power_cap`;",
-               f"timed regions except C3 FP64 ({c3['clocks']['sm_mhz']} MHz median) and C5 ({c5['clocks']['sm_mhz']} "
-               f"MHz), both under `sw_power_cap`;", s)
+    # the clocks sentence: every config whose timed region ran below the max clock
+    low = []
+    for c, *_ in ROWS:
+        try:
+            d = L(c)
+        except FileNotFoundError:
+            continue
+        ck = d.get("clocks", {})
+        if ck.get("sm_mhz") and ck.get("sm_max_mhz") and ck["sm_mhz"] < ck["sm_max_mhz"]:
+            low.append(f"{c} ({ck['sm_mhz']} MHz median, {', '.join('`%s`' % r for r in ck.get('reasons', [])) or 'no reason'})")
+    sent = ("SM clock at its maximum during every timed region" if not low else
+            "SM clock at its maximum during the timed regions except " + "; ".join(low))
+    a2 = s.index("SM clock ")
+    b2 = s.index("\n", s.index(").", a2))  # end of the sentence's line
+    s = s[:a2] + sent + " (`clocks` in each bench line; `sw_power_cap` moves a run by a few %)." + s[b2:]
     s = re.sub(r"CPU oracle \(plain C, the `--impl reference` arm\): [0-9.]+ s per 513³ cycle \+ norm on 16 threads\n"
                r"= [0-9.e]+ unknowns/s",
                f"CPU oracle (plain C, the `--impl reference` arm): {ref['ms_per_step'] / 1000:.2f} s per 513³ cycle + "
