@@ -380,15 +380,8 @@ __device__ __forceinline__ double div_rn_via(double a, double b, double y) {
 // ||f - A u|| of a level into *P.norm_out: FP64 sum of squares per thread in for_rows order,
 // warp shuffles, the CTA's warps in order, then (cluster mode) the CTAs in rank order — a fixed
 // order for a given launch shape (k_tail's norm-only and fused uses share it)
-template <typename T, int DIM>
-__device__ double tail_norm(const Mode& M, const LG& g, const Coef<T>& c, const T* u, const T* f,
-                            const TailParams<T>& P) {
-  if (!M.active()) return 0.0;
-  double acc = 0.0;
-  for_rows<DIM>(M, g, -1, [&](int, int, int, int p) {
-    const double r = (double)pres<T, DIM>(u, p, g, c, f[p]);
-    acc = __dadd_rn(acc, __dmul_rn(r, r));
-  });
+template <typename T>
+__device__ double norm_reduce(const Mode& M, double acc, const TailParams<T>& P) {
   __shared__ double wsum[WPC];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
@@ -413,6 +406,39 @@ __device__ double tail_norm(const Mode& M, const LG& g, const Coef<T>& c, const 
     if (P.norm_out) *P.norm_out = sum;
   }
   return sum;
+}
+
+template <typename T, int DIM>
+__device__ double tail_norm(const Mode& M, const LG& g, const Coef<T>& c, const T* u, const T* f,
+                            const TailParams<T>& P) {
+  if (!M.active()) return 0.0;
+  double acc = 0.0;
+  for_rows<DIM>(M, g, -1, [&](int, int, int, int p) {
+    const double r = (double)pres<T, DIM>(u, p, g, c, f[p]);
+    acc = __dadd_rn(acc, __dmul_rn(r, r));
+  });
+  return norm_reduce(M, acc, P);
+}
+
+// a Jacobi sweep u -> t that also returns ||f - A u|| of its input (thread 0 of CTA 0): the
+// per-node residual the sweep forms anyway, the traversal and the reduction of tail_norm, so
+// the value is bitwise tail_norm's.  The one-launch solve takes each iterate's norm from the
+// next cycle's first sweep (written to the ping-pong partner: if the stop test then ends the
+// solve, the iterate is untouched) instead of a pass of its own.
+template <typename T, int DIM>
+__device__ double jacobi_norm(const Mode& M, const LG& g, const Coef<T>& c, const T* u, T* t, const T* f,
+                              const Mir<T>& mi, const TailParams<T>& P) {
+  double acc = 0.0;
+  for_rows<DIM>(M, g, -1, [&](int, int, int, int p) {
+    const T r = pres<T, DIM>(u, p, g, c, f[p]);
+    t[p] = add(u[p], mul(c.wd, r));
+    const double rd = (double)r;
+    acc = __dadd_rn(acc, __dmul_rn(rd, rd));
+  });
+  mi.push(t);
+  M.sync();
+  if (!M.active()) return 0.0;
+  return norm_reduce(M, acc, P);
 }
 
 template <typename T, int DIM>
@@ -561,13 +587,26 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
     cluster_sync();
     return *g;
   };
-  if (P.solve) {
+  // Jacobi with pre-smoothing: each iterate's norm from the next cycle's first sweep (jacobi_norm)
+  const bool fuse_norm = P.solve && P.rbgs == 0 && P.nu1 >= 1 && !P.zero_first;
+  if (P.solve && !fuse_norm) {
     const double r0 = tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
     int go = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) go = loop_begin(r0, P.solve) ? 1 : 0;
     if (!bcast(go)) return;  // u unchanged
   }
-  for (;;) {
+  for (int cyc = 0;; cyc++) {
+  bool first_done = false;  // level 0's first pre-sweep already ran (fuse_norm)
+  if (fuse_norm) {
+    T* oth = cur[0] == U(0) ? Tt(0) : U(0);
+    const double rk = jacobi_norm<T, DIM>(mode(0), G(0), lvc[0], cur[0], oth, F(0), MI(0), P);
+    int go = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      go = (cyc == 0 ? loop_begin(rk, P.solve) : loop_step(rk, P.solve)) ? 1 : 0;
+    if (!bcast(go)) break;  // cur[0] still holds the iterate
+    cur[0] = oth;
+    first_done = true;
+  }
   // ---- descend
   for (int k = 1; k < P.nl; k++) cur[k] = U(k);
   for (int k = 0; k < P.nl - 1; k++) {
@@ -580,7 +619,7 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
       zero_level(M, g, cur[k]);
       M.sync();
     }
-    for (int s = 0; s < P.nu1; s++) {
+    for (int s = (k == 0 && first_done) ? 1 : 0; s < P.nu1; s++) {
       T* oth = cur[k] == U(k) ? Tt(k) : U(k);
       cur[k] = (s == 0 && fold) ? sweep_from_zero<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k), MI(k))
                                 : sweep<T, DIM>(M, g, c, P.rbgs, cur[k], oth, F(k), MI(k));
@@ -747,11 +786,13 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
       cur[k] = sweep<T, DIM>(M, g, c, P.rbgs, cur[k], cur[k] == U(k) ? Tt(k) : U(k), F(k), MI(k));
   }
   if (!P.solve) break;
-  const double rk = tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
-  int go = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) go = loop_step(rk, P.solve) ? 1 : 0;
-  if (!bcast(go)) break;
-  }  // for (;;)
+  if (!fuse_norm) {
+    const double rk = tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
+    int go = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) go = loop_step(rk, P.solve) ? 1 : 0;
+    if (!bcast(go)) break;
+  }
+  }  // for (cyc)
   // result of the top tail level in u[0]
   if (sm_lv0 || cur[0] != P.u[0]) copy_interior<T, DIM>(mode(0), G(0), (const T*)cur[0], lg_of(P.g[0]), P.u[0]);
   if (P.norm_out && !P.solve) tail_norm<T, DIM>(mode(0), G(0), P.c[0], cur[0], F(0), P);
