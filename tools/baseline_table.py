@@ -69,8 +69,8 @@ def main():
     s = s[:a] + "\n".join(out) + s[s.index("\n\n", a):]
     c3, c5 = L("C3-f64"), L("C5")
     ref = json.loads(open(os.path.join(B, "reference_C3-f64.json")).read().strip().splitlines()[-1])
-    # the clocks sentence: every config whose timed region ran below the max clock
-    low = []
+    # the clocks sentence: configs whose timed region ran below the max clock, and throttle flags
+    low, flagged = [], []
     for c, *_ in ROWS:
         try:
             d = L(c)
@@ -78,9 +78,13 @@ def main():
             continue
         ck = d.get("clocks", {})
         if ck.get("sm_mhz") and ck.get("sm_max_mhz") and ck["sm_mhz"] < ck["sm_max_mhz"]:
-            low.append(f"{c} ({ck['sm_mhz']} MHz median, {', '.join('`%s`' % r for r in ck.get('reasons', [])) or 'no reason'})")
-    sent = ("SM clock at its maximum during every timed region" if not low else
-            "SM clock at its maximum during the timed regions except " + "; ".join(low))
+            low.append(f"{c} ({ck['sm_mhz']} MHz)")
+        if ck.get("reasons"):
+            flagged.append(f"{c} ({', '.join('`%s`' % r for r in ck['reasons'])})")
+    sent = ("SM clock median at its maximum in every timed region" if not low else
+            "SM clock median at its maximum in every timed region except " + ", ".join(low))
+    if flagged:
+        sent += "; throttle reasons sampled during " + ", ".join(flagged)
     a2 = s.index("SM clock ")
     b2 = s.index("\n", s.index(").", a2))  # end of the sentence's line
     s = s[:a2] + sent + " (`clocks` in each bench line; `sw_power_cap` moves a run by a few %)." + s[b2:]
