@@ -173,9 +173,11 @@ mg_status mg_residual_norm(mg_solver* s, const void* u, const void* f, double* o
  * norm is NaN/Inf (the loop stops at that cycle).
  * By default the whole loop runs on the device: one CUDA graph whose WHILE
  * node repeats {cycle, norm, test} with the stopping test evaluated by a kernel,
- * one host synchronisation per solve.  MG_FLAG_HOST_LOOP, MG_FLAG_NO_GRAPH,
+ * one host synchronisation per solve.  On grids whose whole cycle is the coarse tail
+ * (small levels only, e.g. 65^2) the loop runs inside ONE kernel launch instead (also
+ * with MG_FLAG_NO_GRAPH or profiling).  MG_FLAG_HOST_LOOP, MG_FLAG_NO_GRAPH,
  * profiling, or nranks > 1 (NCCL cannot run inside a conditional node) select
- * the host loop; both give bitwise identical iterates and norms. */
+ * the host loop; all give bitwise identical iterates and norms. */
 mg_status mg_solve(mg_solver* s, void* u, const void* f, double rtol, int32_t max_cycles,
                    int32_t* cycles, double* history, void* stream);
 
