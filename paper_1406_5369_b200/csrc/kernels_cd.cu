@@ -30,19 +30,6 @@ struct Cell {
   long long q;
 };
 
-__device__ __forceinline__ long long ncells(const Geom& g) {
-  return (long long)g.nx * (g.three_d ? g.ny : 1) * g.nz;
-}
-__device__ __forceinline__ Cell cell_of(const Geom& g, long long t) {
-  Cell c;
-  c.i = (int)(t % g.nx);
-  const long long r = t / g.nx;
-  const int nr = g.three_d ? g.ny : 1;
-  c.j = (int)(r % nr);
-  c.k = (int)(r / nr);
-  c.q = (long long)c.k * g.pstride + (long long)c.j * g.pitch + c.i;
-  return c;
-}
 
 // Visit every cell of a level: blocks stride over rows (one 32-bit division per row, not
 // per cell); a block covers 2^r rows at once when a row is narrower than the block.
@@ -294,8 +281,6 @@ int grid_rows(const Geom& g, int width) {
   while (((long long)width << (sh + 1)) <= NB) sh++;
   return grid_for(((rows + (1ll << sh) - 1) >> sh) * NB);
 }
-
-long long host_cells(const Geom& g) { return (long long)g.nx * (g.three_d ? g.ny : 1) * g.nz; }
 
 }  // namespace
 

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(NT) k_cd_jacobi2d(const __grid_constant__ CUte
           uR = u0e;
           gR = g0e;
         }
-        V o;
+        V o{};
 #pragma unroll
         for (int j = 0; j < CW; j++) {
           const int ci = ox + j;
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(NT) k_cd_jacobi2d_k(const __grid_constant__ CU
           }
         }
         const bool ym = rho > 0, yp = rho < g.nz - 1;
-        V o;
+        V o{};
 #pragma unroll
         for (int j = 0; j < CW; j++) {
           const C2<T> uc = cell(u0, j), gc = cell(g0, j);

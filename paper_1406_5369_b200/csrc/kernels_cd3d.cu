@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(NT) k_cd_jacobi3d(const __grid_constant__ CUte
       const C2<T> uL = {U0[bo - 2], U0[bo - 1]}, gL = {G0[bo - 2], G0[bo - 1]};
       const C2<T> uR = {U0[bo + 2 * CW], U0[bo + 2 * CW + 1]}, gR = {G0[bo + 2 * CW], G0[bo + 2 * CW + 1]};
       const bool zm = p > 0, zp = p < g.nz - 1;
-      V o;
+      V o{};
 #pragma unroll
       for (int j = 0; j < CW; j++) {
         const C2<T> uc = cell(u0, j), gc = cell(g0, j);

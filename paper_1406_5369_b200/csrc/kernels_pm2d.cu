@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(NT) k_jacobi2d_k(const __grid_constant__ CUten
     // window slot of a row: (row - ts + 1) mod 3; S[k][slot] stage k, e0[slot] stage-0 edge
     V S[K + 1][3];
     T e0[3];
-    V Fw[3];
+    V Fw[3] = {};  // (early slots feed only values that are never stored)
     V Fold;                      // RR with K = 3: f of row t-3 (its window slot is reused by row t)
     T ty1[NRC], ty2[NRC];        // RR: x-sums of the two previous residual rows
 #pragma unroll

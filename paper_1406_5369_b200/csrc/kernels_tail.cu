@@ -86,11 +86,18 @@ __device__ __forceinline__ int lin(const LG& g, int i, int j, int pl) { return (
 // a block barrier; the pass's cluster barrier then publishes them.  (Mirroring each node as it
 // was written cost more than the pass: measured 20% more instructions.)
 template <typename T>
-struct Mir {
-  int plo = -1, phi = -1, nlo = 0, nhi = 0;
-  int sz = 0, zoff = 0;
-  T* a[3] = {nullptr, nullptr, nullptr};  // the local u, t, r arrays (the mirrored ones)
-  T* rem[2][3][3];                        // [side][target][array]
+struct Mir {  // plain data (a __shared__ table): set every field through none()
+  int plo, phi, nlo, nhi;
+  int sz, zoff;
+  T* a[3];            // the local u, t, r arrays (the mirrored ones)
+  T* rem[2][3][3];    // [side][target][array]
+  __device__ static Mir none() {
+    Mir m;
+    m.plo = m.phi = -1;
+    m.nlo = m.nhi = m.sz = m.zoff = 0;
+    m.a[0] = m.a[1] = m.a[2] = nullptr;
+    return m;
+  }
   __device__ __forceinline__ void push(const T* arr) const {
     if (nlo + nhi == 0) return;  // uniform over the CTA (shared-memory table)
     __syncthreads();
@@ -495,7 +502,7 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
       e.a[2] = b + m;                           // f
       e.a[3] = b + 2 * m;                       // r
       e.a[1] = P.rbgs ? nullptr : b + 3 * m;    // t (Jacobi)
-      Mir<T> mi;
+      Mir<T> mi = Mir<T>::none();
       mi.a[0] = e.a[0];
       mi.a[1] = e.a[1];
       mi.a[2] = e.a[3];
@@ -522,7 +529,7 @@ __global__ void __launch_bounds__(NTT, 1) k_tail(TailParams<T> P) {
     lvt[k] = e;
     lvc[k] = P.c[k];
   }
-  if (threadIdx.x == 0) lvm[kTailDistMax] = Mir<T>{};
+  if (threadIdx.x == 0) lvm[kTailDistMax] = Mir<T>::none();
   __syncthreads();
   auto mode = [&](int k) { return Mode{lvt[k].solo != 0, lvt[k].dist != 0}; };
   auto MI = [&](int k) -> const Mir<T>& { return lvm[k < P.dist_n ? k : kTailDistMax]; };
