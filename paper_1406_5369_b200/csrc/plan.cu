@@ -426,9 +426,9 @@ struct Exec {
     P.norm_only = norm_only ? 1 : 0;
     P.nscratch = s->d_partial;
     if (norm_only) return launch(s, st, K_TAIL_NORM, 0, 2 * w(0), [&] { return launch_tail<T>(P, st); });
-    // a whole cycle on one CTA with level 0 in shared memory (the kernel copies u into both
-    // ping-pong arrays there) needs no boundary copy into the global partner t
-    if (lt == 0 && P.smem_from != 0) {
+    // only Jacobi with level 0 in global memory uses the global partner t (whose boundary must
+    // hold u's): in shared memory, one CTA's or dist slabs, the kernel copies u into both
+    if (lt == 0 && P.rbgs == 0 && P.smem_from != 0 && P.dist_n == 0) {
       const mg_status r = cycle_start(u_top, f_top);
       if (r != MG_OK) return r;
     }
@@ -443,7 +443,7 @@ struct Exec {
     TailParams<T> P = tail_params(0, u, f);
     P.solve = s->d_loop;
     P.nscratch = s->d_partial;
-    if (P.smem_from != 0) {
+    if (P.rbgs == 0 && P.smem_from != 0 && P.dist_n == 0) {  // the global Jacobi partner's boundary
       const mg_status r = cycle_start(u, f);
       if (r != MG_OK) return r;
     }

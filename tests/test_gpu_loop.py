@@ -124,3 +124,28 @@ def test_negative_rtol_runs_exactly_max_cycles(host):
     assert k == 7 and len(hist) == 8 and all(h == 0.0 for h in hist)
     with pytest.raises(mgb.MGError):
         S.solve(u, f, float("nan"), 3)
+
+
+@pytest.mark.parametrize("case", [dict(dim=2, cells=(64, 64), levels=5, smoother="jacobi"),
+                                  dict(dim=3, cells=(32, 32, 32), smoother="rbgs")],
+                         ids=["C1-one-CTA", "3D-cluster"])
+def test_whole_cycle_tail_solve_is_one_launch(case):
+    """On a grid whose whole cycle is the coarse tail, mg_solve is ONE kernel launch (r0, the
+    cycles, their norms and the stop test inside k_tail; profiling makes the launch eager, the
+    same kernel), and its results are bitwise those of the per-cycle host loop."""
+    import paper_1406_5369_b200 as mgb
+    S, O = make(**case)
+    u, f = wl.workload("W1", case["dim"], case["cells"], seed=3, dtype=S.np_dtype)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    S.profile_enable(True)
+    k, hist = S.solve(du, df, 0.0, 6)
+    recs = S.profile_read()
+    S.profile_enable(False)
+    ours = [r for r in recs if not r["name"].startswith("memset")]
+    assert [r["name"].split("@")[0] for r in ours] == ["coarse_tail_solve"]
+    assert ours[0]["count"] == 1
+    H, _ = make(**case, flags=mgb.FLAG_HOST_LOOP)
+    dh = H.from_numpy(u)
+    kh, hh = H.solve(dh, H.from_numpy(f), 0.0, 6)
+    assert k == kh and np.array_equal(np.array(hist), np.array(hh))
+    assert np.array_equal(S.to_numpy(du), H.to_numpy(dh))
