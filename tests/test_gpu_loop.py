@@ -149,3 +149,35 @@ def test_whole_cycle_tail_solve_is_one_launch(case):
     kh, hh = H.solve(dh, H.from_numpy(f), 0.0, 6)
     assert k == kh and np.array_equal(np.array(hist), np.array(hh))
     assert np.array_equal(S.to_numpy(du), H.to_numpy(dh))
+
+
+@pytest.mark.parametrize("host", [False, True], ids=["device", "host"])
+def test_whole_cycle_tail_jacobi_stopping_rules(host):
+    """The one-launch Jacobi solve takes each norm from the next cycle's first sweep: max_cycles
+    = 0, a non-finite r0, rtol < 0 (exactly max cycles) and an early rtol stop must leave u
+    exactly as the per-cycle loop does."""
+    import paper_1406_5369_b200 as mgb
+    flags = mgb.FLAG_HOST_LOOP if host else 0
+    case = dict(dim=2, cells=(64, 64), levels=5, smoother="jacobi")
+    S, O = make(**case, flags=flags)
+    u, f = wl.workload("W1", 2, (64, 64), seed=11)
+    du, df = S.from_numpy(u), S.from_numpy(f)
+    k, hist = S.solve(du, df, 0.0, 0)
+    assert k == 0 and len(hist) == 1 and abs(hist[0] / O.norm(0, u, f) - 1) <= 1e-12
+    assert np.array_equal(S.to_numpy(du), u)
+    k, hist = S.solve(du, df, -1.0, 3)
+    assert k == 3 and len(hist) == 4
+    uo = u
+    for _ in range(3):
+        uo = O.vcycle(uo, f)
+    assert np.array_equal(S.to_numpy(du), uo)
+    k, hist = S.solve(du, df, 0.5, 10)
+    assert k == 1
+    assert np.array_equal(S.to_numpy(du), O.vcycle(uo, f))
+    f2 = f.copy()
+    f2[7, 9] = np.nan
+    d2 = S.from_numpy(u)
+    with pytest.raises(mgb.MGError) as ei:
+        S.solve(d2, S.from_numpy(f2), 1e-10, 5)
+    assert ei.value.status == 6
+    assert np.array_equal(S.to_numpy(d2), u)
