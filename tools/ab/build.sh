@@ -1,6 +1,7 @@
 # build an experimental variant of libmgb200 into exp/lib_$1.so from a copy of the tree with a
-# python patch applied: bash exp/build.sh NAME patch.py   (exp/ is scratch, not product)
+# python patch applied: bash tools/ab/build.sh NAME patch.py   (output in exp/, git-ignored scratch)
 set -e
+mkdir -p exp
 N=$1; PATCH=$2; D=/tmp/exp_$N
 rm -rf $D; mkdir -p $D/b; cp -r paper_1406_5369_b200/csrc include $D/
 [ -n "$PATCH" ] && python $PATCH $D/csrc
